@@ -1,0 +1,210 @@
+/*
+ * rdkv_cuda.h — C-ABI of the B200-native RDKV accelerator path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and
+ * a cudaStream_t (passed as void*), no C++ or torch types. Every entry point
+ * replaces a reference C++ entry point under /root/reference/proj/core:
+ *
+ *   rdkv_cuda_weights   attention_probe + token_weights + channel_weights
+ *                       (cache.hpp:123-124, weights.hpp:26,34; called from
+ *                       allocate_head pipeline.cpp:128-146)
+ *   rdkv_cuda_allocate  head_budget + allocate_v + allocate_k + mckp_bisect
+ *                       (pipeline.hpp:73-93, allocator.hpp:62-64;
+ *                       allocate_model pipeline.hpp:109-111)
+ *   rdkv_cuda_pack_plan / rdkv_cuda_pack
+ *                       build_trizone / build_packed_model (trizone.hpp:80,136)
+ *   rdkv_cuda_decode    packed_decode_step + fused_k_logits (trizone.hpp:84,89),
+ *                       batched over every (batch, layer, KV head) tile
+ *   rdkv_cuda_append    append_new_token (trizone.hpp:91)
+ *   rdkv_tile_export    device tile -> the reference TriZoneCache segment
+ *                       layout (PackedSegment payload bytes, QuantParams,
+ *                       members/positions; trizone.hpp:34-78) for parity and
+ *                       for RDKVP001 serialization
+ *   rdkv_cuda_generate  synthetic-cache generator (counter-based replacement
+ *                       for gen_synthetic_cache cache.hpp:138 at scale)
+ *
+ * Status codes map onto the reference's exception types (errors.hpp:9-16):
+ * RDKV_EINVAL <-> std::invalid_argument, RDKV_ENUMERIC <-> rdkv::NumericError,
+ * RDKV_EFORMAT <-> rdkv::FormatError. All device entry points are
+ * asynchronous on the given stream; argument checks that need device data
+ * are reported through the per-head rdkv_head_stats.status field.
+ * Thread-safe across distinct streams; no hidden global stream or state.
+ */
+#ifndef RDKV_CUDA_H
+#define RDKV_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RDKV_API __attribute__((visibility("default")))
+
+enum rdkv_status {
+    RDKV_OK = 0,
+    RDKV_EINVAL = 1,   /* std::invalid_argument */
+    RDKV_ENUMERIC = 2, /* rdkv::NumericError */
+    RDKV_EFORMAT = 3,  /* rdkv::FormatError */
+    RDKV_ECUDA = 4     /* CUDA launch / runtime failure */
+};
+
+enum rdkv_dtype { RDKV_F32 = 0, RDKV_F16 = 1 };
+
+/* Geometry of a batch of independent heads ("tiles"): one unit per
+ * (batch, layer, KV head). K and V are [units][seq_len][head_dim], probe_q is
+ * [units][group][probe_rows][head_dim] (the reference's probe_group view,
+ * cache.hpp:102-104). kv_heads is the model's H_kv, used only for the
+ * per-head budget split (pipeline.cpp:60-72). */
+typedef struct {
+    int32_t units;
+    int32_t seq_len;
+    int32_t head_dim;
+    int32_t group;
+    int32_t probe_rows;
+    int32_t kv_heads;
+} rdkv_shape;
+
+/* BudgetSpec (pipeline.hpp:16-22) + ProbeConfig (cache.hpp:29-34) +
+ * SolverConfig (allocator.hpp:12-19) + PipelineConfig (pipeline.hpp:59-63).
+ * eps_v / eps_k hold DistortionTable::at(widths[i]) (quantizer.hpp:56-64). */
+typedef struct {
+    int32_t n_tokens;
+    int32_t n_widths;
+    double r_k;
+    int32_t widths[8];
+    double eps_v[8];
+    double eps_k[8];
+    int32_t window;
+    int32_t pool_kernel;
+    double tolerance;
+    int32_t max_iterations;
+    int32_t strict_budget;
+    int32_t force_window_retain;
+    int32_t reserved;
+} rdkv_config;
+
+/* HeadAllocation scalars (pipeline.hpp:44-57) + solver diagnostics. */
+typedef struct {
+    double lambda_v, lambda_k;
+    double objective_v, objective_k;
+    double achieved_bits;
+    double avg_v, avg_k;
+    int32_t v_converged, k_converged;
+    int32_t n_kept, n_v16;
+    int32_t k_bits_len; /* 0 when every token was evicted (pipeline.cpp:104) */
+    int32_t status;     /* rdkv_status of this head */
+} rdkv_head_stats;
+
+/* ---- Stage 1: distortion weights ---------------------------------------- */
+RDKV_API size_t rdkv_cuda_weights_workspace(const rdkv_shape* s, int32_t window);
+/* w_t [units][seq_len], w_c [units][head_dim] (f32, device). */
+RDKV_API int rdkv_cuda_weights(const void* k, const void* probe_q, int32_t dtype,
+                               const rdkv_shape* s, int32_t window, int32_t pool_kernel,
+                               float* w_t, float* w_c, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
+/* ---- Stages 2/3: Lagrangian bisection per head --------------------------- */
+/* v_bits [units][seq_len], k_bits [units][head_dim] (u8, device),
+ * stats [units] (device). */
+RDKV_API int rdkv_cuda_allocate(const float* w_t, const float* w_c, const rdkv_shape* s,
+                                const rdkv_config* cfg, uint8_t* v_bits, uint8_t* k_bits,
+                                rdkv_head_stats* stats, void* stream);
+
+/* ---- TriZone packing ---------------------------------------------------- */
+/* tile_offsets [units + 1] (int64, device): byte offset of every tile in the
+ * arena, tile_offsets[units] = arena bytes. */
+RDKV_API int rdkv_cuda_pack_plan(const uint8_t* v_bits, const uint8_t* k_bits,
+                                 const rdkv_shape* s, int64_t* tile_offsets, void* stream);
+/* head_status [units] (device, optional): RDKV_ENUMERIC when a kept row or
+ * column holds a non-finite value (quantize_unit, quantizer.cpp:111-112). */
+RDKV_API int rdkv_cuda_pack(const void* k, const void* v, int32_t dtype, const uint8_t* v_bits,
+                            const uint8_t* k_bits, const rdkv_shape* s,
+                            const int64_t* tile_offsets, uint8_t* arena, int32_t* head_status,
+                            void* stream);
+
+/* ---- Decode ------------------------------------------------------------- */
+typedef struct {
+    const uint8_t* arena;
+    const int64_t* tile_offsets;
+    int32_t units;
+    int32_t group;
+    int32_t head_dim;
+    int32_t io_dtype;   /* q / out element type: RDKV_F32 or RDKV_F16 */
+    const void* q;      /* [units][group][head_dim] */
+    void* out;          /* [units][group][head_dim] */
+    const void* zc_k;   /* Zone C, fp16 [units][zc_cap][head_dim] (may be NULL) */
+    const void* zc_v;
+    const int32_t* zc_len; /* [units] (may be NULL) */
+    int32_t zc_cap;
+    int32_t split;      /* split-K factor (0 = automatic) */
+    void* workspace;    /* split-K partials; rdkv_cuda_decode_workspace() bytes */
+    size_t workspace_bytes;
+    int32_t kernel;     /* 0 = automatic, 1 = generic CUDA-core, 2 = tensor-core */
+    int32_t reserved;
+} rdkv_decode_args;
+
+RDKV_API size_t rdkv_cuda_decode_workspace(int32_t units, int32_t group, int32_t head_dim,
+                                           int32_t split);
+RDKV_API int rdkv_cuda_decode(const rdkv_decode_args* a, void* stream);
+/* End-to-end variant: q_host / out_host are pinned host buffers; the H2D and
+ * D2H copies are enqueued on `stream` around the decode (q_dev / out_dev are
+ * device staging buffers of the same size). */
+RDKV_API int rdkv_cuda_decode_host(const rdkv_decode_args* a, const void* q_host, void* out_host,
+                                   void* stream);
+
+/* ---- Zone C ------------------------------------------------------------- */
+/* Appends one K and one V row per unit (k_new/v_new [units][head_dim] of
+ * dtype) at position zc_len[u], then increments zc_len[u]. */
+RDKV_API int rdkv_cuda_append(void* zc_k, void* zc_v, int32_t* zc_len, int32_t zc_cap,
+                              const void* k_new, const void* v_new, int32_t dtype, int32_t units,
+                              int32_t head_dim, void* stream);
+
+/* ---- Synthetic inputs ---------------------------------------------------- */
+/* Counter-based N(0,1)-like generator, every value FP16-representable:
+ * value(seed, tensor, i) reproducible on the CPU.
+ * tensor: 0 = K, 1 = V, 2 = probe Q. first_index = global element index of
+ * out[0] (lets callers generate any slice). Optional heavy hitters: every
+ * `hh_stride`-th token of K (tensor 0) gets hh_boost added to all channels
+ * of its row; outlier_channels leading K channels are multiplied by
+ * outlier_scale (fp16-rounded). */
+RDKV_API int rdkv_cuda_generate(void* out, int32_t dtype, uint64_t seed, int32_t tensor,
+                                uint64_t first_index, uint64_t count, int32_t head_dim,
+                                int32_t seq_len, int32_t outlier_channels, float outlier_scale,
+                                int32_t hh_stride, float hh_boost, void* stream);
+
+/* ---- Host-side tile inspection ----------------------------------------- */
+/* Tile header fields. */
+typedef struct {
+    int32_t n_kept;
+    int32_t rows[4];     /* V rows at 2,4,8,16 bits */
+    int32_t chans[4];    /* K channels at 2,4,8,16 bits */
+    int32_t kslots, krow_bytes, nslot;
+    int64_t total_bytes;
+    int64_t decode_bytes; /* bytes the decode kernel reads from this tile */
+} rdkv_tile_info;
+
+RDKV_API int rdkv_tile_info_get(const uint8_t* tile_host, rdkv_tile_info* info);
+
+/* Canonical export of one tile (host copy of its bytes) in the reference's
+ * TriZoneCache terms; same layout as oracle's orc_tz_canon:
+ *   kept[n]; vcodes[n*d] (kept order); vscale/vzero[n]; kcodes[d*n]
+ *   channel-major; kscale/kzero[d]; vfp[n*d] Zone B rows; kfp[n*d] k16;
+ *   payload = reference PackedSegment payloads (V 2,4,8 then K 2,4,8);
+ *   segtab[6*6] (side, bits, rows, logical_len, pad_count, nbytes);
+ *   perm[d] channel_perm. */
+RDKV_API int rdkv_tile_export(const uint8_t* tile_host, int32_t head_dim, int32_t* kept,
+                              uint8_t* vcodes, float* vscale, int64_t* vzero, uint8_t* kcodes,
+                              float* kscale, int64_t* kzero, float* vfp, float* kfp,
+                              uint8_t* payload, int32_t* segtab, int32_t* nseg, int32_t* perm,
+                              int32_t* nperm);
+RDKV_API size_t rdkv_tile_export_payload_bytes(const uint8_t* tile_host, int32_t head_dim);
+
+RDKV_API const char* rdkv_status_string(int status);
+RDKV_API int rdkv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RDKV_CUDA_H */

@@ -1,0 +1,298 @@
+// allocate.cu — K2: per-(unit) Lagrangian bisection (Stages 2 and 3).
+//
+// One CTA per unit runs, with all its threads cooperating on every
+// per-unit argmin sweep:
+//   head_budget   pipeline.cpp:60-72
+//   allocate_v    pipeline.cpp:74-94   (target = min(16, B_V / (d T)))
+//   force_window  pipeline.cpp:153-156
+//   allocate_k    pipeline.cpp:96-112  (target = min(16, B_K / (kept d)))
+//   mckp_bisect   allocator.cpp:135-216 (bracket doubling, bisection,
+//                 strict-budget repair)
+//   objectives / achieved bits          pipeline.cpp:169-181
+//
+// Bit-exactness: the per-unit cost w*eps(b) + lambda*b is evaluated with
+// explicit round-to-nearest multiplies and add (__dmul_rn/__dadd_rn, and the
+// file is built with -fmad=false), the strict '<' keeps the lower width on
+// ties, the bit total is an exact integer reduction converted once to fp64
+// (allocator.cpp:55-60), and the lambda sequence uses the same fp64
+// expressions as the reference — so v_bits, k_bits, lambda and the
+// convergence flags are identical given identical weights. Only the reported
+// objective (a plain fp64 sum) uses a tree reduction (<= 1e-12 relative).
+#include "common.cuh"
+
+namespace rdkv_b200 {
+
+constexpr int kAllocThreads = 512;
+
+struct AllocTable {
+    int n;
+    int widths[8];
+    double eps[8];
+};
+
+__device__ __forceinline__ int argmin_bits(float w, const AllocTable& t, double lambda) {
+    // argmin_entry, allocator.cpp:39-50
+    const double wd = (double)w;
+    int best_bits = t.widths[0];
+    double best = __dadd_rn(__dmul_rn(wd, t.eps[0]), __dmul_rn(lambda, (double)best_bits));
+    for (int i = 1; i < t.n; ++i) {
+        const double cost = __dadd_rn(__dmul_rn(wd, t.eps[i]), __dmul_rn(lambda, (double)t.widths[i]));
+        if (cost < best) {
+            best = cost;
+            best_bits = t.widths[i];
+        }
+    }
+    return best_bits;
+}
+
+template <typename Tv>
+__device__ Tv block_reduce_sum(Tv v, Tv* smem) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) smem[wid] = v;
+    __syncthreads();
+    Tv tot = 0;
+    const int nw = blockDim.x >> 5;
+    for (int i = 0; i < nw; ++i) tot += smem[i];
+    return tot;
+}
+
+__device__ float block_reduce_max_f(float v, float* smem) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    v = warp_max(v);
+    __syncthreads();
+    if (lane == 0) smem[wid] = v;
+    __syncthreads();
+    float m = smem[0];
+    const int nw = blockDim.x >> 5;
+    for (int i = 1; i < nw; ++i) m = fmaxf(m, smem[i]);
+    return m;
+}
+
+struct Scratch {
+    long long ll[32];
+    double d[32];
+    float f[32];
+    int i[32];
+};
+
+// assign_all (allocator.cpp:52-61): average bits at lambda, block-wide.
+__device__ double assign_avg(const float* w, int n, const AllocTable& t, double lambda, Scratch& s) {
+    long long tot = 0;
+    for (int u = threadIdx.x; u < n; u += blockDim.x) tot += argmin_bits(w[u], t, lambda);
+    tot = block_reduce_sum<long long>(tot, s.ll);
+    return (double)tot / (double)n;
+}
+
+struct BisectResult {
+    double lambda, avg;
+    int converged;
+};
+
+// mckp_bisect without the final bit materialisation (allocator.cpp:135-216).
+__device__ BisectResult bisect(const float* w, int n, const AllocTable& t, double target,
+                               double tol, int max_it, int strict, Scratch& s) {
+    BisectResult r{0.0, 0.0, 1};
+    const int max_width = t.widths[t.n - 1];
+    if (target >= (double)max_width) {  // :153-161
+        r.avg = max_width;
+        r.lambda = 0.0;
+        return r;
+    }
+    float wmax = 0.0f;
+    for (int u = threadIdx.x; u < n; u += blockDim.x) wmax = fmaxf(wmax, w[u]);
+    double lo = 0.0, hi = (double)block_reduce_max_f(wmax, s.f);
+    const double floor_avg = t.widths[0];
+    if (hi > 0.0) {  // :171-182
+        double hi_avg = assign_avg(w, n, t, hi, s);
+        int guard = 0;
+        while (hi_avg > target && hi_avg > floor_avg && guard++ < 128) {
+            hi = __dmul_rn(hi, 2.0);
+            hi_avg = assign_avg(w, n, t, hi, s);
+        }
+    }
+    double lambda = hi, avg = 0.0;
+    int converged = 0;
+    for (int it = 0; it < max_it; ++it) {  // :187-200
+        lambda = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        avg = assign_avg(w, n, t, lambda, s);
+        if (fabs(avg - target) / target < tol) {
+            converged = 1;
+            break;
+        }
+        if (avg > target) lo = lambda;
+        else hi = lambda;
+    }
+    if (strict && avg > target) {  // :202-210 — hi_bits == assignment at lambda_hi
+        lambda = hi;
+        avg = assign_avg(w, n, t, lambda, s);
+        converged = fabs(avg - target) / target < tol;
+    }
+    r.lambda = lambda;
+    r.avg = avg;
+    r.converged = converged;
+    return r;
+}
+
+__device__ void materialize_bits(const float* w, int n, const AllocTable& t, double lambda,
+                                 int all_max, uint8_t* bits) {
+    const int max_width = t.widths[t.n - 1];
+    for (int u = threadIdx.x; u < n; u += blockDim.x)
+        bits[u] = (uint8_t)(all_max ? max_width : argmin_bits(w[u], t, lambda));
+}
+
+__device__ double eps_of(const AllocTable& t, int b) {
+    for (int i = 0; i < t.n; ++i)
+        if (t.widths[i] == b) return t.eps[i];
+    return 0.0;
+}
+
+__global__ void __launch_bounds__(kAllocThreads) allocate_kernel(
+    const float* __restrict__ w_t, const float* __restrict__ w_c, int t_len, int d, int kv_heads,
+    rdkv_config cfg, int window, uint8_t* __restrict__ v_bits_all, uint8_t* __restrict__ k_bits_all,
+    rdkv_head_stats* __restrict__ stats) {
+    __shared__ Scratch s;
+    const int unit = blockIdx.x;
+    const float* wv = w_t + (size_t)unit * t_len;
+    const float* wk = w_c + (size_t)unit * d;
+    uint8_t* vb = v_bits_all + (size_t)unit * t_len;
+    uint8_t* kb = k_bits_all + (size_t)unit * d;
+    AllocTable tv, tk;
+    tv.n = tk.n = cfg.n_widths;
+    for (int i = 0; i < 8; ++i) {
+        tv.widths[i] = tk.widths[i] = cfg.widths[i];
+        tv.eps[i] = cfg.eps_v[i];
+        tk.eps[i] = cfg.eps_k[i];
+    }
+
+    // check_weights (allocator.cpp:143-149): finite and >= 0
+    int bad = 0;
+    for (int u = threadIdx.x; u < t_len; u += blockDim.x) bad |= !(isfinite(wv[u]) && wv[u] >= 0.0f);
+    for (int u = threadIdx.x; u < d; u += blockDim.x) bad |= !(isfinite(wk[u]) && wk[u] >= 0.0f);
+    bad = block_reduce_sum<int>(bad, s.i);
+
+    // head_budget (pipeline.cpp:60-72)
+    const double tokens_per_head = (double)cfg.n_tokens / (double)kv_heads;
+    const double head_bits = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens_per_head), (double)d), 16.0);
+    const double kbud = __dmul_rn(cfg.r_k, head_bits);
+    const double vbud = __dmul_rn(__dadd_rn(1.0, -cfg.r_k), head_bits);
+
+    rdkv_head_stats out{};
+    if (bad) {
+        out.status = RDKV_EINVAL;
+        if (threadIdx.x == 0) stats[unit] = out;
+        return;
+    }
+
+    // Stage 2: V tokens (allocate_v)
+    double obj_part = 0.0;
+    if (!(vbud > 0.0)) {
+        for (int u = threadIdx.x; u < t_len; u += blockDim.x) vb[u] = 0;
+        out.v_converged = 1;
+    } else {
+        double target = vbud / __dmul_rn((double)d, (double)t_len);
+        if (target > 16.0) target = 16.0;
+        BisectResult r = bisect(wv, t_len, tv, target, cfg.tolerance, cfg.max_iterations,
+                                cfg.strict_budget, s);
+        materialize_bits(wv, t_len, tv, r.lambda, target >= (double)tv.widths[tv.n - 1], vb);
+        out.lambda_v = r.lambda;
+        out.avg_v = r.avg;
+        out.v_converged = r.converged;
+    }
+    __syncthreads();
+    if (cfg.force_window_retain) {
+        for (int i = threadIdx.x; i < window; i += blockDim.x) vb[t_len - window + i] = 16;
+    }
+    __syncthreads();
+    long long kept = 0, v16 = 0, vsum = 0;
+    for (int u = threadIdx.x; u < t_len; u += blockDim.x) {
+        const int b = vb[u];
+        kept += b > 0;
+        v16 += b == 16;
+        vsum += b;
+        obj_part = __dadd_rn(obj_part, __dmul_rn((double)wv[u], eps_of(tv, b)));
+    }
+    kept = block_reduce_sum<long long>(kept, s.ll);
+    v16 = block_reduce_sum<long long>(v16, s.ll);
+    vsum = block_reduce_sum<long long>(vsum, s.ll);
+    out.objective_v = block_reduce_sum<double>(obj_part, s.d);
+
+    // Stage 3: K channels over kept tokens (allocate_k)
+    int k_len = d;
+    long long ksum = 0;
+    if (kept == 0) {
+        k_len = 0;
+        for (int u = threadIdx.x; u < d; u += blockDim.x) kb[u] = 0;
+        out.k_converged = 1;
+    } else if (!(kbud > 0.0)) {
+        for (int u = threadIdx.x; u < d; u += blockDim.x) kb[u] = 0;
+        out.k_converged = 1;
+    } else {
+        double target = kbud / __dmul_rn((double)kept, (double)d);
+        if (target > 16.0) target = 16.0;
+        BisectResult r = bisect(wk, d, tk, target, cfg.tolerance, cfg.max_iterations,
+                                cfg.strict_budget, s);
+        materialize_bits(wk, d, tk, r.lambda, target >= (double)tk.widths[tk.n - 1], kb);
+        out.lambda_k = r.lambda;
+        out.avg_k = r.avg;
+        out.k_converged = r.converged;
+    }
+    __syncthreads();
+    double kobj = 0.0;
+    if (k_len > 0) {
+        for (int u = threadIdx.x; u < d; u += blockDim.x) {
+            ksum += kb[u];
+            kobj = __dadd_rn(kobj, __dmul_rn((double)wk[u], eps_of(tk, kb[u])));
+        }
+    }
+    ksum = block_reduce_sum<long long>(ksum, s.ll);
+    kobj = block_reduce_sum<double>(kobj, s.d);
+    out.objective_k = k_len > 0 ? kobj : 0.0;
+    out.n_kept = (int)kept;
+    out.n_v16 = (int)v16;
+    out.k_bits_len = k_len;
+    out.achieved_bits = __dadd_rn(__dmul_rn((double)vsum, (double)d), __dmul_rn((double)ksum, (double)kept));
+    out.status = RDKV_OK;
+    if (threadIdx.x == 0) stats[unit] = out;
+}
+
+}  // namespace rdkv_b200
+
+using namespace rdkv_b200;
+
+// BudgetSpec::validate (pipeline.cpp:52-58), BitSet::validate (quantizer.cpp:66-88),
+// SolverConfig::validate (allocator.cpp:413-416), ProbeConfig::validate (cache.cpp:107-112).
+extern "C" int rdkv_validate_config(const rdkv_config* c) {
+    if (!c) return RDKV_EINVAL;
+    if (c->n_tokens < 1) return RDKV_EINVAL;
+    if (!(c->r_k > 0.0) || !(c->r_k < 1.0)) return RDKV_EINVAL;
+    if (c->n_widths < 1 || c->n_widths > 8) return RDKV_EINVAL;
+    bool has0 = false, has16 = false;
+    for (int i = 0; i < c->n_widths; ++i) {
+        const int b = c->widths[i];
+        if (b < 0 || b > 16 || b % 2) return RDKV_EINVAL;
+        if (i > 0 && b <= c->widths[i - 1]) return RDKV_EINVAL;
+        if (b != 0 && b != 2 && b != 4 && b != 8 && b != 16) return RDKV_EINVAL;
+        has0 |= b == 0;
+        has16 |= b == 16;
+    }
+    if (!has0 || !has16) return RDKV_EINVAL;
+    if (c->window < 1 || c->pool_kernel < 1 || c->pool_kernel % 2 == 0) return RDKV_EINVAL;
+    if (!(c->tolerance > 0.0) || c->max_iterations < 1) return RDKV_EINVAL;
+    return RDKV_OK;
+}
+
+extern "C" RDKV_API int rdkv_cuda_allocate(const float* w_t, const float* w_c, const rdkv_shape* s,
+                                           const rdkv_config* cfg, uint8_t* v_bits, uint8_t* k_bits,
+                                           rdkv_head_stats* stats, void* stream) {
+    if (!s || !w_t || !w_c || !v_bits || !k_bits || !stats) return RDKV_EINVAL;
+    if (s->units < 1 || s->seq_len < 1 || s->head_dim < 1 || s->kv_heads < 1) return RDKV_EINVAL;
+    if (int st = rdkv_validate_config(cfg)) return st;
+    const int window = cfg->window < s->probe_rows ? cfg->window : s->probe_rows;
+    if (cfg->force_window_retain && window > s->seq_len) return RDKV_EINVAL;
+    allocate_kernel<<<s->units, kAllocThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        w_t, w_c, s->seq_len, s->head_dim, s->kv_heads, *cfg, window, v_bits, k_bits, stats);
+    return launch_status();
+}

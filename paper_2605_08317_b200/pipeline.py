@@ -1,0 +1,324 @@
+"""Device-resident RDKV pipeline over the C-ABI (allocate -> pack -> decode).
+
+Python mirror of the reference's entry points for this path, batched over
+units (one unit = one (batch, layer, KV head)):
+
+    compute_weights     attention_probe + token/channel weights (pipeline.cpp:124-146)
+    allocate            allocate_v + allocate_k via mckp_bisect (pipeline.cpp:74-112)
+    allocate_model      both of the above (pipeline.cpp:191-207)
+    build_packed_model  build_trizone for every unit (trizone.cpp:478-490)
+    packed_decode_step  packed decode for every (unit, query head) (trizone.cpp:251-305)
+    append_new_token    Zone C append (trizone.cpp:307-314)
+
+torch supplies device memory and the current stream only; all compute runs in
+the native sm_100a kernels of _lib/librdkv_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import capi
+from .capi import raise_for
+
+EPS_V = {0: 1.0, 2: 0.313, 4: 0.014, 8: 4.9e-05, 16: 0.0}
+EPS_K = {0: 1.0, 2: 0.149, 4: 0.0062, 8: 2.2e-05, 16: 0.0}
+
+HEAD_STATS_DTYPE = np.dtype([
+    ("lambda_v", "<f8"), ("lambda_k", "<f8"), ("objective_v", "<f8"), ("objective_k", "<f8"),
+    ("achieved_bits", "<f8"), ("avg_v", "<f8"), ("avg_k", "<f8"), ("v_converged", "<i4"),
+    ("k_converged", "<i4"), ("n_kept", "<i4"), ("n_v16", "<i4"), ("k_bits_len", "<i4"),
+    ("status", "<i4"),
+])
+assert HEAD_STATS_DTYPE.itemsize == capi.HEAD_STATS_BYTES
+
+
+def default_config(n_tokens=128, r_k=0.5, widths=(0, 2, 4, 8, 16), eps_v=None, eps_k=None,
+                   window=32, pool_kernel=5, tolerance=1e-2, max_iterations=64,
+                   strict_budget=False, force_window_retain=False) -> capi.Config:
+    """Reference defaults (pipeline.hpp:16-22, cache.hpp:29-34, allocator.hpp:12-19)."""
+    eps_v = eps_v or EPS_V
+    eps_k = eps_k or EPS_K
+    c = capi.Config()
+    c.n_tokens, c.r_k, c.n_widths = n_tokens, r_k, len(widths)
+    for i, b in enumerate(widths):
+        c.widths[i], c.eps_v[i], c.eps_k[i] = b, eps_v[b], eps_k[b]
+    c.window, c.pool_kernel = window, pool_kernel
+    c.tolerance, c.max_iterations = tolerance, max_iterations
+    c.strict_budget, c.force_window_retain = int(strict_budget), int(force_window_retain)
+    return c
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return capi.RDKV_F32
+    if t.dtype == torch.float16:
+        return capi.RDKV_F16
+    raise capi.InvalidArgument(capi.RDKV_EINVAL, f"unsupported dtype {t.dtype}")
+
+
+def _check_cuda(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise capi.InvalidArgument(capi.RDKV_EINVAL, "tensors must be contiguous CUDA tensors")
+
+
+def make_shape(units, seq_len, head_dim, group, probe_rows, kv_heads) -> capi.Shape:
+    return capi.Shape(units, seq_len, head_dim, group, probe_rows, kv_heads)
+
+
+# ---- K0 ---------------------------------------------------------------------
+def generate(shape, dtype=torch.float16, seed=1, tensor=0, first_index=0, seq_len=None,
+             outlier_channels=0, outlier_scale=1.0, hh_stride=0, hh_boost=0.0, device="cuda"):
+    """Counter-based synthetic values (see csrc/generate.cu). shape[-1] = head_dim."""
+    out = torch.empty(shape, dtype=dtype, device=device)
+    d = shape[-1]
+    t_len = seq_len or (shape[-2] if len(shape) >= 2 else 1)
+    raise_for(capi.lib().rdkv_cuda_generate(
+        out.data_ptr(), _dtype_code(out), seed, tensor, first_index, out.numel(), d, t_len,
+        outlier_channels, float(outlier_scale), hh_stride, float(hh_boost), _stream()), "generate")
+    return out
+
+
+# ---- K1 / K2 ----------------------------------------------------------------
+def compute_weights(k: torch.Tensor, probe_q: torch.Tensor, window=32, pool_kernel=5,
+                    kv_heads=1):
+    """k [U, T, d]; probe_q [U, g, rows, d] -> (w_t [U, T] f32, w_c [U, d] f32)."""
+    _check_cuda(k, probe_q)
+    U, T, d = k.shape
+    g, rows = probe_q.shape[1], probe_q.shape[2]
+    shape = make_shape(U, T, d, g, rows, kv_heads)
+    L = capi.lib()
+    ws_bytes = L.rdkv_cuda_weights_workspace(C.byref(shape), window)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=k.device)
+    w_t = torch.empty((U, T), dtype=torch.float32, device=k.device)
+    w_c = torch.empty((U, d), dtype=torch.float32, device=k.device)
+    raise_for(L.rdkv_cuda_weights(k.data_ptr(), probe_q.data_ptr(), _dtype_code(k), C.byref(shape),
+                                  window, pool_kernel, w_t.data_ptr(), w_c.data_ptr(),
+                                  ws.data_ptr(), ws_bytes, _stream()), "weights")
+    return w_t, w_c
+
+
+@dataclass
+class Allocation:
+    """Device ModelAllocation (pipeline.hpp:96-105) for U units."""
+
+    v_bits: torch.Tensor          # [U, T] uint8
+    k_bits: torch.Tensor          # [U, d] uint8
+    stats: torch.Tensor           # [U * sizeof(rdkv_head_stats)] uint8
+    w_t: torch.Tensor | None = None
+    w_c: torch.Tensor | None = None
+
+    def stats_host(self) -> np.ndarray:
+        arr = np.frombuffer(self.stats.cpu().numpy().tobytes(), dtype=HEAD_STATS_DTYPE)
+        return arr
+
+    def check(self) -> None:
+        st = self.stats_host()["status"]
+        bad = np.nonzero(st)[0]
+        if bad.size:
+            raise_for(int(st[bad[0]]), f"allocate (unit {int(bad[0])})")
+
+
+def allocate(w_t, w_c, cfg, group=1, probe_rows=32, kv_heads=1) -> Allocation:
+    _check_cuda(w_t, w_c)
+    U, T = w_t.shape
+    d = w_c.shape[1]
+    shape = make_shape(U, T, d, group, probe_rows, kv_heads)
+    v_bits = torch.empty((U, T), dtype=torch.uint8, device=w_t.device)
+    k_bits = torch.empty((U, d), dtype=torch.uint8, device=w_t.device)
+    stats = torch.empty(U * capi.HEAD_STATS_BYTES, dtype=torch.uint8, device=w_t.device)
+    cfg = capi.config_from(cfg)
+    raise_for(capi.lib().rdkv_cuda_allocate(w_t.data_ptr(), w_c.data_ptr(), C.byref(shape),
+                                            C.byref(cfg), v_bits.data_ptr(), k_bits.data_ptr(),
+                                            stats.data_ptr(), _stream()), "allocate")
+    return Allocation(v_bits, k_bits, stats, w_t, w_c)
+
+
+def allocate_model(k, probe_q, cfg, kv_heads) -> Allocation:
+    """Stages 1-3 for every unit (allocate_model, pipeline.cpp:191-207)."""
+    w_t, w_c = compute_weights(k, probe_q, window=cfg.window, pool_kernel=cfg.pool_kernel,
+                               kv_heads=kv_heads)
+    return allocate(w_t, w_c, cfg, group=probe_q.shape[1], probe_rows=probe_q.shape[2],
+                    kv_heads=kv_heads)
+
+
+# ---- K3 ---------------------------------------------------------------------
+@dataclass
+class PackedModel:
+    """Device TriZone tiles of U units plus Zone C (PackedModel, trizone.hpp:128-136)."""
+
+    arena: torch.Tensor
+    offsets: torch.Tensor            # [U + 1] int64 (device)
+    offsets_host: np.ndarray
+    units: int
+    group: int
+    head_dim: int
+    zc_k: torch.Tensor | None = None  # [U, cap, d] fp16
+    zc_v: torch.Tensor | None = None
+    zc_len: torch.Tensor | None = None  # [U] int32
+    zc_cap: int = 0
+    head_status: torch.Tensor | None = None
+    _infos: list = field(default_factory=list)
+
+    @property
+    def arena_bytes(self) -> int:
+        return int(self.offsets_host[-1])
+
+    def tile_bytes(self, unit: int) -> np.ndarray:
+        a, b = int(self.offsets_host[unit]), int(self.offsets_host[unit + 1])
+        return self.arena[a:b].cpu().numpy()
+
+    def info(self, unit: int) -> capi.TileInfo:
+        t = self.tile_bytes(unit)
+        info = capi.TileInfo()
+        raise_for(capi.lib().rdkv_tile_info_get(t.ctypes.data, C.byref(info)), "tile_info")
+        return info
+
+    def infos(self) -> list:
+        """TileInfo of every unit (one bulk D2H copy of the arena)."""
+        host = self.arena.cpu().numpy()
+        out = []
+        for u in range(self.units):
+            info = capi.TileInfo()
+            raise_for(capi.lib().rdkv_tile_info_get(host[int(self.offsets_host[u]):].ctypes.data,
+                                                    C.byref(info)), "tile_info")
+            out.append(info)
+        return out
+
+    def decode_bytes(self, io_bytes=2) -> int:
+        """Algorithmic bytes of one decode step: every tile's decode region, Zone C
+        rows, q and out."""
+        tiles = sum(int(i.decode_bytes) for i in self.infos())
+        zc = 0 if self.zc_len is None else int(self.zc_len.sum().item()) * self.head_dim * 2 * 2
+        qo = self.units * self.group * self.head_dim * io_bytes * 2
+        return tiles + zc + qo
+
+    def export(self, unit: int) -> dict:
+        """Canonical reference view of one tile (see rdkv_tile_export)."""
+        t = self.tile_bytes(unit)
+        return export_tile(t, self.head_dim)
+
+    def check(self) -> None:
+        if self.head_status is None:
+            return
+        st = self.head_status.cpu().numpy()
+        bad = np.nonzero(st)[0]
+        if bad.size:
+            raise_for(int(st[bad[0]]), f"pack (unit {int(bad[0])})")
+
+
+def export_tile(tile: np.ndarray, d: int) -> dict:
+    tile = np.ascontiguousarray(tile, np.uint8)
+    L = capi.lib()
+    info = capi.TileInfo()
+    raise_for(L.rdkv_tile_info_get(tile.ctypes.data, C.byref(info)), "tile_info")
+    n = int(info.n_kept)
+    nb = int(L.rdkv_tile_export_payload_bytes(tile.ctypes.data, d))
+    m = max(n, 1)
+    kept = np.zeros(m, np.int32)
+    vcodes = np.zeros((m, d), np.uint8)
+    vscale = np.zeros(m, np.float32)
+    vzero = np.zeros(m, np.int64)
+    kcodes = np.zeros((d, m), np.uint8)
+    kscale = np.zeros(d, np.float32)
+    kzero = np.zeros(d, np.int64)
+    vfp = np.zeros((m, d), np.float32)
+    kfp = np.zeros((m, d), np.float32)
+    payload = np.zeros(max(nb, 1), np.uint8)
+    segtab = np.zeros((6, 6), np.int32)
+    nseg = C.c_int32()
+    perm = np.zeros(d, np.int32)
+    nperm = C.c_int32()
+    raise_for(L.rdkv_tile_export(tile.ctypes.data, d, kept.ctypes.data, vcodes.ctypes.data,
+                                 vscale.ctypes.data, vzero.ctypes.data, kcodes.ctypes.data,
+                                 kscale.ctypes.data, kzero.ctypes.data, vfp.ctypes.data,
+                                 kfp.ctypes.data, payload.ctypes.data, segtab.ctypes.data,
+                                 C.addressof(nseg), perm.ctypes.data, C.addressof(nperm)), "export")
+    # kcodes was written channel-major with row stride n
+    kc = kcodes.reshape(-1)[: d * n].reshape(d, n) if n else np.zeros((d, 0), np.uint8)
+    return {"kept": kept[:n], "vcodes": vcodes[:n], "vscale": vscale[:n], "vzero": vzero[:n],
+            "kcodes": kc, "kscale": kscale, "kzero": kzero, "vfp": vfp[:n], "kfp": kfp[:n],
+            "payload": payload[:nb], "segtab": segtab[: nseg.value], "perm": perm[: nperm.value],
+            "info": info}
+
+
+def build_packed_model(k, v, alloc: Allocation, group, zc_cap=0) -> PackedModel:
+    """build_trizone for every unit into one arena (trizone.cpp:478-490)."""
+    _check_cuda(k, v)
+    U, T, d = k.shape
+    shape = make_shape(U, T, d, group, 1, 1)
+    L = capi.lib()
+    offsets = torch.empty(U + 1, dtype=torch.int64, device=k.device)
+    raise_for(L.rdkv_cuda_pack_plan(alloc.v_bits.data_ptr(), alloc.k_bits.data_ptr(),
+                                    C.byref(shape), offsets.data_ptr(), _stream()), "pack_plan")
+    offsets_host = offsets.cpu().numpy()
+    arena = torch.empty(int(offsets_host[-1]) + 256, dtype=torch.uint8, device=k.device)
+    status = torch.zeros(U, dtype=torch.int32, device=k.device)
+    raise_for(L.rdkv_cuda_pack(k.data_ptr(), v.data_ptr(), _dtype_code(k), alloc.v_bits.data_ptr(),
+                               alloc.k_bits.data_ptr(), C.byref(shape), offsets.data_ptr(),
+                               arena.data_ptr(), status.data_ptr(), _stream()), "pack")
+    model = PackedModel(arena, offsets, offsets_host, U, group, d, head_status=status)
+    if zc_cap > 0:
+        model.zc_k = torch.zeros((U, zc_cap, d), dtype=torch.float16, device=k.device)
+        model.zc_v = torch.zeros((U, zc_cap, d), dtype=torch.float16, device=k.device)
+        model.zc_len = torch.zeros(U, dtype=torch.int32, device=k.device)
+        model.zc_cap = zc_cap
+    return model
+
+
+# ---- K4 / K5 ----------------------------------------------------------------
+def decode_args(model: PackedModel, q, out, split=1, kernel=0, workspace=None) -> capi.DecodeArgs:
+    a = capi.DecodeArgs()
+    a.arena = model.arena.data_ptr()
+    a.tile_offsets = model.offsets.data_ptr()
+    a.units, a.group, a.head_dim = model.units, model.group, model.head_dim
+    a.io_dtype = _dtype_code(q)
+    a.q, a.out = q.data_ptr(), out.data_ptr()
+    if model.zc_len is not None:
+        a.zc_k, a.zc_v, a.zc_len = model.zc_k.data_ptr(), model.zc_v.data_ptr(), model.zc_len.data_ptr()
+        a.zc_cap = model.zc_cap
+    a.split = split
+    a.kernel = kernel
+    if workspace is not None:
+        a.workspace, a.workspace_bytes = workspace.data_ptr(), workspace.numel()
+    return a
+
+
+def decode_workspace(model: PackedModel, split: int, device="cuda"):
+    n = capi.lib().rdkv_cuda_decode_workspace(model.units, model.group, model.head_dim, split)
+    return torch.empty(max(n, 1), dtype=torch.uint8, device=device) if n else None
+
+
+def packed_decode_step(model: PackedModel, q, out=None, split=1, kernel=0, workspace=None):
+    """q [U, g, d] (f32 or f16) -> out, same shape/dtype (trizone.cpp:251-305)."""
+    _check_cuda(q)
+    if out is None:
+        out = torch.empty_like(q)
+    if split > 1 and workspace is None:
+        workspace = decode_workspace(model, split, q.device)
+    a = decode_args(model, q, out, split, kernel, workspace)
+    raise_for(capi.lib().rdkv_cuda_decode(C.byref(a), _stream()), "decode")
+    return out
+
+
+def append_new_token(model: PackedModel, k_new, v_new) -> None:
+    """One K/V row per unit into Zone C (trizone.cpp:307-314)."""
+    if model.zc_len is None:
+        raise capi.InvalidArgument(capi.RDKV_EINVAL, "model built without Zone C capacity")
+    _check_cuda(k_new, v_new)
+    raise_for(capi.lib().rdkv_cuda_append(model.zc_k.data_ptr(), model.zc_v.data_ptr(),
+                                          model.zc_len.data_ptr(), model.zc_cap, k_new.data_ptr(),
+                                          v_new.data_ptr(), _dtype_code(k_new), model.units,
+                                          model.head_dim, _stream()), "append")
