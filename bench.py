@@ -1,0 +1,524 @@
+#!/usr/bin/env python
+"""RDKV decode benchmark on B200 (BASELINE.json metric: decode tok/s & us/step at
+128K context; HBM GB/s vs peak; speedup vs FP16 full-KV).
+
+Workload (BASELINE.json configs[2] at N=1): LLaMA-3.1-8B KV shape (32 layers,
+32 q / 8 kv heads, d=128), 128K context, 128 FP16-equivalent tokens per layer,
+16 sequences per GPU (weak scaling). Prefill-time allocate+pack runs once in
+setup; one timed *step* = packed decode attention of one new token for every
+(sequence, layer, KV head) tile and all 4 GQA query heads (one launch).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Under torchrun each rank packs and decodes its own 16 sequences (no data-path
+collective); the step time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batch", type=int, default=16, help="sequences per GPU")
+    p.add_argument("--layers", type=int, default=32)
+    p.add_argument("--ctx", type=int, default=131072)
+    p.add_argument("--n-tokens", type=int, default=128)
+    p.add_argument("--zc", type=int, default=0, help="Zone C tokens appended per tile before timing")
+    p.add_argument("--hh", action="store_true", help="heavy-hitter synthetic cache (mixed bit tiers)")
+    p.add_argument("--kernel", type=int, default=0, help="0 auto, 1 generic, 2 tensor-core")
+    p.add_argument("--no-fp16-baseline", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-pipeline", action="store_true")
+    p.add_argument("--cpu-budget-s", type=float, default=8.0)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------------
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks / throttle reasons while the timed loop runs."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+               0x1: "gpu_idle"}
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.nv = None
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append(mhz)
+                self.reasons |= int(r) & ~0x1
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def report(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier_sync(world):
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x, world):
+    import torch
+
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------------
+def reference_sample(spec, cfg_kwargs, budget_s):
+    """The reference CPU path on one (sequence 0, layer 0) slice of the same synthetic
+    workload: allocate_model + build_packed_model (oracle/_ref = the unmodified
+    reference core), then packed_decode_step for all 32 q-heads through the
+    reference's parallel_for, repeated for ~budget_s. Returns timing + outputs."""
+    import oracle
+    from paper_2605_08317_b200.workload import chunk_seed
+
+    orc = oracle.load()
+    ref = oracle.load_ref() if oracle.ref_available() else None
+    lib = ref if ref is not None else orc
+    H, T, d, g, Sw = spec.kv_heads, spec.ctx, spec.head_dim, spec.group, spec.probe_rows
+    s = chunk_seed(spec.seed, spec.rank, 0, 0)
+    k = orc.gen_counter(s, 0, 0, H * T * d, d, T, spec.outlier_channels, spec.outlier_scale,
+                        spec.hh_stride, spec.hh_boost).reshape(1, H, T, d)
+    v = orc.gen_counter(s, 1, 0, H * T * d, d, T).reshape(1, H, T, d)
+    pq = orc.gen_counter(s, 2, 0, H * g * Sw * d, d, T, 0, 1.0, spec.hh_stride).reshape(1, H * g, Sw, d)
+    q = orc.gen_counter(QSEED, 2, 0, H * g * d, d, T).reshape(1, H * g, d)
+    cfg = oracle.default_config(**cfg_kwargs)
+    t0 = time.perf_counter()
+    info = {"kind": "reference" if ref is not None else "port"}
+    if ref is not None:
+        model = oracle.RefModel(ref, k, v, pq, cfg)
+        info["alloc_s"], info["pack_s"] = model.alloc_seconds, model.pack_seconds
+        heads = [model.head(0, h) for h in range(H)]
+        out, _ = model.decode(q)
+        times = []
+        t_end = time.perf_counter() + budget_s
+        while time.perf_counter() < t_end or len(times) < 3:
+            _, sec = model.decode(q)
+            times.append(sec)
+        cores = ref.lib.ref_worker_count()
+    else:  # port: serial oracle
+        heads, tzs = [], []
+        for h in range(H):
+            r = orc.allocate_head(k[0, h], pq[0, h * g:(h + 1) * g], H, cfg)
+            heads.append(r)
+            tzs.append(orc.tz_build(k[0, h], v[0, h], r["v_bits"], r["k_bits"]))
+        out = np.stack([tzs[j // g].decode(q[0, j]) for j in range(H * g)])[None]
+        times = []
+        t_end = time.perf_counter() + budget_s
+        while time.perf_counter() < t_end or len(times) < 3:
+            t1 = time.perf_counter()
+            for j in range(H * g):
+                tzs[j // g].decode(q[0, j])
+            times.append(time.perf_counter() - t1)
+        cores = 1
+    info["setup_s"] = time.perf_counter() - t0
+    info["sample_step_s"] = statistics.median(times)
+    info["cores"] = cores
+    info["heads"] = heads
+    info["out"] = out
+    info["q"] = q
+    return info
+
+
+QSEED = 0xD15C0
+
+
+def run_reference_arm(args, world, rank):
+    """--impl reference: the reference's own CPU path, rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2605_08317_b200.workload import WorkloadSpec
+
+    spec = WorkloadSpec(batch=args.batch, layers=args.layers, ctx=args.ctx, n_tokens=args.n_tokens,
+                        hh_stride=64 if args.hh else 0, hh_boost=1.0 if args.hh else 0.0)
+    per_step = max(0.2, args.cpu_budget_s / max(args.steps, 1))
+    info = reference_sample(spec, dict(n_tokens=spec.n_tokens, window=spec.probe_rows), per_step * args.steps)
+    sample_units = spec.kv_heads  # one (sequence, layer) slice = 8 tiles, 32 q-heads
+    scale = (spec.batch * args.gpus * spec.layers * spec.kv_heads) / sample_units
+    step_s = info["sample_step_s"] * scale
+    value = spec.batch * args.gpus / step_s
+    line = {
+        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (K0 counter-based generator, FP16-representable)",
+        "impl": "reference",
+        "config": workload_config(spec, args),
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": info["cores"], "kind": info["kind"],
+                         "sample": f"1 of {int(scale)} (sequence, layer) slices (8 KV heads x 4 q-heads, T={spec.ctx}) timed "
+                                   f"{info['sample_step_s'] * 1e3:.3f} ms/step via parallel_for; step = x{int(scale)}"},
+        "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "decode tok/s & us/step at 128K ctx; HBM GB/s vs peak; speedup vs FP16 full-KV"
+
+
+def workload_config(spec, args):
+    return {
+        "workload": f"LLaMA-3.1-8B KV shape ({spec.layers} layers, {spec.q_heads} q / {spec.kv_heads} kv heads, "
+                    f"d={spec.head_dim}), {spec.ctx} ctx, {spec.n_tokens}-token/layer budget, batch {spec.batch}/GPU, "
+                    "one decode step over all layers (configs[2])",
+        "layers": spec.layers, "q_heads": spec.q_heads, "kv_heads": spec.kv_heads, "head_dim": spec.head_dim,
+        "ctx": spec.ctx, "batch_per_gpu": spec.batch, "global_batch": spec.batch * args.gpus,
+        "n_tokens": spec.n_tokens, "zone_c": args.zc, "heavy_hitters": bool(args.hh),
+        "parallelism": f"shard by sequence x{args.gpus} (no collective)",
+        "l2": "flushed before every step (512 MiB memset, outside the timed events)",
+        "io": "fp16 q/out",
+    }
+
+
+# ---------------------------------------------------------------------------------
+def fp16_fullkv_baseline(spec, steps, warmup):
+    """FlashInfer 0.6.11 batch decode over an FP16 paged full KV cache (same shapes).
+    One layer's KV (batch x 128K) is resident; a step runs it for all layers."""
+    import torch
+    import flashinfer
+
+    B, T, H, Hq, d = spec.batch, spec.ctx, spec.kv_heads, spec.q_heads, spec.head_dim
+    page = 16
+    pps = T // page
+    kv = torch.empty((B * pps, 2, page, H, d), dtype=torch.float16, device="cuda").normal_()
+    indptr = (torch.arange(B + 1, dtype=torch.int32, device="cuda") * pps)
+    indices = torch.arange(B * pps, dtype=torch.int32, device="cuda")
+    last = torch.full((B,), page, dtype=torch.int32, device="cuda")
+    ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    w = flashinfer.BatchDecodeWithPagedKVCacheWrapper(ws, "NHD", use_tensor_cores=True)
+    w.plan(indptr, indices, last, Hq, H, d, page, q_data_type=torch.float16, kv_data_type=torch.float16)
+    q = torch.randn((B, Hq, d), dtype=torch.float16, device="cuda")
+    out = torch.empty_like(q)
+    for _ in range(max(warmup, 2)):
+        w.run(q, kv, out=out)
+    torch.cuda.synchronize()
+    n = max(2, min(steps, 10))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(n):
+        for _layer in range(spec.layers):
+            w.run(q, kv, out=out)
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / n
+    bytes_step = spec.layers * (B * T * H * d * 2 * 2 + 2 * B * Hq * d * 2)
+    del kv
+    torch.cuda.empty_cache()
+    return {"impl": f"flashinfer {flashinfer.__version__} BatchDecodeWithPagedKVCacheWrapper (fp16, tensor cores, page 16)",
+            "ms_per_step": ms, "tok_s": B / (ms / 1e3), "GB_s": bytes_step / (ms / 1e3) / 1e9,
+            "bytes_per_step": bytes_step}
+
+
+def pipeline_config2(P, steps):
+    """configs[1]: 32 layers, 32K context, batch 1 — full allocate+pack+decode on 1 B200."""
+    import torch
+    from paper_2605_08317_b200.workload import WorkloadSpec, build
+
+    spec = WorkloadSpec(batch=1, layers=32, ctx=32768, n_tokens=128, seed=2)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    model, timing, _, _ = build(spec)
+    torch.cuda.synchronize()
+    setup = time.perf_counter() - t0
+    q = P.generate((model.units, spec.group, spec.head_dim), torch.float16, seed=QSEED, tensor=2)
+    out = torch.empty_like(q)
+    for _ in range(5):
+        P.packed_decode_step(model, q, out)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    for _ in range(steps):
+        P.packed_decode_step(model, q, out)
+    e[1].record()
+    torch.cuda.synchronize()
+    return {"config": "configs[1]: LLaMA-3.1-8B shape, 32 layers, 32K ctx, batch 1 (allocate+pack+decode)",
+            "allocate_pack_s": setup, **{k: round(v, 4) for k, v in timing.items()},
+            "decode_us_per_step": e[0].elapsed_time(e[1]) / steps * 1e3,
+            "note": "allocate/pack timed per (layer) chunk incl. host syncs; decode back-to-back (L2-warm)"}
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+    import torch
+
+    from paper_2605_08317_b200 import capi
+    from paper_2605_08317_b200 import pipeline as P
+    from paper_2605_08317_b200.workload import WorkloadSpec, build
+
+    capi.lib()
+    spec = WorkloadSpec(batch=args.batch, layers=args.layers, ctx=args.ctx, n_tokens=args.n_tokens, rank=rank,
+                        hh_stride=64 if args.hh else 0, hh_boost=1.0 if args.hh else 0.0, zc_cap=max(args.zc, 0))
+    t0 = time.perf_counter()
+    model, build_timing, stats, first_alloc = build(spec)
+    build_s = time.perf_counter() - t0
+    U, g, d = model.units, spec.group, spec.head_dim
+    if args.zc:
+        for _ in range(args.zc):
+            kn = P.generate((U, d), torch.float16, seed=77, tensor=1)
+            P.append_new_token(model, kn, kn)
+    q = P.generate((U, g, d), torch.float16, seed=QSEED, tensor=2)
+    out = torch.empty_like(q)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        P.packed_decode_step(model, q, out, kernel=args.kernel)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    # ---- timed region: K decode steps, device events around each launch
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sampler = ClockSampler(torch.cuda.current_device())
+    barrier_sync(world)
+    with sampler:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        barrier_sync(world)
+    per = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = sum(per) / len(per)
+    ms = max_over_ranks(ms_local, world)
+    value = spec.batch * world / (ms / 1e3)
+
+    # ---- end to end through the C-ABI with pinned host buffers
+    import ctypes as C
+
+    qh = q.cpu().pin_memory()
+    oh = torch.empty_like(qh).pin_memory()
+    args_c = P.decode_args(model, q, out, 1, args.kernel)
+    L = capi.lib()
+    e_starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e_ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier_sync(world)
+    for i in range(args.steps):
+        flush.zero_()
+        e_starts[i].record(stream)
+        rc = L.rdkv_cuda_decode_host(C.byref(args_c), qh.data_ptr(), oh.data_ptr(), stream.cuda_stream)
+        e_ends[i].record(stream)
+        assert rc == 0, rc
+    barrier_sync(world)
+    e2e_ms = max_over_ranks(sum(s.elapsed_time(e) for s, e in zip(e_starts, e_ends)) / args.steps, world)
+    assert torch.equal(oh.cuda(), out)
+
+    # ---- roofline of the decode kernel
+    peak, peak_kind = load_peaks()
+    alg_bytes = model.decode_bytes(io_bytes=2)
+    achieved = alg_bytes / (ms_local / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "decode_ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                pj = json.load(f)
+            if pj.get("units") == U and pj.get("kernel_mode") == args.kernel:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+
+    # ---- per-layer launches (honest model-integrated number: one launch per layer)
+    per_layer = None
+    try:
+        per_layer = per_layer_launch_ms(P, model, spec, q, out, flush, args)
+    except Exception as e:  # noqa: BLE001
+        per_layer = {"error": str(e)[:200]}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp32-accum/fp16-io, int codes",
+        "data": "synthetic (K0 counter-based N(0,1)-like KV, FP16-representable), random-init",
+        "config": workload_config(spec, args),
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "e2e": {"value": spec.batch * world / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": qh.numel() * qh.element_size(),
+                "d2h_bytes_per_step": oh.numel() * oh.element_size(),
+                "path": "rdkv_cuda_decode_host (C-ABI): pinned q H2D + decode + out D2H"},
+        "clocks": sampler.report(),
+        "per_layer_launch": per_layer,
+        "setup": {"build_s": round(build_s, 2), **{k: round(v, 3) for k, v in build_timing.items()},
+                  "arena_bytes": model.arena_bytes,
+                  "kept_tokens_mean": float(np.mean([s["n_kept"].mean() for s in stats])),
+                  "v16_rows": int(sum(s["n_v16"].sum() for s in stats))},
+    }
+    if rank == 0 and not args.no_fp16_baseline:
+        try:
+            fb = fp16_fullkv_baseline(spec, args.steps, args.warmup)
+            fb["speedup_ours_vs_fp16"] = fb["ms_per_step"] / ms
+            line["fp16_fullkv"] = fb
+        except Exception as e:  # noqa: BLE001
+            line["fp16_fullkv"] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            info = reference_sample(spec, dict(n_tokens=spec.n_tokens, window=spec.probe_rows), args.cpu_budget_s)
+            scale = spec.batch * spec.layers
+            cpu_step = info["sample_step_s"] * scale
+            line["cpu_baseline"] = {"value": spec.batch / cpu_step, "unit": "tok/s", "cores": info["cores"],
+                                    "kind": info["kind"],
+                                    "sample": f"sequence 0 layer 0 (8 KV heads, 32 q-heads, T={spec.ctx}): "
+                                              f"{info['sample_step_s'] * 1e3:.3f} ms per slice-step x {scale} slices",
+                                    "alloc_s_sample": info.get("alloc_s"), "pack_s_sample": info.get("pack_s")}
+            # parity on the same slice: allocation and decode outputs vs the reference
+            vb, kb, st = first_alloc
+            match = all(np.array_equal(vb[h], info["heads"][h]["v_bits"]) and
+                        np.array_equal(kb[h][: len(info["heads"][h]["k_bits"])], info["heads"][h]["k_bits"])
+                        for h in range(spec.kv_heads))
+            q0 = torch.from_numpy(info["q"][0].reshape(spec.kv_heads, g, d)).cuda().half()
+            sub = P.PackedModel(model.arena, model.offsets, model.offsets_host, spec.kv_heads, g, d)
+            o0 = P.packed_decode_step(sub, q0).float().cpu().numpy().reshape(-1, d)
+            want = info["out"][0]
+            err = float(max(np.linalg.norm(o0[j] - want[j]) / np.linalg.norm(want[j]) for j in range(len(want))))
+            line["parity"] = {"slice": "sequence 0, layer 0 (8 KV heads, T=%d)" % spec.ctx,
+                              "allocation_bit_exact": bool(match), "decode_max_rel_err": err,
+                              "tolerance": 1e-3}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if rank == 0 and world == 1 and not args.no_pipeline:
+        try:
+            pj = pipeline_config2(P, 50)
+            print(json.dumps({"pipeline": pj}), file=sys.stderr, flush=True)
+        except Exception as e:  # noqa: BLE001
+            print(json.dumps({"pipeline_error": str(e)[:300]}), file=sys.stderr, flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def per_layer_launch_ms(P, model, spec, q, out, flush, args):
+    """One launch per layer (what a model-integrated decode does), captured in a CUDA graph."""
+    import torch
+
+    subs = []
+    H = spec.kv_heads
+    for layer in range(spec.layers):
+        # units of this layer across the batch are not contiguous; build a per-layer offsets view
+        idx = np.array([(b * spec.layers + layer) * H + h for b in range(spec.batch) for h in range(H)])
+        offs = np.concatenate([model.offsets_host[idx], [0]])
+        sub = P.PackedModel(model.arena, torch.from_numpy(offs).cuda(), offs, len(idx), spec.group, spec.head_dim)
+        qi = torch.from_numpy(idx).cuda()
+        subs.append((sub, q[qi].contiguous(), torch.empty_like(q[qi])))
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for sub, qq, oo in subs:
+            P.packed_decode_step(sub, qq, oo, kernel=args.kernel)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for sub, qq, oo in subs:
+                P.packed_decode_step(sub, qq, oo, kernel=args.kernel)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    n = max(10, min(args.steps, 100))
+    st = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    en = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+    for i in range(n):
+        flush.zero_()
+        st[i].record()
+        g.replay()
+        en[i].record()
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in zip(st, en)) / n
+    return {"ms_per_step": ms, "tok_s": spec.batch / (ms / 1e3), "launches_per_step": spec.layers,
+            "note": "32 per-layer launches replayed from one CUDA graph"}
+
+
+if __name__ == "__main__":
+    main()

@@ -228,6 +228,9 @@ class OracleLib:
             L.orc_pack_bits.argtypes = [U8, C.c_int, C.c_int, U8]
             L.orc_head_budget.argtypes = [C.c_int, C.c_double, C.c_int, C.c_int, F64, F64, F64, I32]
             L.orc_per_unit_argmin.argtypes = [C.c_double, I32, F64, C.c_int, C.c_double]
+            L.orc_gen_counter.argtypes = [F32, C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
+                                          C.c_int, C.c_int, C.c_float, C.c_int, C.c_float]
+            L.orc_gen_counter.restype = None
 
     # ---- API ---------------------------------------------------------------
     def gen_synthetic(self, seed, layers, q_heads, kv_heads, d, t_len, probe_window,
@@ -326,6 +329,14 @@ class OracleLib:
         return TriZone(self, h, t_len, d)
 
     # oracle-only helpers
+    def gen_counter(self, seed, tensor, first, count, d, seq_len, outlier_channels=0,
+                    outlier_scale=1.0, hh_stride=0, hh_boost=0.0):
+        """K0 values (FP16-representable float32), same as csrc/generate.cu."""
+        out = np.empty(count, np.float32)
+        self.lib.orc_gen_counter(_p(out, C.c_float), seed, tensor, first, count, d, seq_len,
+                                 outlier_channels, outlier_scale, hh_stride, hh_boost)
+        return out
+
     def normal_stream(self, seed, n):
         out = np.zeros(n, np.float32)
         self.lib.orc_normal_stream(seed, _p(out, C.c_float), n)

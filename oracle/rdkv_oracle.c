@@ -954,3 +954,67 @@ int orc_dense_decode(const float* q, const float* k_rows, const float* v_rows, i
     free(logits);
     return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* K0 counter-based generator — CPU restatement of                           */
+/* paper_2605_08317_b200/csrc/generate.cu (not a reference function: the     */
+/* reference's serial mt19937 generator does not scale to 128K contexts).    */
+/* Emits float32 values that are exactly FP16-representable.                 */
+/* ------------------------------------------------------------------------ */
+static uint64_t splitmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+/* IEEE binary32 -> binary16 -> binary32, round to nearest even */
+static float round_to_half(float x) {
+    union { float f; uint32_t u; } in = {x};
+    uint32_t sign = in.u & 0x80000000u;
+    uint32_t ax = in.u & 0x7FFFFFFFu;
+    union { uint32_t u; float f; } out;
+    if (ax >= 0x477FF000u) { /* >= 65520: overflow to inf (or NaN passthrough) */
+        out.u = sign | (ax > 0x7F800000u ? ax : 0x7F800000u);
+        return out.f;
+    }
+    if (ax < 0x38800000u) { /* below 2^-14: subnormal half, quantum 2^-24 */
+        float a = fabsf(x);
+        float q = nearbyintf(a * 16777216.0f) / 16777216.0f; /* exact scaling by 2^24 */
+        return sign ? -q : q;
+    }
+    /* normal: keep 10 mantissa bits, RNE on the dropped 13 */
+    uint32_t lsb = (ax >> 13) & 1u;
+    ax += 0xFFFu + lsb;
+    ax &= 0xFFFFE000u;
+    out.u = sign | ax;
+    return out.f;
+}
+
+static float channel_sign(uint64_t seed, int c) {
+    return (splitmix64(seed ^ 0x5BD1E9955BD1E995ULL ^ (uint64_t)c) & 1ULL) ? 1.0f : -1.0f;
+}
+
+void orc_gen_counter(float* out, uint64_t seed, int tensor, uint64_t first, uint64_t count, int d,
+                     int seq_len, int outlier_channels, float outlier_scale, int hh_stride,
+                     float hh_boost) {
+    const uint64_t base = seed * 0x9E3779B97F4A7C15ULL + (uint64_t)(tensor + 1) * 0xD1B54A32D192ED03ULL;
+    const float inv = 1.0f / 37836.5f;
+    for (uint64_t j = 0; j < count; ++j) {
+        const uint64_t i = first + j;
+        const uint64_t z = splitmix64(base + i);
+        const int s = (int)(z & 0xFFFF) + (int)((z >> 16) & 0xFFFF) + (int)((z >> 32) & 0xFFFF) +
+                      (int)((z >> 48) & 0xFFFF);
+        float x = (float)(s - 131070) * inv;
+        const int c = (int)(i % (uint64_t)d);
+        if (tensor == 0) {
+            if (c < outlier_channels) x = x * outlier_scale;
+            if (hh_stride > 0) {
+                const uint64_t t = (i / (uint64_t)d) % (uint64_t)seq_len;
+                if (t % (uint64_t)hh_stride == 0) x = x + hh_boost * channel_sign(seed, c);
+            }
+        } else if (tensor == 2 && hh_stride > 0) {
+            x = x + 0.5f * channel_sign(seed, c);
+        }
+        out[j] = round_to_half(x);
+    }
+}

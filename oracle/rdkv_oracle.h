@@ -68,6 +68,11 @@ int orc_gen_synthetic(uint64_t seed, int layers, int q_heads, int kv_heads, int 
 /* raw NormalSampler stream (used for query vectors in tests) */
 void orc_normal_stream(uint64_t seed, float* out, size_t n);
 
+/* K0 counter-based generator (CPU restatement of csrc/generate.cu) */
+void orc_gen_counter(float* out, uint64_t seed, int tensor, uint64_t first, uint64_t count, int d,
+                     int seq_len, int outlier_channels, float outlier_scale, int hh_stride,
+                     float hh_boost);
+
 /* ---- stage 1 (cache.cpp:140-184, weights.cpp:8-46, 69-91) ---- */
 int orc_attention_probe(const float* q, int rows, const float* k, int t_len, int d,
                         const int* offsets, double* a);

@@ -1,0 +1,115 @@
+"""Builds a packed multi-sequence, multi-layer decode workload on the device.
+
+Every (sequence, layer) chunk of KV heads is generated on the device by K0,
+run through weights -> allocate -> pack, and its tiles appended to one arena
+(one unit per (sequence, layer, KV head), unit = (b * L + l) * H_kv + h), so a
+single decode launch covers the whole step. Prefill-time work only; nothing
+here runs inside a timed decode step.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import pipeline as P
+
+
+def chunk_seed(base: int, rank: int, b: int, layer: int) -> int:
+    return (base * 1_000_003 + rank * 7919 + b * 131 + layer) & ((1 << 63) - 1)
+
+
+@dataclass
+class WorkloadSpec:
+    batch: int = 16
+    layers: int = 32
+    q_heads: int = 32
+    kv_heads: int = 8
+    head_dim: int = 128
+    ctx: int = 131072
+    probe_rows: int = 32
+    n_tokens: int = 128
+    seed: int = 1
+    rank: int = 0
+    hh_stride: int = 0      # heavy hitters (0 = plain Gaussian, like gen_synthetic_cache)
+    hh_boost: float = 0.0
+    outlier_channels: int = 0
+    outlier_scale: float = 1.0
+    zc_cap: int = 0
+
+    @property
+    def group(self):
+        return self.q_heads // self.kv_heads
+
+    @property
+    def units(self):
+        return self.batch * self.layers * self.kv_heads
+
+
+def gen_chunk(spec: WorkloadSpec, b: int, layer: int, dtype=torch.float16):
+    """K, V [H_kv, T, d] and probe Q [H_kv, g, S_w, d] of one (sequence, layer)."""
+    s = chunk_seed(spec.seed, spec.rank, b, layer)
+    H, T, d = spec.kv_heads, spec.ctx, spec.head_dim
+    k = P.generate((H, T, d), dtype, seed=s, tensor=0, seq_len=T, outlier_channels=spec.outlier_channels,
+                   outlier_scale=spec.outlier_scale, hh_stride=spec.hh_stride, hh_boost=spec.hh_boost)
+    v = P.generate((H, T, d), dtype, seed=s, tensor=1, seq_len=T)
+    q = P.generate((H, spec.group, spec.probe_rows, d), dtype, seed=s, tensor=2, seq_len=T,
+                   hh_stride=spec.hh_stride)
+    return k, v, q
+
+
+def build(spec: WorkloadSpec, cfg=None, log=None):
+    """Returns (PackedModel over all units, timing dict, per-chunk allocation stats)."""
+    cfg = cfg or P.default_config(n_tokens=spec.n_tokens, window=spec.probe_rows)
+    chunks = []
+    t_alloc = t_pack = t_gen = 0.0
+    stats = []
+    first_alloc = None
+    for b in range(spec.batch):
+        for layer in range(spec.layers):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            k, v, q = gen_chunk(spec, b, layer)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            alloc = P.allocate_model(k, q, cfg, kv_heads=spec.kv_heads)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            model = P.build_packed_model(k, v, alloc, group=spec.group)
+            torch.cuda.synchronize()
+            t3 = time.perf_counter()
+            t_gen += t1 - t0
+            t_alloc += t2 - t1
+            t_pack += t3 - t2
+            st = alloc.stats_host()
+            if np.any(st["status"]):
+                alloc.check()
+            model.check()
+            stats.append(st)
+            if first_alloc is None:
+                first_alloc = (alloc.v_bits.cpu().numpy(), alloc.k_bits.cpu().numpy(), st)
+            chunks.append((model.arena[: model.arena_bytes], model.offsets_host))
+            del k, v, q, alloc
+    total = sum(int(o[-1]) for _, o in chunks)
+    arena = torch.empty(total + 256, dtype=torch.uint8, device="cuda")
+    offsets = np.zeros(spec.units + 1, np.int64)
+    pos = 0
+    u = 0
+    for a, o in chunks:
+        n = len(o) - 1
+        arena[pos:pos + int(o[-1])] = a
+        offsets[u:u + n] = o[:-1] + pos
+        pos += int(o[-1])
+        u += n
+    offsets[u] = pos
+    model = P.PackedModel(arena, torch.from_numpy(offsets).cuda(), offsets, spec.units, spec.group,
+                          spec.head_dim)
+    if spec.zc_cap:
+        model.zc_k = torch.zeros((spec.units, spec.zc_cap, spec.head_dim), dtype=torch.float16, device="cuda")
+        model.zc_v = torch.zeros_like(model.zc_k)
+        model.zc_len = torch.zeros(spec.units, dtype=torch.int32, device="cuda")
+        model.zc_cap = spec.zc_cap
+    timing = {"gen_s": t_gen, "weights_alloc_s": t_alloc, "pack_s": t_pack}
+    return model, timing, stats, first_alloc
