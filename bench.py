@@ -459,6 +459,7 @@ def main():
                         for h in range(spec.kv_heads))
             q0 = torch.from_numpy(info["q"][0].reshape(spec.kv_heads, g, d)).cuda().half()
             sub = P.PackedModel(model.arena, model.offsets, model.offsets_host, spec.kv_heads, g, d)
+            sub.decode_sizes, sub.plan = model.decode_sizes, model.plan
             o0 = P.packed_decode_step(sub, q0).float().cpu().numpy().reshape(-1, d)
             want = info["out"][0]
             err = float(max(np.linalg.norm(o0[j] - want[j]) / np.linalg.norm(want[j]) for j in range(len(want))))
@@ -492,6 +493,7 @@ def per_layer_launch_ms(P, model, spec, q, out, flush, args):
         idx = np.array([(b * spec.layers + layer) * H + h for b in range(spec.batch) for h in range(H)])
         offs = np.concatenate([model.offsets_host[idx], [0]])
         sub = P.PackedModel(model.arena, torch.from_numpy(offs).cuda(), offs, len(idx), spec.group, spec.head_dim)
+        sub.prepare()
         qi = torch.from_numpy(idx).cuda()
         subs.append((sub, q[qi].contiguous(), torch.empty_like(q[qi])))
     g = torch.cuda.CUDAGraph()

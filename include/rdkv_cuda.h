@@ -125,6 +125,14 @@ RDKV_API int rdkv_cuda_pack(const void* k, const void* v, int32_t dtype, const u
                             void* stream);
 
 /* ---- Decode ------------------------------------------------------------- */
+/* Maxima over the tiles of a packed arena (rdkv_cuda_decode_prepare). */
+typedef struct {
+    int32_t max_decode_bytes; /* largest per-tile decode region */
+    int32_t max_slots;        /* largest token-slot count */
+    int32_t max_zone_b_rows;  /* largest Zone B (16-bit V) row count */
+    int32_t max_kq_slots;     /* largest quantised-K slot count */
+} rdkv_decode_plan;
+
 typedef struct {
     const uint8_t* arena;
     const int64_t* tile_offsets;
@@ -143,7 +151,15 @@ typedef struct {
     size_t workspace_bytes;
     int32_t kernel;     /* 0 = automatic, 1 = generic CUDA-core, 2 = tensor-core */
     int32_t reserved;
+    const int32_t* tile_decode_bytes; /* [units] device, from rdkv_cuda_decode_prepare (NULL: generic) */
+    rdkv_decode_plan plan;
 } rdkv_decode_args;
+
+/* One-time scan of a packed arena: writes the per-tile decode sizes
+ * (device, [units]) and the plan that enables the tensor-core kernel. */
+RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int64_t* tile_offsets_host,
+                                      int32_t units, int32_t* tile_decode_bytes,
+                                      rdkv_decode_plan* plan, void* stream);
 
 RDKV_API size_t rdkv_cuda_decode_workspace(int32_t units, int32_t group, int32_t head_dim,
                                            int32_t split);

@@ -77,6 +77,11 @@ class HeadStats(C.Structure):
 HEAD_STATS_BYTES = C.sizeof(HeadStats)
 
 
+class DecodePlan(C.Structure):
+    _fields_ = [("max_decode_bytes", C.c_int32), ("max_slots", C.c_int32),
+                ("max_zone_b_rows", C.c_int32), ("max_kq_slots", C.c_int32)]
+
+
 class DecodeArgs(C.Structure):
     _fields_ = [
         ("arena", C.c_void_p), ("tile_offsets", C.c_void_p), ("units", C.c_int32),
@@ -84,7 +89,7 @@ class DecodeArgs(C.Structure):
         ("q", C.c_void_p), ("out", C.c_void_p), ("zc_k", C.c_void_p), ("zc_v", C.c_void_p),
         ("zc_len", C.c_void_p), ("zc_cap", C.c_int32), ("split", C.c_int32),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("kernel", C.c_int32),
-        ("reserved", C.c_int32),
+        ("reserved", C.c_int32), ("tile_decode_bytes", C.c_void_p), ("plan", DecodePlan),
     ]
 
 
@@ -106,6 +111,7 @@ _SIGS = {
                                  _VP]),
     "rdkv_cuda_decode_workspace": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "rdkv_cuda_decode": (C.c_int, [C.POINTER(DecodeArgs), _VP]),
+    "rdkv_cuda_decode_prepare": (C.c_int, [_VP, _VP, C.c_int32, _VP, C.POINTER(DecodePlan), _VP]),
     "rdkv_cuda_decode_host": (C.c_int, [C.POINTER(DecodeArgs), _VP, _VP, _VP]),
     "rdkv_cuda_append": (C.c_int, [_VP, _VP, _VP, C.c_int32, _VP, _VP, C.c_int32, C.c_int32,
                                    C.c_int32, _VP]),

@@ -170,7 +170,20 @@ class PackedModel:
     zc_len: torch.Tensor | None = None  # [U] int32
     zc_cap: int = 0
     head_status: torch.Tensor | None = None
+    decode_sizes: torch.Tensor | None = None   # [U] int32, from prepare()
+    plan: capi.DecodePlan | None = None
     _infos: list = field(default_factory=list)
+
+    def prepare(self) -> capi.DecodePlan:
+        """One-time tile scan enabling the tensor-core decode (rdkv_cuda_decode_prepare)."""
+        offs = np.ascontiguousarray(self.offsets_host, np.int64)
+        self.decode_sizes = torch.empty(self.units, dtype=torch.int32, device=self.arena.device)
+        plan = capi.DecodePlan()
+        raise_for(capi.lib().rdkv_cuda_decode_prepare(self.arena.data_ptr(), offs.ctypes.data, self.units,
+                                                      self.decode_sizes.data_ptr(), C.byref(plan),
+                                                      _stream()), "decode_prepare")
+        self.plan = plan
+        return plan
 
     @property
     def arena_bytes(self) -> int:
@@ -270,6 +283,7 @@ def build_packed_model(k, v, alloc: Allocation, group, zc_cap=0) -> PackedModel:
                                alloc.k_bits.data_ptr(), C.byref(shape), offsets.data_ptr(),
                                arena.data_ptr(), status.data_ptr(), _stream()), "pack")
     model = PackedModel(arena, offsets, offsets_host, U, group, d, head_status=status)
+    model.prepare()
     if zc_cap > 0:
         model.zc_k = torch.zeros((U, zc_cap, d), dtype=torch.float16, device=k.device)
         model.zc_v = torch.zeros((U, zc_cap, d), dtype=torch.float16, device=k.device)
@@ -291,6 +305,9 @@ def decode_args(model: PackedModel, q, out, split=1, kernel=0, workspace=None) -
         a.zc_cap = model.zc_cap
     a.split = split
     a.kernel = kernel
+    if model.plan is not None:
+        a.tile_decode_bytes = model.decode_sizes.data_ptr()
+        a.plan = model.plan
     if workspace is not None:
         a.workspace, a.workspace_bytes = workspace.data_ptr(), workspace.numel()
     return a

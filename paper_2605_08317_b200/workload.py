@@ -106,6 +106,7 @@ def build(spec: WorkloadSpec, cfg=None, log=None):
     offsets[u] = pos
     model = P.PackedModel(arena, torch.from_numpy(offsets).cuda(), offsets, spec.units, spec.group,
                           spec.head_dim)
+    model.prepare()
     if spec.zc_cap:
         model.zc_k = torch.zeros((spec.units, spec.zc_cap, spec.head_dim), dtype=torch.float16, device="cuda")
         model.zc_v = torch.zeros_like(model.zc_k)

@@ -1,0 +1,155 @@
+"""Tensor-core decode kernel (csrc/decode_mma.cu) vs the oracle and vs the generic kernel.
+
+Covers every bit class of V rows and K channels, Zone B (16-bit V rows),
+k16 (16-bit K channels), Zone C appends, GQA groups 1..8, fp16 and f32 I/O,
+and batches of many tiles in one persistent launch.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2605_08317_b200 import capi
+from paper_2605_08317_b200 import pipeline as P
+
+pytestmark = pytest.mark.gpu
+
+D = 128
+FP16_INPUT_TOL = 1e-4
+
+
+def f16r(x):
+    return np.asarray(x, np.float32).astype(np.float16).astype(np.float32)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _random_case(rng, T, g, p_bits=(0.2, 0.2, 0.2, 0.2, 0.2), kp=(0.2, 0.2, 0.2, 0.2, 0.2), max16=60):
+    choices = np.array([0, 2, 4, 8, 16])
+    k = f16r(rng.standard_normal((T, D)) * rng.uniform(0.3, 3.0))
+    v = f16r(rng.standard_normal((T, D)))
+    vb = choices[rng.choice(5, T, p=p_bits)].astype(np.int32)
+    idx16 = np.nonzero(vb == 16)[0]
+    if len(idx16) > max16:
+        vb[idx16[max16:]] = 8
+    vb[rng.integers(0, T)] = 2
+    kb = choices[rng.choice(5, D, p=kp)].astype(np.int32)
+    q = f16r(rng.standard_normal((g, D)))
+    return k, v, vb, kb, q
+
+
+def _run_batch(cuda, orc, cases, g, io=torch.float32, appends=0, rng=None):
+    """Pack all cases (same T) as units of one model; decode with both kernels."""
+    T = cases[0][0].shape[0]
+    K = torch.from_numpy(np.stack([c[0] for c in cases])).to(cuda)
+    V = torch.from_numpy(np.stack([c[1] for c in cases])).to(cuda)
+    vb = torch.from_numpy(np.stack([c[2] for c in cases]).astype(np.uint8)).to(cuda)
+    kb = torch.from_numpy(np.stack([c[3] for c in cases]).astype(np.uint8)).to(cuda)
+    stats = torch.zeros(len(cases) * capi.HEAD_STATS_BYTES, dtype=torch.uint8, device=cuda)
+    model = P.build_packed_model(K, V, P.Allocation(vb, kb, stats), group=g, zc_cap=max(appends, 1))
+    model.check()
+    zk = zv = None
+    if appends:
+        zk = f16r(rng.standard_normal((appends, len(cases), D)))
+        zv = f16r(rng.standard_normal((appends, len(cases), D)))
+        for a in range(appends):
+            P.append_new_token(model, torch.from_numpy(zk[a]).to(cuda), torch.from_numpy(zv[a]).to(cuda))
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).to(io)
+    out_mma = P.packed_decode_step(model, q, kernel=2).float().cpu().numpy()
+    out_gen = P.packed_decode_step(model, q, kernel=1).float().cpu().numpy()
+    worst = 0.0
+    for u, (k, v, vbs, kbs, qq) in enumerate(cases):
+        tz = orc.tz_build(k, v, vbs, kbs)
+        for a in range(appends):
+            tz.append(zk[a, u], zv[a, u])
+        for j in range(g):
+            want = tz.decode(qq[j])
+            worst = max(worst, rel(out_mma[u, j], want))
+            assert rel(out_mma[u, j], out_gen[u, j]) < 2 * FP16_INPUT_TOL
+    return worst, model
+
+
+def test_mma_all_two_bit_default_budget_shape(cuda, orc):
+    """The C1/C3 allocation shape: 128 kept tokens, every V row and K channel at 2 bits."""
+    rng = np.random.default_rng(1)
+    cases = []
+    for _ in range(16):
+        k, v, vb, kb, q = _random_case(rng, 512, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(512, 128, replace=False))] = 2
+        kb[:] = 2
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, 4)
+    assert model.plan.max_slots == 128
+    assert worst < FP16_INPUT_TOL, worst
+
+
+@pytest.mark.parametrize("g", [1, 2, 4, 7, 8])
+def test_mma_mixed_classes(cuda, orc, g):
+    rng = np.random.default_rng(100 + g)
+    cases = [_random_case(rng, 280, g) for _ in range(12)]
+    worst, model = _run_batch(cuda, orc, cases, g)
+    assert model.plan.max_slots <= 256
+    assert worst < FP16_INPUT_TOL, worst
+
+
+def test_mma_zone_c_and_fp16_io(cuda, orc):
+    rng = np.random.default_rng(7)
+    cases = [_random_case(rng, 200, 4) for _ in range(9)]
+    worst, _ = _run_batch(cuda, orc, cases, 4, appends=6, rng=rng)
+    assert worst < FP16_INPUT_TOL, worst
+    worst, _ = _run_batch(cuda, orc, cases, 4, io=torch.float16, appends=3, rng=rng)
+    assert worst < 1e-3, worst
+
+
+def test_mma_edge_allocations(cuda, orc):
+    rng = np.random.default_rng(9)
+    T = 64
+    base = _random_case(rng, T, 4)
+    cases = []
+    # all K channels removed -> uniform attention over V_hat
+    k, v, vb, kb, q = [x.copy() for x in base]
+    kb[:] = 0
+    cases.append((k, v, vb, kb, q))
+    # all K channels 16-bit (k16 only)
+    k, v, vb, kb, q = [x.copy() for x in base]
+    kb[:] = 16
+    cases.append((k, v, vb, kb, q))
+    # single kept token at 8 bits
+    k, v, vb, kb, q = [x.copy() for x in base]
+    vb[:] = 0
+    vb[5] = 8
+    cases.append((k, v, vb, kb, q))
+    # constant V row and constant K column (degenerate 1e-12 ranges)
+    k, v, vb, kb, q = [x.copy() for x in base]
+    v[:, :] = f16r(1.25)
+    k[:, 3] = f16r(-0.5)
+    cases.append((k, v, vb, kb, q))
+    worst, _ = _run_batch(cuda, orc, cases, 4)
+    assert worst < FP16_INPUT_TOL, worst
+
+
+def test_mma_large_batch_persistent(cuda, orc):
+    """More tiles than resident warps: every worker walks several tiles through its ring."""
+    rng = np.random.default_rng(11)
+    cases = []
+    for i in range(600):
+        k, v, vb, kb, q = _random_case(rng, 96, 4, p_bits=(0.4, 0.3, 0.15, 0.1, 0.05))
+        cases.append((k, v, vb, kb, q))
+    # check only a sample against the oracle (all against the generic kernel)
+    worst, _ = _run_batch(cuda, orc, cases[:40], 4)
+    assert worst < FP16_INPUT_TOL
+    T = 96
+    K = torch.from_numpy(np.stack([c[0] for c in cases])).to(cuda)
+    V = torch.from_numpy(np.stack([c[1] for c in cases])).to(cuda)
+    vb = torch.from_numpy(np.stack([c[2] for c in cases]).astype(np.uint8)).to(cuda)
+    kb = torch.from_numpy(np.stack([c[3] for c in cases]).astype(np.uint8)).to(cuda)
+    stats = torch.zeros(len(cases) * capi.HEAD_STATS_BYTES, dtype=torch.uint8, device=cuda)
+    model = P.build_packed_model(K, V, P.Allocation(vb, kb, stats), group=4)
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda)
+    a = P.packed_decode_step(model, q, kernel=2)
+    b = P.packed_decode_step(model, q, kernel=1)
+    err = (a - b).norm(dim=-1) / b.norm(dim=-1)
+    assert float(err.max()) < 2 * FP16_INPUT_TOL
+    del T
