@@ -16,17 +16,18 @@
 //  1. cp.async.bulk (TMA 1-D) stages the tile's decode region and its g
 //     query rows into the warp's smem ring (mbarrier completion), NSTAGE deep.
 //  2. q~ = scale_s * q[perm_s] per K slot, quantised per (bit class, head) to
-//     a 16-bit fixed-point value split into two signed 8-bit digits (the B
+//     a 24-bit fixed-point value split into three signed 8-bit digits (the B
 //     operand, N = heads x digits); bias = sum q * offset.
 //  3. QK: A = K codes of 16 token slots x 32 K slots (u8), B = digits (s8),
 //     s32 accumulate; logit = (hi*256 + lo) / sigma + bias, * 1/sqrt(d).
 //  4. softmax over the tile + Zone C with warp shuffles; p~ = p * vscale
-//     quantised per (V class, head) to two unsigned 8-bit digits.
+//     quantised per (V class, head) to three unsigned 8-bit digits.
 //  5. PV: A = V codes of 16 channels x 32 tokens (u8, 4-token interleave makes
 //     one 32-bit word = 4 tokens), B = p~ digits (u8), s32 accumulate;
 //     out = (PV + sum p * voffset + Zone B/C rows) / l.
-// Fixed-point error: <= 2^-16 relative to the per-class max per element,
-// ~1e-5 relative on outputs (tolerance 1e-3, tests assert 1e-4 on FP16 inputs).
+// Fixed-point error: q~ <= 2^-24 and p~ <= 2^-25 relative to the per-class
+// max per element, ~1e-6 relative on outputs (tolerance 1e-3, tests assert
+// 1e-4 on FP16-representable inputs).
 #include "common.cuh"
 
 namespace rdkv_b200 {
@@ -92,10 +93,9 @@ __device__ __forceinline__ void mma_u8u8(int (&c)[4], const uint32_t (&a)[4], ui
 
 __device__ __forceinline__ uint32_t lds32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
 __device__ __forceinline__ uint2 lds64(const uint8_t* p) { return *reinterpret_cast<const uint2*>(p); }
-__device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
 // Position (0..31) inside a k32 step of K slot `j` (0..31) of a class, for the
-// A-fragment extraction used in qk_class(): a 2-bit word (16 slots) yields
+// A-fragment extraction of the QK loop: a 2-bit word (16 slots) yields
 // slots {4e + tig} into K positions 4*tig + e; 4-bit words (8 slots) yield
 // slots {2e + (tig & 1)} of word tig >> 1; 8-bit words are already bytes.
 __device__ __forceinline__ int kpos_of_slot(int cls, int j) {
@@ -120,8 +120,8 @@ template <>
 __device__ __forceinline__ float ld_io<__half>(const __half* p, int i) { return __half2float(p[i]); }
 
 struct WarpSmem {
-    uint8_t bq[kMaxKSteps * 2 * 8 * 32];   // QK B digits [kstep][n-tile*8 + n][32]
-    uint8_t bp[kMaxVSteps * 3 * 2 * 8 * 32];  // PV B digits [class][kstep][n][32]
+    uint8_t bq[kMaxKSteps * 4 * 8 * 32];   // QK B digits [kstep][n-tile (2 per 4 heads)][n][32]
+    uint8_t bp[(kMaxVSteps + 3) * 4 * 8 * 32];  // PV B digits [kstep][n-tile (2 per 4 heads)][n][32]
     float acc[8 * kD];                     // [head][channel]
     float zl[8 * kMaxZc];                  // Zone C logits / probabilities
     float p16[8 * 64];                     // Zone B probabilities [head][row] (<= 64 rows)
@@ -183,45 +183,54 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
             acc += (h.c[c] + 31) >> 5;
         }
     }
+    // q~ in 24-bit signed fixed point per (K class, head): three signed 8-bit
+    // digits hi, mid, lo. B n-tiles come in pairs per 4 heads: tile 2*hb holds
+    // columns (hi, mid) of head 4*hb + n/2, tile 2*hb + 1 holds (lo, 0).
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         const int nc = h.c[c];
         if (nc == 0) continue;
         const int P = (nc + 31) & ~31;
         for (int hh = 0; hh < 4 * NT; ++hh) {
-            if (hh >= g) break;
+            const int nt = hh >> 2, n0 = 2 * (hh & 3);
+            if (hh >= g) {
+                for (int j = lane; j < P; j += 32) {
+                    const int ks = ks_base[c] + (j >> 5);
+                    uint8_t* a0 = w.bq + ((ks * 2 * NT + 2 * nt) * 8) * 32;
+                    uint8_t* a1 = a0 + 8 * 32;
+                    a0[n0 * 32 + (j & 31)] = 0;
+                    a0[(n0 + 1) * 32 + (j & 31)] = 0;
+                    a1[n0 * 32 + (j & 31)] = 0;
+                    a1[(n0 + 1) * 32 + (j & 31)] = 0;
+                }
+                continue;
+            }
             float mx = 0.0f;
             for (int j = lane; j < nc; j += 32) {
                 const int s = h.kslot_base[c] + j;
                 mx = fmaxf(mx, fabsf(chan[s].x * ld_io(qs, hh * kD + perm[s])));
             }
             mx = warp_max(mx);
-            const float sig = mx > 0.0f ? 32512.0f / mx : 1.0f;
+            const float sig = mx > 0.0f ? 8.2e6f / mx : 1.0f;
             if (lane == 0) w.qsig[c][hh] = sig;
-            const int nt = hh >> 2, n0 = 2 * (hh & 3);
             for (int j = lane; j < P; j += 32) {
-                int dh = 0, dl = 0;
+                int dh = 0, dm = 0, dl = 0;
                 if (j < nc) {
                     const int s = h.kslot_base[c] + j;
                     const int N = __float2int_rn(chan[s].x * ld_io(qs, hh * kD + perm[s]) * sig);
-                    dh = (N + 128) >> 8;
-                    dl = N - dh * 256;
+                    dl = ((N + 128) & 255) - 128;
+                    const int N1 = (N - dl) >> 8;
+                    dm = ((N1 + 128) & 255) - 128;
+                    dh = (N1 - dm) >> 8;
                 }
                 const int ks = ks_base[c] + (j >> 5);
                 const int kp = kpos_of_slot(c, j & 31);
-                uint8_t* base = w.bq + ((ks * NT + nt) * 8) * 32;
-                base[n0 * 32 + kp] = (uint8_t)(int8_t)dh;
-                base[(n0 + 1) * 32 + kp] = (uint8_t)(int8_t)dl;
-            }
-        }
-        // unused head columns of this class's k-steps stay zero
-        for (int hh = g; hh < 4 * NT; ++hh) {
-            const int nt = hh >> 2, n0 = 2 * (hh & 3);
-            for (int j = lane; j < P; j += 32) {
-                const int ks = ks_base[c] + (j >> 5);
-                uint8_t* base = w.bq + ((ks * NT + nt) * 8) * 32;
-                base[n0 * 32 + (j & 31)] = 0;
-                base[(n0 + 1) * 32 + (j & 31)] = 0;
+                uint8_t* a0 = w.bq + ((ks * 2 * NT + 2 * nt) * 8) * 32;
+                uint8_t* a1 = a0 + 8 * 32;
+                a0[n0 * 32 + kp] = (uint8_t)(int8_t)dh;
+                a0[(n0 + 1) * 32 + kp] = (uint8_t)(int8_t)dm;
+                a1[n0 * 32 + kp] = (uint8_t)(int8_t)dl;
+                a1[(n0 + 1) * 32 + kp] = 0;
             }
         }
     }
@@ -245,9 +254,9 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
         const int step_bytes = 32 * kBits(c) / 8;  // 8 / 16 / 32
         for (int mt = 0; mt < mtiles; ++mt) {
             const int r0 = mt * 16 + gid, r1 = r0 + 8;
-            int acc[NT][4];
+            int acc[2 * NT][4];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
+            for (int nt = 0; nt < 2 * NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
             for (int kk = 0; kk < nks; ++kk) {
                 const uint8_t* p0 = krows + (size_t)r0 * h.krow_bytes + kb0 + kk * step_bytes;
                 const uint8_t* p1 = krows + (size_t)r1 * h.krow_bytes + kb0 + kk * step_bytes;
@@ -260,10 +269,11 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
                     a[1] = (w1.x >> sh) & 0x03030303u;
                     a[3] = (w1.y >> sh) & 0x03030303u;
                 } else if (c == 1) {
-                    const uint4 w0 = lds128(p0), w1 = lds128(p1);
+                    // class regions are 8-byte aligned inside a K row: two 8-byte loads
+                    const uint2 x0 = lds64(p0), y0 = lds64(p0 + 8), x1 = lds64(p1), y1 = lds64(p1 + 8);
                     const int sh = 4 * (tig & 1);
-                    const uint32_t lo0 = (tig >> 1) ? w0.y : w0.x, hi0 = (tig >> 1) ? w0.w : w0.z;
-                    const uint32_t lo1 = (tig >> 1) ? w1.y : w1.x, hi1 = (tig >> 1) ? w1.w : w1.z;
+                    const uint32_t lo0 = (tig >> 1) ? x0.y : x0.x, hi0 = (tig >> 1) ? y0.y : y0.x;
+                    const uint32_t lo1 = (tig >> 1) ? x1.y : x1.x, hi1 = (tig >> 1) ? y1.y : y1.x;
                     a[0] = (lo0 >> sh) & 0x0F0F0F0Fu;
                     a[2] = (hi0 >> sh) & 0x0F0F0F0Fu;
                     a[1] = (lo1 >> sh) & 0x0F0F0F0Fu;
@@ -276,8 +286,8 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
                 }
                 const int ks = ks_base[c] + kk;
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const uint8_t* bb = w.bq + ((ks * NT + nt) * 8 + gid) * 32 + 4 * tig;
+                for (int nt = 0; nt < 2 * NT; ++nt) {
+                    const uint8_t* bb = w.bq + ((ks * 2 * NT + nt) * 8 + gid) * 32 + 4 * tig;
                     mma_u8s8(acc[nt], a, lds32(bb), lds32(bb + 16));
                 }
             }
@@ -285,8 +295,10 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
             for (int nt = 0; nt < NT; ++nt) {
                 const int hh = nt * 4 + tig;
                 const float inv = hh < g ? 1.0f / w.qsig[c][hh] : 0.0f;
-                const float v0 = fmaf((float)acc[nt][0], 256.0f, (float)acc[nt][1]) * inv;
-                const float v1 = fmaf((float)acc[nt][2], 256.0f, (float)acc[nt][3]) * inv;
+                const int* A = acc[2 * nt];
+                const int* B = acc[2 * nt + 1];
+                const float v0 = fmaf((float)A[0], 65536.0f, fmaf((float)A[1], 256.0f, (float)B[0])) * inv;
+                const float v1 = fmaf((float)A[2], 65536.0f, fmaf((float)A[3], 256.0f, (float)B[2])) * inv;
 #pragma unroll
                 for (int m = 0; m < kMaxSlots / 16; ++m)
                     if (m == mt) {
@@ -448,7 +460,7 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) psig[c][nt] = pmax[c][nt] > 0.0f ? 65280.0f / pmax[c][nt] : 0.0f;
+        for (int nt = 0; nt < NT; ++nt) psig[c][nt] = pmax[c][nt] > 0.0f ? 1.6e7f / pmax[c][nt] : 0.0f;
     // zero the B-digit area of every V class k-step (tails of the last step)
     int vks[3], vks_base[3];
     {
@@ -460,7 +472,7 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
             acc += vks[c];
         }
         uint4* z = reinterpret_cast<uint4*>(w.bp);
-        const int n16 = acc * NT * 8 * 32 / 16;
+        const int n16 = acc * 2 * NT * 8 * 32 / 16;
         for (int i = lane; i < n16; i += 32) z[i] = make_uint4(0, 0, 0, 0);
     }
     __syncwarp();
@@ -482,9 +494,10 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
                     if (c == cls) sg = psig[c][nt];
                 const int N = __float2int_rn(lg[mt][half][nt] * sg);
                 const int ks = vks_base[cls] + (li >> 5);
-                uint8_t* base = w.bp + ((ks * NT + nt) * 8 + 2 * tig) * 32 + (li & 31);
-                base[0] = (uint8_t)(N >> 8);
-                base[32] = (uint8_t)(N & 255);
+                uint8_t* base = w.bp + ((ks * 2 * NT + 2 * nt) * 8 + 2 * tig) * 32 + (li & 31);
+                base[0] = (uint8_t)(N >> 16);            // tile 2nt,   column 2tig   : hi
+                base[32] = (uint8_t)((N >> 8) & 255);    // tile 2nt,   column 2tig+1 : mid
+                base[8 * 32] = (uint8_t)(N & 255);       // tile 2nt+1, column 2tig   : lo
             }
         }
     }
@@ -506,9 +519,9 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
         const int rb = kD * kBits(c) / 8;  // packed row bytes at d = 128
         const uint8_t* vbase = t + h.off_vseg[c];
         for (int mt = 0; mt < kD / 16; ++mt) {
-            int acc[NT][4];
+            int acc[2 * NT][4];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
+            for (int nt = 0; nt < 2 * NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
             int ch0, ch1;
             for (int kk = 0; kk < vks[c]; ++kk) {
                 const int gr0 = kk * 8 + tig, gr1 = gr0 + 4;  // token groups of this k-step
@@ -539,8 +552,8 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
                 }
                 const int ks = vks_base[c] + kk;
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const uint8_t* bb = w.bp + ((ks * NT + nt) * 8 + gid) * 32 + 4 * tig;
+                for (int nt = 0; nt < 2 * NT; ++nt) {
+                    const uint8_t* bb = w.bp + ((ks * 2 * NT + nt) * 8 + gid) * 32 + 4 * tig;
                     mma_u8u8(acc[nt], a, lds32(bb), lds32(bb + 16));
                 }
             }
@@ -560,8 +573,10 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
                 if (hh >= g) continue;
                 const float sg = w.sig[c][hh];
                 const float inv = sg > 0.0f ? 1.0f / sg : 0.0f;
-                w.acc[hh * kD + ch0] += fmaf((float)acc[nt][0], 256.0f, (float)acc[nt][1]) * inv;
-                w.acc[hh * kD + ch1] += fmaf((float)acc[nt][2], 256.0f, (float)acc[nt][3]) * inv;
+                const int* A = acc[2 * nt];
+                const int* B = acc[2 * nt + 1];
+                w.acc[hh * kD + ch0] += fmaf((float)A[0], 65536.0f, fmaf((float)A[1], 256.0f, (float)B[0])) * inv;
+                w.acc[hh * kD + ch1] += fmaf((float)A[2], 65536.0f, fmaf((float)A[3], 256.0f, (float)B[2])) * inv;
             }
         }
         __syncwarp();
@@ -638,7 +653,7 @@ __device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const
 }
 
 template <int NT, typename IO>
-__global__ void __launch_bounds__(256) decode_mma_kernel(
+__global__ void __launch_bounds__(256, 1) decode_mma_kernel(
     const uint8_t* __restrict__ arena, const int64_t* __restrict__ offsets, const int32_t* __restrict__ dsize,
     int units, int g, const IO* __restrict__ q_all, IO* __restrict__ out_all, const __half* __restrict__ zc_k,
     const __half* __restrict__ zc_v, const int32_t* __restrict__ zc_len, int zc_cap, int stage_bytes,
