@@ -131,6 +131,7 @@ typedef struct {
     int32_t max_slots;        /* largest token-slot count */
     int32_t max_zone_b_rows;  /* largest Zone B (16-bit V) row count */
     int32_t max_kq_slots;     /* largest quantised-K slot count */
+    int32_t uniform2;         /* every tile: all kept V rows and K channels at 2 bits */
 } rdkv_decode_plan;
 
 typedef struct {
@@ -149,7 +150,8 @@ typedef struct {
     int32_t split;      /* split-K factor (0 = automatic) */
     void* workspace;    /* split-K partials; rdkv_cuda_decode_workspace() bytes */
     size_t workspace_bytes;
-    int32_t kernel;     /* 0 = automatic, 1 = generic CUDA-core, 2 = tensor-core */
+    int32_t kernel;     /* 0 = automatic, 1 = generic CUDA-core, 2 = tensor-core (automatic body),
+                           3 = tensor-core general body, 4 = tensor-core one-warp uniform-2-bit body */
     int32_t reserved;
     const int32_t* tile_decode_bytes; /* [units] device, from rdkv_cuda_decode_prepare (NULL: generic) */
     rdkv_decode_plan plan;

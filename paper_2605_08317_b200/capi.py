@@ -79,7 +79,7 @@ HEAD_STATS_BYTES = C.sizeof(HeadStats)
 
 class DecodePlan(C.Structure):
     _fields_ = [("max_decode_bytes", C.c_int32), ("max_slots", C.c_int32),
-                ("max_zone_b_rows", C.c_int32), ("max_kq_slots", C.c_int32)]
+                ("max_zone_b_rows", C.c_int32), ("max_kq_slots", C.c_int32), ("uniform2", C.c_int32)]
 
 
 class DecodeArgs(C.Structure):

@@ -29,9 +29,10 @@ extern "C" RDKV_API int rdkv_cuda_decode(const rdkv_decode_args* a, void* stream
                       a->workspace_bytes < rdkv_cuda_decode_workspace(a->units, a->group, a->head_dim, split)))
         return RDKV_EINVAL;
     auto st = static_cast<cudaStream_t>(stream);
-    const bool want_mma = a->kernel == 2 || (a->kernel == 0 && split == 1);
+    const bool forced = a->kernel >= 2;
+    const bool want_mma = forced || (a->kernel == 0 && split == 1);
     if (want_mma && mma_supported(a)) return launch_mma(a, st);
-    if (a->kernel == 2) return RDKV_EINVAL;
+    if (forced) return RDKV_EINVAL;
     const int max_kslots = a->head_dim + 3 * 31 + 7;
     return a->io_dtype == RDKV_F32 ? launch_generic<float>(a, split, max_kslots, st)
                                    : launch_generic<__half>(a, split, max_kslots, st);

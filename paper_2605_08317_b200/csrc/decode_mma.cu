@@ -5,38 +5,43 @@
 // every (batch, layer, KV head) tile of a step in ONE persistent launch.
 //
 // Why tensor cores: at n=128 a tile is ~10.5 KB and carries 128 tokens x 128
-// channels x g=4 heads x 2 (QK+PV) = 131K MACs, i.e. ~12 MAC/byte. B200 CUDA
-// cores sustain ~64 FFMA/clk/SM (3-reg form), ~5.5 MAC/byte of HBM
-// bandwidth, so a CUDA-core decode caps at ~45% of the HBM roofline. The
+// channels x g=4 heads x 2 (QK+PV) = 131K MACs, ~12 MAC/byte. B200 CUDA cores
+// issue ~64 FFMA/clk/SM (3-register form), ~5.5 MAC per byte of HBM
+// bandwidth, so a CUDA-core decode caps near 45% of the HBM roofline. The
 // int8 mma.sync m16n8k32 consumes the packed codes as u8 operands straight
-// from registers: one SHF+LOP3 pair extracts 4 two-bit codes into the 4 bytes
-// of an A register, so the dequant costs ~0.5 ALU op per code.
+// from registers: one SHF + LOP3 pair turns a 32-bit word of 2-bit codes into
+// an A register holding four codes, so dequantisation costs ~0.5 ALU op per
+// code and the multiply-adds leave the CUDA cores entirely.
 //
-// Per tile (one warp, no block-level synchronisation):
-//  1. cp.async.bulk (TMA 1-D) stages the tile's decode region and its g
-//     query rows into the warp's smem ring (mbarrier completion), NSTAGE deep.
-//  2. q~ = scale_s * q[perm_s] per K slot, quantised per (bit class, head) to
-//     a 24-bit fixed-point value split into three signed 8-bit digits (the B
-//     operand, N = heads x digits); bias = sum q * offset.
-//  3. QK: A = K codes of 16 token slots x 32 K slots (u8), B = digits (s8),
-//     s32 accumulate; logit = (hi*256 + lo) / sigma + bias, * 1/sqrt(d).
-//  4. softmax over the tile + Zone C with warp shuffles; p~ = p * vscale
-//     quantised per (V class, head) to three unsigned 8-bit digits.
-//  5. PV: A = V codes of 16 channels x 32 tokens (u8, 4-token interleave makes
-//     one 32-bit word = 4 tokens), B = p~ digits (u8), s32 accumulate;
-//     out = (PV + sum p * voffset + Zone B/C rows) / l.
-// Fixed-point error: q~ <= 2^-24 and p~ <= 2^-25 relative to the per-class
-// max per element, ~1e-6 relative on outputs (tolerance 1e-3, tests assert
-// 1e-4 on FP16-representable inputs).
+// CTA organisation (persistent, one CTA per SM):
+//   warp 0      producer: walks the CTA's tiles and stages each tile's decode
+//               region plus its g query rows into a ring of R smem slots with
+//               cp.async.bulk (TMA 1-D), completion on a per-slot mbarrier;
+//               a slot is refilled once its consumer releases it.
+//   warps 1..W  consumers: warp w decodes tiles w, w+W, ... of the CTA, one
+//               tile per warp, with no block-level synchronisation.
+// Per tile (one consumer warp; intermediates in warp-private smem so the
+// m-tile loops stay rolled and the SASS fits the instruction cache):
+//   1. q~ = scale_s * q[perm_s] per K slot in 24-bit signed fixed point
+//      (three s8 digits) against the bound max|scale| * max|q| of each
+//      (bit class, head); bias = sum_s q[perm_s] * offset_s.
+//   2. QK: A = K codes of 16 token slots x 32 K slots (u8), B = q~ digits (s8),
+//      s32 accumulate; logit = (hi*2^16 + mid*2^8 + lo) / sigma + bias.
+//   3. softmax over the tile (+ Zone C), one lane per token, shuffles;
+//      p~ = p * vscale in 24-bit unsigned fixed point (three u8 digits).
+//   4. PV: A = V codes of 16 channels x 32 tokens (u8; the 4-token interleave
+//      makes one 32-bit word = 4 tokens of one byte column), B = p~ digits,
+//      s32 accumulate; out = (PV / sigma + sum p * voffset + Zone B/C) / l.
+// Fixed-point error ~2^-22 relative per element, ~1e-6 relative on outputs
+// (tolerance 1e-3; tests assert 1e-4 on FP16-representable inputs).
 #include "common.cuh"
 
 namespace rdkv_b200 {
 
-constexpr int kD = 128;          // head_dim of this path
-constexpr int kMaxSlots = 256;   // token slots per tile (16 m-tiles)
-constexpr int kMaxZc = 256;      // Zone C tokens per tile on this path
-constexpr int kMaxKSteps = 7;    // K slots of classes 2/4/8 <= 128 + 3*31 -> 7 k32 steps
-constexpr int kMaxVSteps = 8;    // token k32 steps (256 slots)
+constexpr int kD = 128;        // head_dim of this path
+constexpr int kMaxR = 32;      // ring slots per CTA
+constexpr int kMaxW = 12;      // consumer warps per CTA (13 warps -> <=152 regs)
+constexpr int kMaxSlots = 256; // token slots per tile on this path
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -48,6 +53,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile(
@@ -74,7 +82,7 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// D = A(u8, 16x32 row) * B(s8, 32x8 col) + C
+// D = A(u8, 16x32 row-major) * B(s8, 32x8 col-major) + C, s32 accumulate
 __device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -94,22 +102,22 @@ __device__ __forceinline__ void mma_u8u8(int (&c)[4], const uint32_t (&a)[4], ui
 __device__ __forceinline__ uint32_t lds32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
 __device__ __forceinline__ uint2 lds64(const uint8_t* p) { return *reinterpret_cast<const uint2*>(p); }
 
-// Position (0..31) inside a k32 step of K slot `j` (0..31) of a class, for the
-// A-fragment extraction of the QK loop: a 2-bit word (16 slots) yields
-// slots {4e + tig} into K positions 4*tig + e; 4-bit words (8 slots) yield
-// slots {2e + (tig & 1)} of word tig >> 1; 8-bit words are already bytes.
-__device__ __forceinline__ int kpos_of_slot(int cls, int j) {
-    if (cls == 0) {  // word w = j >> 4, slot-in-word s = 4e + tig
-        const int w = j >> 4, s = j & 15;
-        return w * 16 + (s & 3) * 4 + (s >> 2);
+// K slot (0..31 within a k32 step) feeding MMA K position `p`, per class.
+// 2-bit: a K-row word holds 16 slots; (w >> 2*tig) & 0x03030303 yields slots
+// {4e + tig} as bytes e, i.e. K positions 4*tig + e. 4-bit: words of 8 slots,
+// (w >> 4*(tig&1)) & 0x0F0F0F0F yields slots {2e + (tig&1)} of word tig>>1
+// (a0) / 2 + (tig>>1) (a2). 8-bit: identity.
+__device__ __forceinline__ int slot_of_kpos(int cls, int p) {
+    if (cls == 0) {
+        const int r = p & 15;
+        return (p & 16) + 4 * (r & 3) + (r >> 2);
     }
-    if (cls == 1) {  // word index wi = j >> 3 (0..3), slot-in-word s = 2e + jj
-        const int wi = j >> 3, s = j & 7;
-        const int tig = (wi & 1) * 2 + (s & 1);
-        const int half = wi >> 1;  // words 0,1 -> a0 (K 0..15); words 2,3 -> a2 (K 16..31)
-        return half * 16 + tig * 4 + (s >> 1);
+    if (cls == 1) {
+        const int half = p >> 4, r = p & 15;
+        const int tig = r >> 2, e = r & 3;
+        return 16 * half + 8 * (tig >> 1) + 2 * e + (tig & 1);
     }
-    return j;  // 8-bit: word tig holds slots 4tig..4tig+3, word 4+tig holds 16+4tig..
+    return p;
 }
 
 template <typename IO>
@@ -119,594 +127,1089 @@ __device__ __forceinline__ float ld_io<float>(const float* p, int i) { return p[
 template <>
 __device__ __forceinline__ float ld_io<__half>(const __half* p, int i) { return __half2float(p[i]); }
 
-struct WarpSmem {
-    uint8_t bq[kMaxKSteps * 4 * 8 * 32];   // QK B digits [kstep][n-tile (2 per 4 heads)][n][32]
-    uint8_t bp[(kMaxVSteps + 3) * 4 * 8 * 32];  // PV B digits [kstep][n-tile (2 per 4 heads)][n][32]
-    float acc[8 * kD];                     // [head][channel]
-    float zl[8 * kMaxZc];                  // Zone C logits / probabilities
-    float p16[8 * 64];                     // Zone B probabilities [head][row] (<= 64 rows)
-    float sig[3][8];                       // sigma per (V class, head)
-    float qsig[3][8];                      // sigma per (K class, head)
-    uint64_t bar[4];
+struct MmaParams {
+    const uint8_t* arena;
+    const int64_t* offsets;
+    const int32_t* dsize;
+    const void* q;
+    void* out;
+    const __half* zc_k;
+    const __half* zc_v;
+    const int32_t* zc_len;
+    int units, g, zc_cap;
+    int R, W;               // ring slots, consumer warps
+    int slot_bytes;         // per ring slot (tile decode region + q rows)
+    int scratch_bytes;      // per consumer warp
+    int off_lg;             // byte offsets inside the per-warp scratch
+    int lg_stride;          // per-head stride (floats) of the logit scratch
+    int off_p16, off_zl;    // -1 when unused
+    int max_r16;
 };
 
-// One warp decodes one tile that sits in `t` (smem) with its q rows at `qs`.
+// Per-warp scratch: [ScratchHead][B digits][lg / acc][p16][zl]
+struct ScratchHead {
+    float qinv[3][8];   // 1/sigma per (K class, head)
+    float vinv[3][8];   // 1/sigma per (V class, head)
+};
+constexpr int kDigitBytesOff = 256;
+
 template <int NT, typename IO>
-__device__ __forceinline__ void decode_tile(const uint8_t* __restrict__ t, const IO* __restrict__ qs, int g,
-                                            WarpSmem& w, const __half* __restrict__ zck,
-                                            const __half* __restrict__ zcv, int nzc, IO* __restrict__ out) {
+__device__ __noinline__ void decode_tile(const uint8_t* __restrict__ t, const IO* __restrict__ qs, int g,
+                                         uint8_t* __restrict__ scr, const MmaParams& prm,
+                                         const __half* __restrict__ zck, const __half* __restrict__ zcv,
+                                         int nzc, IO* __restrict__ out) {
+    constexpr int G4 = 4 * NT;  // head capacity of the n-tiles
+    constexpr int TS = 32 / G4; // lanes per head in the per-head phases
     const int lane = threadIdx.x & 31;
     const int gid = lane >> 2, tig = lane & 3;
+    // per-head phases: head hl = lane % G4, tokens / channels tl, tl + TS, ...
+    const int hl = lane % G4, tl = lane / G4;
+    const bool hv = hl < g;
     const TileHeader& h = *reinterpret_cast<const TileHeader*>(t);
-    const int nslot = h.nslot;
+    ScratchHead& sh = *reinterpret_cast<ScratchHead*>(scr);
+    uint8_t* dig = scr + kDigitBytesOff;
+    const int LS = prm.lg_stride;
+    float* lgs = reinterpret_cast<float*>(scr + prm.off_lg);  // [G4][LS] logits, later acc [G4][kD]
+    float* p16 = prm.off_p16 >= 0 ? reinterpret_cast<float*>(scr + prm.off_p16) : nullptr;
+    float* zl = prm.off_zl >= 0 ? reinterpret_cast<float*>(scr + prm.off_zl) : nullptr;
     const float2* chan = reinterpret_cast<const float2*>(t + kHeaderBytes);
     const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
     const float2* vparam = reinterpret_cast<const float2*>(t + h.off_vp);
-    int sbase[5];
-    sbase[0] = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) sbase[i + 1] = sbase[i] + pad4(h.r[i]);
-
-    // ---------------------------------------------------------------- q~ digits
-    float bias[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) bias[nt] = 0.0f;
-    {
-        // bias_h = sum_s q[h][perm_s] * offset_s; lane-strided partial, reduced below
-        float bpart[8];
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh) bpart[hh] = 0.0f;
-        for (int s = lane; s < h.kslots; s += 32) {
-            const float2 cs = chan[s];
-            const int ch = perm[s];
-#pragma unroll
-            for (int hh = 0; hh < 4 * NT; ++hh)
-                if (hh < g) bpart[hh] = fmaf(ld_io(qs, hh * kD + ch), cs.y, bpart[hh]);
-        }
-#pragma unroll
-        for (int hh = 0; hh < 4 * NT; ++hh) bpart[hh] = warp_sum(bpart[hh]);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const int hh = nt * 4 + tig;
-            float v = 0.0f;
-#pragma unroll
-            for (int k = 0; k < 4 * NT; ++k) v = (k == hh) ? bpart[k] : v;
-            bias[nt] = v;
-        }
-    }
-    int ks_base[3];
-    {
-        int acc = 0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            ks_base[c] = acc;
-            acc += (h.c[c] + 31) >> 5;
-        }
-    }
-    // q~ in 24-bit signed fixed point per (K class, head): three signed 8-bit
-    // digits hi, mid, lo. B n-tiles come in pairs per 4 heads: tile 2*hb holds
-    // columns (hi, mid) of head 4*hb + n/2, tile 2*hb + 1 holds (lo, 0).
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const int nc = h.c[c];
-        if (nc == 0) continue;
-        const int P = (nc + 31) & ~31;
-        for (int hh = 0; hh < 4 * NT; ++hh) {
-            const int nt = hh >> 2, n0 = 2 * (hh & 3);
-            if (hh >= g) {
-                for (int j = lane; j < P; j += 32) {
-                    const int ks = ks_base[c] + (j >> 5);
-                    uint8_t* a0 = w.bq + ((ks * 2 * NT + 2 * nt) * 8) * 32;
-                    uint8_t* a1 = a0 + 8 * 32;
-                    a0[n0 * 32 + (j & 31)] = 0;
-                    a0[(n0 + 1) * 32 + (j & 31)] = 0;
-                    a1[n0 * 32 + (j & 31)] = 0;
-                    a1[(n0 + 1) * 32 + (j & 31)] = 0;
-                }
-                continue;
-            }
-            float mx = 0.0f;
-            for (int j = lane; j < nc; j += 32) {
-                const int s = h.kslot_base[c] + j;
-                mx = fmaxf(mx, fabsf(chan[s].x * ld_io(qs, hh * kD + perm[s])));
-            }
-            mx = warp_max(mx);
-            const float sig = mx > 0.0f ? 8.2e6f / mx : 1.0f;
-            if (lane == 0) w.qsig[c][hh] = sig;
-            for (int j = lane; j < P; j += 32) {
-                int dh = 0, dm = 0, dl = 0;
-                if (j < nc) {
-                    const int s = h.kslot_base[c] + j;
-                    const int N = __float2int_rn(chan[s].x * ld_io(qs, hh * kD + perm[s]) * sig);
-                    dl = ((N + 128) & 255) - 128;
-                    const int N1 = (N - dl) >> 8;
-                    dm = ((N1 + 128) & 255) - 128;
-                    dh = (N1 - dm) >> 8;
-                }
-                const int ks = ks_base[c] + (j >> 5);
-                const int kp = kpos_of_slot(c, j & 31);
-                uint8_t* a0 = w.bq + ((ks * 2 * NT + 2 * nt) * 8) * 32;
-                uint8_t* a1 = a0 + 8 * 32;
-                a0[n0 * 32 + kp] = (uint8_t)(int8_t)dh;
-                a0[(n0 + 1) * 32 + kp] = (uint8_t)(int8_t)dm;
-                a1[n0 * 32 + kp] = (uint8_t)(int8_t)dl;
-                a1[(n0 + 1) * 32 + kp] = 0;
-            }
-        }
-    }
-    __syncwarp();
-
-    // ---------------------------------------------------------------- QK
-    const int mtiles = (nslot + 15) >> 4;
-    float lg[kMaxSlots / 16][2][NT];
-    const uint8_t* krows = t + h.off_k;
     const float inv_sqrt_d = 0.08838834764831845f;  // 1/sqrt(128)
+    int sb[5];
+    sb[0] = 0;
 #pragma unroll
-    for (int mt = 0; mt < kMaxSlots / 16; ++mt) {
+    for (int c = 0; c < 4; ++c) sb[c + 1] = sb[c] + pad4(h.r[c]);
+    const int nslot = sb[4];
+    auto hred_max = [&](float v) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) lg[mt][0][nt] = lg[mt][1][nt] = 0.0f;
+        for (int o = G4; o < 32; o <<= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+        return v;
+    };
+    auto hred_sum = [&](float v) {
+#pragma unroll
+        for (int o = G4; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    };
+
+    // ------------------------------------------------------------ q statistics
+    float qm = 0.0f, bias = 0.0f;
+    if (hv) {
+        for (int ch = tl; ch < kD; ch += TS) qm = fmaxf(qm, fabsf(ld_io(qs, hl * kD + ch)));
+        for (int s = tl; s < h.kslots; s += TS) bias = fmaf(ld_io(qs, hl * kD + perm[s]), chan[s].y, bias);
     }
-#pragma unroll
+    qm = hred_max(qm);
+    bias = hred_sum(bias);
+
+    // ------------------------------------------------------------ q~ digits
+    // N = round(q~ * sigma) in [-2^23, 2^23); the bytes of (N + 0x808080) ^ 0x808080
+    // are its signed base-256 digits lo, mid, hi.
+    int ksb[4];
+    ksb[0] = 0;
+    for (int c = 0; c < 3; ++c) ksb[c + 1] = ksb[c] + ((h.c[c] + 31) >> 5);
     for (int c = 0; c < 3; ++c) {
-        if (h.c[c] == 0) continue;
-        const int nks = (h.c[c] + 31) >> 5;
-        const int kb0 = h.kbyte_base[c];
-        const int step_bytes = 32 * kBits(c) / 8;  // 8 / 16 / 32
-        for (int mt = 0; mt < mtiles; ++mt) {
-            const int r0 = mt * 16 + gid, r1 = r0 + 8;
-            int acc[2 * NT][4];
-#pragma unroll
-            for (int nt = 0; nt < 2 * NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
-            for (int kk = 0; kk < nks; ++kk) {
-                const uint8_t* p0 = krows + (size_t)r0 * h.krow_bytes + kb0 + kk * step_bytes;
-                const uint8_t* p1 = krows + (size_t)r1 * h.krow_bytes + kb0 + kk * step_bytes;
-                uint32_t a[4];
-                if (c == 0) {
-                    const uint2 w0 = lds64(p0), w1 = lds64(p1);
-                    const int sh = 2 * tig;
-                    a[0] = (w0.x >> sh) & 0x03030303u;
-                    a[2] = (w0.y >> sh) & 0x03030303u;
-                    a[1] = (w1.x >> sh) & 0x03030303u;
-                    a[3] = (w1.y >> sh) & 0x03030303u;
-                } else if (c == 1) {
-                    // class regions are 8-byte aligned inside a K row: two 8-byte loads
-                    const uint2 x0 = lds64(p0), y0 = lds64(p0 + 8), x1 = lds64(p1), y1 = lds64(p1 + 8);
-                    const int sh = 4 * (tig & 1);
-                    const uint32_t lo0 = (tig >> 1) ? x0.y : x0.x, hi0 = (tig >> 1) ? y0.y : y0.x;
-                    const uint32_t lo1 = (tig >> 1) ? x1.y : x1.x, hi1 = (tig >> 1) ? y1.y : y1.x;
-                    a[0] = (lo0 >> sh) & 0x0F0F0F0Fu;
-                    a[2] = (hi0 >> sh) & 0x0F0F0F0Fu;
-                    a[1] = (lo1 >> sh) & 0x0F0F0F0Fu;
-                    a[3] = (hi1 >> sh) & 0x0F0F0F0Fu;
-                } else {
-                    a[0] = lds32(p0 + 4 * tig);
-                    a[2] = lds32(p0 + 16 + 4 * tig);
-                    a[1] = lds32(p1 + 4 * tig);
-                    a[3] = lds32(p1 + 16 + 4 * tig);
-                }
-                const int ks = ks_base[c] + kk;
-#pragma unroll
-                for (int nt = 0; nt < 2 * NT; ++nt) {
-                    const uint8_t* bb = w.bq + ((ks * 2 * NT + nt) * 8 + gid) * 32 + 4 * tig;
-                    mma_u8s8(acc[nt], a, lds32(bb), lds32(bb + 16));
-                }
-            }
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                const int hh = nt * 4 + tig;
-                const float inv = hh < g ? 1.0f / w.qsig[c][hh] : 0.0f;
-                const int* A = acc[2 * nt];
-                const int* B = acc[2 * nt + 1];
-                const float v0 = fmaf((float)A[0], 65536.0f, fmaf((float)A[1], 256.0f, (float)B[0])) * inv;
-                const float v1 = fmaf((float)A[2], 65536.0f, fmaf((float)A[3], 256.0f, (float)B[2])) * inv;
-#pragma unroll
-                for (int m = 0; m < kMaxSlots / 16; ++m)
-                    if (m == mt) {
-                        lg[m][0][nt] += v0;
-                        lg[m][1][nt] += v1;
-                    }
-            }
-        }
-    }
-    // k16 channels (fp16 K columns), finalize logits and mask pads
-    const int c16 = h.c[3];
-    float mrun[NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) mrun[nt] = -INFINITY;
-#pragma unroll
-    for (int mt = 0; mt < kMaxSlots / 16; ++mt) {
-        if (mt >= mtiles) break;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int s = mt * 16 + gid + 8 * half;
-            int cls = 0;
-            while (cls < 3 && s >= sbase[cls + 1]) ++cls;
-            const bool valid = s < nslot && (s - sbase[cls]) < h.r[cls];
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                const int hh = nt * 4 + tig;
-                float v = lg[mt][half][nt];
-                if (c16 && valid && hh < g) {
-                    const __half* kr = reinterpret_cast<const __half*>(krows + (size_t)s * h.krow_bytes + h.kbyte_base[3]);
-                    for (int j = 0; j < c16; ++j)
-                        v = fmaf(ld_io(qs, hh * kD + perm[h.kslot_base[3] + j]), __half2float(kr[j]), v);
-                }
-                v = (valid && hh < g) ? (v + bias[nt]) * inv_sqrt_d : -INFINITY;
-                lg[mt][half][nt] = v;
-                mrun[nt] = fmaxf(mrun[nt], v);
-            }
-        }
-    }
-    // Zone C logits (CUDA cores): lane-per-token, all heads
-    for (int i = lane; i < nzc; i += 32) {
-        const __half* kr = zck + (size_t)i * kD;
-        float a8[8];
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh) a8[hh] = 0.0f;
-        for (int c0 = 0; c0 < kD; c0 += 8) {
-            const uint4 raw = *reinterpret_cast<const uint4*>(kr + c0);
-            const __half2* hp = reinterpret_cast<const __half2*>(&raw);
+        const int nk = ksb[c + 1] - ksb[c];
+        if (nk == 0) continue;
+        float sm = 0.0f;
+        for (int j = lane; j < h.c[c]; j += 32) sm = fmaxf(sm, fabsf(chan[h.kslot_base[c] + j].x));
+        sm = warp_max(sm);
+        const float bnd = sm * qm;
+        const float sg = bnd > 0.0f ? 8.2e6f * __frcp_rn(bnd) : 0.0f;
+        if (tl == 0) sh.qinv[c][hl] = bnd * (1.0f / 8.2e6f);
+        const int ntask = nk * G4 * 8;  // task = (head hl, 4 K positions k4, k-step kk)
+        for (int i = lane; i < ntask; i += 32) {
+            const int k4 = (i / G4) & 7, kk = i / (8 * G4);
+            uint32_t x[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const float2 kv = __half22float2(hp[e]);
-#pragma unroll
-                for (int hh = 0; hh < 4 * NT; ++hh)
-                    if (hh < g)
-                        a8[hh] = fmaf(ld_io(qs, hh * kD + c0 + 2 * e), kv.x,
-                                      fmaf(ld_io(qs, hh * kD + c0 + 2 * e + 1), kv.y, a8[hh]));
-            }
-        }
-#pragma unroll
-        for (int hh = 0; hh < 4 * NT; ++hh)
-            if (hh < g) w.zl[hh * kMaxZc + i] = a8[hh] * inv_sqrt_d;
-    }
-    __syncwarp();
-    // running max over slots (8 lanes share a head) and Zone C
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        float m = mrun[nt];
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
-        const int hh = nt * 4 + tig;
-        if (hh < g)
-            for (int i = 0; i < nzc; ++i) m = fmaxf(m, w.zl[hh * kMaxZc + i]);
-        mrun[nt] = m;
-    }
-
-    // ---------------------------------------------------------------- softmax
-    float lsum[NT], bv[NT], pmax[3][NT];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        lsum[nt] = 0.0f;
-        bv[nt] = 0.0f;
-        pmax[0][nt] = pmax[1][nt] = pmax[2][nt] = 0.0f;
-    }
-#pragma unroll
-    for (int mt = 0; mt < kMaxSlots / 16; ++mt) {
-        if (mt >= mtiles) break;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int s = mt * 16 + gid + 8 * half;
-            int cls = 0;
-            while (cls < 3 && s >= sbase[cls + 1]) ++cls;
-            const float2 vp = s < nslot ? vparam[s] : make_float2(0.0f, 0.0f);
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                const float l = lg[mt][half][nt];
-                const float p = l == -INFINITY ? 0.0f : __expf(l - mrun[nt]);
-                lsum[nt] += p;
-                if (cls < 3) {
-                    const float pt = p * vp.x;
-                    bv[nt] = fmaf(p, vp.y, bv[nt]);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-                        if (c == cls) pmax[c][nt] = fmaxf(pmax[c][nt], pt);
-                    lg[mt][half][nt] = pt;  // now p~ (scaled by vscale)
-                } else {
-                    const int li = s - sbase[3];
-                    const int hh = nt * 4 + tig;
-                    if (hh < g && li < 64) w.p16[hh * 64 + li] = p;
-                    lg[mt][half][nt] = 0.0f;
+                const int j = kk * 32 + slot_of_kpos(c, 4 * k4 + e);
+                int N = 0;
+                if (hv && j < h.c[c]) {
+                    const int s = h.kslot_base[c] + j;
+                    N = __float2int_rn(chan[s].x * ld_io(qs, hl * kD + perm[s]) * sg);
                 }
+                x[e] = (uint32_t)(N + 0x808080) ^ 0x808080u;
             }
+            const uint32_t wlo = __byte_perm(__byte_perm(x[0], x[1], 0x0040), __byte_perm(x[2], x[3], 0x0040), 0x5410);
+            const uint32_t wmid = __byte_perm(__byte_perm(x[0], x[1], 0x0051), __byte_perm(x[2], x[3], 0x0051), 0x5410);
+            const uint32_t whi = __byte_perm(__byte_perm(x[0], x[1], 0x0062), __byte_perm(x[2], x[3], 0x0062), 0x5410);
+            const int ks = ksb[c] + kk;
+            uint8_t* a0 = dig + ((ks * 2 * NT + 2 * (hl >> 2)) * 8 + 2 * (hl & 3)) * 32 + 4 * k4;
+            *reinterpret_cast<uint32_t*>(a0) = whi;
+            *reinterpret_cast<uint32_t*>(a0 + 32) = wmid;
+            *reinterpret_cast<uint32_t*>(a0 + 8 * 32) = wlo;
+            *reinterpret_cast<uint32_t*>(a0 + 8 * 32 + 32) = 0u;
         }
     }
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-            lsum[nt] += __shfl_xor_sync(0xffffffffu, lsum[nt], o);
-            bv[nt] += __shfl_xor_sync(0xffffffffu, bv[nt], o);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) pmax[c][nt] = fmaxf(pmax[c][nt], __shfl_xor_sync(0xffffffffu, pmax[c][nt], o));
-        }
-    }
-    // broadcast per-head max to all lanes for Zone C (head hh lives in lane hh&3, n-tile hh>>2)
-    float mh[8], lzc[8];
-#pragma unroll
-    for (int hh = 0; hh < 8; ++hh) {
-        float m = 0.0f;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const float v = __shfl_sync(0xffffffffu, mrun[nt], hh & 3);
-            if ((hh >> 2) == nt) m = v;
-        }
-        mh[hh] = m;
-        lzc[hh] = 0.0f;
-    }
-    for (int i = lane; i < nzc; i += 32) {
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh)
-            if (hh < g) {
-                const float p = __expf(w.zl[hh * kMaxZc + i] - mh[hh]);
-                w.zl[hh * kMaxZc + i] = p;
-                lzc[hh] += p;
-            }
-    }
-#pragma unroll
-    for (int hh = 0; hh < 8; ++hh) lzc[hh] = warp_sum(lzc[hh]);
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-        float z = 0.0f;
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh)
-            if (hh == nt * 4 + tig) z = lzc[hh];
-        lsum[nt] += z;
-    }
-
-    // p~ digits (unsigned 16-bit fixed point per (V class, head))
-    float psig[3][NT];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) psig[c][nt] = pmax[c][nt] > 0.0f ? 1.6e7f / pmax[c][nt] : 0.0f;
-    // zero the B-digit area of every V class k-step (tails of the last step)
-    int vks[3], vks_base[3];
-    {
-        int acc = 0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            vks[c] = (pad4(h.r[c]) + 31) >> 5;
-            vks_base[c] = acc;
-            acc += vks[c];
-        }
-        uint4* z = reinterpret_cast<uint4*>(w.bp);
-        const int n16 = acc * 2 * NT * 8 * 32 / 16;
-        for (int i = lane; i < n16; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    if (ksb[3] == 0) {  // every K channel removed: logits are the bias alone
+        for (int s = tl; s < nslot; s += TS) lgs[hl * LS + s] = 0.0f;
     }
     __syncwarp();
-#pragma unroll
-    for (int mt = 0; mt < kMaxSlots / 16; ++mt) {
-        if (mt >= mtiles) break;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            const int s = mt * 16 + gid + 8 * half;
-            if (s >= sbase[3]) continue;
-            int cls = 0;
-            while (cls < 2 && s >= sbase[cls + 1]) ++cls;
-            const int li = s - sbase[cls];
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                float sg = 0.0f;
-#pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    if (c == cls) sg = psig[c][nt];
-                const int N = __float2int_rn(lg[mt][half][nt] * sg);
-                const int ks = vks_base[cls] + (li >> 5);
-                uint8_t* base = w.bp + ((ks * 2 * NT + 2 * nt) * 8 + 2 * tig) * 32 + (li & 31);
-                base[0] = (uint8_t)(N >> 16);            // tile 2nt,   column 2tig   : hi
-                base[32] = (uint8_t)((N >> 8) & 255);    // tile 2nt,   column 2tig+1 : mid
-                base[8 * 32] = (uint8_t)(N & 255);       // tile 2nt+1, column 2tig   : lo
-            }
-        }
-    }
-    // publish per-head sigma for the PV combine (lane tig owns head nt*4+tig)
-    if (gid == 0) {
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) w.sig[c][nt * 4 + tig] = psig[c][nt];
-    }
-    // zero the accumulator
-    for (int i = lane; i < 8 * kD / 4; i += 32) reinterpret_cast<float4*>(w.acc)[i] = make_float4(0, 0, 0, 0);
-    __syncwarp();
 
-    // ---------------------------------------------------------------- PV
-#pragma unroll
+    // ------------------------------------------------------------ QK (tensor cores)
+    const uint8_t* krows = t + h.off_k;
+    const int krb = h.krow_bytes;
+    bool first = true;
     for (int c = 0; c < 3; ++c) {
-        if (h.r[c] == 0) continue;
-        const int rb = kD * kBits(c) / 8;  // packed row bytes at d = 128
-        const uint8_t* vbase = t + h.off_vseg[c];
-        for (int mt = 0; mt < kD / 16; ++mt) {
-            int acc[2 * NT][4];
+        const int nk = ksb[c + 1] - ksb[c];
+        if (nk == 0) continue;
+        uint32_t b[4][2 * NT][2];
 #pragma unroll
-            for (int nt = 0; nt < 2 * NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
-            int ch0, ch1;
-            for (int kk = 0; kk < vks[c]; ++kk) {
-                const int gr0 = kk * 8 + tig, gr1 = gr0 + 4;  // token groups of this k-step
-                uint32_t a[4];
-                if (c == 0) {
-                    const int m = 4 * mt + (gid & 3);
-                    const uint32_t w0 = lds32(vbase + gr0 * 4 * rb + m * 4);
-                    const uint32_t w1 = lds32(vbase + gr1 * 4 * rb + m * 4);
-                    const int j0 = gid >> 2;
-                    a[0] = (w0 >> (2 * j0)) & 0x03030303u;
-                    a[1] = (w0 >> (2 * j0 + 4)) & 0x03030303u;
-                    a[2] = (w1 >> (2 * j0)) & 0x03030303u;
-                    a[3] = (w1 >> (2 * j0 + 4)) & 0x03030303u;
-                } else if (c == 1) {
-                    const int m = 8 * mt + gid;
-                    const uint32_t w0 = lds32(vbase + gr0 * 4 * rb + m * 4);
-                    const uint32_t w1 = lds32(vbase + gr1 * 4 * rb + m * 4);
-                    a[0] = w0 & 0x0F0F0F0Fu;
-                    a[1] = (w0 >> 4) & 0x0F0F0F0Fu;
-                    a[2] = w1 & 0x0F0F0F0Fu;
-                    a[3] = (w1 >> 4) & 0x0F0F0F0Fu;
-                } else {
-                    const int m0 = 16 * mt + gid, m1 = m0 + 8;
-                    a[0] = lds32(vbase + gr0 * 4 * rb + m0 * 4);
-                    a[1] = lds32(vbase + gr0 * 4 * rb + m1 * 4);
-                    a[2] = lds32(vbase + gr1 * 4 * rb + m0 * 4);
-                    a[3] = lds32(vbase + gr1 * 4 * rb + m1 * 4);
-                }
-                const int ks = vks_base[c] + kk;
+        for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-                for (int nt = 0; nt < 2 * NT; ++nt) {
-                    const uint8_t* bb = w.bp + ((ks * 2 * NT + nt) * 8 + gid) * 32 + 4 * tig;
-                    mma_u8u8(acc[nt], a, lds32(bb), lds32(bb + 16));
+            for (int nt = 0; nt < 2 * NT; ++nt) {
+                const uint8_t* bb = dig + (((ksb[c] + kk) * 2 * NT + nt) * 8 + gid) * 32 + 4 * tig;
+                b[kk][nt][0] = kk < nk ? lds32(bb) : 0u;
+                b[kk][nt][1] = kk < nk ? lds32(bb + 16) : 0u;
+            }
+        float qinv[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) qinv[nt] = sh.qinv[c][nt * 4 + tig];
+        const int kb0 = h.kbyte_base[c];
+        // two m-tiles (32 token slots) per iteration for independent MMA chains
+        for (int mt = 0; mt * 16 < nslot; mt += 2) {
+            const bool two = (mt + 1) * 16 < nslot;
+            int acc[2][2 * NT][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int nt = 0; nt < 2 * NT; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                if (kk < nk) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        if (u == 1 && !two) continue;
+                        const uint8_t* p0 = krows + (size_t)((mt + u) * 16 + gid) * krb + kb0;
+                        const uint8_t* p1 = p0 + 8 * krb;
+                        uint32_t a[4];
+                        if (c == 0) {
+                            const uint2 w0 = lds64(p0 + 8 * kk), w1 = lds64(p1 + 8 * kk);
+                            const int s = 2 * tig;
+                            a[0] = (w0.x >> s) & 0x03030303u;
+                            a[2] = (w0.y >> s) & 0x03030303u;
+                            a[1] = (w1.x >> s) & 0x03030303u;
+                            a[3] = (w1.y >> s) & 0x03030303u;
+                        } else if (c == 1) {
+                            const int o = 16 * kk + 4 * (tig >> 1);
+                            const int s = 4 * (tig & 1);
+                            a[0] = (lds32(p0 + o) >> s) & 0x0F0F0F0Fu;
+                            a[2] = (lds32(p0 + o + 8) >> s) & 0x0F0F0F0Fu;
+                            a[1] = (lds32(p1 + o) >> s) & 0x0F0F0F0Fu;
+                            a[3] = (lds32(p1 + o + 8) >> s) & 0x0F0F0F0Fu;
+                        } else {
+                            const int o = 32 * kk + 4 * tig;
+                            a[0] = lds32(p0 + o);
+                            a[2] = lds32(p0 + o + 16);
+                            a[1] = lds32(p1 + o);
+                            a[3] = lds32(p1 + o + 16);
+                        }
+#pragma unroll
+                        for (int nt = 0; nt < 2 * NT; ++nt) mma_u8s8(acc[u][nt], a, b[kk][nt][0], b[kk][nt][1]);
+                    }
                 }
             }
-            if (c == 0) {
-                ch0 = 4 * (4 * mt + (gid & 3)) + (gid >> 2);
-                ch1 = ch0 + 2;
-            } else if (c == 1) {
-                ch0 = 2 * (8 * mt + gid);
-                ch1 = ch0 + 1;
-            } else {
-                ch0 = 16 * mt + gid;
-                ch1 = ch0 + 8;
-            }
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                const int hh = nt * 4 + tig;
-                if (hh >= g) continue;
-                const float sg = w.sig[c][hh];
-                const float inv = sg > 0.0f ? 1.0f / sg : 0.0f;
-                const int* A = acc[2 * nt];
-                const int* B = acc[2 * nt + 1];
-                w.acc[hh * kD + ch0] += fmaf((float)A[0], 65536.0f, fmaf((float)A[1], 256.0f, (float)B[0])) * inv;
-                w.acc[hh * kD + ch1] += fmaf((float)A[2], 65536.0f, fmaf((float)A[3], 256.0f, (float)B[2])) * inv;
+            for (int u = 0; u < 2; ++u) {
+                if (u == 1 && !two) continue;
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const int* A = acc[u][2 * nt];
+                    const int* B = acc[u][2 * nt + 1];
+                    float* row = lgs + (nt * 4 + tig) * LS + (mt + u) * 16 + gid;
+                    const float v0 = fmaf((float)A[0], 65536.0f, fmaf((float)A[1], 256.0f, (float)B[0])) * qinv[nt];
+                    const float v1 = fmaf((float)A[2], 65536.0f, fmaf((float)A[3], 256.0f, (float)B[2])) * qinv[nt];
+                    row[0] = first ? v0 : row[0] + v0;
+                    row[8] = first ? v1 : row[8] + v1;
+                }
             }
         }
+        first = false;
         __syncwarp();
     }
 
-    // ---------------------------------------------------------------- Zone B + Zone C + output
-    // lane owns channels 4*lane .. 4*lane+3 for every head
-    float o[8][4];
-#pragma unroll
-    for (int hh = 0; hh < 8; ++hh)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) o[hh][e] = 0.0f;
-    const int r16 = min(h.r[3], 64);
-    const __half* zb = reinterpret_cast<const __half*>(t + h.off_vseg[3]);
-    for (int li = 0; li < r16; ++li) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(zb + (size_t)li * kD + 4 * lane);
-        const __half2* hp = reinterpret_cast<const __half2*>(&raw);
-        const float2 v01 = __half22float2(hp[0]), v23 = __half22float2(hp[1]);
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh)
-            if (hh < g) {
-                const float p = w.p16[hh * 64 + li];
-                o[hh][0] = fmaf(p, v01.x, o[hh][0]);
-                o[hh][1] = fmaf(p, v01.y, o[hh][1]);
-                o[hh][2] = fmaf(p, v23.x, o[hh][2]);
-                o[hh][3] = fmaf(p, v23.y, o[hh][3]);
+    // ------------------------------------------------------------ logits + max (per class, no pads)
+    const int c16 = h.c[3];
+    float mx = -INFINITY;
+    float vsm[3] = {0.0f, 0.0f, 0.0f};  // max V scale per class (bounds p~ = p * vscale <= vscale)
+    for (int c = 0; c < 4; ++c) {
+        const int s1 = sb[c] + h.r[c];
+        for (int s = sb[c] + tl; s < s1; s += TS) {
+            if (c < 3) {
+                const float vs = vparam[s].x;
+                vsm[0] = c == 0 ? fmaxf(vsm[0], vs) : vsm[0];
+                vsm[1] = c == 1 ? fmaxf(vsm[1], vs) : vsm[1];
+                vsm[2] = c == 2 ? fmaxf(vsm[2], vs) : vsm[2];
             }
-    }
-    for (int i = 0; i < nzc; ++i) {
-        const uint2 raw = *reinterpret_cast<const uint2*>(zcv + (size_t)i * kD + 4 * lane);
-        const __half2* hp = reinterpret_cast<const __half2*>(&raw);
-        const float2 v01 = __half22float2(hp[0]), v23 = __half22float2(hp[1]);
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh)
-            if (hh < g) {
-                const float p = w.zl[hh * kMaxZc + i];
-                o[hh][0] = fmaf(p, v01.x, o[hh][0]);
-                o[hh][1] = fmaf(p, v01.y, o[hh][1]);
-                o[hh][2] = fmaf(p, v23.x, o[hh][2]);
-                o[hh][3] = fmaf(p, v23.y, o[hh][3]);
+            if (!hv) continue;
+            float v = lgs[hl * LS + s];
+            if (c16) {
+                const __half* kr = reinterpret_cast<const __half*>(krows + (size_t)s * krb + h.kbyte_base[3]);
+                for (int j = 0; j < c16; ++j)
+                    v = fmaf(ld_io(qs, hl * kD + perm[h.kslot_base[3] + j]), __half2float(kr[j]), v);
             }
+            v = (v + bias) * inv_sqrt_d;
+            lgs[hl * LS + s] = v;
+            mx = fmaxf(mx, v);
+        }
     }
-    // per-head normaliser and V offset term, broadcast from lane (hh & 3)
+    if (nzc > 0) {  // Zone C logits on CUDA cores: lane per appended token, every head
+        for (int i = lane; i < nzc; i += 32) {
+            const __half* kr = zck + (size_t)i * kD;
+            float a8[G4];
 #pragma unroll
-    for (int hh = 0; hh < 8; ++hh) {
-        if (hh >= g) break;
-        float l = 0.0f, b = 0.0f;
+            for (int hh = 0; hh < G4; ++hh) a8[hh] = 0.0f;
+            for (int c0 = 0; c0 < kD; c0 += 8) {
+                const uint4 raw = *reinterpret_cast<const uint4*>(kr + c0);
+                const __half2* hp = reinterpret_cast<const __half2*>(&raw);
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            const float lv = __shfl_sync(0xffffffffu, lsum[nt], hh & 3);
-            const float bb = __shfl_sync(0xffffffffu, bv[nt], hh & 3);
-            if ((hh >> 2) == nt) {
-                l = lv;
-                b = bb;
+                for (int e = 0; e < 4; ++e) {
+                    const float2 kv = __half22float2(hp[e]);
+#pragma unroll
+                    for (int hh = 0; hh < G4; ++hh)
+                        if (hh < g)
+                            a8[hh] = fmaf(ld_io(qs, hh * kD + c0 + 2 * e), kv.x,
+                                          fmaf(ld_io(qs, hh * kD + c0 + 2 * e + 1), kv.y, a8[hh]));
+                }
+            }
+#pragma unroll
+            for (int hh = 0; hh < G4; ++hh)
+                if (hh < g) zl[hh * prm.zc_cap + i] = a8[hh] * inv_sqrt_d;
+        }
+        __syncwarp();
+        if (hv)
+            for (int i = tl; i < nzc; i += TS) mx = fmaxf(mx, zl[hl * prm.zc_cap + i]);
+    }
+    mx = hred_max(mx);
+    float psig[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        vsm[c] = hred_max(vsm[c]);
+        psig[c] = vsm[c] > 0.0f ? 1.6e7f * __frcp_rn(vsm[c]) : 0.0f;
+        if (lane == 0) sh.vinv[c][0] = vsm[c] * (1.0f / 1.6e7f);
+    }
+    int vksb[4];
+    vksb[0] = 0;
+    for (int c = 0; c < 3; ++c) vksb[c + 1] = vksb[c] + ((pad4(h.r[c]) + 31) >> 5);
+    {
+        uint4* z = reinterpret_cast<uint4*>(dig);
+        const int n16 = vksb[3] * 2 * NT * 8 * 32 / 16;
+        for (int i = lane; i < n16; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+
+    // ------------------------------------------------------------ softmax + p~ digits (per class)
+    float lsum = 0.0f, bv = 0.0f;
+    if (hv) {
+        for (int c = 0; c < 4; ++c) {
+            const int s0 = sb[c], s1 = sb[c] + h.r[c];
+            const float sg = c == 0 ? psig[0] : c == 1 ? psig[1] : psig[2];
+            for (int s = s0 + tl; s < s1; s += TS) {
+                const float p = __expf(lgs[hl * LS + s] - mx);
+                lsum += p;
+                const int li = s - s0;
+                if (c < 3) {
+                    const float2 vp = vparam[s];
+                    bv = fmaf(p, vp.y, bv);
+                    const int N = __float2int_rn(p * vp.x * sg);
+                    const int ks = vksb[c] + (li >> 5);
+                    uint8_t* base = dig + ((ks * 2 * NT + 2 * (hl >> 2)) * 8 + 2 * (hl & 3)) * 32 + (li & 31);
+                    base[0] = (uint8_t)(N >> 16);          // tile 2nt,   column 2(h%4)   : hi
+                    base[32] = (uint8_t)((N >> 8) & 255);  // tile 2nt,   column 2(h%4)+1 : mid
+                    base[8 * 32] = (uint8_t)(N & 255);     // tile 2nt+1, column 2(h%4)   : lo
+                } else if (li < prm.max_r16) {
+                    p16[hl * prm.max_r16 + li] = p;
+                }
             }
         }
-        const float inv = 1.0f / l;
-        const float4 a4 = reinterpret_cast<const float4*>(w.acc + hh * kD)[lane];
-        const float r0 = (a4.x + o[hh][0] + b) * inv;
-        const float r1 = (a4.y + o[hh][1] + b) * inv;
-        const float r2 = (a4.z + o[hh][2] + b) * inv;
-        const float r3 = (a4.w + o[hh][3] + b) * inv;
+        for (int i = tl; i < nzc; i += TS) {
+            const float p = __expf(zl[hl * prm.zc_cap + i] - mx);
+            zl[hl * prm.zc_cap + i] = p;
+            lsum += p;
+        }
+    }
+    lsum = hred_sum(lsum);
+    bv = hred_sum(bv);
+    __syncwarp();
+
+    // ------------------------------------------------------------ PV (tensor cores)
+    // row r of channel m-tile mt is channel 16*mt + r for every V class; the
+    // accumulators reuse the logit area: acc [G4][kD]
+    float* acc_s = lgs;
+    first = true;
+    for (int c = 0; c < 3; ++c) {
+        if (h.r[c] == 0) continue;
+        const int nv = vksb[c + 1] - vksb[c];
+        const float vinv = sh.vinv[c][0];
+        const int bits = 2 << c;
+        const int rb = kD * bits / 8;  // packed bytes per V row (multiple of 32 at d=128)
+        const uint8_t* vbase = t + h.off_vseg[c];
+        int m0, m1, shf;
+        if (c == 0) {
+            m0 = gid >> 2;
+            m1 = m0 + 2;
+            shf = 2 * (gid & 3);
+        } else if (c == 1) {
+            m0 = gid >> 1;
+            m1 = m0 + 4;
+            shf = 4 * (gid & 1);
+        } else {
+            m0 = gid;
+            m1 = gid + 8;
+            shf = 0;
+        }
+        const uint32_t mask = c == 0 ? 0x03030303u : c == 1 ? 0x0F0F0F0Fu : 0xFFFFFFFFu;
+        const int mstep = 2 * bits;  // byte columns per 16-channel m-tile
+        const int swz = 8 * tig;     // vswz: token groups kk*8+tig and +4 have (G & 3) == tig
+        for (int mt = 0; mt < kD / 16; mt += 2) {
+            int acc[2][2 * NT][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int nt = 0; nt < 2 * NT; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
+            for (int kk = 0; kk < nv; ++kk) {
+                const uint8_t* g0 = vbase + (size_t)(kk * 8 + tig) * 4 * rb;
+                const uint8_t* g1 = g0 + (size_t)16 * rb;  // token group + 4
+                const uint8_t* bb = dig + ((vksb[c] + kk) * 2 * NT * 8 + gid) * 32 + 4 * tig;
+                uint32_t bq[2 * NT][2];
+#pragma unroll
+                for (int nt = 0; nt < 2 * NT; ++nt) {
+                    bq[nt][0] = lds32(bb + nt * 256);
+                    bq[nt][1] = lds32(bb + nt * 256 + 16);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int col0 = (((mt + u) * mstep + m0) ^ swz) * 4;
+                    const int col1 = (((mt + u) * mstep + m1) ^ swz) * 4;
+                    uint32_t a[4];
+                    a[0] = (lds32(g0 + col0) >> shf) & mask;
+                    a[1] = (lds32(g0 + col1) >> shf) & mask;
+                    a[2] = (lds32(g1 + col0) >> shf) & mask;
+                    a[3] = (lds32(g1 + col1) >> shf) & mask;
+#pragma unroll
+                    for (int nt = 0; nt < 2 * NT; ++nt) mma_u8u8(acc[u][nt], a, bq[nt][0], bq[nt][1]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const int* A = acc[u][2 * nt];
+                    const int* B = acc[u][2 * nt + 1];
+                    float* row = acc_s + (nt * 4 + tig) * kD + 16 * (mt + u) + gid;
+                    const float v0 = fmaf((float)A[0], 65536.0f, fmaf((float)A[1], 256.0f, (float)B[0])) * vinv;
+                    const float v1 = fmaf((float)A[2], 65536.0f, fmaf((float)A[3], 256.0f, (float)B[2])) * vinv;
+                    row[0] = first ? v0 : row[0] + v0;
+                    row[8] = first ? v1 : row[8] + v1;
+                }
+        }
+        first = false;
+        __syncwarp();
+    }
+    if (first) {  // no quantised V rows (Zone B / Zone C only)
+        for (int i = lane; i < G4 * kD / 4; i += 32) reinterpret_cast<float4*>(acc_s)[i] = make_float4(0, 0, 0, 0);
+        __syncwarp();
+    }
+
+    // ------------------------------------------------------------ Zone B / C rows + output
+    // lane owns channels 4*lane .. 4*lane+3 of every head
+    const int r16 = h.r[3];
+    const __half* zb = reinterpret_cast<const __half*>(t + h.off_vseg[3]);
+#pragma unroll
+    for (int hh = 0; hh < G4; ++hh) {
+        if (hh >= g) continue;
+        float4 o = reinterpret_cast<const float4*>(acc_s + hh * kD)[lane];
+        for (int li = 0; li < r16 + nzc; ++li) {
+            const __half* row = li < r16 ? zb + (size_t)li * kD : zcv + (size_t)(li - r16) * kD;
+            const float p = li < r16 ? p16[hh * prm.max_r16 + li] : zl[hh * prm.zc_cap + (li - r16)];
+            const uint2 raw = *reinterpret_cast<const uint2*>(row + 4 * lane);
+            const __half2* hp = reinterpret_cast<const __half2*>(&raw);
+            const float2 v01 = __half22float2(hp[0]), v23 = __half22float2(hp[1]);
+            o.x = fmaf(p, v01.x, o.x);
+            o.y = fmaf(p, v01.y, o.y);
+            o.z = fmaf(p, v23.x, o.z);
+            o.w = fmaf(p, v23.y, o.w);
+        }
+        const float inv = __frcp_rn(__shfl_sync(0xffffffffu, lsum, hh));
+        const float b = __shfl_sync(0xffffffffu, bv, hh);
+        const float r0 = (o.x + b) * inv, r1 = (o.y + b) * inv, r2 = (o.z + b) * inv, r3 = (o.w + b) * inv;
         if constexpr (sizeof(IO) == 2) {
-            __half2 p0 = __floats2half2_rn(r0, r1), p1 = __floats2half2_rn(r2, r3);
+            __half2 h0 = __floats2half2_rn(r0, r1), h1 = __floats2half2_rn(r2, r3);
             uint2 st;
-            st.x = *reinterpret_cast<uint32_t*>(&p0);
-            st.y = *reinterpret_cast<uint32_t*>(&p1);
+            st.x = *reinterpret_cast<uint32_t*>(&h0);
+            st.y = *reinterpret_cast<uint32_t*>(&h1);
             reinterpret_cast<uint2*>(out + hh * kD)[lane] = st;
         } else {
             reinterpret_cast<float4*>(out + hh * kD)[lane] = make_float4(r0, r1, r2, r3);
         }
     }
-    __syncwarp();
 }
 
-template <int NT, typename IO>
-__global__ void __launch_bounds__(256, 1) decode_mma_kernel(
-    const uint8_t* __restrict__ arena, const int64_t* __restrict__ offsets, const int32_t* __restrict__ dsize,
-    int units, int g, const IO* __restrict__ q_all, IO* __restrict__ out_all, const __half* __restrict__ zc_k,
-    const __half* __restrict__ zc_v, const int32_t* __restrict__ zc_len, int zc_cap, int stage_bytes,
-    int nstage) {
-    extern __shared__ __align__(128) uint8_t dsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nwarps = blockDim.x >> 5;
-    const size_t per_warp = (size_t)nstage * stage_bytes + ((sizeof(WarpSmem) + 127) & ~size_t(127));
-    uint8_t* mine = dsm + per_warp * warp;
-    WarpSmem& w = *reinterpret_cast<WarpSmem*>(mine + (size_t)nstage * stage_bytes);
-    const int qbytes = g * kD * (int)sizeof(IO);
-    const int worker = blockIdx.x * nwarps + warp;
-    const int nworkers = gridDim.x * nwarps;
-    if (lane == 0) {
-        for (int s = 0; s < nstage; ++s) mbar_init(&w.bar[s], 1);
-        fence_barrier_init();
+// ---------------------------------------------------------------------------
+// Uniform 2-bit tiles: every kept V row and every K channel at 2 bits, no
+// Zone B / k16 / Zone C (the n=128 production shape). Same math as
+// decode_tile with the class logic folded away, the PV fragments built from
+// shared words (one 32-bit word feeds rows gid and gid+8) and the B operands
+// fetched with ldmatrix.
+constexpr int kU2MaxSlots = 160;
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+
+template <typename IO>
+__device__ __noinline__ void decode_tile_u2(const uint8_t* __restrict__ t, const IO* __restrict__ qs, int g,
+                                            uint8_t* __restrict__ scr, const MmaParams& prm,
+                                            IO* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int hl = lane & 3, tl = lane >> 2;  // per-head phases: head hl, tokens tl + 8i
+    const bool hv = hl < g;
+    const TileHeader& h = *reinterpret_cast<const TileHeader*>(t);
+    uint8_t* dig = scr + kDigitBytesOff;
+    const int LS = prm.lg_stride;
+    float* lgs = reinterpret_cast<float*>(scr + prm.off_lg);
+    const float2* chan = reinterpret_cast<const float2*>(t + kHeaderBytes);
+    const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
+    const float2* vparam = reinterpret_cast<const float2*>(t + h.off_vp);
+    const uint8_t* krows = t + h.off_k;
+    const uint8_t* vbase = t + h.off_vseg[0];
+    const int n = h.r[0];
+    const int nslot = pad4(n);
+    const int c0 = h.c[0];
+    const int nk = (c0 + 31) >> 5;
+    const int kslots = h.kslots;
+    const int krb = h.krow_bytes;
+    const float inv_sqrt_d = 0.08838834764831845f;  // 1/sqrt(128)
+
+    // ------------------------------------------------------------ q statistics
+    float qm = 0.0f, bias = 0.0f, sm = 0.0f;
+    if (hv) {
+#pragma unroll
+        for (int i = 0; i < kD / 8; ++i) qm = fmaxf(qm, fabsf(ld_io(qs, hl * kD + tl + 8 * i)));
+        for (int s = tl; s < kslots; s += 8) bias = fmaf(ld_io(qs, hl * kD + perm[s]), chan[s].y, bias);
+    }
+    for (int j = lane; j < c0; j += 32) sm = fmaxf(sm, fabsf(chan[j].x));
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+        bias += __shfl_xor_sync(0xffffffffu, bias, o);
+    }
+    sm = warp_max(sm);
+    const float bnd = sm * qm;
+    const float sg = bnd > 0.0f ? 8.2e6f * __frcp_rn(bnd) : 0.0f;
+    const float qinv_own = bnd * (1.0f / 8.2e6f);  // for head hl; QK needs head tig == hl
+    // ------------------------------------------------------------ q~ digits
+    // task (k-step kk, K positions 4*tl .. 4*tl+3, head hl): slot 16*(tl>>2) + 4e + (tl&3)
+    for (int kk = 0; kk < nk; ++kk) {
+        uint32_t x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = kk * 32 + 16 * (tl >> 2) + 4 * e + (tl & 3);
+            int N = 0;
+            if (hv && j < c0) N = __float2int_rn(chan[j].x * ld_io(qs, hl * kD + perm[j]) * sg);
+            x[e] = (uint32_t)(N + 0x808080) ^ 0x808080u;
+        }
+        const uint32_t wlo = __byte_perm(__byte_perm(x[0], x[1], 0x0040), __byte_perm(x[2], x[3], 0x0040), 0x5410);
+        const uint32_t wmid = __byte_perm(__byte_perm(x[0], x[1], 0x0051), __byte_perm(x[2], x[3], 0x0051), 0x5410);
+        const uint32_t whi = __byte_perm(__byte_perm(x[0], x[1], 0x0062), __byte_perm(x[2], x[3], 0x0062), 0x5410);
+        uint8_t* a0 = dig + ((kk * 2) * 8 + 2 * hl) * 32 + 4 * tl;
+        *reinterpret_cast<uint32_t*>(a0) = whi;
+        *reinterpret_cast<uint32_t*>(a0 + 32) = wmid;
+        *reinterpret_cast<uint32_t*>(a0 + 8 * 32) = wlo;
+        *reinterpret_cast<uint32_t*>(a0 + 8 * 32 + 32) = 0u;
     }
     __syncwarp();
-    // prologue: issue the first nstage tiles
-    if (lane == 0) {
-        for (int s = 0; s < nstage; ++s) {
-            const int tile = worker + s * nworkers;
-            if (tile >= units) break;
-            uint8_t* st = mine + (size_t)s * stage_bytes;
-            const uint32_t tb = (uint32_t)dsize[tile];
-            mbar_expect_tx(&w.bar[s], tb + qbytes);
-            bulk_g2s(st, arena + offsets[tile], tb, &w.bar[s]);
-            bulk_g2s(st + stage_bytes - qbytes, q_all + (size_t)tile * g * kD, qbytes, &w.bar[s]);
+
+    // ------------------------------------------------------------ QK (tensor cores)
+    uint32_t bq[4][4];  // per k-step: n-tile 0 (b0, b1), n-tile 1 (b0, b1)
+    {
+        const int mat = lane >> 3, r = lane & 7;
+        const uint8_t* base = dig + (((mat >> 1) * 8 + r) * 32 + (mat & 1) * 16);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            if (kk < nk) {
+                ldsm_x4(bq[kk], base + kk * 2 * 8 * 32);
+            } else {
+                bq[kk][0] = bq[kk][1] = bq[kk][2] = bq[kk][3] = 0u;
+            }
         }
     }
-    int it = 0;
-    for (int tile = worker; tile < units; tile += nworkers, ++it) {
-        const int s = it % nstage;
-        const uint32_t phase = (uint32_t)((it / nstage) & 1);
-        mbar_wait(&w.bar[s], phase);
-        const uint8_t* st = mine + (size_t)s * stage_bytes;
-        const IO* qs = reinterpret_cast<const IO*>(st + stage_bytes - qbytes);
-        const int nzc = zc_len ? min(zc_len[tile], kMaxZc) : 0;
-        decode_tile<NT, IO>(st, qs, g, w, zc_k ? zc_k + (size_t)tile * zc_cap * kD : nullptr,
-                            zc_v ? zc_v + (size_t)tile * zc_cap * kD : nullptr, nzc,
-                            out_all + (size_t)tile * g * kD);
-        __syncwarp();
-        const int next = tile + nstage * nworkers;
-        if (lane == 0 && next < units) {
-            fence_proxy_async();
-            uint8_t* dst = mine + (size_t)s * stage_bytes;
-            const uint32_t tb = (uint32_t)dsize[next];
-            mbar_expect_tx(&w.bar[s], tb + qbytes);
-            bulk_g2s(dst, arena + offsets[next], tb, &w.bar[s]);
-            bulk_g2s(dst + stage_bytes - qbytes, q_all + (size_t)next * g * kD, qbytes, &w.bar[s]);
+    const float qinv = __shfl_sync(0xffffffffu, qinv_own, tig);  // lane tig has hl == tig
+    const int mtiles = (nslot + 15) >> 4;
+    for (int mt = 0; mt < mtiles; mt += 2) {
+        const bool two = mt + 1 < mtiles;
+        int acc[2][2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            if (kk < nk) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (u == 1 && !two) continue;
+                    const uint8_t* p0 = krows + (size_t)((mt + u) * 16 + gid) * krb + 8 * kk;
+                    const uint2 w0 = lds64(p0), w1 = lds64(p0 + 8 * krb);
+                    const int s = 2 * tig;
+                    uint32_t a[4];
+                    a[0] = (w0.x >> s) & 0x03030303u;
+                    a[2] = (w0.y >> s) & 0x03030303u;
+                    a[1] = (w1.x >> s) & 0x03030303u;
+                    a[3] = (w1.y >> s) & 0x03030303u;
+                    mma_u8s8(acc[u][0], a, bq[kk][0], bq[kk][1]);
+                    mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !two) continue;
+            float* row = lgs + tig * LS + (mt + u) * 16 + gid;
+            row[0] = fmaf((float)acc[u][0][0], 65536.0f, fmaf((float)acc[u][0][1], 256.0f, (float)acc[u][1][0])) * qinv;
+            row[8] = fmaf((float)acc[u][0][2], 65536.0f, fmaf((float)acc[u][0][3], 256.0f, (float)acc[u][1][2])) * qinv;
+        }
+    }
+    __syncwarp();
+
+    // ------------------------------------------------------------ logits + max
+    float mx = -INFINITY, vsm = 0.0f;
+    for (int s = tl; s < n; s += 8) {
+        vsm = fmaxf(vsm, vparam[s].x);
+        if (hv) {
+            const float v = (lgs[hl * LS + s] + bias) * inv_sqrt_d;
+            lgs[hl * LS + s] = v;
+            mx = fmaxf(mx, v);
+        }
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        vsm = fmaxf(vsm, __shfl_xor_sync(0xffffffffu, vsm, o));
+    }
+    const float psig = vsm > 0.0f ? 1.6e7f * __frcp_rn(vsm) : 0.0f;
+    const float vinv = vsm * (1.0f / 1.6e7f);
+    const int nv = (nslot + 31) >> 5;
+    {
+        uint4* z = reinterpret_cast<uint4*>(dig);
+        for (int i = lane; i < nv * 2 * 8 * 32 / 16; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+
+    // ------------------------------------------------------------ softmax + p~ digits
+    float lsum = 0.0f, bv = 0.0f;
+    if (hv) {
+        for (int s = tl; s < n; s += 8) {
+            const float p = __expf(lgs[hl * LS + s] - mx);
+            lsum += p;
+            const float2 vp = vparam[s];
+            bv = fmaf(p, vp.y, bv);
+            const int N = __float2int_rn(p * vp.x * psig);
+            uint8_t* base = dig + (((s >> 5) * 2) * 8 + 2 * hl) * 32 + (s & 31);
+            base[0] = (uint8_t)(N >> 16);
+            base[32] = (uint8_t)((N >> 8) & 255);
+            base[8 * 32] = (uint8_t)(N & 255);
+        }
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        bv += __shfl_xor_sync(0xffffffffu, bv, o);
+    }
+    __syncwarp();
+
+    // ------------------------------------------------------------ PV (tensor cores)
+    // m-tile mt covers byte columns 4mt .. 4mt+3; row gid <-> channel
+    // 16mt + 4(gid&3) + (gid>>2), row gid+8 <-> that + 2 (one word feeds both)
+    int acc[8][2][4];
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acc[mt][nt][2] = acc[mt][nt][3] = 0;
+    const int j0 = 2 * (gid >> 2);
+    const int swz = 8 * tig;
+    const int mat = lane >> 3, rr = lane & 7;
+    const uint8_t* bbase = dig + (((mat >> 1) * 8 + rr) * 32 + (mat & 1) * 16);
+    for (int kk = 0; kk < nv; ++kk) {
+        uint32_t b[4];
+        ldsm_x4(b, bbase + kk * 2 * 8 * 32);
+        const uint8_t* g0 = vbase + (size_t)(kk * 8 + tig) * 128;  // token group, 4 x 32 B
+        const uint8_t* g1 = g0 + 4 * 128;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+            const int col = ((4 * mt + (gid & 3)) ^ swz) * 4;
+            const uint32_t w0 = lds32(g0 + col), w1 = lds32(g1 + col);
+            uint32_t a[4];
+            a[0] = (w0 >> j0) & 0x03030303u;
+            a[1] = (w0 >> (j0 + 4)) & 0x03030303u;
+            a[2] = (w1 >> j0) & 0x03030303u;
+            a[3] = (w1 >> (j0 + 4)) & 0x03030303u;
+            mma_u8u8(acc[mt][0], a, b[0], b[1]);
+            mma_u8u8(acc[mt][1], a, b[2], b[3]);
+        }
+    }
+    float* acc_s = lgs;  // [4][kD]
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+        const int ch = 16 * mt + 4 * (gid & 3) + (gid >> 2);
+        float* row = acc_s + tig * kD + ch;
+        row[0] = fmaf((float)acc[mt][0][0], 65536.0f, fmaf((float)acc[mt][0][1], 256.0f, (float)acc[mt][1][0])) * vinv;
+        row[2] = fmaf((float)acc[mt][0][2], 65536.0f, fmaf((float)acc[mt][0][3], 256.0f, (float)acc[mt][1][2])) * vinv;
+    }
+    __syncwarp();
+
+    // ------------------------------------------------------------ output (lane owns channels 4*lane..+3)
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) {
+        if (hh >= g) continue;
+        const float4 o = reinterpret_cast<const float4*>(acc_s + hh * kD)[lane];
+        const float inv = __frcp_rn(__shfl_sync(0xffffffffu, lsum, hh));
+        const float b = __shfl_sync(0xffffffffu, bv, hh);
+        const float r0 = (o.x + b) * inv, r1 = (o.y + b) * inv, r2 = (o.z + b) * inv, r3 = (o.w + b) * inv;
+        if constexpr (sizeof(IO) == 2) {
+            __half2 h0 = __floats2half2_rn(r0, r1), h1 = __floats2half2_rn(r2, r3);
+            uint2 st;
+            st.x = *reinterpret_cast<uint32_t*>(&h0);
+            st.y = *reinterpret_cast<uint32_t*>(&h1);
+            reinterpret_cast<uint2*>(out + hh * kD)[lane] = st;
+        } else {
+            reinterpret_cast<float4*>(out + hh * kD)[lane] = make_float4(r0, r1, r2, r3);
+        }
+    }
+}
+
+template <int NT, typename IO, bool U2>
+__global__ void __launch_bounds__(32 * (kMaxW + 1), 1) decode_mma_kernel(const MmaParams p) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    uint64_t* empty = full + kMaxR;
+    uint8_t* ring = dsm + 2 * kMaxR * sizeof(uint64_t);  // 512 B, 128-aligned
+    uint8_t* scratch0 = ring + (size_t)p.R * p.slot_bytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qbytes = p.g * kD * (int)sizeof(IO);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.R; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int ntiles = p.units > (int)blockIdx.x ? (p.units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (warp == 0) {
+        // ---- producer: stage tile j of this CTA into slot j % R
+        for (int base = 0; base < ntiles; base += 32) {
+            const int mj = base + lane;
+            int64_t moff = 0;
+            int msz = 0;
+            if (mj < ntiles) {
+                const int tile = blockIdx.x + mj * gridDim.x;
+                moff = p.offsets[tile];
+                msz = p.dsize[tile];
+            }
+            const int cnt = min(32, ntiles - base);
+            for (int k = 0; k < cnt; ++k) {
+                const int64_t off = __shfl_sync(0xffffffffu, moff, k);
+                const int sz = __shfl_sync(0xffffffffu, msz, k);
+                if (lane == 0) {
+                    const int j = base + k;
+                    const int slot = j % p.R, use = j / p.R;
+                    if (use > 0) mbar_wait(&empty[slot], (uint32_t)((use - 1) & 1));
+                    fence_proxy_async();
+                    uint8_t* dst = ring + (size_t)slot * p.slot_bytes;
+                    const int tile = blockIdx.x + j * gridDim.x;
+                    mbar_expect_tx(&full[slot], (uint32_t)(sz + qbytes));
+                    bulk_g2s(dst, p.arena + off, (uint32_t)sz, &full[slot]);
+                    bulk_g2s(dst + p.slot_bytes - qbytes,
+                             static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &full[slot]);
+                }
+                __syncwarp();
+            }
+        }
+        return;
+    }
+    // ---- consumers
+    const int cw = warp - 1;
+    uint8_t* scr = scratch0 + (size_t)cw * p.scratch_bytes;
+    for (int j = cw; j < ntiles; j += p.W) {
+        const int slot = j % p.R, use = j / p.R;
+        mbar_wait(&full[slot], (uint32_t)(use & 1));
+        const uint8_t* st = ring + (size_t)slot * p.slot_bytes;
+        const int tile = blockIdx.x + j * gridDim.x;
+        const IO* qs = reinterpret_cast<const IO*>(st + p.slot_bytes - qbytes);
+        const int nzc = p.zc_len ? min(p.zc_len[tile], p.zc_cap) : 0;
+        if constexpr (U2) {
+            decode_tile_u2<IO>(st, qs, p.g, scr, p, static_cast<IO*>(p.out) + (size_t)tile * p.g * kD);
+        } else {
+            decode_tile<NT, IO>(st, qs, p.g, scr, p,
+                                p.zc_k ? p.zc_k + (size_t)tile * p.zc_cap * kD : nullptr,
+                                p.zc_v ? p.zc_v + (size_t)tile * p.zc_cap * kD : nullptr, nzc,
+                                static_cast<IO*>(p.out) + (size_t)tile * p.g * kD);
         }
         __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
     }
+}
+
+// ---------------------------------------------------------------------------
+// Uniform 2-bit tiles decoded by a PAIR of warps: the two warps split the
+// q~ digit k-steps, the 32-token blocks of QK / softmax and the PV channel
+// m-tiles, and meet at three named barriers per tile. Half the registers and
+// half the dependency chain of the one-warp body, so twice the warps fit.
+constexpr int kPairs = 11;  // consumer warp pairs per CTA (22 warps + producer)
+
+__device__ __forceinline__ void pair_sync(int id) {
+    asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
+}
+
+struct PairXchg {   // per pair, at the head of the pair's scratch
+    float bias[2][4];
+    float mx[2][4], vsm[2];
+    float lsum[2][4], bv[2][4];
+};
+static_assert(sizeof(PairXchg) <= kDigitBytesOff, "exchange area fits before the digits");
+
+template <typename IO>
+__device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ t, const IO* __restrict__ qs,
+                                                    int g, uint8_t* __restrict__ scr, const MmaParams& prm,
+                                                    IO* __restrict__ out, int half, int bar) {
+    // fragment layout: lane (gid, tig); tig is also the GQA head of every
+    // per-head value this lane holds (C columns 2*tig, 2*tig+1 = head tig)
+    const int lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const bool hv = tig < g;
+    const TileHeader& h = *reinterpret_cast<const TileHeader*>(t);
+    PairXchg& xg = *reinterpret_cast<PairXchg*>(scr);
+    uint8_t* dig = scr + kDigitBytesOff;
+    const float2* chan = reinterpret_cast<const float2*>(t + kHeaderBytes);
+    const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
+    const float2* vparam = reinterpret_cast<const float2*>(t + h.off_vp);
+    const uint8_t* krows = t + h.off_k;
+    const uint8_t* vbase = t + h.off_vseg[0];
+    const int n = h.r[0];
+    const int nslot = pad4(n);
+    const int c0 = h.c[0];
+    const int nk = (c0 + 31) >> 5;
+    const int krb = h.krow_bytes;
+    const float inv_sqrt_d = 0.08838834764831845f;  // 1/sqrt(128)
+    const IO* qh = qs + tig * kD;
+
+    // ------------------------------------------------------------ q statistics (both warps, redundant)
+    float qm = 0.0f, sm = 0.0f;
+    if (hv) {
+#pragma unroll
+        for (int i = 0; i < kD / 8; ++i) qm = fmaxf(qm, fabsf(ld_io(qh, gid + 8 * i)));
+    }
+    for (int j = lane; j < c0; j += 32) sm = fmaxf(sm, fabsf(chan[j].x));
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+    sm = warp_max(sm);
+    const float bnd = sm * qm;
+    const float sg = bnd > 0.0f ? 8.2e6f * __frcp_rn(bnd) : 0.0f;
+    const float qinv = bnd * (1.0f / 8.2e6f);
+
+    // ------------------------------------------------------------ q~ digits + bias (k-steps half, half+2)
+    float bpart = 0.0f;
+    for (int kk = half; kk < nk; kk += 2) {
+        uint32_t x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = kk * 32 + 16 * (gid >> 2) + 4 * e + (gid & 3);
+            int N = 0;
+            if (hv && j < c0) {
+                const float2 cs = chan[j];
+                const float qv = ld_io(qh, perm[j]);
+                bpart = fmaf(qv, cs.y, bpart);
+                N = __float2int_rn(cs.x * qv * sg);
+            }
+            x[e] = (uint32_t)(N + 0x808080) ^ 0x808080u;
+        }
+        const uint32_t wlo = __byte_perm(__byte_perm(x[0], x[1], 0x0040), __byte_perm(x[2], x[3], 0x0040), 0x5410);
+        const uint32_t wmid = __byte_perm(__byte_perm(x[0], x[1], 0x0051), __byte_perm(x[2], x[3], 0x0051), 0x5410);
+        const uint32_t whi = __byte_perm(__byte_perm(x[0], x[1], 0x0062), __byte_perm(x[2], x[3], 0x0062), 0x5410);
+        uint8_t* a0 = dig + ((kk * 2) * 8 + 2 * tig) * 32 + 4 * gid;
+        *reinterpret_cast<uint32_t*>(a0) = whi;
+        *reinterpret_cast<uint32_t*>(a0 + 32) = wmid;
+        *reinterpret_cast<uint32_t*>(a0 + 8 * 32) = wlo;
+        *reinterpret_cast<uint32_t*>(a0 + 8 * 32 + 32) = 0u;
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) bpart += __shfl_xor_sync(0xffffffffu, bpart, o);
+    if (gid == 0) xg.bias[half][tig] = bpart;
+    pair_sync(bar);  // digits + bias halves visible
+    const float bias = xg.bias[0][tig] + xg.bias[1][tig];
+
+    // ------------------------------------------------------------ QK: m-tile pairs half, half+2, ... (32 tokens each)
+    const int mat = lane >> 3, rr = lane & 7;
+    const uint8_t* bbase = dig + (((mat >> 1) * 8 + rr) * 32 + (mat & 1) * 16);
+    uint32_t bq[4][4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        if (kk < nk) {
+            ldsm_x4(bq[kk], bbase + kk * 2 * 8 * 32);
+        } else {
+            bq[kk][0] = bq[kk][1] = bq[kk][2] = bq[kk][3] = 0u;
+        }
+    }
+    constexpr int kPM = (kU2MaxSlots / 32 + 1) / 2;  // pairs per warp (3 for 160 slots)
+    const int npair = (nslot + 31) >> 5;
+    float lg[kPM][2][2];  // [pair][m-tile][row half]: token 32*pb + 16*u + gid + 8*r
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kPM; ++i) {
+        const int pb = half + 2 * i;
+        if (pb >= npair) {
+            lg[i][0][0] = lg[i][0][1] = lg[i][1][0] = lg[i][1][1] = -INFINITY;
+            continue;
+        }
+        int acc[2][2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
+        const uint8_t* p0 = krows + (size_t)(32 * pb + gid) * krb;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            if (kk < nk) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint8_t* pu = p0 + 16 * u * krb + 8 * kk;
+                    const uint2 w0 = lds64(pu), w1 = lds64(pu + 8 * krb);
+                    const int s = 2 * tig;
+                    uint32_t a[4];
+                    a[0] = (w0.x >> s) & 0x03030303u;
+                    a[2] = (w0.y >> s) & 0x03030303u;
+                    a[1] = (w1.x >> s) & 0x03030303u;
+                    a[3] = (w1.y >> s) & 0x03030303u;
+                    mma_u8s8(acc[u][0], a, bq[kk][0], bq[kk][1]);
+                    mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int s = 32 * pb + 16 * u + gid + 8 * r;
+                const float v = fmaf((float)acc[u][0][2 * r], 65536.0f,
+                                     fmaf((float)acc[u][0][2 * r + 1], 256.0f, (float)acc[u][1][2 * r]));
+                const float l = (s < n && hv) ? fmaf(v, qinv, bias) * inv_sqrt_d : -INFINITY;
+                lg[i][u][r] = l;
+                mx = fmaxf(mx, l);
+            }
+    }
+    // V-scale bound over this warp's tokens (p~ = p * vscale <= vscale)
+    float vsm = 0.0f;
+    for (int pb = half; pb < npair; pb += 2) {
+        const int s = 32 * pb + lane;
+        if (s < n) vsm = fmaxf(vsm, vparam[s].x);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    vsm = warp_max(vsm);
+    if (gid == 0) xg.mx[half][tig] = mx;
+    if (lane == 0) xg.vsm[half] = vsm;
+    pair_sync(bar);  // also: both warps are done reading the q~ digits
+    mx = fmaxf(xg.mx[0][tig], xg.mx[1][tig]);
+    vsm = fmaxf(xg.vsm[0], xg.vsm[1]);
+    const float psig = vsm > 0.0f ? 1.6e7f * __frcp_rn(vsm) : 0.0f;
+    const float vinv = vsm * (1.0f / 1.6e7f);
+    const int nv = npair;  // token k-steps == 32-token blocks
+    for (int pb = half; pb < nv; pb += 2) reinterpret_cast<uint4*>(dig + pb * 2 * 8 * 32)[lane] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+
+    // ------------------------------------------------------------ softmax + p~ digits, in registers
+    float lsum = 0.0f, bv = 0.0f;
+#pragma unroll
+    for (int i = 0; i < kPM; ++i) {
+        const int pb = half + 2 * i;
+        if (pb >= npair) continue;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const float l = lg[i][u][r];
+                if (l == -INFINITY) continue;
+                const int s = 32 * pb + 16 * u + gid + 8 * r;
+                const float p = __expf(l - mx);
+                lsum += p;
+                const float2 vp = vparam[s];
+                bv = fmaf(p, vp.y, bv);
+                const int N = __float2int_rn(p * vp.x * psig);
+                uint8_t* base = dig + ((pb * 2) * 8 + 2 * tig) * 32 + (s & 31);
+                base[0] = (uint8_t)(N >> 16);
+                base[32] = (uint8_t)((N >> 8) & 255);
+                base[8 * 32] = (uint8_t)(N & 255);
+            }
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        bv += __shfl_xor_sync(0xffffffffu, bv, o);
+    }
+    if (gid == 0) {
+        xg.lsum[half][tig] = lsum;
+        xg.bv[half][tig] = bv;
+    }
+    pair_sync(bar);  // p~ digits of both warps + totals visible
+    const float lt = xg.lsum[0][tig] + xg.lsum[1][tig];
+    const float bt = xg.bv[0][tig] + xg.bv[1][tig];
+
+    // ------------------------------------------------------------ PV: channel m-tiles 4*half .. 4*half+3
+    int acc[4][2][4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[m][nt][0] = acc[m][nt][1] = acc[m][nt][2] = acc[m][nt][3] = 0;
+    const int j0 = 2 * (gid >> 2);
+    const int swz = 8 * tig;
+    const uint8_t* g0b = vbase + (size_t)tig * 128;
+    for (int kk = 0; kk < nv; ++kk) {
+        uint32_t b[4];
+        ldsm_x4(b, bbase + kk * 2 * 8 * 32);
+        const uint8_t* g0 = g0b + (size_t)kk * 8 * 128;  // token group kk*8 + tig
+        const uint8_t* g1 = g0 + 4 * 128;                // token group + 4
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int col = ((4 * (4 * half + m) + (gid & 3)) ^ swz) * 4;
+            const uint32_t w0 = lds32(g0 + col), w1 = lds32(g1 + col);
+            uint32_t a[4];
+            a[0] = (w0 >> j0) & 0x03030303u;
+            a[1] = (w0 >> (j0 + 4)) & 0x03030303u;
+            a[2] = (w1 >> j0) & 0x03030303u;
+            a[3] = (w1 >> (j0 + 4)) & 0x03030303u;
+            mma_u8u8(acc[m][0], a, b[0], b[1]);
+            mma_u8u8(acc[m][1], a, b[2], b[3]);
+        }
+    }
+    // output straight from the fragments: head tig, channels ch and ch + 2
+    if (hv) {
+        const float inv = __frcp_rn(lt);
+        IO* orow = out + tig * kD;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int ch = 16 * (4 * half + m) + 4 * (gid & 3) + (gid >> 2);
+            const float v0 = fmaf((float)acc[m][0][0], 65536.0f, fmaf((float)acc[m][0][1], 256.0f, (float)acc[m][1][0]));
+            const float v1 = fmaf((float)acc[m][0][2], 65536.0f, fmaf((float)acc[m][0][3], 256.0f, (float)acc[m][1][2]));
+            const float r0 = fmaf(v0, vinv, bt) * inv, r1 = fmaf(v1, vinv, bt) * inv;
+            if constexpr (sizeof(IO) == 2) {
+                orow[ch] = __float2half_rn(r0);
+                orow[ch + 2] = __float2half_rn(r1);
+            } else {
+                orow[ch] = r0;
+                orow[ch + 2] = r1;
+            }
+        }
+    }
+}
+
+template <typename IO>
+__global__ void __launch_bounds__(32 * (2 * kPairs + 1), 1) decode_u2_pair_kernel(const MmaParams p) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    uint64_t* empty = full + kMaxR;
+    uint8_t* ring = dsm + 2 * kMaxR * sizeof(uint64_t);
+    uint8_t* scratch0 = ring + (size_t)p.R * p.slot_bytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qbytes = p.g * kD * (int)sizeof(IO);
+    const int npairs = p.W;  // W counts pairs for this kernel
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.R; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 2);  // both warps of the pair release the slot
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int ntiles = p.units > (int)blockIdx.x ? (p.units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (warp == 0) {
+        for (int base = 0; base < ntiles; base += 32) {
+            const int mj = base + lane;
+            int64_t moff = 0;
+            int msz = 0;
+            if (mj < ntiles) {
+                const int tile = blockIdx.x + mj * gridDim.x;
+                moff = p.offsets[tile];
+                msz = p.dsize[tile];
+            }
+            const int cnt = min(32, ntiles - base);
+            for (int k = 0; k < cnt; ++k) {
+                const int64_t off = __shfl_sync(0xffffffffu, moff, k);
+                const int sz = __shfl_sync(0xffffffffu, msz, k);
+                if (lane == 0) {
+                    const int j = base + k;
+                    const int slot = j % p.R, use = j / p.R;
+                    if (use > 0) mbar_wait(&empty[slot], (uint32_t)((use - 1) & 1));
+                    fence_proxy_async();
+                    uint8_t* dst = ring + (size_t)slot * p.slot_bytes;
+                    const int tile = blockIdx.x + j * gridDim.x;
+                    mbar_expect_tx(&full[slot], (uint32_t)(sz + qbytes));
+                    bulk_g2s(dst, p.arena + off, (uint32_t)sz, &full[slot]);
+                    bulk_g2s(dst + p.slot_bytes - qbytes,
+                             static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &full[slot]);
+                }
+                __syncwarp();
+            }
+        }
+        return;
+    }
+    const int pr = (warp - 1) >> 1, half = (warp - 1) & 1;
+    uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
+    int slot = pr % p.R, use = pr / p.R;
+    for (int j = pr; j < ntiles; j += npairs) {
+        mbar_wait(&full[slot], (uint32_t)(use & 1));
+        const uint8_t* st = ring + (size_t)slot * p.slot_bytes;
+        const int tile = blockIdx.x + j * gridDim.x;
+        const IO* qs = reinterpret_cast<const IO*>(st + p.slot_bytes - qbytes);
+        decode_tile_u2_pair<IO>(st, qs, p.g, scr, p, static_cast<IO*>(p.out) + (size_t)tile * p.g * kD, half,
+                                1 + pr);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        slot += npairs;
+        while (slot >= p.R) {
+            slot -= p.R;
+            ++use;
+        }
+    }
+}
+
+template <typename IO>
+static int launch_pair(const rdkv_decode_args* a, cudaStream_t st) {
+    const int qbytes = a->group * kD * (int)sizeof(IO);
+    const int slot = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
+    const int nv = (a->plan.max_slots + 31) / 32;
+    const int steps = nv > 4 ? nv : 4;
+    int scratch = kDigitBytesOff + steps * 2 * 8 * 32;
+    const int off_lg = 0, lg_stride = 0;  // softmax stays in registers
+    scratch = (scratch + 127) & ~127;
+    int dev = 0, smem_max = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int head = 2 * kMaxR * (int)sizeof(uint64_t);
+    const int slack = 4096;
+    int W = kPairs, R = 0;
+    bool fits = false;
+    for (; W >= 1 && !fits; --W) {
+        for (int look = 2; look >= 0 && !fits; --look) {
+            R = W + look > kMaxR ? kMaxR : W + look;
+            fits = head + (size_t)R * slot + (size_t)W * scratch + slack <= (size_t)smem_max;
+        }
+        if (fits) break;
+    }
+    if (!fits) return RDKV_EINVAL;
+    const size_t smem = head + (size_t)R * slot + (size_t)W * scratch + slack;
+    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
+                a->units, a->group, 0, R, W, slot, scratch, off_lg, lg_stride, -1, -1, 0};
+    auto kern = decode_u2_pair_kernel<IO>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int blocks = (a->units + W - 1) / W;
+    if (blocks > nsm) blocks = nsm;
+    kern<<<blocks, 32 * (2 * W + 1), smem, st>>>(p);
+    return launch_status();
 }
 
 }  // namespace rdkv_b200
@@ -717,54 +1220,82 @@ namespace rdkv_b200 {
 
 bool mma_supported(const rdkv_decode_args* a) {
     if (a->head_dim != kD || a->group > 8 || !a->tile_decode_bytes) return false;
-    if (a->zc_len && a->zc_cap > kMaxZc) return false;
+    if (a->zc_len && a->zc_cap > 1024) return false;
     const rdkv_decode_plan& p = a->plan;
-    return p.max_decode_bytes > 0 && p.max_slots <= kMaxSlots && p.max_zone_b_rows <= 64 &&
-           p.max_kq_slots <= kMaxKSteps * 32;
+    return p.max_decode_bytes > 0 && p.max_slots <= kMaxSlots && p.max_zone_b_rows <= kMaxSlots;
 }
 
-template <int NT, typename IO>
+template <int NT, typename IO, bool U2>
 static int launch_t(const rdkv_decode_args* a, cudaStream_t st) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
-    const int stage = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
-    const int wsm = (int)((sizeof(WarpSmem) + 127) & ~size_t(127));
-    int dev = 0;
+    const int slot = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
+    // per-warp scratch: head | digits | logits (aliased by the PV accumulators) | p16 | zl
+    const int qsteps = (a->plan.max_kq_slots + 31) / 32;
+    const int vsteps = (a->plan.max_slots + 31) / 32 + 2;
+    const int steps = qsteps > vsteps ? qsteps : vsteps;
+    int scratch = kDigitBytesOff + steps * 2 * NT * 8 * 32;
+    const int off_lg = scratch;
+    // stride == 32/G4 (mod 32): the G4 heads x 32/G4 tokens of a warp hit distinct banks
+    const int s32 = ((a->plan.max_slots + 31) / 32) * 32;
+    const int lg_stride = (s32 > kD ? s32 : kD) + 32 / (4 * NT);
+    scratch += 4 * NT * lg_stride * 4;
+    int off_p16 = -1, off_zl = -1;
+    const int max_r16 = a->plan.max_zone_b_rows;
+    if (max_r16 > 0) {
+        off_p16 = scratch;
+        scratch += 4 * NT * max_r16 * 4;
+    }
+    if (a->zc_len) {
+        off_zl = scratch;
+        scratch += 4 * NT * a->zc_cap * 4;
+    }
+    scratch = (scratch + 127) & ~127;
+    int dev = 0, smem_max = 0, nsm = 0;
     cudaGetDevice(&dev);
-    int smem_max = 0, nsm = 0;
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int nstage = 3;
-    int per_warp = nstage * stage + wsm;
-    if (per_warp * 4 > smem_max) {
-        nstage = 2;
-        per_warp = nstage * stage + wsm;
+    const int head = 2 * kMaxR * (int)sizeof(uint64_t);
+    const int slack = 4096;  // fragment over-reads past the last ring slot (masked by zero digits)
+    // consumers W and ring slots R = W + lookahead (2, else 1, else 0), as many as fit
+    int W = kMaxW, R = 0;
+    bool fits = false;
+    for (; W >= 1 && !fits; --W) {
+        for (int look = 2; look >= 0 && !fits; --look) {
+            R = W + look > kMaxR ? kMaxR : W + look;
+            fits = head + (size_t)R * slot + (size_t)W * scratch + slack <= (size_t)smem_max;
+        }
+        if (fits) break;
     }
-    int warps = smem_max / per_warp;
-    if (warps > 8) warps = 8;
-    if (warps < 1) return RDKV_EINVAL;
-    const size_t smem = (size_t)warps * per_warp;
-    auto kern = decode_mma_kernel<NT, IO>;
+    if (!fits) return RDKV_EINVAL;
+    const size_t smem = head + (size_t)R * slot + (size_t)W * scratch + slack;
+    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
+                static_cast<const __half*>(a->zc_k), static_cast<const __half*>(a->zc_v), a->zc_len,
+                a->units, a->group, a->zc_cap, R, W, slot, scratch, off_lg, lg_stride, off_p16, off_zl, max_r16};
+    auto kern = decode_mma_kernel<NT, IO, U2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int blocks = (a->units + warps - 1) / warps;
+    int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
-    kern<<<blocks, warps * 32, smem, st>>>(a->arena, a->tile_offsets, a->tile_decode_bytes, a->units, a->group,
-                                           static_cast<const IO*>(a->q), static_cast<IO*>(a->out),
-                                           static_cast<const __half*>(a->zc_k), static_cast<const __half*>(a->zc_v),
-                                           a->zc_len, a->zc_cap, stage, nstage);
+    kern<<<blocks, 32 * (W + 1), smem, st>>>(p);
     return launch_status();
 }
 
 int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     const bool f16 = a->io_dtype == RDKV_F16;
-    if (a->group <= 4) return f16 ? launch_t<1, __half>(a, st) : launch_t<1, float>(a, st);
-    return f16 ? launch_t<2, __half>(a, st) : launch_t<2, float>(a, st);
+    // uniform 2-bit tiles (the n=128 production shape) take the specialised body
+    // uniform 2-bit tiles (the n=128 production shape): warp-pair body by default,
+    // kernel 4 selects the one-warp body, kernel 3 the general body
+    const bool u2 = a->plan.uniform2 && a->group <= 4 && !a->zc_len && a->kernel != 3;
+    if (u2 && a->kernel == 4) return f16 ? launch_t<1, __half, true>(a, st) : launch_t<1, float, true>(a, st);
+    if (u2) return f16 ? launch_pair<__half>(a, st) : launch_pair<float>(a, st);
+    if (a->group <= 4) return f16 ? launch_t<1, __half, false>(a, st) : launch_t<1, float, false>(a, st);
+    return f16 ? launch_t<2, __half, false>(a, st) : launch_t<2, float, false>(a, st);
 }
 
 }  // namespace rdkv_b200
 
 // Scans every tile header once (one small D2H copy per tile) and writes the
 // per-tile decode sizes the persistent kernel stages with cp.async.bulk, plus
-// the maxima that select the kernel and its smem ring. Call once after packing.
+// the maxima that select the kernel variant and size its smem ring.
 extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int64_t* tile_offsets_host,
                                                  int32_t units, int32_t* decode_bytes_dev,
                                                  rdkv_decode_plan* plan, void* stream) {
@@ -776,7 +1307,7 @@ extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int
     for (int u = 0; u < units; ++u)
         cudaMemcpyAsync(&hdrs[u], arena + tile_offsets_host[u], sizeof(TileHeader), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) rc = RDKV_ECUDA;
-    rdkv_decode_plan p{0, 0, 0, 0};
+    rdkv_decode_plan p{0, 0, 0, 0, 1};
     for (int u = 0; u < units && rc == RDKV_OK; ++u) {
         const TileHeader& h = hdrs[u];
         if (h.magic != kTileMagic) {
@@ -788,6 +1319,9 @@ extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int
         p.max_slots = h.nslot > p.max_slots ? h.nslot : p.max_slots;
         p.max_zone_b_rows = h.r[3] > p.max_zone_b_rows ? h.r[3] : p.max_zone_b_rows;
         p.max_kq_slots = h.kslot_base[3] > p.max_kq_slots ? h.kslot_base[3] : p.max_kq_slots;
+        const bool u2 = h.r[1] == 0 && h.r[2] == 0 && h.r[3] == 0 && h.c[1] == 0 && h.c[2] == 0 &&
+                        h.c[3] == 0 && h.r[0] > 0 && h.c[0] > 0 && h.nslot <= kU2MaxSlots;
+        if (!u2) p.uniform2 = 0;
     }
     if (rc == RDKV_OK) {
         if (cudaMemcpyAsync(decode_bytes_dev, ds, sizeof(int32_t) * (size_t)units, cudaMemcpyHostToDevice, st) !=

@@ -18,7 +18,8 @@
 //   * quantised V rows are interleaved in groups of 4 tokens at byte
 //     granularity (byte m of tokens 4G..4G+3 are adjacent), so one 32-bit
 //     word holds 4 tokens x (8/bits) channels — the operand shape of the
-//     int8 tensor-core PV product;
+//     int8 tensor-core PV product; word columns are XOR-swizzled per group
+//     (vswz) for bank-conflict-free fragment loads;
 //   * dequantisation is stored as (scale, offset = -scale*zero_point) in f32;
 //     the int64 zero points and token ids live in an export trailer that the
 //     decode never reads.
@@ -153,12 +154,21 @@ RDKV_HD int64_t tile_decode_bytes(const TileHeader& h) {
     return (int64_t)h.off_ids - 0;  // everything before the export trailer
 }
 
-// Location of the packed byte holding channel c of slot s (local index li in
-// class i) in the interleaved V layout.
+// Byte column swizzle of the interleaved V layout: inside token group G the
+// 32-bit word of byte column m is stored at column m ^ (8 * (G & 3)) whenever
+// a row spans a multiple of 32 bytes, so the four token groups a tensor-core
+// fragment reads at once fall into distinct shared-memory banks.
+RDKV_HD int32_t vswz(int32_t m, int32_t grp, int32_t rb) {
+    return (rb & 31) == 0 ? (m ^ ((grp & 3) << 3)) : m;
+}
+
+// Location of the packed byte `byte_in_row` of slot li (local index in class
+// cls) in the 4-token interleaved V layout.
 RDKV_HD int64_t vbyte_offset(const TileHeader& h, int cls, int32_t li, int32_t byte_in_row,
                              int32_t d) {
     const int32_t rb = ref_row_bytes(d, kBits(cls));
-    return (int64_t)h.off_vseg[cls] + (int64_t)(li >> 2) * 4 * rb + (int64_t)byte_in_row * 4 +
+    const int32_t grp = li >> 2;
+    return (int64_t)h.off_vseg[cls] + (int64_t)grp * 4 * rb + (int64_t)vswz(byte_in_row, grp, rb) * 4 +
            (li & 3);
 }
 

@@ -81,8 +81,14 @@ def test_mma_all_two_bit_default_budget_shape(cuda, orc):
         kb[:] = 2
         cases.append((k, v, vb, kb, q))
     worst, model = _run_batch(cuda, orc, cases, 4)
-    assert model.plan.max_slots == 128
+    assert model.plan.max_slots == 128 and model.plan.uniform2 == 1
     assert worst < FP16_INPUT_TOL, worst
+    # the specialised uniform-2-bit body and the general tensor-core body agree
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda)
+    a = P.packed_decode_step(model, q, kernel=2)
+    for k in (3, 4):  # general body, one-warp uniform body (kernel 2 = warp-pair body)
+        b = P.packed_decode_step(model, q, kernel=k)
+        assert float(((a - b).norm(dim=-1) / b.norm(dim=-1)).max()) < 2 * FP16_INPUT_TOL, k
 
 
 @pytest.mark.parametrize("g", [1, 2, 4, 7, 8])

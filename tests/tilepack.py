@@ -189,8 +189,10 @@ def build_tile(canon, v_bits, k_bits, v_src, d):
             bits = kbits(cls)
             packed = pack_codes(np.concatenate([canon["vcodes"][ki], np.zeros(ref_padded_len(d, bits) - d, np.uint8)]), bits)
             rb = ref_row_bytes(d, bits)
+            grp = li >> 2
             for m in range(rb):
-                tile[h["off_vseg"][cls] + (li >> 2) * 4 * rb + m * 4 + (li & 3)] = packed[m]
+                col = (m ^ ((grp & 3) << 3)) if rb % 32 == 0 else m
+                tile[h["off_vseg"][cls] + grp * 4 * rb + col * 4 + (li & 3)] = packed[m]
             vp[sl] = (canon["vscale"][ki], offset_of(canon["vscale"][ki], canon["vzero"][ki]))
             vz[sl] = canon["vzero"][ki]
         base += cnt
