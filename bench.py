@@ -259,6 +259,10 @@ def fp16_fullkv_baseline(spec, steps, warmup):
     """FlashInfer 0.6.11 batch decode over an FP16 paged full KV cache (same shapes).
     One layer's KV (batch x 128K) is resident; a step runs it for all layers."""
     import torch
+
+    # prebuilt (cross-compiled) FlashInfer module, see baseline/prebuild_flashinfer.py
+    os.environ.setdefault("FLASHINFER_WORKSPACE_BASE", os.path.join(ROOT, "baseline", "flashinfer_ws"))
+    os.environ.setdefault("FLASHINFER_CUDA_ARCH_LIST", "10.0a")
     import flashinfer
 
     B, T, H, Hq, d = spec.batch, spec.ctx, spec.kv_heads, spec.q_heads, spec.head_dim

@@ -892,6 +892,7 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
     const int n = h.r[0];
     const int nslot = pad4(n);
     const int c0 = h.c[0];
+    const bool full_k = c0 == kD;  // every channel at 2 bits: channel_perm is the identity
     const int nk = (c0 + 31) >> 5;
     const int krb = h.krow_bytes;
     const float inv_sqrt_d = 0.08838834764831845f;  // 1/sqrt(128)
@@ -901,7 +902,7 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
     float qm = 0.0f, sm = 0.0f;
     if (hv) {
 #pragma unroll
-        for (int i = 0; i < kD / 8; ++i) qm = fmaxf(qm, fabsf(ld_io(qh, gid + 8 * i)));
+        for (int i = 0; i < kD / 8; ++i) qm = fmaxf(qm, fabsf(ld_io(qh, 16 * (i >> 1) + 2 * gid + (i & 1))));
     }
     for (int j = lane; j < c0; j += 32) sm = fmaxf(sm, fabsf(chan[j].x));
 #pragma unroll
@@ -909,10 +910,14 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
     sm = warp_max(sm);
     const float bnd = sm * qm;
     const float sg = bnd > 0.0f ? 8.2e6f * __frcp_rn(bnd) : 0.0f;
-    const float qinv = bnd * (1.0f / 8.2e6f);
 
     // ------------------------------------------------------------ q~ digits + bias (k-steps half, half+2)
+    // K position p = 4*gid + e of a k-step is read by A-lane tig(p) = gid & 3,
+    // whose codes enter the MMA masked in place, i.e. scaled by 4^tig(p); the
+    // fixed point N is pre-scaled by 4^(3 - tig(p)) so every product carries
+    // 4^3 = 64, and split into four signed bytes (n-tile 0: d3 d2, n-tile 1: d1 d0).
     float bpart = 0.0f;
+    const int pshift = 2 * (3 - (gid & 3));
     for (int kk = half; kk < nk; kk += 2) {
         uint32_t x[4];
 #pragma unroll
@@ -921,26 +926,29 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
             int N = 0;
             if (hv && j < c0) {
                 const float2 cs = chan[j];
-                const float qv = ld_io(qh, perm[j]);
+                const float qv = ld_io(qh, full_k ? j : perm[j]);
                 bpart = fmaf(qv, cs.y, bpart);
                 N = __float2int_rn(cs.x * qv * sg);
             }
-            x[e] = (uint32_t)(N + 0x808080) ^ 0x808080u;
+            x[e] = ((uint32_t)N << pshift) + 0x80808080u ^ 0x80808080u;
         }
-        const uint32_t wlo = __byte_perm(__byte_perm(x[0], x[1], 0x0040), __byte_perm(x[2], x[3], 0x0040), 0x5410);
-        const uint32_t wmid = __byte_perm(__byte_perm(x[0], x[1], 0x0051), __byte_perm(x[2], x[3], 0x0051), 0x5410);
-        const uint32_t whi = __byte_perm(__byte_perm(x[0], x[1], 0x0062), __byte_perm(x[2], x[3], 0x0062), 0x5410);
+        const uint32_t w0 = __byte_perm(__byte_perm(x[0], x[1], 0x0040), __byte_perm(x[2], x[3], 0x0040), 0x5410);
+        const uint32_t w1 = __byte_perm(__byte_perm(x[0], x[1], 0x0051), __byte_perm(x[2], x[3], 0x0051), 0x5410);
+        const uint32_t w2 = __byte_perm(__byte_perm(x[0], x[1], 0x0062), __byte_perm(x[2], x[3], 0x0062), 0x5410);
+        const uint32_t w3 = __byte_perm(__byte_perm(x[0], x[1], 0x0073), __byte_perm(x[2], x[3], 0x0073), 0x5410);
         uint8_t* a0 = dig + ((kk * 2) * 8 + 2 * tig) * 32 + 4 * gid;
-        *reinterpret_cast<uint32_t*>(a0) = whi;
-        *reinterpret_cast<uint32_t*>(a0 + 32) = wmid;
-        *reinterpret_cast<uint32_t*>(a0 + 8 * 32) = wlo;
-        *reinterpret_cast<uint32_t*>(a0 + 8 * 32 + 32) = 0u;
+        *reinterpret_cast<uint32_t*>(a0) = w3;
+        *reinterpret_cast<uint32_t*>(a0 + 32) = w2;
+        *reinterpret_cast<uint32_t*>(a0 + 8 * 32) = w1;
+        *reinterpret_cast<uint32_t*>(a0 + 8 * 32 + 32) = w0;
     }
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) bpart += __shfl_xor_sync(0xffffffffu, bpart, o);
     if (gid == 0) xg.bias[half][tig] = bpart;
     pair_sync(bar);  // digits + bias halves visible
-    const float bias = xg.bias[0][tig] + xg.bias[1][tig];
+    const float bias_s = (xg.bias[0][tig] + xg.bias[1][tig]) * inv_sqrt_d;
+    // logit = (v / (64 sigma) + bias) / sqrt(d), v = sum code * 4^tig * N * 4^(3-tig)
+    const float qscale = bnd * (1.0f / (64.0f * 8.2e6f)) * inv_sqrt_d;
 
     // ------------------------------------------------------------ QK: m-tile pairs half, half+2, ... (32 tokens each)
     const int mat = lane >> 3, rr = lane & 7;
@@ -954,6 +962,7 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
             bq[kk][0] = bq[kk][1] = bq[kk][2] = bq[kk][3] = 0u;
         }
     }
+    const uint32_t kmask = 0x03030303u << (2 * tig);
     constexpr int kPM = (kU2MaxSlots / 32 + 1) / 2;  // pairs per warp (3 for 160 slots)
     const int npair = (nslot + 31) >> 5;
     float lg[kPM][2][2];  // [pair][m-tile][row half]: token 32*pb + 16*u + gid + 8*r
@@ -970,20 +979,32 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
         for (int u = 0; u < 2; ++u)
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
-        const uint8_t* p0 = krows + (size_t)(32 * pb + gid) * krb;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            if (kk < nk) {
+        for (int u = 0; u < 2; ++u) {
+            const uint8_t* r0 = krows + (size_t)(32 * pb + 16 * u + gid) * krb;
+            const uint8_t* r1 = r0 + 8 * krb;
+            uint32_t w0[8], w1[8];  // the 32 K bytes (128 codes) of rows gid and gid + 8
+            if (krb == 32) {
+                const uint4 x0 = *reinterpret_cast<const uint4*>(r0), x1 = *reinterpret_cast<const uint4*>(r0 + 16);
+                const uint4 y0 = *reinterpret_cast<const uint4*>(r1), y1 = *reinterpret_cast<const uint4*>(r1 + 16);
+                w0[0] = x0.x; w0[1] = x0.y; w0[2] = x0.z; w0[3] = x0.w; w0[4] = x1.x; w0[5] = x1.y; w0[6] = x1.z; w0[7] = x1.w;
+                w1[0] = y0.x; w1[1] = y0.y; w1[2] = y0.z; w1[3] = y0.w; w1[4] = y1.x; w1[5] = y1.y; w1[6] = y1.z; w1[7] = y1.w;
+            } else {
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const uint8_t* pu = p0 + 16 * u * krb + 8 * kk;
-                    const uint2 w0 = lds64(pu), w1 = lds64(pu + 8 * krb);
-                    const int s = 2 * tig;
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint2 a = kk < nk ? lds64(r0 + 8 * kk) : make_uint2(0, 0);
+                    const uint2 b = kk < nk ? lds64(r1 + 8 * kk) : make_uint2(0, 0);
+                    w0[2 * kk] = a.x; w0[2 * kk + 1] = a.y; w1[2 * kk] = b.x; w1[2 * kk + 1] = b.y;
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                if (kk < nk) {
                     uint32_t a[4];
-                    a[0] = (w0.x >> s) & 0x03030303u;
-                    a[2] = (w0.y >> s) & 0x03030303u;
-                    a[1] = (w1.x >> s) & 0x03030303u;
-                    a[3] = (w1.y >> s) & 0x03030303u;
+                    a[0] = w0[2 * kk] & kmask;
+                    a[2] = w0[2 * kk + 1] & kmask;
+                    a[1] = w1[2 * kk] & kmask;
+                    a[3] = w1[2 * kk + 1] & kmask;
                     mma_u8s8(acc[u][0], a, bq[kk][0], bq[kk][1]);
                     mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
                 }
@@ -994,9 +1015,10 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int s = 32 * pb + 16 * u + gid + 8 * r;
-                const float v = fmaf((float)acc[u][0][2 * r], 65536.0f,
-                                     fmaf((float)acc[u][0][2 * r + 1], 256.0f, (float)acc[u][1][2 * r]));
-                const float l = (s < n && hv) ? fmaf(v, qinv, bias) * inv_sqrt_d : -INFINITY;
+                const float v = fmaf(fmaf(fmaf((float)acc[u][0][2 * r], 256.0f, (float)acc[u][0][2 * r + 1]), 256.0f,
+                                          (float)acc[u][1][2 * r]),
+                                     256.0f, (float)acc[u][1][2 * r + 1]);
+                const float l = (s < n && hv) ? fmaf(v, qscale, bias_s) : -INFINITY;
                 lg[i][u][r] = l;
                 mx = fmaxf(mx, l);
             }
@@ -1058,43 +1080,47 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
     const float lt = xg.lsum[0][tig] + xg.lsum[1][tig];
     const float bt = xg.bv[0][tig] + xg.bv[1][tig];
 
-    // ------------------------------------------------------------ PV: channel m-tiles 4*half .. 4*half+3
+    // ------------------------------------------------------------ PV: 4 m-tiles per warp, codes masked in place
+    // byte column c = 16*half + 4*(gid&3) + m (m = 0..3, one LDS.128 per token group);
+    // row gid <-> channel 4c + jj, row gid+8 <-> 4c + jj + 2, jj = gid >> 2; the
+    // in-place mask scales those rows by 4^jj and 4^(jj+2)
     int acc[4][2][4];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) acc[m][nt][0] = acc[m][nt][1] = acc[m][nt][2] = acc[m][nt][3] = 0;
-    const int j0 = 2 * (gid >> 2);
-    const int swz = 8 * tig;
-    const uint8_t* g0b = vbase + (size_t)tig * 128;
+    const int jj = gid >> 2;
+    const uint32_t vm0 = 0x03030303u << (2 * jj), vm1 = 0x03030303u << (2 * jj + 4);
+    const int colb = ((16 * half + 4 * (gid & 3)) ^ (8 * tig)) * 4;  // vswz: (G & 3) == tig
+    const uint8_t* g0b = vbase + (size_t)tig * 128 + colb;
     for (int kk = 0; kk < nv; ++kk) {
         uint32_t b[4];
         ldsm_x4(b, bbase + kk * 2 * 8 * 32);
-        const uint8_t* g0 = g0b + (size_t)kk * 8 * 128;  // token group kk*8 + tig
-        const uint8_t* g1 = g0 + 4 * 128;                // token group + 4
+        const uint4 x0 = *reinterpret_cast<const uint4*>(g0b + (size_t)kk * 8 * 128);        // group kk*8 + tig
+        const uint4 x1 = *reinterpret_cast<const uint4*>(g0b + (size_t)kk * 8 * 128 + 512);  // group + 4
+        const uint32_t u0[4] = {x0.x, x0.y, x0.z, x0.w}, u1[4] = {x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const int col = ((4 * (4 * half + m) + (gid & 3)) ^ swz) * 4;
-            const uint32_t w0 = lds32(g0 + col), w1 = lds32(g1 + col);
             uint32_t a[4];
-            a[0] = (w0 >> j0) & 0x03030303u;
-            a[1] = (w0 >> (j0 + 4)) & 0x03030303u;
-            a[2] = (w1 >> j0) & 0x03030303u;
-            a[3] = (w1 >> (j0 + 4)) & 0x03030303u;
+            a[0] = u0[m] & vm0;
+            a[1] = u0[m] & vm1;
+            a[2] = u1[m] & vm0;
+            a[3] = u1[m] & vm1;
             mma_u8u8(acc[m][0], a, b[0], b[1]);
             mma_u8u8(acc[m][1], a, b[2], b[3]);
         }
     }
-    // output straight from the fragments: head tig, channels ch and ch + 2
+    // output straight from the fragments: head tig, channels 4c + jj and 4c + jj + 2
     if (hv) {
         const float inv = __frcp_rn(lt);
+        const float s0 = vinv * (jj ? 0.25f : 1.0f), s1 = s0 * 0.0625f;
         IO* orow = out + tig * kD;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const int ch = 16 * (4 * half + m) + 4 * (gid & 3) + (gid >> 2);
+            const int ch = 4 * (16 * half + 4 * (gid & 3) + m) + jj;
             const float v0 = fmaf((float)acc[m][0][0], 65536.0f, fmaf((float)acc[m][0][1], 256.0f, (float)acc[m][1][0]));
             const float v1 = fmaf((float)acc[m][0][2], 65536.0f, fmaf((float)acc[m][0][3], 256.0f, (float)acc[m][1][2]));
-            const float r0 = fmaf(v0, vinv, bt) * inv, r1 = fmaf(v1, vinv, bt) * inv;
+            const float r0 = fmaf(v0, s0, bt) * inv, r1 = fmaf(v1, s1, bt) * inv;
             if constexpr (sizeof(IO) == 2) {
                 orow[ch] = __float2half_rn(r0);
                 orow[ch + 2] = __float2half_rn(r1);
