@@ -192,6 +192,59 @@ RDKV_API int rdkv_cuda_generate(void* out, int32_t dtype, uint64_t seed, int32_t
                                 int32_t seq_len, int32_t outlier_channels, float outlier_scale,
                                 int32_t hh_stride, float hh_boost, void* stream);
 
+
+/* ---- Single-function entry points (C++ drop-in layer, include/rdkv/cuda.hpp) */
+/* attention_probe (cache.cpp:140-184): a[r][t] = softmax_t(q_r . k_t / sqrt(d))
+ * over t <= offsets[r], exactly 0 beyond; q [rows][d], k [t_len][d] f32,
+ * offsets [rows] int32, a [rows][t_len] fp64 (all device). EINVAL when an
+ * offset is outside [0, t_len) (cache.cpp:162-164). */
+RDKV_API size_t rdkv_cuda_attention_probe_workspace(int32_t rows, int32_t t_len);
+RDKV_API int rdkv_cuda_attention_probe(const float* q, int32_t rows, const float* k, int32_t t_len,
+                                       int32_t d, const int32_t* offsets, double* a, void* workspace,
+                                       size_t workspace_bytes, void* stream);
+/* token_weights (weights.cpp:25-46): a = heads x [rows][t_len] fp64 stacked;
+ * raw_scratch [t_len] f32; out [t_len] f32 pooled weights. */
+RDKV_API int rdkv_cuda_token_weights(const double* a, int32_t heads, int32_t rows, int32_t t_len,
+                                     int32_t pool_kernel, float* raw_scratch, float* out, void* stream);
+/* moving_average (weights.cpp:8-23). */
+RDKV_API int rdkv_cuda_moving_average(const float* raw, int32_t n, int32_t kernel, float* out,
+                                      void* stream);
+/* channel_weights (weights.cpp:69-91): q [q_rows][d], k [k_rows][d] -> out [d]. */
+RDKV_API int rdkv_cuda_channel_weights(const float* q, int32_t q_rows, const float* k, int32_t k_rows,
+                                       int32_t d, float* out, void* stream);
+
+typedef struct {
+    double lambda;
+    double achieved_avg_bits;
+    double objective;
+    int32_t converged;
+    int32_t status; /* RDKV_EINVAL: a weight is negative or non-finite */
+} rdkv_bisect_result;
+
+/* mckp_bisect (allocator.cpp:135-216) over `instances` weight vectors of
+ * length n (device, [instances][n]); widths/eps (host) = the argmin table
+ * (make_argmin_table, allocator.cpp:32-37); bits [instances][n] u8 and
+ * results [instances] (device). */
+RDKV_API int rdkv_cuda_mckp_bisect(const float* weights, int32_t instances, int32_t n,
+                                   const int32_t* widths, const double* eps, int32_t n_widths,
+                                   double target_avg_bits, double tolerance, int32_t max_iterations,
+                                   int32_t strict_budget, uint8_t* bits, rdkv_bisect_result* results,
+                                   void* stream);
+
+/* quantize_unit (quantizer.cpp:104-131) over `units` rows of `len` f32
+ * values (device): codes [units][len], scale/zero_point [units],
+ * status [units] (RDKV_ENUMERIC for a non-finite unit). */
+RDKV_API int rdkv_cuda_quantize_units(const float* values, int32_t units, int32_t len, int32_t bits,
+                                      uint8_t* codes, float* scale, int64_t* zero_point,
+                                      int32_t* status, void* stream);
+
+/* fused_k_logits (trizone.cpp:210-249) per token slot of every tile:
+ * q [units][group][head_dim] f32 -> logits [units][group][max_slots] f32
+ * (slot order; NaN for pad slots). max_slots / max_kslots from the plan. */
+RDKV_API int rdkv_cuda_tile_logits(const uint8_t* arena, const int64_t* tile_offsets, int32_t units,
+                                   int32_t group, int32_t head_dim, const float* q, int32_t max_slots,
+                                   int32_t max_kslots, float* logits, void* stream);
+
 /* ---- Host-side tile inspection ----------------------------------------- */
 /* Tile header fields. */
 typedef struct {
@@ -218,6 +271,20 @@ RDKV_API int rdkv_tile_export(const uint8_t* tile_host, int32_t head_dim, int32_
                               uint8_t* payload, int32_t* segtab, int32_t* nseg, int32_t* perm,
                               int32_t* nperm);
 RDKV_API size_t rdkv_tile_export_payload_bytes(const uint8_t* tile_host, int32_t head_dim);
+
+
+/* Canonical import: the inverse of rdkv_tile_export — builds a device tile
+ * (host bytes) from the reference's TriZoneCache content: kept [n] ascending
+ * token ids, vbits_kept [n] in {2,4,8,16}, vcodes [n*d] (kept order),
+ * vscale/vzero [n], vfp [n*d] Zone B rows, kbits [d] in {0,2,4,8,16},
+ * kcodes [d*n] channel-major, kscale/kzero [d], kfp [n*d] k16 values. */
+RDKV_API size_t rdkv_tile_import_bytes(int32_t d, int32_t n, const uint8_t* vbits_kept,
+                                       const uint8_t* kbits);
+RDKV_API int rdkv_tile_import(int32_t d, int32_t n, const int32_t* kept, const uint8_t* vbits_kept,
+                              const uint8_t* vcodes, const float* vscale, const int64_t* vzero,
+                              const float* vfp, const uint8_t* kbits, const uint8_t* kcodes,
+                              const float* kscale, const int64_t* kzero, const float* kfp,
+                              uint8_t* tile, size_t tile_bytes);
 
 RDKV_API const char* rdkv_status_string(int status);
 RDKV_API int rdkv_version(void);

@@ -99,6 +99,11 @@ class TileInfo(C.Structure):
                 ("total_bytes", C.c_int64), ("decode_bytes", C.c_int64)]
 
 
+class BisectResult(C.Structure):
+    _fields_ = [("lambda_", C.c_double), ("achieved_avg_bits", C.c_double), ("objective", C.c_double),
+                ("converged", C.c_int32), ("status", C.c_int32)]
+
+
 _VP = C.c_void_p
 _SIGS = {
     "rdkv_cuda_weights_workspace": (C.c_size_t, [C.POINTER(Shape), C.c_int32]),
@@ -118,6 +123,19 @@ _SIGS = {
     "rdkv_cuda_generate": (C.c_int, [_VP, C.c_int32, C.c_uint64, C.c_int32, C.c_uint64,
                                      C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_float,
                                      C.c_int32, C.c_float, _VP]),
+    "rdkv_cuda_attention_probe_workspace": (C.c_size_t, [C.c_int32, C.c_int32]),
+    "rdkv_cuda_attention_probe": (C.c_int, [_VP, C.c_int32, _VP, C.c_int32, C.c_int32, _VP, _VP, _VP,
+                                            C.c_size_t, _VP]),
+    "rdkv_cuda_token_weights": (C.c_int, [_VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP]),
+    "rdkv_cuda_moving_average": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP, _VP]),
+    "rdkv_cuda_channel_weights": (C.c_int, [_VP, C.c_int32, _VP, C.c_int32, C.c_int32, _VP, _VP]),
+    "rdkv_cuda_mckp_bisect": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP, _VP, C.c_int32, C.c_double,
+                                        C.c_double, C.c_int32, C.c_int32, _VP, _VP, _VP]),
+    "rdkv_cuda_quantize_units": (C.c_int, [_VP, C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP, _VP]),
+    "rdkv_cuda_tile_logits": (C.c_int, [_VP, _VP, C.c_int32, C.c_int32, C.c_int32, _VP, C.c_int32,
+                                        C.c_int32, _VP, _VP]),
+    "rdkv_tile_import_bytes": (C.c_size_t, [C.c_int32, C.c_int32, _VP, _VP]),
+    "rdkv_tile_import": (C.c_int, [C.c_int32, C.c_int32] + [_VP] * 12 + [C.c_size_t]),
     "rdkv_tile_info_get": (C.c_int, [_VP, C.POINTER(TileInfo)]),
     "rdkv_tile_export": (C.c_int, [_VP, C.c_int32] + [_VP] * 14),
     "rdkv_tile_export_payload_bytes": (C.c_size_t, [_VP, C.c_int32]),

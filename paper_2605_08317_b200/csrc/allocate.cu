@@ -16,8 +16,9 @@
 // ties, the bit total is an exact integer reduction converted once to fp64
 // (allocator.cpp:55-60), and the lambda sequence uses the same fp64
 // expressions as the reference — so v_bits, k_bits, lambda and the
-// convergence flags are identical given identical weights. Only the reported
-// objective (a plain fp64 sum) uses a tree reduction (<= 1e-12 relative).
+// convergence flags are identical given identical weights. The reported
+// objectives are summed by one thread in the reference's order (a sequential
+// fp64 sum, allocator.cpp:301-311), so they are bit-identical too.
 #include "common.cuh"
 
 namespace rdkv_b200 {
@@ -149,6 +150,12 @@ __device__ double eps_of(const AllocTable& t, int b) {
     return 0.0;
 }
 
+__device__ double sequential_objective(const float* w, const uint8_t* bits, int n, const AllocTable& t) {
+    double obj = 0.0;
+    for (int u = 0; u < n; ++u) obj = __dadd_rn(obj, __dmul_rn((double)w[u], eps_of(t, bits[u])));
+    return obj;
+}
+
 __global__ void __launch_bounds__(kAllocThreads) allocate_kernel(
     const float* __restrict__ w_t, const float* __restrict__ w_c, int t_len, int d, int kv_heads,
     rdkv_config cfg, int window, uint8_t* __restrict__ v_bits_all, uint8_t* __restrict__ k_bits_all,
@@ -187,7 +194,6 @@ __global__ void __launch_bounds__(kAllocThreads) allocate_kernel(
     }
 
     // Stage 2: V tokens (allocate_v)
-    double obj_part = 0.0;
     if (!(vbud > 0.0)) {
         for (int u = threadIdx.x; u < t_len; u += blockDim.x) vb[u] = 0;
         out.v_converged = 1;
@@ -212,12 +218,12 @@ __global__ void __launch_bounds__(kAllocThreads) allocate_kernel(
         kept += b > 0;
         v16 += b == 16;
         vsum += b;
-        obj_part = __dadd_rn(obj_part, __dmul_rn((double)wv[u], eps_of(tv, b)));
     }
     kept = block_reduce_sum<long long>(kept, s.ll);
     v16 = block_reduce_sum<long long>(v16, s.ll);
     vsum = block_reduce_sum<long long>(vsum, s.ll);
-    out.objective_v = block_reduce_sum<double>(obj_part, s.d);
+    // allocation_objective (allocator.cpp:301-311) in the reference's sequential order
+    if (threadIdx.x == 0) out.objective_v = sequential_objective(wv, vb, t_len, tv);
 
     // Stage 3: K channels over kept tokens (allocate_k)
     int k_len = d;
@@ -240,16 +246,10 @@ __global__ void __launch_bounds__(kAllocThreads) allocate_kernel(
         out.k_converged = r.converged;
     }
     __syncthreads();
-    double kobj = 0.0;
-    if (k_len > 0) {
-        for (int u = threadIdx.x; u < d; u += blockDim.x) {
-            ksum += kb[u];
-            kobj = __dadd_rn(kobj, __dmul_rn((double)wk[u], eps_of(tk, kb[u])));
-        }
-    }
+    if (k_len > 0)
+        for (int u = threadIdx.x; u < d; u += blockDim.x) ksum += kb[u];
     ksum = block_reduce_sum<long long>(ksum, s.ll);
-    kobj = block_reduce_sum<double>(kobj, s.d);
-    out.objective_k = k_len > 0 ? kobj : 0.0;
+    if (threadIdx.x == 0) out.objective_k = k_len > 0 ? sequential_objective(wk, kb, d, tk) : 0.0;
     out.n_kept = (int)kept;
     out.n_v16 = (int)v16;
     out.k_bits_len = k_len;
@@ -294,5 +294,62 @@ extern "C" RDKV_API int rdkv_cuda_allocate(const float* w_t, const float* w_c, c
     if (cfg->force_window_retain && window > s->seq_len) return RDKV_EINVAL;
     allocate_kernel<<<s->units, kAllocThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         w_t, w_c, s->seq_len, s->head_dim, s->kv_heads, *cfg, window, v_bits, k_bits, stats);
+    return launch_status();
+}
+
+// ---------------------------------------------------------------------------
+// Stand-alone mckp_bisect (allocator.cpp:135-216) over `instances`
+// independent weight vectors of length n, one CTA each.
+__global__ void __launch_bounds__(kAllocThreads) mckp_kernel(const float* __restrict__ w_all, int n,
+                                                            AllocTable t, double target, double tol, int max_it,
+                                                            int strict, uint8_t* __restrict__ bits_all,
+                                                            rdkv_bisect_result* __restrict__ res) {
+    __shared__ Scratch s;
+    const float* w = w_all + (size_t)blockIdx.x * n;
+    uint8_t* bits = bits_all + (size_t)blockIdx.x * n;
+    int bad = 0;
+    for (int u = threadIdx.x; u < n; u += blockDim.x) bad |= !(isfinite(w[u]) && w[u] >= 0.0f);
+    bad = block_reduce_sum<int>(bad, s.i);
+    rdkv_bisect_result out{};
+    if (bad) {  // check_weights (allocator.cpp:63-69)
+        out.status = RDKV_EINVAL;
+        if (threadIdx.x == 0) res[blockIdx.x] = out;
+        return;
+    }
+    const int all_max = target >= (double)t.widths[t.n - 1];
+    BisectResult r = bisect(w, n, t, target, tol, max_it, strict, s);
+    materialize_bits(w, n, t, r.lambda, all_max, bits);
+    __syncthreads();
+    out.lambda = r.lambda;
+    out.achieved_avg_bits = r.avg;
+    if (threadIdx.x == 0) out.objective = sequential_objective(w, bits, n, t);
+    out.converged = r.converged;
+    out.status = RDKV_OK;
+    if (threadIdx.x == 0) res[blockIdx.x] = out;
+}
+
+extern "C" RDKV_API int rdkv_cuda_mckp_bisect(const float* weights, int32_t instances, int32_t n,
+                                              const int32_t* widths, const double* eps, int32_t n_widths,
+                                              double target_avg_bits, double tolerance, int32_t max_iterations,
+                                              int32_t strict_budget, uint8_t* bits, rdkv_bisect_result* results,
+                                              void* stream) {
+    if (!widths || !eps || n_widths < 1 || n_widths > 8) return RDKV_EINVAL;
+    AllocTable t{};
+    t.n = n_widths;
+    for (int i = 0; i < n_widths; ++i) {  // BitSet::validate_relaxed (quantizer.cpp:66-80)
+        const int b = widths[i];
+        if (b < 0 || b > 16 || b % 2 || (i > 0 && b <= widths[i - 1])) return RDKV_EINVAL;
+        if (b != 0 && b != 2 && b != 4 && b != 8 && b != 16) return RDKV_EINVAL;
+        if (!(eps[i] >= 0.0) || !isfinite(eps[i])) return RDKV_EINVAL;
+        t.widths[i] = b;
+        t.eps[i] = eps[i];
+    }
+    if (!(tolerance > 0.0) || max_iterations < 1) return RDKV_EINVAL;      // SolverConfig::validate
+    if (!(target_avg_bits > 0.0) || target_avg_bits > 16.0) return RDKV_EINVAL;  // allocator.cpp:140-142
+    if (instances < 0 || n < 0 || (instances > 0 && n > 0 && (!weights || !bits || !results)))
+        return RDKV_EINVAL;
+    if (instances == 0 || n == 0) return RDKV_OK;
+    mckp_kernel<<<instances, kAllocThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        weights, n, t, target_avg_bits, tolerance, max_iterations, strict_budget, bits, results);
     return launch_status();
 }

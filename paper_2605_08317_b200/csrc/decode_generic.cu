@@ -362,3 +362,84 @@ extern "C" RDKV_API int rdkv_cuda_append(void* zc_k, void* zc_v, int32_t* zc_len
         return RDKV_EINVAL;
     return launch_status();
 }
+
+// ---------------------------------------------------------------------------
+// fused_k_logits (trizone.cpp:210-249) per token slot: the decode kernel's
+// QK product without the 1/sqrt(d) scale, for every (tile, query head).
+// logits [units][group][max_slots] f32, NaN in pad slots and past nslot.
+namespace rdkv_b200 {
+
+__global__ void tile_logits_kernel(const uint8_t* __restrict__ arena, const int64_t* __restrict__ offsets,
+                                   int g, int d, const float* __restrict__ q_all, int max_slots,
+                                   float* __restrict__ logits) {
+    extern __shared__ float smem[];
+    __shared__ TileHeader h;
+    __shared__ int sbase[5];
+    const int unit = blockIdx.x, hh = blockIdx.y;
+    const uint8_t* tile = arena + offsets[unit];
+    if (threadIdx.x == 0) {
+        h = *reinterpret_cast<const TileHeader*>(tile);
+        int acc = 0;
+        for (int i = 0; i < 4; ++i) {
+            sbase[i] = acc;
+            acc += pad4(h.r[i]);
+        }
+        sbase[4] = acc;
+    }
+    __syncthreads();
+    float* qs = smem;          // [d]
+    float* qt = smem + d;      // [kslots]
+    const float* q = q_all + ((size_t)unit * g + hh) * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) qs[i] = q[i];
+    __syncthreads();
+    const float2* chan = reinterpret_cast<const float2*>(tile + chan_table_off());
+    const uint16_t* perm = reinterpret_cast<const uint16_t*>(tile + perm_off(h));
+    for (int sl = threadIdx.x; sl < h.kslots; sl += blockDim.x) qt[sl] = chan[sl].x * qs[perm[sl]];
+    __shared__ float bias;
+    if (threadIdx.x == 0) {
+        float b = 0.0f;
+        for (int sl = 0; sl < h.kslots; ++sl) b = fmaf(qs[perm[sl]], chan[sl].y, b);
+        bias = b;
+    }
+    __syncthreads();
+    float* outp = logits + ((size_t)unit * g + hh) * max_slots;
+    for (int i = threadIdx.x; i < max_slots; i += blockDim.x) {
+        float acc = __int_as_float(0x7fc00000);
+        if (i < h.nslot) {
+            int li;
+            const int cls = slot_class(h, sbase, i, li);
+            if (li < h.r[cls]) {
+                acc = 0.0f;
+                const uint8_t* row = tile + h.off_k + (size_t)i * h.krow_bytes;
+                for (int kc = 0; kc < 3; ++kc) {
+                    const int bits = kBits(kc);
+                    for (int j = 0; j < h.c[kc]; ++j) {
+                        const int bit = j * bits;
+                        const uint32_t code = (row[h.kbyte_base[kc] + (bit >> 3)] >> (bit & 7)) & ((1u << bits) - 1u);
+                        acc = fmaf(qt[h.kslot_base[kc] + j], (float)code, acc);
+                    }
+                }
+                const __half* k16 = reinterpret_cast<const __half*>(row + h.kbyte_base[3]);
+                for (int j = 0; j < h.c[3]; ++j) acc = fmaf(qt[h.kslot_base[3] + j], __half2float(k16[j]), acc);
+                acc += bias;
+            }
+        }
+        outp[i] = acc;
+    }
+}
+
+}  // namespace rdkv_b200
+
+extern "C" RDKV_API int rdkv_cuda_tile_logits(const uint8_t* arena, const int64_t* tile_offsets, int32_t units,
+                                              int32_t group, int32_t head_dim, const float* q, int32_t max_slots,
+                                              int32_t max_kslots, float* logits, void* stream) {
+    if (!arena || !tile_offsets || !q || !logits || units < 0 || group < 1 || head_dim < 1 || max_slots < 0 ||
+        max_kslots < 0)
+        return RDKV_EINVAL;
+    if (units == 0 || max_slots == 0) return RDKV_OK;
+    const size_t smem = sizeof(float) * ((size_t)head_dim + max_kslots);
+    if (smem > 48 * 1024) return RDKV_EINVAL;
+    tile_logits_kernel<<<dim3(units, group), 128, smem, static_cast<cudaStream_t>(stream)>>>(
+        arena, tile_offsets, group, head_dim, q, max_slots, logits);
+    return launch_status();
+}

@@ -215,6 +215,130 @@ extern "C" RDKV_API int rdkv_tile_export(const uint8_t* tile_host, int32_t d, in
     return RDKV_OK;
 }
 
+namespace {
+
+int import_header(int32_t d, int32_t n, const uint8_t* vbits_kept, const uint8_t* kbits, TileHeader& h) {
+    if (d < 1 || d > 65535 || n < 0 || (n > 0 && !vbits_kept) || !kbits) return RDKV_EINVAL;
+    std::memset(&h, 0, sizeof(h));
+    for (int i = 0; i < n; ++i) {
+        const int cls = class_of_bits(vbits_kept[i]);
+        if (cls < 0) return RDKV_EINVAL;
+        h.r[cls]++;
+    }
+    for (int c = 0; c < d; ++c) {
+        if (kbits[c] == 0) continue;
+        const int cls = class_of_bits(kbits[c]);
+        if (cls < 0) return RDKV_EINVAL;
+        h.c[cls]++;
+    }
+    tile_layout(h, d);
+    return RDKV_OK;
+}
+
+void put_bits(uint8_t* row, int j, int bits, unsigned code) {
+    if (bits == 8) row[j] = (uint8_t)code;
+    else if (bits == 4) row[j >> 1] |= (uint8_t)((code & 15u) << ((j & 1) * 4));
+    else row[j >> 2] |= (uint8_t)((code & 3u) << ((j & 3) * 2));
+}
+
+void put_half(uint8_t* p, float x) {
+    const __half v = __float2half_rn(x);
+    std::memcpy(p, &v, 2);
+}
+
+float offset_of(float scale, int64_t zero) { return (float)(-(double)scale * (double)zero); }
+
+}  // namespace
+
+extern "C" RDKV_API size_t rdkv_tile_import_bytes(int32_t d, int32_t n, const uint8_t* vbits_kept,
+                                                  const uint8_t* kbits) {
+    TileHeader h;
+    return import_header(d, n, vbits_kept, kbits, h) ? 0 : (size_t)h.total_bytes;
+}
+
+extern "C" RDKV_API int rdkv_tile_import(int32_t d, int32_t n, const int32_t* kept, const uint8_t* vbits_kept,
+                                         const uint8_t* vcodes, const float* vscale, const int64_t* vzero,
+                                         const float* vfp, const uint8_t* kbits, const uint8_t* kcodes,
+                                         const float* kscale, const int64_t* kzero, const float* kfp,
+                                         uint8_t* tile, size_t tile_bytes) {
+    TileHeader h;
+    if (int rc = import_header(d, n, vbits_kept, kbits, h)) return rc;
+    if (!tile || tile_bytes < (size_t)h.total_bytes) return RDKV_EINVAL;
+    if (n > 0 && (!kept || !vcodes || !vscale || !vzero || !vfp || !kcodes || !kscale || !kzero || !kfp))
+        return RDKV_EINVAL;
+    for (int i = 1; i < n; ++i)
+        if (kept[i] <= kept[i - 1]) return RDKV_EINVAL;  // kept is ascending (trizone.hpp:63)
+    std::memset(tile, 0, h.total_bytes);
+    std::memcpy(tile, &h, sizeof(h));
+
+    // token slots: class order, ascending id inside a class (pads carry id -1)
+    std::vector<int> slot_of(n);
+    int32_t* ids = reinterpret_cast<int32_t*>(tile + h.off_ids);
+    for (int s = 0; s < h.nslot; ++s) ids[s] = -1;
+    int cursor[4];
+    for (int cls = 0; cls < 4; ++cls) cursor[cls] = slot_base(h, cls);
+    for (int i = 0; i < n; ++i) {
+        const int cls = class_of_bits(vbits_kept[i]);
+        slot_of[i] = cursor[cls]++;
+        ids[slot_of[i]] = kept[i];
+    }
+    if (n == 0) return RDKV_OK;
+
+    // K slots (channel_perm order) with their dequantisation table
+    float* chan = reinterpret_cast<float*>(tile + chan_table_off());
+    uint16_t* perm = reinterpret_cast<uint16_t*>(tile + perm_off(h));
+    int64_t* kz = reinterpret_cast<int64_t*>(tile + h.off_kz);
+    std::vector<int> kslot_of(d, -1);
+    int kc[4] = {0, 0, 0, 0};
+    for (int c = 0; c < d; ++c) {
+        if (kbits[c] == 0) continue;
+        const int cls = class_of_bits(kbits[c]);
+        const int ks = h.kslot_base[cls] + kc[cls]++;
+        kslot_of[c] = ks;
+        perm[ks] = (uint16_t)c;
+        if (cls == 3) {
+            chan[2 * ks] = 1.0f;
+        } else {
+            chan[2 * ks] = kscale[c];
+            chan[2 * ks + 1] = offset_of(kscale[c], kzero[c]);
+            kz[ks] = kzero[c];
+        }
+    }
+    // K rows per slot
+    for (int i = 0; i < n; ++i) {
+        uint8_t* row = tile + h.off_k + (size_t)slot_of[i] * h.krow_bytes;
+        for (int c = 0; c < d; ++c) {
+            const int ks = kslot_of[c];
+            if (ks < 0) continue;
+            const int cls = class_of_bits(kbits[c]);
+            const int j = ks - h.kslot_base[cls];
+            if (cls == 3) put_half(row + h.kbyte_base[3] + 2 * j, kfp[(size_t)i * d + c]);
+            else put_bits(row + h.kbyte_base[cls], j, kBits(cls), kcodes[(size_t)c * n + i]);
+        }
+    }
+    // V rows + parameters
+    float* vp = reinterpret_cast<float*>(tile + h.off_vp);
+    int64_t* vz = reinterpret_cast<int64_t*>(tile + h.off_vz);
+    std::vector<uint8_t> packed;
+    for (int i = 0; i < n; ++i) {
+        const int cls = class_of_bits(vbits_kept[i]);
+        const int li = slot_of[i] - slot_base(h, cls);
+        if (cls == 3) {
+            uint8_t* dst = tile + h.off_vseg[3] + (size_t)li * d * 2;
+            for (int c = 0; c < d; ++c) put_half(dst + 2 * c, vfp[(size_t)i * d + c]);
+            continue;
+        }
+        const int bits = kBits(cls), rb = ref_row_bytes(d, bits);
+        packed.assign(rb, 0);
+        for (int c = 0; c < d; ++c) put_bits(packed.data(), c, bits, vcodes[(size_t)i * d + c]);
+        for (int m = 0; m < rb; ++m) tile[vbyte_offset(h, cls, li, m, d)] = packed[m];
+        vp[2 * slot_of[i]] = vscale[i];
+        vp[2 * slot_of[i] + 1] = offset_of(vscale[i], vzero[i]);
+        vz[slot_of[i]] = vzero[i];
+    }
+    return RDKV_OK;
+}
+
 extern "C" RDKV_API const char* rdkv_status_string(int status) {
     switch (status) {
         case RDKV_OK: return "ok";

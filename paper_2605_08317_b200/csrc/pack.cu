@@ -392,3 +392,56 @@ extern "C" RDKV_API int rdkv_cuda_pack(const void* k, const void* v, int32_t dty
         return RDKV_EINVAL;
     return launch_status();
 }
+
+// ---------------------------------------------------------------------------
+// quantize_unit (quantizer.cpp:104-131) over many independent units: one
+// warp per unit of `len` contiguous f32 values. Codes [units][len] u8,
+// params per unit; status[u] = RDKV_ENUMERIC for a non-finite unit.
+namespace rdkv_b200 {
+
+__global__ void quantize_units_kernel(const float* __restrict__ x, int units, int len, int bits,
+                                      uint8_t* __restrict__ codes, float* __restrict__ scale_out,
+                                      int64_t* __restrict__ zero_out, int32_t* __restrict__ status) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= units) return;
+    const float* row = x + (size_t)warp * len;
+    float lo = row[0], hi = row[0];
+    int bad = 0;
+    for (int i = lane; i < len; i += 32) {
+        const float v = row[i];
+        bad |= !isfinite(v);
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+    }
+    lo = -warp_max(-lo);
+    hi = warp_max(hi);
+    bad = __any_sync(0xffffffffu, bad);
+    if (bad) {
+        if (lane == 0) status[warp] = RDKV_ENUMERIC;
+        return;
+    }
+    double scale, zd;
+    quant_params(lo, hi, bits, scale, zd);
+    for (int i = lane; i < len; i += 32) codes[(size_t)warp * len + i] = (uint8_t)quant_code(row[i], scale, zd, bits);
+    if (lane == 0) {
+        scale_out[warp] = (float)scale;
+        zero_out[warp] = (int64_t)zd;
+        status[warp] = RDKV_OK;
+    }
+}
+
+}  // namespace rdkv_b200
+
+extern "C" RDKV_API int rdkv_cuda_quantize_units(const float* values, int32_t units, int32_t len, int32_t bits,
+                                                 uint8_t* codes, float* scale, int64_t* zero_point,
+                                                 int32_t* status, void* stream) {
+    if (bits != 2 && bits != 4 && bits != 8) return RDKV_EINVAL;  // quantizer.cpp:105-107
+    if (len < 1) return RDKV_EINVAL;                               // :108
+    if (units < 0 || !values || !codes || !scale || !zero_point || !status) return RDKV_EINVAL;
+    if (units == 0) return RDKV_OK;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)(((size_t)units * 32 + threads - 1) / threads);
+    quantize_units_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+        values, units, len, bits, codes, scale, zero_point, status);
+    return launch_status();
+}

@@ -38,7 +38,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) probe_logits_kernel(
     const T* __restrict__ k, const T* __restrict__ q, int t_len, int d, int rows_total,
     int window, int probe_rows, int group, double inv_sqrt_d, int row_tiles,
-    double* __restrict__ logits, double* __restrict__ tile_max) {
+    double* __restrict__ logits, double* __restrict__ tile_max, const int* __restrict__ offsets) {
     __shared__ double qs[kW1Rows][kW1Chunk + 1];
     __shared__ double ks[kW1Toks][kW1Chunk + 1];
     const int unit = blockIdx.y / row_tiles;
@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(256) probe_logits_kernel(
     for (int i = 0; i < 4; ++i) {
         const int row = row0 + ty + 16 * i;
         const int r = row % window;
-        const int off = t_len - window + r;  // causal offset, pipeline.cpp:129-130
+        // causal offset (pipeline.cpp:129-130) unless the caller gives one per row
+        const int off = offsets ? offsets[row] : t_len - window + r;
         double mx = -INFINITY;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -114,11 +115,12 @@ __global__ void __launch_bounds__(256) probe_softmax_kernel(double* __restrict__
                                                             const double* __restrict__ tile_max,
                                                             int ntt, int t_len, int window,
                                                             int rows_total,
-                                                            double* __restrict__ denom) {
+                                                            double* __restrict__ denom,
+                                                            const int* __restrict__ offsets) {
     __shared__ double red[8];
     const int ur = blockIdx.x;  // unit * rows_total + row
     const int row = ur % rows_total;
-    const int off = t_len - window + (row % window);
+    const int off = offsets ? offsets[row] : t_len - window + (row % window);
     double mx = -INFINITY;
     for (int i = threadIdx.x; i < ntt; i += blockDim.x) mx = fmax(mx, tile_max[(size_t)ur * ntt + i]);
     mx = warp_max_d(mx);
@@ -239,8 +241,8 @@ static int run_weights(const T* k, const T* q, const rdkv_shape* s, int window, 
     const int row_tiles = (R + kW1Rows - 1) / kW1Rows;
     dim3 grid1(ntt, U * row_tiles);
     probe_logits_kernel<T><<<grid1, 256, 0, st>>>(k, q, t_len, d, R, window, s->probe_rows, g,
-                                                  inv_sqrt_d, row_tiles, ws.logits, ws.tile_max);
-    probe_softmax_kernel<<<U * R, 256, 0, st>>>(ws.logits, ws.tile_max, ntt, t_len, window, R, ws.denom);
+                                                  inv_sqrt_d, row_tiles, ws.logits, ws.tile_max, nullptr);
+    probe_softmax_kernel<<<U * R, 256, 0, st>>>(ws.logits, ws.tile_max, ntt, t_len, window, R, ws.denom, nullptr);
     const size_t nt = (size_t)U * t_len;
     token_raw_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(ws.logits, ws.denom, U, R, t_len, ws.rawf);
     token_pool_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(ws.rawf, U, t_len, pool_kernel, w_t);
@@ -279,4 +281,111 @@ extern "C" RDKV_API int rdkv_cuda_weights(const void* k, const void* probe_q, in
         return run_weights(static_cast<const __half*>(k), static_cast<const __half*>(probe_q), s, w,
                            pool_kernel, w_t, w_c, ws, st);
     return RDKV_EINVAL;
+}
+
+// ---------------------------------------------------------------------------
+// Single-function entry points behind the C++ drop-in API (include/rdkv/):
+// attention_probe with arbitrary causal offsets (cache.cpp:140-184),
+// token_weights over given attention matrices (weights.cpp:25-46),
+// moving_average (weights.cpp:8-23), channel_weights (weights.cpp:69-91).
+namespace rdkv_b200 {
+
+__global__ void probe_normalize_kernel(double* __restrict__ e, const double* __restrict__ denom, int rows,
+                                       int t_len, const int* __restrict__ offsets) {
+    const size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (idx >= (size_t)rows * t_len) return;
+    const int r = (int)(idx / t_len), t = (int)(idx % t_len);
+    e[idx] = t <= offsets[r] ? e[idx] / denom[r] : 0.0;
+}
+
+__global__ void offsets_check_kernel(const int* __restrict__ offsets, int rows, int t_len, int* __restrict__ bad) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < rows && (offsets[r] < 0 || offsets[r] >= t_len)) atomicOr(bad, 1);
+}
+
+__global__ void column_sum_kernel(const double* __restrict__ a, int heads, int rows, int t_len,
+                                  float* __restrict__ rawf) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= t_len) return;
+    double acc = 0.0;
+    for (int hr = 0; hr < heads * rows; ++hr) acc = __dadd_rn(acc, a[(size_t)hr * t_len + t]);
+    rawf[t] = (float)acc;
+}
+
+template <typename T>
+__global__ void channel_norm_rows_kernel(const T* __restrict__ q, int q_rows, const T* __restrict__ k, int k_rows,
+                                         int d, double inv_sqrt_d, float* __restrict__ w_c) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= d) return;
+    double qq = 0.0, kk = 0.0;
+    for (int r = 0; r < q_rows; ++r) {
+        const double x = load_as_float(q, (size_t)r * d + c);
+        qq = __fma_rn(x, x, qq);
+    }
+#pragma unroll 8
+    for (int r = 0; r < k_rows; ++r) {
+        const double x = load_as_float(k, (size_t)r * d + c);
+        kk = __fma_rn(x, x, kk);
+    }
+    w_c[c] = (float)__dmul_rn(__dmul_rn(sqrt(qq), sqrt(kk)), inv_sqrt_d);
+}
+
+}  // namespace rdkv_b200
+
+extern "C" RDKV_API size_t rdkv_cuda_attention_probe_workspace(int32_t rows, int32_t t_len) {
+    rdkv_shape s{1, t_len, 1, 1, rows, 1};
+    return carve(&s, rows, nullptr).bytes + 256;
+}
+
+extern "C" RDKV_API int rdkv_cuda_attention_probe(const float* q, int32_t rows, const float* k, int32_t t_len,
+                                                  int32_t d, const int32_t* offsets, double* a, void* workspace,
+                                                  size_t workspace_bytes, void* stream) {
+    if (!q || !k || !offsets || !a || rows < 1 || t_len < 1 || d < 1) return RDKV_EINVAL;
+    rdkv_shape s{1, t_len, d, 1, rows, 1};
+    WeightsWorkspace ws = carve(&s, rows, workspace);
+    if (!workspace || workspace_bytes < ws.bytes + 256) return RDKV_EINVAL;
+    int* bad = reinterpret_cast<int*>(static_cast<char*>(workspace) + ws.bytes);
+    auto st = static_cast<cudaStream_t>(stream);
+    RDKV_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    offsets_check_kernel<<<(rows + 127) / 128, 128, 0, st>>>(offsets, rows, t_len, bad);
+    int hbad = 0;
+    RDKV_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RDKV_CUDA_TRY(cudaStreamSynchronize(st));
+    if (hbad) return RDKV_EINVAL;  // cache.cpp:162-164
+    const double inv_sqrt_d = 1.0 / sqrt((double)d);
+    const int ntt = (t_len + kW1Toks - 1) / kW1Toks;
+    const int row_tiles = (rows + kW1Rows - 1) / kW1Rows;
+    probe_logits_kernel<float><<<dim3(ntt, row_tiles), 256, 0, st>>>(k, q, t_len, d, rows, rows, rows, 1, inv_sqrt_d,
+                                                                   row_tiles, ws.logits, ws.tile_max, offsets);
+    probe_softmax_kernel<<<rows, 256, 0, st>>>(ws.logits, ws.tile_max, ntt, t_len, rows, rows, ws.denom, offsets);
+    const size_t n = (size_t)rows * t_len;
+    probe_normalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ws.logits, ws.denom, rows, t_len, offsets);
+    RDKV_CUDA_TRY(cudaMemcpyAsync(a, ws.logits, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return launch_status();
+}
+
+extern "C" RDKV_API int rdkv_cuda_token_weights(const double* a, int32_t heads, int32_t rows, int32_t t_len,
+                                                int32_t pool_kernel, float* raw_scratch, float* out, void* stream) {
+    if (!a || !raw_scratch || !out || heads < 1 || rows < 0 || t_len < 1) return RDKV_EINVAL;
+    if (pool_kernel < 1 || pool_kernel % 2 == 0) return RDKV_EINVAL;
+    auto st = static_cast<cudaStream_t>(stream);
+    column_sum_kernel<<<(t_len + 255) / 256, 256, 0, st>>>(a, heads, rows, t_len, raw_scratch);
+    token_pool_kernel<<<(t_len + 255) / 256, 256, 0, st>>>(raw_scratch, 1, t_len, pool_kernel, out);
+    return launch_status();
+}
+
+extern "C" RDKV_API int rdkv_cuda_moving_average(const float* raw, int32_t n, int32_t kernel, float* out,
+                                                 void* stream) {
+    if (!raw || !out || n < 0 || kernel < 1 || kernel % 2 == 0) return RDKV_EINVAL;
+    if (n == 0) return RDKV_OK;
+    token_pool_kernel<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(raw, 1, n, kernel, out);
+    return launch_status();
+}
+
+extern "C" RDKV_API int rdkv_cuda_channel_weights(const float* q, int32_t q_rows, const float* k, int32_t k_rows,
+                                                  int32_t d, float* out, void* stream) {
+    if (!q || !k || !out || q_rows < 0 || k_rows < 0 || d < 1) return RDKV_EINVAL;
+    channel_norm_rows_kernel<float><<<(d + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        q, q_rows, k, k_rows, d, 1.0 / sqrt((double)d), out);
+    return launch_status();
 }

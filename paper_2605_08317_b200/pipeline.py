@@ -267,6 +267,41 @@ def export_tile(tile: np.ndarray, d: int) -> dict:
             "info": info}
 
 
+def import_tile(d: int, kept, v_bits_kept, vcodes, vscale, vzero, vfp, k_bits, kcodes, kscale, kzero,
+                kfp) -> np.ndarray:
+    """Device tile bytes (host copy) from a reference TriZone view (rdkv_tile_import)."""
+    L = capi.lib()
+    n = len(kept)
+    m = max(n, 1)
+
+    def arr(x, dt, shape):
+        a = np.zeros(shape, dt)
+        x = np.asarray(x, dt)
+        if x.size:
+            a.reshape(-1)[: x.size] = x.reshape(-1)
+        return a
+
+    kept_a = arr(kept, np.int32, m)
+    vb = arr(v_bits_kept, np.uint8, m)
+    kb = arr(k_bits, np.uint8, d)
+    vc = arr(vcodes, np.uint8, (m, d))
+    vs = arr(vscale, np.float32, m)
+    vz = arr(vzero, np.int64, m)
+    vf = arr(vfp, np.float32, (m, d))
+    kc = arr(kcodes, np.uint8, (d, m))  # channel-major, row stride n
+    ks = arr(kscale, np.float32, d)
+    kz = arr(kzero, np.int64, d)
+    kf = arr(kfp, np.float32, (m, d))
+    nbytes = int(L.rdkv_tile_import_bytes(d, n, vb.ctypes.data, kb.ctypes.data))
+    if nbytes == 0:
+        raise_for(capi.RDKV_EINVAL, "tile_import_bytes")
+    tile = np.zeros(nbytes, np.uint8)
+    raise_for(L.rdkv_tile_import(d, n, kept_a.ctypes.data, vb.ctypes.data, vc.ctypes.data, vs.ctypes.data,
+                                 vz.ctypes.data, vf.ctypes.data, kb.ctypes.data, kc.ctypes.data, ks.ctypes.data,
+                                 kz.ctypes.data, kf.ctypes.data, tile.ctypes.data, nbytes), "tile_import")
+    return tile
+
+
 def build_packed_model(k, v, alloc: Allocation, group, zc_cap=0) -> PackedModel:
     """build_trizone for every unit into one arena (trizone.cpp:478-490)."""
     _check_cuda(k, v)

@@ -1,0 +1,611 @@
+// test_dropin.cpp — parity of the C++ drop-in (rdkv::cuda, include/rdkv/cuda.hpp,
+// running on the B200) against the UNMODIFIED reference library (rdkv::,
+// compiled from /root/reference by oracle/Makefile into oracle/_ref/librdkv_core.a).
+//
+// Test infrastructure only. Mirrors the reference's own suites:
+//   KATs          test_quantizer.cpp:33-41, test_weights.cpp:15-21, 99-112,
+//                 test_cache.cpp:47-71, test_trizone.cpp:191-232,
+//                 test_allocator.cpp:119-130, 189-210
+//   properties    acceptance.cpp:253-330 (random allocations over every tier),
+//                 test_trizone.cpp:256-352 (all-K-removed, Zone-C-only, appends)
+//   pipeline      allocate_model / build_packed_model / packed_decode_step on
+//                 gen_synthetic_cache inputs (test_pipeline.cpp)
+// Bars: bit-exact for allocations, codes, params, payload bytes and
+// objectives; attention probe within 1e-12 relative (CUDA vs glibc exp);
+// decode within 1e-3 l2-relative (fp16 storage of Zone B / k16 / Zone C,
+// f32 accumulation), logits within 1e-5.
+//
+// Prints one line per check and exits non-zero on any failure.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "rdkv/cuda.hpp"
+
+namespace {
+
+int g_fail = 0, g_pass = 0;
+
+void report(const std::string& name, bool ok, const std::string& detail = "") {
+    std::printf("%s %-44s %s\n", ok ? "PASS" : "FAIL", name.c_str(), detail.c_str());
+    std::fflush(stdout);
+    (ok ? g_pass : g_fail)++;
+}
+
+void run(const std::string& name, const std::function<bool(std::string&)>& fn) {
+    std::string detail;
+    bool ok = false;
+    try {
+        ok = fn(detail);
+    } catch (const std::exception& e) {
+        detail = std::string("unexpected exception: ") + e.what();
+    }
+    report(name, ok, detail);
+}
+
+template <typename Ex, typename F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const Ex&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+struct Gen {
+    std::mt19937_64 eng;
+    explicit Gen(uint64_t s) : eng(s) {}
+    double uni() { return (double)(eng() >> 11) * 0x1p-53; }
+    float gauss() {
+        double u1 = uni(), u2 = uni();
+        if (u1 < 1e-300) u1 = 1e-300;
+        return (float)(std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2));
+    }
+    int pick(int lo, int hi) { return lo + (int)(eng() % (uint64_t)(hi - lo + 1)); }
+};
+
+rdkv::DistortionTable eps_table(bool token) {
+    rdkv::DistortionTable t;
+    t.granularity = token ? rdkv::Granularity::token : rdkv::Granularity::channel;
+    if (token)
+        t.eps = {{0, 1.0}, {2, 0.313}, {4, 0.014}, {8, 4.9e-5}, {16, 0.0}};
+    else
+        t.eps = {{0, 1.0}, {2, 0.149}, {4, 0.0062}, {8, 2.2e-5}, {16, 0.0}};
+    return t;
+}
+
+double l2_rel(const std::vector<double>& got, const std::vector<double>& want) {
+    double num = 0, den = 0;
+    for (size_t i = 0; i < want.size(); ++i) {
+        num += (got[i] - want[i]) * (got[i] - want[i]);
+        den += want[i] * want[i];
+    }
+    return std::sqrt(num) / std::max(std::sqrt(den), 1e-300);
+}
+
+bool same_params(const std::vector<rdkv::QuantParams>& a, const std::vector<rdkv::QuantParams>& b) {
+    if (a.size() != b.size()) return false;
+    for (size_t i = 0; i < a.size(); ++i)
+        if (a[i].scale != b[i].scale || a[i].zero_point != b[i].zero_point || a[i].bits != b[i].bits) return false;
+    return true;
+}
+
+bool same_segment(const rdkv::PackedSegment& a, const rdkv::PackedSegment& b) {
+    return a.bits == b.bits && a.logical_len == b.logical_len && a.pad_count == b.pad_count && a.rows == b.rows &&
+           a.members == b.members && a.positions == b.positions && same_params(a.params, b.params) &&
+           a.payload == b.payload;
+}
+
+// Field-by-field equality of two TriZoneCaches; `what` names the first difference.
+bool same_trizone(const rdkv::TriZoneCache& a, const rdkv::TriZoneCache& b, std::string& what) {
+    auto fail = [&](const char* f) {
+        what = f;
+        return false;
+    };
+    if (a.head_dim != b.head_dim) return fail("head_dim");
+    if (a.kept != b.kept) return fail("kept");
+    if (a.evicted != b.evicted) return fail("evicted");
+    if (a.v_bits != b.v_bits) return fail("v_bits");
+    if (a.k_bits != b.k_bits) return fail("k_bits");
+    if (a.zone_a_v.size() != b.zone_a_v.size()) return fail("zone_a_v count");
+    for (size_t i = 0; i < a.zone_a_v.size(); ++i)
+        if (!same_segment(a.zone_a_v[i], b.zone_a_v[i])) return fail("zone_a_v segment");
+    if (a.zone_a_k.size() != b.zone_a_k.size()) return fail("zone_a_k count");
+    for (size_t i = 0; i < a.zone_a_k.size(); ++i)
+        if (!same_segment(a.zone_a_k[i], b.zone_a_k[i])) return fail("zone_a_k segment");
+    if (a.k16.members != b.k16.members || a.k16.width != b.k16.width || a.k16.data != b.k16.data) return fail("k16");
+    if (a.zone_b.members != b.zone_b.members || a.zone_b.positions != b.zone_b.positions ||
+        a.zone_b.width != b.zone_b.width || a.zone_b.data != b.zone_b.data)
+        return fail("zone_b");
+    if (a.channel_perm != b.channel_perm) return fail("channel_perm");
+    if (a.zone_c_len != b.zone_c_len) return fail("zone_c_len");
+    return true;
+}
+
+rdkv::HeadAllocation make_alloc(const std::vector<int>& v_bits, const std::vector<int>& k_bits) {
+    rdkv::HeadAllocation a;
+    a.v_bits = v_bits;
+    a.k_bits = k_bits;
+    for (int t = 0; t < (int)v_bits.size(); ++t) {
+        if (v_bits[t] > 0) {
+            a.kept.kept.push_back(t);
+            if (v_bits[t] == 16) a.kept.v16.push_back(t);
+        } else {
+            a.kept.evicted.push_back(t);
+        }
+    }
+    if (a.kept.kept.empty()) a.k_bits.clear();
+    return a;
+}
+
+rdkv::Tensor3 random_tensor(Gen& g, int rows, int cols, float scale = 1.0f) {
+    rdkv::Tensor3 t(1, rows, cols);
+    for (auto& x : t.data()) x = g.gauss() * scale;
+    return t;
+}
+
+std::vector<float> random_vec(Gen& g, int n) {
+    std::vector<float> v(n);
+    for (auto& x : v) x = g.gauss();
+    return v;
+}
+
+// ---- KATs ---------------------------------------------------------------------
+void kats() {
+    run("kat quantize_unit [0,1,2,3]@2", [](std::string& d) {
+        std::vector<float> x{0, 1, 2, 3};
+        auto q = rdkv::cuda::quantize_unit(x, 2);
+        d = "scale=" + std::to_string(q.params.scale) + " zero=" + std::to_string(q.params.zero_point);
+        return q.params.scale == 1.0f && q.params.zero_point == 0 && q.codes == std::vector<uint8_t>{0, 1, 2, 3};
+    });
+    run("kat moving_average [0,3,0,0,0] k=3", [](std::string&) {
+        std::vector<float> x{0, 3, 0, 0, 0};
+        return rdkv::cuda::moving_average(x, 3) == std::vector<float>{1, 1, 1, 0, 0};
+    });
+    run("kat channel_weights norm product 5.0", [](std::string& d) {
+        rdkv::Tensor3 q(1, 2, 4), k(1, 2, 4);
+        q.at(0, 0, 0) = 3.0f;
+        q.at(0, 1, 0) = 4.0f;
+        k.at(0, 0, 0) = 2.0f;
+        auto w = rdkv::cuda::channel_weights(q.slice(0), k.slice(0));
+        d = "w0=" + std::to_string(w.values[0]);
+        rdkv::Tensor3 bad(1, 2, 3);
+        return w.kind == rdkv::WeightKind::channel && std::abs(w.values[0] - 5.0f) < 5e-6f && w.values[1] == 0.0f &&
+               throws<std::invalid_argument>([&] { rdkv::cuda::channel_weights(q.slice(0), bad.slice(0)); });
+    });
+    run("kat two-token softmax [0.2, 0.8]", [](std::string& d) {
+        rdkv::Tensor3 k(1, 2, 1), q(1, 1, 1);
+        k.at(0, 1, 0) = std::log(4.0f);
+        q.at(0, 0, 0) = 1.0f;
+        std::vector<int> off{1};
+        auto a = rdkv::cuda::attention_probe(q.slice(0), k.slice(0), off);
+        d = std::to_string(a.a[0]) + "," + std::to_string(a.a[1]);
+        return std::abs(a.a[0] - 0.2) < 1e-6 && std::abs(a.a[1] - 0.8) < 1e-6;
+    });
+    run("kat zero query -> uniform row", [](std::string&) {
+        Gen g(11);
+        auto k = random_tensor(g, 7, 3);
+        rdkv::Tensor3 q(1, 1, 3);
+        std::vector<int> off{6};
+        auto a = rdkv::cuda::attention_probe(q.slice(0), k.slice(0), off);
+        for (double x : a.a)
+            if (std::abs(x - 1.0 / 7) > 1e-12 / 7) return false;
+        return true;
+    });
+    run("kat mckp brute-force instance [10,1,0.1]", [](std::string& d) {
+        // test_allocator.cpp:189-210: target 4 on this instance is not reachable within 1%
+        std::vector<float> w{10.0f, 1.0f, 0.1f};
+        rdkv::DistortionTable eps;
+        eps.eps = {{0, 1.0}, {2, 0.3}, {4, 0.014}, {8, 5e-5}, {16, 0.0}};
+        auto got = rdkv::cuda::mckp_bisect(w, eps, 4.0);
+        auto want = rdkv::mckp_bisect(w, eps, 4.0);
+        d = "converged=" + std::to_string(got.converged) + " lambda=" + std::to_string(got.lambda);
+        return got.bits == want.bits && got.lambda == want.lambda && got.converged == want.converged &&
+               got.objective == want.objective && !got.converged;
+    });
+    run("kat fused one-channel identity = 2.0", [](std::string& d) {
+        rdkv::TriZoneCache c;
+        c.head_dim = 1;
+        c.kept = {0};
+        c.v_bits = {16};
+        c.k_bits = {4};
+        rdkv::PackedSegment s;
+        s.bits = 4;
+        s.logical_len = 1;
+        s.pad_count = 1;
+        s.rows = 1;
+        s.members = {0};
+        s.params = {rdkv::QuantParams{2.0f, 1, 4}};
+        s.payload = rdkv::pack_bits(std::vector<uint8_t>{3, 0}, 4);
+        c.zone_a_k.push_back(s);
+        c.channel_perm = {0};
+        std::vector<float> q{0.5f};
+        auto l = rdkv::cuda::fused_k_logits(q, c);
+        d = l.empty() ? "empty" : std::to_string(l[0]);
+        return l.size() == 1 && std::abs(l[0] - 2.0) < 1e-6;
+    });
+}
+
+// ---- argument / error behaviour ----------------------------------------------------
+void errors() {
+    run("errors: invalid arguments and numeric errors", [](std::string& d) {
+        std::vector<float> x{1, 2, 3};
+        std::vector<float> nan{1, NAN};
+        rdkv::DistortionTable eps = eps_table(true);
+        bool ok = true;
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::quantize_unit(x, 3); });
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::quantize_unit(std::vector<float>{}, 2); });
+        ok &= throws<rdkv::NumericError>([&] { rdkv::cuda::quantize_unit(nan, 4); });
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::moving_average(x, 2); });
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::mckp_bisect(x, eps, 0.0); });
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::mckp_bisect(x, eps, 17.0); });
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::mckp_bisect(std::vector<float>{-1.0f}, eps, 2.0); });
+        rdkv::DistortionTable partial;
+        partial.eps = {{0, 1.0}, {16, 0.0}};
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::mckp_bisect(x, partial, 2.0); });
+        rdkv::Tensor3 k(1, 4, 2), q(1, 1, 2);
+        std::vector<int> off{4};
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::attention_probe(q.slice(0), k.slice(0), off); });
+        k.at(0, 1, 1) = INFINITY;
+        std::vector<int> off0{0};
+        ok &= throws<rdkv::NumericError>([&] { rdkv::cuda::attention_probe(q.slice(0), k.slice(0), off0); });
+        rdkv::TriZoneCache empty;
+        empty.head_dim = 2;
+        std::vector<float> q2{1, 1};
+        ok &= throws<rdkv::NumericError>([&] { rdkv::cuda::packed_decode_step(q2, empty); });
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::packed_decode_step(x, empty); });
+        Gen g(3);
+        auto kk = random_tensor(g, 3, 4), vv = random_tensor(g, 3, 4);
+        auto alloc = make_alloc({8, 8, 0}, {4, 4, 4, 4});
+        alloc.kept.kept.push_back(2);  // claims an evicted token (test_trizone.cpp:185-188)
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::build_trizone(kk.slice(0), vv.slice(0), alloc); });
+        auto short_bits = make_alloc({8, 8, 0}, {4, 4, 4});
+        ok &= throws<std::invalid_argument>([&] { rdkv::cuda::build_trizone(kk.slice(0), vv.slice(0), short_bits); });
+        d = ok ? "" : "an expected exception was not thrown";
+        return ok;
+    });
+}
+
+// ---- randomized single-function parity ---------------------------------------------
+void functions() {
+    run("moving_average bit-exact (200 vectors)", [](std::string& d) {
+        Gen g(5);
+        int bad = 0;
+        for (int it = 0; it < 200; ++it) {
+            auto x = random_vec(g, g.pick(1, 3000));
+            const int k = 2 * g.pick(0, 6) + 1;
+            bad += rdkv::cuda::moving_average(x, k) != rdkv::moving_average(x, k);
+        }
+        d = std::to_string(bad) + " mismatches";
+        return bad == 0;
+    });
+    run("channel_weights bit-exact (100 shapes)", [](std::string& d) {
+        Gen g(6);
+        int bad = 0;
+        for (int it = 0; it < 100; ++it) {
+            const int m = g.pick(1, 64), n = g.pick(1, 2000), dd = g.pick(1, 160);
+            auto q = random_tensor(g, m, dd), k = random_tensor(g, n, dd);
+            bad += rdkv::cuda::channel_weights(q.slice(0), k.slice(0)).values !=
+                   rdkv::channel_weights(q.slice(0), k.slice(0)).values;
+        }
+        d = std::to_string(bad) + " mismatches";
+        return bad == 0;
+    });
+    run("attention_probe vs reference (1e-12 rel)", [](std::string& d) {
+        Gen g(7);
+        double worst = 0;
+        size_t exact = 0, total = 0;
+        for (int it = 0; it < 30; ++it) {
+            const int rows = g.pick(1, 40), t = g.pick(1, 1500), dd = g.pick(1, 130);
+            auto q = random_tensor(g, rows, dd), k = random_tensor(g, t, dd);
+            std::vector<int> off(rows);
+            for (auto& o : off) o = g.pick(0, t - 1);
+            auto a = rdkv::cuda::attention_probe(q.slice(0), k.slice(0), off);
+            auto b = rdkv::attention_probe(q.slice(0), k.slice(0), off);
+            for (size_t i = 0; i < b.a.size(); ++i) {
+                worst = std::max(worst, std::abs(a.a[i] - b.a[i]) / std::max(std::abs(b.a[i]), 1e-300));
+                exact += a.a[i] == b.a[i];
+                ++total;
+            }
+        }
+        d = "worst rel " + std::to_string(worst) + ", exact " + std::to_string(100.0 * exact / total) + "%";
+        return worst < 1e-12;
+    });
+    run("token_weights bit-exact on reference probes", [](std::string& d) {
+        Gen g(8);
+        int bad = 0;
+        for (int it = 0; it < 20; ++it) {
+            const int group = g.pick(1, 8), rows = g.pick(1, 32), t = g.pick(1, 1200), dd = 32;
+            std::vector<rdkv::AttentionMatrix> heads;
+            auto k = random_tensor(g, t, dd);
+            for (int h = 0; h < group; ++h) {
+                auto q = random_tensor(g, rows, dd);
+                std::vector<int> off(rows);
+                for (int r = 0; r < rows; ++r) off[r] = std::max(0, t - rows + r);
+                heads.push_back(rdkv::attention_probe(q.slice(0), k.slice(0), off));
+            }
+            const int pk = 2 * g.pick(0, 4) + 1;
+            bad += rdkv::cuda::token_weights(heads, group, pk).values != rdkv::token_weights(heads, group, pk).values;
+        }
+        d = std::to_string(bad) + " mismatches";
+        return bad == 0;
+    });
+    run("mckp_bisect bit-exact (300 instances)", [](std::string& d) {
+        Gen g(9);
+        int bad = 0;
+        auto eps = eps_table(true);
+        for (int it = 0; it < 300; ++it) {
+            const int n = g.pick(1, 5000);
+            std::vector<float> w(n);
+            for (auto& x : w) x = (float)std::exp(3.0 * g.gauss()) * (g.pick(0, 9) == 0 ? 0.0f : 1.0f);
+            const double target = std::min(16.0, std::exp(g.uni() * std::log(64.0)) * 0.25);
+            rdkv::SolverConfig cfg;
+            cfg.strict_budget = g.pick(0, 1);
+            cfg.tolerance = g.pick(0, 1) ? 1e-2 : 1e-4;
+            rdkv::BitSet bits;
+            if (g.pick(0, 3) == 0) bits.widths = {0, 4, 16};
+            auto a = rdkv::cuda::mckp_bisect(w, eps, target, bits, cfg);
+            auto b = rdkv::mckp_bisect(w, eps, target, bits, cfg);
+            bad += !(a.bits == b.bits && a.lambda == b.lambda && a.converged == b.converged &&
+                     a.achieved_avg_bits == b.achieved_avg_bits && a.objective == b.objective);
+        }
+        d = std::to_string(bad) + " mismatches";
+        return bad == 0;
+    });
+    run("quantize_unit bit-exact (incl. constant units)", [](std::string& d) {
+        Gen g(10);
+        int bad = 0;
+        for (int it = 0; it < 300; ++it) {
+            const int n = g.pick(1, 600), bits = 2 << g.pick(0, 2);
+            auto x = random_vec(g, n);
+            if (it % 10 == 0) std::fill(x.begin(), x.end(), x[0]);
+            if (it % 10 == 1) for (auto& v : x) v *= 1e-30f;
+            auto a = rdkv::cuda::quantize_unit(x, bits);
+            auto b = rdkv::quantize_unit(x, bits);
+            bad += !(a.codes == b.codes && a.params.scale == b.params.scale &&
+                     a.params.zero_point == b.params.zero_point && a.params.bits == b.params.bits);
+        }
+        d = std::to_string(bad) + " mismatches";
+        return bad == 0;
+    });
+}
+
+// ---- TriZone packing and decode -----------------------------------------------------
+std::vector<int> random_bits(Gen& g, int n, bool allow_zero) {
+    static const int w[] = {0, 2, 4, 8, 16};
+    std::vector<int> b(n);
+    for (auto& x : b) x = w[g.pick(allow_zero ? 0 : 1, 4)];
+    return b;
+}
+
+void trizone() {
+    run("build_trizone identical, random tiers (acc. 7)", [](std::string& d) {
+        Gen g(12);
+        for (int it = 0; it < 60; ++it) {
+            const int t = g.pick(1, 300), dd = g.pick(1, 136);
+            auto k = random_tensor(g, t, dd), v = random_tensor(g, t, dd);
+            auto alloc = make_alloc(random_bits(g, t, true), random_bits(g, dd, true));
+            auto a = rdkv::cuda::build_trizone(k.slice(0), v.slice(0), alloc);
+            auto b = rdkv::build_trizone(k.slice(0), v.slice(0), alloc);
+            if (!same_trizone(a, b, d)) {
+                d += " (case " + std::to_string(it) + ", T=" + std::to_string(t) + ", d=" + std::to_string(dd) + ")";
+                return false;
+            }
+        }
+        return true;
+    });
+    run("all-K-removed / all-evicted caches", [](std::string& d) {
+        Gen g(13);
+        const int t = 40, dd = 16;
+        auto k = random_tensor(g, t, dd), v = random_tensor(g, t, dd);
+        auto a1 = make_alloc(random_bits(g, t, false), std::vector<int>(dd, 0));
+        auto ev = make_alloc(std::vector<int>(t, 0), {});
+        std::string w1, w2;
+        const bool ok1 = same_trizone(rdkv::cuda::build_trizone(k.slice(0), v.slice(0), a1),
+                                      rdkv::build_trizone(k.slice(0), v.slice(0), a1), w1);
+        const bool ok2 = same_trizone(rdkv::cuda::build_trizone(k.slice(0), v.slice(0), ev),
+                                      rdkv::build_trizone(k.slice(0), v.slice(0), ev), w2);
+        // all K removed: logits are all zero -> uniform attention over kept V
+        auto c = rdkv::build_trizone(k.slice(0), v.slice(0), a1);
+        auto q = random_vec(g, dd);
+        const double err = l2_rel(rdkv::cuda::packed_decode_step(q, c), rdkv::packed_decode_step(q, c));
+        d = w1 + w2 + " decode rel " + std::to_string(err);
+        return ok1 && ok2 && err < 1e-3;
+    });
+    run("fused_k_logits vs reference (1e-5)", [](std::string& d) {
+        Gen g(14);
+        double worst = 0;
+        for (int it = 0; it < 40; ++it) {
+            const int t = g.pick(1, 400), dd = g.pick(1, 136);
+            auto k = random_tensor(g, t, dd), v = random_tensor(g, t, dd);
+            auto alloc = make_alloc(random_bits(g, t, true), random_bits(g, dd, true));
+            auto c = rdkv::build_trizone(k.slice(0), v.slice(0), alloc);
+            if (c.kept.empty()) continue;
+            auto q = random_vec(g, dd);
+            auto a = rdkv::cuda::fused_k_logits(q, c), b = rdkv::fused_k_logits(q, c);
+            double scale = 0;
+            for (double x : b) scale = std::max(scale, std::abs(x));
+            for (size_t i = 0; i < b.size(); ++i) worst = std::max(worst, std::abs(a[i] - b[i]) / std::max(scale, 1e-30));
+        }
+        d = "worst " + std::to_string(worst) + " (relative to max |logit|)";
+        return worst < 1e-5;
+    });
+    run("pad bits never leak (test_trizone.cpp:214-232)", [](std::string& d) {
+        Gen g(17);
+        const int t = 6, dd = 5;
+        auto k = random_tensor(g, t, dd), v = random_tensor(g, t, dd);
+        auto c = rdkv::build_trizone(k.slice(0), v.slice(0), make_alloc({8, 8, 8, 8, 8, 8}, {4, 4, 4, 4, 4}));
+        auto q = random_vec(g, dd);
+        auto before = rdkv::cuda::fused_k_logits(q, c);
+        auto dec_before = rdkv::cuda::packed_decode_step(q, c);
+        auto& seg = c.zone_a_k.front();
+        for (int r = 0; r < seg.rows; ++r) seg.payload[(size_t)r * seg.row_bytes() + seg.row_bytes() - 1] |= 0xF0;
+        d = "pad_count=" + std::to_string(seg.pad_count);
+        return seg.pad_count == 1 && before == rdkv::cuda::fused_k_logits(q, c) &&
+               dec_before == rdkv::cuda::packed_decode_step(q, c);
+    });
+    run("packed_decode_step, every tier + Zone C", [](std::string& d) {
+        Gen g(18);
+        double worst = 0;
+        for (int it = 0; it < 60; ++it) {
+            const int t = g.pick(1, 400), dd = g.pick(1, 136);
+            auto k = random_tensor(g, t, dd), v = random_tensor(g, t, dd);
+            auto alloc = make_alloc(random_bits(g, t, true), random_bits(g, dd, true));
+            auto c = rdkv::build_trizone(k.slice(0), v.slice(0), alloc);
+            const int appends = it % 3 == 0 ? g.pick(1, 20) : 0;
+            for (int a = 0; a < appends; ++a) rdkv::append_new_token(c, random_vec(g, dd), random_vec(g, dd));
+            if (c.kept.empty() && c.zone_c_len == 0) continue;
+            auto q = random_vec(g, dd);
+            worst = std::max(worst, l2_rel(rdkv::cuda::packed_decode_step(q, c), rdkv::packed_decode_step(q, c)));
+        }
+        d = "worst l2 rel " + std::to_string(worst);
+        return worst < 1e-3;
+    });
+    run("Zone-C-only cache (all evicted + appends)", [](std::string& d) {
+        Gen g(19);
+        const int t = 30, dd = 24;
+        auto k = random_tensor(g, t, dd), v = random_tensor(g, t, dd);
+        auto c = rdkv::build_trizone(k.slice(0), v.slice(0), make_alloc(std::vector<int>(t, 0), {}));
+        for (int a = 0; a < 5; ++a) rdkv::cuda::append_new_token(c, random_vec(g, dd), random_vec(g, dd));
+        auto q = random_vec(g, dd);
+        const double err = l2_rel(rdkv::cuda::packed_decode_step(q, c), rdkv::packed_decode_step(q, c));
+        d = "l2 rel " + std::to_string(err);
+        return err < 1e-3;
+    });
+}
+
+// ---- pipeline on gen_synthetic_cache ----------------------------------------------
+void pipeline() {
+    struct Case {
+        const char* name;
+        rdkv::CacheShape shape;
+        int probe, outliers, n_tokens;
+        double outlier_scale;
+        bool force_window;
+    };
+    const Case cases[] = {
+        {"C1-like 1x32/8 d128 T4096 n128", {1, 32, 8, 128, 4096}, 32, 0, 128, 1.0, false},
+        {"2x8/2 d64 T1024, outliers, n512", {2, 8, 2, 64, 1024}, 32, 4, 512, 8.0, false},
+        {"1x7/1 d128 T2048 force-window", {1, 7, 1, 128, 2048}, 32, 4, 1024, 8.0, true},
+        {"1x4/4 d96 T700 n2048 window 16", {1, 4, 4, 96, 700}, 16, 2, 2048, 6.0, false},
+    };
+    int seed = 100;
+    for (const auto& c : cases) {
+        ++seed;
+        const auto cache = rdkv::gen_synthetic_cache(seed, c.shape, c.probe, c.outliers, c.outlier_scale);
+        rdkv::BudgetSpec spec;
+        spec.n_tokens = c.n_tokens;
+        rdkv::PipelineConfig cfg;
+        cfg.force_window_retain = c.force_window;
+        cfg.probe.window = c.probe;
+        const auto ev = eps_table(true), ek = eps_table(false);
+        rdkv::ModelAllocation ga, ra;
+        run(std::string("allocate_model ") + c.name, [&](std::string& d) {
+            ra = rdkv::allocate_model(cache, spec, ev, ek, cfg);
+            ga = rdkv::cuda::allocate_model(cache, spec, ev, ek, cfg);
+            size_t wexact = 0, wtotal = 0, kept = 0;
+            double wworst = 0;
+            bool ok = ga.heads.size() == ra.heads.size();
+            for (size_t i = 0; ok && i < ra.heads.size(); ++i) {
+                const auto &a = ga.heads[i], &b = ra.heads[i];
+                ok &= a.v_bits == b.v_bits && a.k_bits == b.k_bits && a.kept.kept == b.kept.kept &&
+                      a.kept.v16 == b.kept.v16 && a.kept.evicted == b.kept.evicted && a.lambda_v == b.lambda_v &&
+                      a.lambda_k == b.lambda_k && a.v_converged == b.v_converged && a.k_converged == b.k_converged &&
+                      a.objective_v == b.objective_v && a.objective_k == b.objective_k &&
+                      a.achieved_bits == b.achieved_bits && a.k_weights == b.k_weights;
+                for (size_t t = 0; t < b.v_weights.size(); ++t) {
+                    wexact += a.v_weights[t] == b.v_weights[t];
+                    wworst = std::max(wworst, (double)std::abs(a.v_weights[t] - b.v_weights[t]) /
+                                                  std::max((double)std::abs(b.v_weights[t]), 1e-30));
+                    ++wtotal;
+                }
+                kept += b.kept.kept.size();
+            }
+            d = "kept " + std::to_string(kept) + ", w_t exact " + std::to_string(100.0 * wexact / wtotal) +
+                "%, worst rel " + std::to_string(wworst);
+            return ok && wworst < 1e-6;
+        });
+        run(std::string("build_packed_model ") + c.name, [&](std::string& d) {
+            auto a = rdkv::cuda::build_packed_model(cache, ra);
+            auto b = rdkv::build_packed_model(cache, ra);
+            for (size_t i = 0; i < b.heads.size(); ++i)
+                if (!same_trizone(a.heads[i], b.heads[i], d)) return false;
+            return true;
+        });
+        run(std::string("decode (drop-in + device model) ") + c.name, [&](std::string& d) {
+            auto ref = rdkv::build_packed_model(cache, ra);
+            auto dev = rdkv::cuda::DevicePackedModel::build(cache, ra, 8);
+            Gen g(seed);
+            const auto& s = c.shape;
+            const int gq = s.group();
+            double worst = 0, worst_single = 0;
+            for (int step = 0; step < 3; ++step) {
+                std::vector<float> q((size_t)s.layers * s.q_heads * s.head_dim);
+                for (auto& x : q) x = g.gauss();
+                auto out = dev.decode(q);
+                for (int l = 0; l < s.layers; ++l)
+                    for (int h = 0; h < s.q_heads; ++h) {
+                        const size_t o = ((size_t)l * s.q_heads + h) * s.head_dim;
+                        std::span<const float> qh(q.data() + o, s.head_dim);
+                        const auto& tz = ref.at(l, h / gq);
+                        const auto want = rdkv::packed_decode_step(qh, tz);
+                        worst = std::max(worst, l2_rel(std::vector<double>(out.begin() + o, out.begin() + o + s.head_dim), want));
+                        if (step == 0 && h % gq == 0)
+                            worst_single = std::max(worst_single, l2_rel(rdkv::cuda::packed_decode_step(qh, tz), want));
+                    }
+                // one appended token per (layer, KV head) before the next step
+                std::vector<float> kn((size_t)s.layers * s.kv_heads * s.head_dim), vn(kn.size());
+                for (auto& x : kn) x = g.gauss();
+                for (auto& x : vn) x = g.gauss();
+                dev.append(kn, vn);
+                for (int u = 0; u < s.layers * s.kv_heads; ++u)
+                    rdkv::append_new_token(ref.heads[u], std::span<const float>(kn.data() + (size_t)u * s.head_dim, s.head_dim),
+                                           std::span<const float>(vn.data() + (size_t)u * s.head_dim, s.head_dim));
+            }
+            // download() gives back the reference layout (quantised fields exact)
+            auto back = dev.download();
+            bool same = true;
+            for (size_t i = 0; i < back.heads.size(); ++i) {
+                const auto &a = back.heads[i], &b = ref.heads[i];
+                same &= a.kept == b.kept && a.channel_perm == b.channel_perm && a.zone_c_len == b.zone_c_len &&
+                        a.zone_a_v.size() == b.zone_a_v.size() && a.zone_a_k.size() == b.zone_a_k.size();
+                for (size_t j = 0; same && j < a.zone_a_v.size(); ++j) same &= same_segment(a.zone_a_v[j], b.zone_a_v[j]);
+                for (size_t j = 0; same && j < a.zone_a_k.size(); ++j) same &= same_segment(a.zone_a_k[j], b.zone_a_k[j]);
+            }
+            // upload() of the reference model decodes like build()
+            auto up = rdkv::cuda::DevicePackedModel::upload(ref, 0);
+            std::vector<float> q((size_t)s.layers * s.q_heads * s.head_dim);
+            for (auto& x : q) x = g.gauss();
+            auto o1 = up.decode(q);
+            double worst_up = 0;
+            for (int l = 0; l < s.layers; ++l)
+                for (int h = 0; h < s.q_heads; ++h) {
+                    const size_t o = ((size_t)l * s.q_heads + h) * s.head_dim;
+                    std::span<const float> qh(q.data() + o, s.head_dim);
+                    worst_up = std::max(worst_up, l2_rel(std::vector<double>(o1.begin() + o, o1.begin() + o + s.head_dim),
+                                                         rdkv::packed_decode_step(qh, ref.at(l, h / gq))));
+                }
+            d = "device " + std::to_string(worst) + ", single " + std::to_string(worst_single) + ", upload " +
+                std::to_string(worst_up) + (same ? "" : ", download differs");
+            return worst < 1e-3 && worst_single < 1e-3 && worst_up < 1e-3 && same;
+        });
+    }
+}
+
+}  // namespace
+
+int main() {
+    kats();
+    errors();
+    functions();
+    trizone();
+    pipeline();
+    std::printf("%d passed, %d failed\n", g_pass, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}

@@ -73,9 +73,54 @@ def test_tile_spec_roundtrips_through_exporter(golden):
         assert int(got["info"].total_bytes) == len(tile)
 
 
+def test_import_is_inverse_of_export(golden):
+    """rdkv_tile_import(canonical view) rebuilds the tile byte-for-byte."""
+    from paper_2605_08317_b200.pipeline import import_tile
+
+    for name, k, v, vb, kb, canon in _golden_cases(golden):
+        d = k.shape[1]
+        tile = tilepack.build_tile(canon, vb, kb, v, d)
+        got = export_tile(tile, d)
+        kept = np.asarray(got["kept"])
+        back = import_tile(d, kept, np.asarray(vb)[kept], got["vcodes"], got["vscale"], got["vzero"], got["vfp"],
+                           np.asarray(kb) if len(kept) else np.zeros(d), got["kcodes"], got["kscale"],
+                           got["kzero"], got["kfp"])
+        assert np.array_equal(back, tile), name
+
+
+def test_import_rejects_bad_input():
+    from paper_2605_08317_b200.pipeline import import_tile
+
+    d = 4
+    with pytest.raises(capi.InvalidArgument):  # kept not ascending
+        import_tile(d, [3, 1], [2, 2], np.zeros((2, d)), [1, 1], [0, 0], np.zeros((2, d)), [2] * d,
+                    np.zeros((d, 2)), [1] * d, [0] * d, np.zeros((2, d)))
+    with pytest.raises(capi.InvalidArgument):  # 3-bit width
+        import_tile(d, [1], [3], np.zeros((1, d)), [1], [0], np.zeros((1, d)), [2] * d,
+                    np.zeros((d, 1)), [1] * d, [0] * d, np.zeros((1, d)))
+
+
 def test_exporter_rejects_bad_magic():
     tile = np.zeros(256, np.uint8)
     info = capi.TileInfo()
     assert capi.lib().rdkv_tile_info_get(tile.ctypes.data, C.byref(info)) == capi.RDKV_EFORMAT
     with pytest.raises(capi.RdkvError):
         export_tile(tile, 8)
+
+
+def test_cpp_dropin_library_is_self_contained():
+    """librdkv_cuda_dropin.so defines the rdkv::cuda API and needs no reference
+    symbol (it only uses the reference's header types)."""
+    import os
+    import subprocess
+
+    so = os.path.join(os.path.dirname(capi.LIB_PATH), "librdkv_cuda_dropin.so")
+    if not os.path.exists(so):
+        pytest.skip("drop-in not built (needs the reference headers at build time)")
+    out = subprocess.run(["nm", "-DC", so], capture_output=True, text=True, check=True).stdout
+    undefined = [l for l in out.splitlines() if " U " in l and "rdkv::" in l]
+    assert not undefined, undefined
+    for fn in ("rdkv::cuda::allocate_model(", "rdkv::cuda::build_packed_model(", "rdkv::cuda::packed_decode_step(",
+               "rdkv::cuda::mckp_bisect(", "rdkv::cuda::attention_probe(", "rdkv::cuda::build_trizone(",
+               "rdkv::cuda::fused_k_logits(", "rdkv::cuda::DevicePackedModel::decode("):
+        assert any(fn in l and " T " in l for l in out.splitlines()), fn
