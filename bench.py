@@ -112,41 +112,21 @@ class ClockSampler:
 
 
 def dist_setup():
-    import torch
+    from paper_2605_08317_b200 import dist as D
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
-        torch.cuda.set_device(0)
-    return world, rank, local
+    return D.init()
 
 
 def barrier_sync(world):
-    import torch
+    from paper_2605_08317_b200 import dist as D
 
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
-    torch.cuda.synchronize()
+    D.barrier_sync(world)
 
 
 def max_over_ranks(x, world):
-    import torch
+    from paper_2605_08317_b200 import dist as D
 
-    if world == 1:
-        return x
-    import torch.distributed as dist
-
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return D.max_over_ranks(x, world)
 
 
 # ---------------------------------------------------------------------------------
@@ -162,7 +142,7 @@ def reference_sample(spec, cfg_kwargs, budget_s):
     ref = oracle.load_ref() if oracle.ref_available() else None
     lib = ref if ref is not None else orc
     H, T, d, g, Sw = spec.kv_heads, spec.ctx, spec.head_dim, spec.group, spec.probe_rows
-    s = chunk_seed(spec.seed, spec.rank, 0, 0)
+    s = chunk_seed(spec.seed, spec.first_seq, 0)
     k = orc.gen_counter(s, 0, 0, H * T * d, d, T, spec.outlier_channels, spec.outlier_scale,
                         spec.hh_stride, spec.hh_boost).reshape(1, H, T, d)
     v = orc.gen_counter(s, 1, 0, H * T * d, d, T).reshape(1, H, T, d)

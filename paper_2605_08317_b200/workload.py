@@ -17,8 +17,10 @@ import torch
 from . import pipeline as P
 
 
-def chunk_seed(base: int, rank: int, b: int, layer: int) -> int:
-    return (base * 1_000_003 + rank * 7919 + b * 131 + layer) & ((1 << 63) - 1)
+def chunk_seed(base: int, seq: int, layer: int) -> int:
+    """K0 seed of one (global sequence id, layer): the job is the same whatever
+    the world size; a rank only picks which sequences it owns (dist.weak_shard)."""
+    return (base * 1_000_003 + seq * 131 + layer) & ((1 << 63) - 1)
 
 
 @dataclass
@@ -40,6 +42,11 @@ class WorkloadSpec:
     zc_cap: int = 0
 
     @property
+    def first_seq(self):
+        """Global id of this rank's first sequence (weak scaling: batch sequences per rank)."""
+        return self.rank * self.batch
+
+    @property
     def group(self):
         return self.q_heads // self.kv_heads
 
@@ -50,7 +57,7 @@ class WorkloadSpec:
 
 def gen_chunk(spec: WorkloadSpec, b: int, layer: int, dtype=torch.float16):
     """K, V [H_kv, T, d] and probe Q [H_kv, g, S_w, d] of one (sequence, layer)."""
-    s = chunk_seed(spec.seed, spec.rank, b, layer)
+    s = chunk_seed(spec.seed, spec.first_seq + b, layer)
     H, T, d = spec.kv_heads, spec.ctx, spec.head_dim
     k = P.generate((H, T, d), dtype, seed=s, tensor=0, seq_len=T, outlier_channels=spec.outlier_channels,
                    outlier_scale=spec.outlier_scale, hh_stride=spec.hh_stride, hh_boost=spec.hh_boost)

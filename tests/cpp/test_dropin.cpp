@@ -418,9 +418,11 @@ void trizone() {
         d = w1 + w2 + " decode rel " + std::to_string(err);
         return ok1 && ok2 && err < 1e-3;
     });
-    run("fused_k_logits vs reference (1e-5)", [](std::string& d) {
+    run("fused_k_logits vs reference (1e-5 / 1e-3 with k16)", [](std::string& d) {
+        // f32 accumulation: 1e-5 of max |logit|; caches with 16-bit K channels
+        // (stored fp16 on the device): 1e-3
         Gen g(14);
-        double worst = 0;
+        double worst = 0, worst16 = 0;
         for (int it = 0; it < 40; ++it) {
             const int t = g.pick(1, 400), dd = g.pick(1, 136);
             auto k = random_tensor(g, t, dd), v = random_tensor(g, t, dd);
@@ -431,10 +433,11 @@ void trizone() {
             auto a = rdkv::cuda::fused_k_logits(q, c), b = rdkv::fused_k_logits(q, c);
             double scale = 0;
             for (double x : b) scale = std::max(scale, std::abs(x));
-            for (size_t i = 0; i < b.size(); ++i) worst = std::max(worst, std::abs(a[i] - b[i]) / std::max(scale, 1e-30));
+            double& w = c.k16.width > 0 ? worst16 : worst;
+            for (size_t i = 0; i < b.size(); ++i) w = std::max(w, std::abs(a[i] - b[i]) / std::max(scale, 1e-30));
         }
-        d = "worst " + std::to_string(worst) + " (relative to max |logit|)";
-        return worst < 1e-5;
+        d = "worst " + std::to_string(worst) + ", with k16 " + std::to_string(worst16) + " (of max |logit|)";
+        return worst < 1e-5 && worst16 < 1e-3;
     });
     run("pad bits never leak (test_trizone.cpp:214-232)", [](std::string& d) {
         Gen g(17);
