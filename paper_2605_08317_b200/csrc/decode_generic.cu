@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(
                 int li;
                 const int cls = slot_class(h, sbase, i, li);
                 pad = li >= h.r[cls];
-                const uint8_t* row = krows + (size_t)i * h.krow_bytes;
+                const uint8_t* row = krows + (size_t)krow_pos(h, i) * h.krow_bytes;
                 if (!pad) {
                     for (int kc = 0; kc < 3; ++kc) {
                         const int bits = kBits(kc);
@@ -410,7 +410,7 @@ __global__ void tile_logits_kernel(const uint8_t* __restrict__ arena, const int6
             const int cls = slot_class(h, sbase, i, li);
             if (li < h.r[cls]) {
                 acc = 0.0f;
-                const uint8_t* row = tile + h.off_k + (size_t)i * h.krow_bytes;
+                const uint8_t* row = tile + krow_offset(h, i);
                 for (int kc = 0; kc < 3; ++kc) {
                     const int bits = kBits(kc);
                     for (int j = 0; j < h.c[kc]; ++j) {

@@ -280,8 +280,8 @@ __device__ __noinline__ void decode_tile(const uint8_t* __restrict__ t, const IO
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
                         if (u == 1 && !two) continue;
-                        const uint8_t* p0 = krows + (size_t)((mt + u) * 16 + gid) * krb + kb0;
-                        const uint8_t* p1 = p0 + 8 * krb;
+                        const uint8_t* p0 = krows + (size_t)krow_pos(h, (mt + u) * 16 + gid) * krb + kb0;
+                        const uint8_t* p1 = krows + (size_t)krow_pos(h, (mt + u) * 16 + gid + 8) * krb + kb0;
                         uint32_t a[4];
                         if (c == 0) {
                             const uint2 w0 = lds64(p0 + 8 * kk), w1 = lds64(p1 + 8 * kk);
@@ -344,7 +344,7 @@ __device__ __noinline__ void decode_tile(const uint8_t* __restrict__ t, const IO
             if (!hv) continue;
             float v = lgs[hl * LS + s];
             if (c16) {
-                const __half* kr = reinterpret_cast<const __half*>(krows + (size_t)s * krb + h.kbyte_base[3]);
+                const __half* kr = reinterpret_cast<const __half*>(krows + (size_t)krow_pos(h, s) * krb + h.kbyte_base[3]);
                 for (int j = 0; j < c16; ++j)
                     v = fmaf(ld_io(qs, hl * kD + perm[h.kslot_base[3] + j]), __half2float(kr[j]), v);
             }
@@ -652,8 +652,9 @@ __device__ __noinline__ void decode_tile_u2(const uint8_t* __restrict__ t, const
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
                     if (u == 1 && !two) continue;
-                    const uint8_t* p0 = krows + (size_t)((mt + u) * 16 + gid) * krb + 8 * kk;
-                    const uint2 w0 = lds64(p0), w1 = lds64(p0 + 8 * krb);
+                    const uint8_t* p0 = krows + (size_t)krow_pos(h, (mt + u) * 16 + gid) * krb + 8 * kk;
+                    const uint8_t* p1 = krows + (size_t)krow_pos(h, (mt + u) * 16 + gid + 8) * krb + 8 * kk;
+                    const uint2 w0 = lds64(p0), w1 = lds64(p1);
                     const int s = 2 * tig;
                     uint32_t a[4];
                     a[0] = (w0.x >> s) & 0x03030303u;
@@ -981,8 +982,8 @@ __device__ __forceinline__ void decode_tile_u2_pair(const uint8_t* __restrict__ 
             for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const uint8_t* r0 = krows + (size_t)(32 * pb + 16 * u + gid) * krb;
-            const uint8_t* r1 = r0 + 8 * krb;
+            const uint8_t* r0 = krows + (size_t)krow_pos(h, 32 * pb + 16 * u + gid) * krb;
+            const uint8_t* r1 = krows + (size_t)krow_pos(h, 32 * pb + 16 * u + gid + 8) * krb;
             uint32_t w0[8], w1[8];  // the 32 K bytes (128 codes) of rows gid and gid + 8
             if (krb == 32) {
                 const uint4 x0 = *reinterpret_cast<const uint4*>(r0), x1 = *reinterpret_cast<const uint4*>(r0 + 16);
@@ -1238,6 +1239,418 @@ static int launch_pair(const rdkv_decode_args* a, cudaStream_t st) {
     return launch_status();
 }
 
+// ============================================================================
+// Uniform-2-bit warp-pair body, v2 ("u2x"): the same digit arithmetic as
+// decode_tile_u2_pair with the instruction count cut for the issue-bound
+// regime (~3.6K -> ~1.5K warp instructions per tile):
+//   * compile-time block loops: BPW 32-token blocks per warp (a ghost block
+//     with zero weights evens out odd block counts), no data-dependent
+//     branches around the mma.sync / ldmatrix / shuffle collectives;
+//   * QK A rows <-> token slots 32b + 4*gid + 2u + r, so every lane ends up
+//     with four CONSECUTIVE slots per block: their V parameters are two
+//     LDS.128 and their p~ digits pack (PRMT) into one 32-bit word per digit
+//     (3 STS.32 instead of 12 STS.U8); K rows are stored slot-transposed
+//     (tile_layout.h krow_pos) so those A-row loads stay conflict-free;
+//   * fixed-point ranges from the header's scale bounds (no per-tile scans);
+//   * digit sums combined in integer registers before one I2F pair (QK);
+//   * log2(e) folded into the logit scale: p = ex2(l' - m').
+constexpr int kXQDig = 256;                   // q~ digits: 4 k-steps x 2 n-tiles x 8 rows x 32 B
+constexpr int kXPDig = kXQDig + 4 * 512;      // p~ digits: 2 * BPW blocks x 512 B
+
+struct PairX {
+    float bias[2][4];
+    float mx[2][4];
+    float lsum[2][4], bv[2][4];
+};
+static_assert(sizeof(PairX) <= kXQDig, "exchange area");
+
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+template <typename IO>
+__device__ __forceinline__ float absmax16(const IO* q);
+template <>
+__device__ __forceinline__ float absmax16<__half>(const __half* q) {
+    const uint4 a = *reinterpret_cast<const uint4*>(q), b = *reinterpret_cast<const uint4*>(q + 8);
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    __half2 m = __habs2(*reinterpret_cast<const __half2*>(&w[0]));
+#pragma unroll
+    for (int i = 1; i < 8; ++i) m = __hmax2(m, __habs2(*reinterpret_cast<const __half2*>(&w[i])));
+    return fmaxf(__low2float(m), __high2float(m));
+}
+template <>
+__device__ __forceinline__ float absmax16<float>(const float* q) {
+    float m = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float4 v = reinterpret_cast<const float4*>(q)[i];
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    return m;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <typename IO, int BPW>
+__device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const IO* __restrict__ qs, int g,
+                                                uint8_t* __restrict__ scr, IO* __restrict__ out, int half,
+                                                int bar) {
+    const int lane = threadIdx.x & 31;
+    const int gid = lane >> 2, tig = lane & 3;
+    const bool hv = tig < g;
+    const TileHeader& h = *reinterpret_cast<const TileHeader*>(t);
+    PairX& xg = *reinterpret_cast<PairX*>(scr);
+    uint8_t* qdig = scr + kXQDig;
+    uint8_t* pdig = scr + kXPDig;
+    const float2* chan = reinterpret_cast<const float2*>(t + kHeaderBytes);
+    const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
+    const uint8_t* krows = t + h.off_k;
+    const int n = h.r[0];
+    const int c0 = h.c[0];
+    const int kmax_slot = h.kslots - 1;
+    const int krb = h.krow_bytes;
+    const int Q = h.nslot >> 2;
+    const uint32_t sbits = h.scale_bounds;
+    const float smax = bf16_bits_to_float(sbits & 0xFFFFu), vmax = bf16_bits_to_float(sbits >> 16);
+    constexpr float kInvSqrtD = 0.08838834764831845f;
+    constexpr float kLog2e = 1.4426950408889634f;
+
+    // ---- q range of head tig (lanes gid cover 16 channels each)
+    float qm = hv ? absmax16<IO>(qs + tig * kD + 16 * gid) : 0.0f;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+    const float bnd = smax * qm;
+    const float sg = bnd > 0.0f ? 8.2e6f * rcp_approx(bnd) : 0.0f;
+
+    // ---- q~ digits (k-steps half, half + 2) and the bias sum_c q_c * offset_c
+    float bpart = 0.0f;
+    const int pshift = 2 * (3 - (gid & 3));
+    const IO* qh = qs + (hv ? tig : 0) * kD;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const int kk = half + 2 * i;
+        uint32_t x[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int j = kk * 32 + 16 * (gid >> 2) + 4 * e + (gid & 3);
+            const bool ok = hv && j < c0;
+            const int js = min(j, kmax_slot);
+            const float2 cs = chan[js];
+            const float qv = ok ? ld_io(qh, perm[js]) : 0.0f;
+            bpart = fmaf(qv, cs.y, bpart);
+            const int N = __float2int_rn(cs.x * qv * sg);
+            x[e] = ((uint32_t)N << pshift) + 0x80808080u ^ 0x80808080u;
+        }
+        const uint32_t w0 = __byte_perm(__byte_perm(x[0], x[1], 0x0040), __byte_perm(x[2], x[3], 0x0040), 0x5410);
+        const uint32_t w1 = __byte_perm(__byte_perm(x[0], x[1], 0x0051), __byte_perm(x[2], x[3], 0x0051), 0x5410);
+        const uint32_t w2 = __byte_perm(__byte_perm(x[0], x[1], 0x0062), __byte_perm(x[2], x[3], 0x0062), 0x5410);
+        const uint32_t w3 = __byte_perm(__byte_perm(x[0], x[1], 0x0073), __byte_perm(x[2], x[3], 0x0073), 0x5410);
+        uint8_t* a0 = qdig + kk * 512 + 2 * tig * 32 + 4 * gid;
+        *reinterpret_cast<uint32_t*>(a0) = w3;
+        *reinterpret_cast<uint32_t*>(a0 + 32) = w2;
+        *reinterpret_cast<uint32_t*>(a0 + 256) = w1;
+        *reinterpret_cast<uint32_t*>(a0 + 288) = w0;
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) bpart += __shfl_xor_sync(0xffffffffu, bpart, o);
+    if (gid == 0) xg.bias[half][tig] = bpart;
+    pair_sync(bar);
+    // l' = log2(e) * (v / (64 sigma) + bias) / sqrt(d)
+    const float bias2 = (xg.bias[0][tig] + xg.bias[1][tig]) * (kInvSqrtD * kLog2e);
+    const float qscale2 = bnd * (kInvSqrtD * kLog2e / (64.0f * 8.2e6f));
+
+    // ---- QK
+    const int mat = lane >> 3, rr = lane & 7;
+    const int bofs = ((mat >> 1) * 8 + rr) * 32 + (mat & 1) * 16;
+    uint32_t bq[4][4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) ldsm_x4(bq[kk], qdig + kk * 512 + bofs);
+    const uint32_t kmask = 0x03030303u << (2 * tig);
+    float lg[BPW][4];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < BPW; ++i) {
+        const int pb = half + 2 * i;
+        int acc[2][2][4];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            // A rows gid / gid + 8 = slots 32pb + 4gid + 2u / + 1 (positions (2u + r) Q + 8pb + gid)
+            const uint8_t* r0 = krows + (size_t)((2 * u) * Q + 8 * pb + gid) * krb;
+            const uint8_t* r1 = r0 + (size_t)Q * krb;
+            const uint4 x0 = lds128(r0), x1 = lds128(r0 + 16), y0 = lds128(r1), y1 = lds128(r1 + 16);
+            const uint32_t w0[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+            const uint32_t w1[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t a[4] = {w0[2 * kk] & kmask, w1[2 * kk] & kmask, w0[2 * kk + 1] & kmask,
+                                       w1[2 * kk + 1] & kmask};
+                mma_u8s8(acc[u][0], a, bq[kk][0], bq[kk][1]);
+                mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int s = 32 * pb + 4 * gid + 2 * u + r;
+                const int hi = acc[u][0][2 * r] * 256 + acc[u][0][2 * r + 1];
+                const int lo = acc[u][1][2 * r] * 256 + acc[u][1][2 * r + 1];
+                const float v = fmaf((float)hi, 65536.0f, (float)lo);
+                const float l = (s < n && hv) ? fmaf(v, qscale2, bias2) : -INFINITY;
+                lg[i][2 * u + r] = l;
+                mx = fmaxf(mx, l);
+            }
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (gid == 0) xg.mx[half][tig] = mx;
+    pair_sync(bar);
+    mx = fmaxf(xg.mx[0][tig], xg.mx[1][tig]);
+    if (mx == -INFINITY) mx = 0.0f;  // head without tokens (tig >= g)
+    const float psig = vmax > 0.0f ? 1.6e7f * rcp_approx(vmax) : 0.0f;
+    const float vinv = vmax * (1.0f / 1.6e7f);
+
+    // ---- softmax + p~ digits: four consecutive slots per lane and block
+    float lsum = 0.0f, bv = 0.0f;
+    const float2* vparam = reinterpret_cast<const float2*>(t + h.off_vp);
+#pragma unroll
+    for (int i = 0; i < BPW; ++i) {
+        const int pb = half + 2 * i;
+        // slots past the tile (partial / ghost blocks) read the last real group's
+        // finite parameters; their weights are exactly zero
+        const float4* vp4 = reinterpret_cast<const float4*>(vparam + min(32 * pb + 4 * gid, h.nslot - 4));
+        const float4 va = vp4[0], vb = vp4[1];
+        const float vs[4] = {va.x, va.z, vb.x, vb.z}, vo[4] = {va.y, va.w, vb.y, vb.w};
+        uint32_t N[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float p = ex2_approx(lg[i][j] - mx);
+            lsum += p;
+            bv = fmaf(p, vo[j], bv);
+            N[j] = (uint32_t)__float2int_rn(p * (vs[j] * psig));
+        }
+        const uint32_t d0 = __byte_perm(__byte_perm(N[0], N[1], 0x0040), __byte_perm(N[2], N[3], 0x0040), 0x5410);
+        const uint32_t d1 = __byte_perm(__byte_perm(N[0], N[1], 0x0051), __byte_perm(N[2], N[3], 0x0051), 0x5410);
+        const uint32_t d2 = __byte_perm(__byte_perm(N[0], N[1], 0x0062), __byte_perm(N[2], N[3], 0x0062), 0x5410);
+        uint8_t* pw = pdig + pb * 512 + 2 * tig * 32 + 4 * gid;
+        *reinterpret_cast<uint32_t*>(pw) = d2;
+        *reinterpret_cast<uint32_t*>(pw + 32) = d1;
+        *reinterpret_cast<uint32_t*>(pw + 256) = d0;
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        bv += __shfl_xor_sync(0xffffffffu, bv, o);
+    }
+    if (gid == 0) {
+        xg.lsum[half][tig] = lsum;
+        xg.bv[half][tig] = bv;
+    }
+    pair_sync(bar);
+    const float lt = xg.lsum[0][tig] + xg.lsum[1][tig];
+    const float bt = xg.bv[0][tig] + xg.bv[1][tig];
+
+    // ---- PV: this warp's 4 m-tiles (byte columns 16 half + 4 (gid & 3) + m)
+    int acc[4][2][4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[m][nt][0] = acc[m][nt][1] = acc[m][nt][2] = acc[m][nt][3] = 0;
+    const int jj = gid >> 2;
+    const uint32_t vm0 = 0x03030303u << (2 * jj), vm1 = 0x03030303u << (2 * jj + 4);
+    const int colb = ((16 * half + 4 * (gid & 3)) ^ (8 * tig)) * 4;  // vswz: (G & 3) == tig
+    const uint8_t* g0b = t + h.off_vseg[0] + (size_t)tig * 128 + colb;
+#pragma unroll
+    for (int kk = 0; kk < 2 * BPW; ++kk) {
+        uint32_t b[4];
+        ldsm_x4(b, pdig + kk * 512 + bofs);
+        const uint4 x0 = lds128(g0b + (size_t)kk * 1024), x1 = lds128(g0b + (size_t)kk * 1024 + 512);
+        const uint32_t u0[4] = {x0.x, x0.y, x0.z, x0.w}, u1[4] = {x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const uint32_t a[4] = {u0[m] & vm0, u0[m] & vm1, u1[m] & vm0, u1[m] & vm1};
+            mma_u8u8(acc[m][0], a, b[0], b[1]);
+            mma_u8u8(acc[m][1], a, b[2], b[3]);
+        }
+    }
+    if (hv) {
+        const float inv = rcp_approx(lt);
+        const float s0 = vinv * (jj ? 0.25f : 1.0f), s1 = s0 * 0.0625f;
+        IO* orow = out + tig * kD;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int ch = 4 * (16 * half + 4 * (gid & 3) + m) + jj;
+            const float v0 = fmaf(fmaf((float)acc[m][0][0], 256.0f, (float)acc[m][0][1]), 256.0f, (float)acc[m][1][0]);
+            const float v1 = fmaf(fmaf((float)acc[m][0][2], 256.0f, (float)acc[m][0][3]), 256.0f, (float)acc[m][1][2]);
+            const float r0 = fmaf(v0, s0, bt) * inv, r1 = fmaf(v1, s1, bt) * inv;
+            if constexpr (sizeof(IO) == 2) {
+                orow[ch] = __float2half_rn(r0);
+                orow[ch + 2] = __float2half_rn(r1);
+            } else {
+                orow[ch] = r0;
+                orow[ch + 2] = r1;
+            }
+        }
+    }
+}
+
+template <typename IO, int BPW>
+__global__ void __launch_bounds__(32 * (2 * kPairs + 1), 1) decode_u2x_kernel(const MmaParams p) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    uint64_t* empty = full + kMaxR;
+    uint8_t* ring = dsm + 2 * kMaxR * sizeof(uint64_t);
+    uint8_t* scratch0 = ring + (size_t)p.R * p.slot_bytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qbytes = p.g * kD * (int)sizeof(IO);
+    const int npairs = p.W;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.R; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 2);
+        }
+        fence_barrier_init();
+    }
+    // p~ digit columns that are never written (n-tile 1, odd rows) stay zero
+    for (int i = threadIdx.x; i < npairs * p.scratch_bytes / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(scratch0)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int ntiles = p.units > (int)blockIdx.x ? (p.units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (warp == 0) {
+        for (int base = 0; base < ntiles; base += 32) {
+            const int mj = base + lane;
+            int64_t moff = 0;
+            int msz = 0;
+            if (mj < ntiles) {
+                const int tile = blockIdx.x + mj * gridDim.x;
+                moff = p.offsets[tile];
+                msz = p.dsize[tile];
+            }
+            const int cnt = min(32, ntiles - base);
+            for (int k = 0; k < cnt; ++k) {
+                const int64_t off = __shfl_sync(0xffffffffu, moff, k);
+                const int sz = __shfl_sync(0xffffffffu, msz, k);
+                if (lane == 0) {
+                    const int j = base + k;
+                    const int slot = j % p.R, use = j / p.R;
+                    if (use > 0) mbar_wait(&empty[slot], (uint32_t)((use - 1) & 1));
+                    fence_proxy_async();
+                    uint8_t* dst = ring + (size_t)slot * p.slot_bytes;
+                    const int tile = blockIdx.x + j * gridDim.x;
+                    mbar_expect_tx(&full[slot], (uint32_t)(sz + qbytes));
+                    bulk_g2s(dst, p.arena + off, (uint32_t)sz, &full[slot]);
+                    bulk_g2s(dst + p.slot_bytes - qbytes,
+                             static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &full[slot]);
+                }
+                __syncwarp();
+            }
+        }
+        return;
+    }
+    const int pr = (warp - 1) >> 1, half = (warp - 1) & 1;
+    uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
+    int slot = pr % p.R, use = pr / p.R;
+    for (int j = pr; j < ntiles; j += npairs) {
+        mbar_wait(&full[slot], (uint32_t)(use & 1));
+        __syncwarp();
+        const uint8_t* st = ring + (size_t)slot * p.slot_bytes;
+        const int tile = blockIdx.x + j * gridDim.x;
+        const IO* qs = reinterpret_cast<const IO*>(st + p.slot_bytes - qbytes);
+        IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
+        // blocks per warp of THIS tile (warp-uniform via redux): tiles with a few
+        // tokens over a 64-token boundary do not pay ghost blocks for the others
+        const int bpw = __reduce_max_sync(0xffffffffu, (reinterpret_cast<const TileHeader*>(st)->r[0] + 63) >> 6);
+        if (BPW >= 3 && bpw == 3)
+            decode_tile_u2x<IO, (BPW >= 3 ? 3 : BPW)>(st, qs, p.g, scr, o, half, 1 + pr);
+        else if (BPW >= 2 && bpw == 2)
+            decode_tile_u2x<IO, (BPW >= 2 ? 2 : BPW)>(st, qs, p.g, scr, o, half, 1 + pr);
+        else
+            decode_tile_u2x<IO, 1>(st, qs, p.g, scr, o, half, 1 + pr);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        slot += npairs;
+        while (slot >= p.R) {
+            slot -= p.R;
+            ++use;
+        }
+    }
+}
+
+// Pairs per CTA and ring depth. The tiles of a CTA are dealt round-robin to
+// its pairs, so a CTA takes ceil(T / W) tile rounds for its T tiles: W is
+// chosen to waste as few pair-rounds as possible (e.g. 7 pairs for the 27-28
+// tiles per SM of a 4096-tile step rather than 11, which needs 3 rounds for
+// 2.5 tiles of work), then the ring gets every slot that still fits as TMA
+// lookahead.
+static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, int& W, int& R) {
+    const int head = 2 * kMaxR * (int)sizeof(uint64_t);
+    const int slack = 4096;  // ghost-block fragment over-reads past the last ring slot
+    const char* env = getenv("RDKV_DECODE_PAIRS");
+    const int forced = env ? atoi(env) : 0;
+    const int per_sm = (units + nsm - 1) / nsm;
+    double best = 1e30;
+    W = 0;
+    for (int w = 1; w <= kPairs; ++w) {
+        if (forced && w != forced) continue;
+        if (head + (size_t)(w + 1) * slot + (size_t)w * scratch + slack > (size_t)smem_max) continue;
+        const int rounds = (per_sm + w - 1) / w;
+        // time ~ rounds x per-round latency; a round's latency grows with the
+        // warps sharing the SM but not below the ~6-pair latency floor
+        const double cost = rounds * (double)(w > 6 ? w : 6);
+        if (cost < best - 1e-9 || (cost < best + 1e-9 && w > W)) {
+            best = cost;
+            W = w;
+        }
+    }
+    if (W == 0) return false;
+    R = W;
+    while (R < kMaxR && head + (size_t)(R + 1) * slot + (size_t)W * scratch + slack <= (size_t)smem_max) ++R;
+    return true;
+}
+
+template <typename IO, int BPW>
+static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
+    const int qbytes = a->group * kD * (int)sizeof(IO);
+    const int slot = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
+    const int scratch = kXPDig + 2 * BPW * 512;
+    int dev = 0, smem_max = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int W = 0, R = 0;
+    if (!pick_pairs(a->units, nsm, slot, scratch, smem_max, W, R)) return RDKV_EINVAL;
+    const size_t smem = 2 * kMaxR * sizeof(uint64_t) + (size_t)R * slot + (size_t)W * scratch + 4096;
+    const char* null_env = getenv("RDKV_DECODE_NULL");  // experiment: stream tiles, skip the math
+    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
+                a->units, a->group, 0, R, W, slot, scratch, 0, 0, -1, -1,
+                null_env && *null_env == '1' ? 777 : 0};
+    auto kern = decode_u2x_kernel<IO, BPW>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int blocks = (a->units + W - 1) / W;
+    if (blocks > nsm) blocks = nsm;
+    kern<<<blocks, 32 * (2 * W + 1), smem, st>>>(p);
+    return launch_status();
+}
+
+template <typename IO>
+static int launch_u2x(const rdkv_decode_args* a, cudaStream_t st) {
+    const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
+    if (nb <= 2) return launch_u2x_t<IO, 1>(a, st);
+    if (nb <= 4) return launch_u2x_t<IO, 2>(a, st);
+    return launch_u2x_t<IO, 3>(a, st);
+}
+
 }  // namespace rdkv_b200
 
 using namespace rdkv_b200;
@@ -1312,7 +1725,8 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     // kernel 4 selects the one-warp body, kernel 3 the general body
     const bool u2 = a->plan.uniform2 && a->group <= 4 && !a->zc_len && a->kernel != 3;
     if (u2 && a->kernel == 4) return f16 ? launch_t<1, __half, true>(a, st) : launch_t<1, float, true>(a, st);
-    if (u2) return f16 ? launch_pair<__half>(a, st) : launch_pair<float>(a, st);
+    if (u2 && a->kernel == 5) return f16 ? launch_pair<__half>(a, st) : launch_pair<float>(a, st);
+    if (u2) return f16 ? launch_u2x<__half>(a, st) : launch_u2x<float>(a, st);
     if (a->group <= 4) return f16 ? launch_t<1, __half, false>(a, st) : launch_t<1, float, false>(a, st);
     return f16 ? launch_t<2, __half, false>(a, st) : launch_t<2, float, false>(a, st);
 }

@@ -10,6 +10,7 @@
 // (byte-for-byte against build_trizone) and by the C++ drop-in layer to hand
 // a reference-shaped TriZoneCache back to callers.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <vector>
 
@@ -74,7 +75,7 @@ struct TileView {
         std::memcpy(&v, base + perm_off(h) + 2 * ks, 2);
         return v;
     }
-    const uint8_t* krow(int slot) const { return base + h.off_k + (size_t)slot * h.krow_bytes; }
+    const uint8_t* krow(int slot) const { return base + krow_offset(h, slot); }
 };
 
 unsigned extract(const uint8_t* row, int j, int bits) {
@@ -306,7 +307,7 @@ extern "C" RDKV_API int rdkv_tile_import(int32_t d, int32_t n, const int32_t* ke
     }
     // K rows per slot
     for (int i = 0; i < n; ++i) {
-        uint8_t* row = tile + h.off_k + (size_t)slot_of[i] * h.krow_bytes;
+        uint8_t* row = tile + krow_offset(h, slot_of[i]);
         for (int c = 0; c < d; ++c) {
             const int ks = kslot_of[c];
             if (ks < 0) continue;
@@ -336,6 +337,11 @@ extern "C" RDKV_API int rdkv_tile_import(int32_t d, int32_t n, const int32_t* ke
         vp[2 * slot_of[i] + 1] = offset_of(vscale[i], vzero[i]);
         vz[slot_of[i]] = vzero[i];
     }
+    // scale bounds of the 2-bit class (same as the device packer)
+    float km = 0.0f, vm = 0.0f;
+    for (int j = 0; j < h.c[0]; ++j) km = std::max(km, std::fabs(chan[2 * (h.kslot_base[0] + j)]));
+    for (int j = 0; j < h.r[0]; ++j) vm = std::max(vm, std::fabs(vp[2 * j]));
+    reinterpret_cast<TileHeader*>(tile)->scale_bounds = bf16_bound_bits(km) | (bf16_bound_bits(vm) << 16);
     return RDKV_OK;
 }
 

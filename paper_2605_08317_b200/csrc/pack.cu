@@ -96,6 +96,7 @@ struct PackSmem {
     double kscale[384];   // fp64 scale per K slot of classes 0-2 (d <= 256 + pads)
     double kzd[384];      // fp64 zero point
     int bad;
+    unsigned int kmax, vmax;
 };
 
 // quantize_unit parameters from f32 lo/hi (quantizer.cpp:110-123)
@@ -280,15 +281,14 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(
                     val |= quant_code(x, s.kscale[ks], s.kzd[ks], bits) << (j * bits);
                 }
             }
-            tile[h.off_k + (size_t)sl * h.krow_bytes + byte] = (uint8_t)val;
+            tile[krow_offset(h, sl) + byte] = (uint8_t)val;
         }
         const int n16 = h.c[3];
         for (int it = tid; it < h.nslot * n16; it += blockDim.x) {
             const int sl = it / n16, j = it % n16;
             const int t = ids[sl];
             const float x = t >= 0 ? load_as_float(K, (size_t)t * d + perm[h.kslot_base[3] + j]) : 0.0f;
-            reinterpret_cast<__half*>(tile + h.off_k + (size_t)sl * h.krow_bytes + h.kbyte_base[3])[j] =
-                __float2half_rn(x);
+            reinterpret_cast<__half*>(tile + krow_offset(h, sl) + h.kbyte_base[3])[j] = __float2half_rn(x);
         }
         (void)kq_slots;
     }
@@ -352,7 +352,22 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(
         }
     }
     __syncthreads();
-    if (tid == 0 && head_status) head_status[unit] = s.bad ? RDKV_ENUMERIC : RDKV_OK;
+    // scale bounds of the 2-bit class (the tensor-core body's fixed-point ranges)
+    if (tid == 0) s.kmax = s.vmax = 0u;
+    __syncthreads();
+    {
+        uint32_t km = 0u, vm = 0u;  // non-negative floats order like their bit patterns
+        for (int j = tid; j < h.c[0]; j += blockDim.x) km = max(km, __float_as_uint(fabsf(chan[h.kslot_base[0] + j].x)));
+        for (int j = tid; j < h.r[0]; j += blockDim.x) vm = max(vm, __float_as_uint(fabsf(vparam[j].x)));
+        atomicMax(&s.kmax, km);
+        atomicMax(&s.vmax, vm);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        reinterpret_cast<TileHeader*>(tile)->scale_bounds =
+            bf16_bound_bits(__uint_as_float(s.kmax)) | (bf16_bound_bits(__uint_as_float(s.vmax)) << 16);
+        if (head_status) head_status[unit] = s.bad ? RDKV_ENUMERIC : RDKV_OK;
+    }
 }
 
 }  // namespace rdkv_b200

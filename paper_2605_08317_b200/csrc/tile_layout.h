@@ -28,7 +28,7 @@
 //   [0,128)            TileHeader
 //   [128, +8*kslots)   per K slot float2 {scale, offset}
 //   [.., +2*kslots)    per K slot uint16 channel id (16-B padded)
-//   off_k              nslot K rows x krow_bytes:
+//   off_k              nslot K rows x krow_bytes, slot-transposed (krow_pos):
 //                        [P2/4 B 2-bit][P4/2 B 4-bit][P8 B 8-bit][2*P16 B fp16]
 //   off_vseg[0..2]     V classes 2/4/8: (slots/4) groups x 4*rb(bits)
 //   off_vseg[3]        V class 16: slots x d fp16, row-major
@@ -61,7 +61,7 @@ struct TileHeader {
     int32_t krow_bytes;  // bytes per K row
     int32_t nslot;       // token slots
     int32_t off_k;
-    int32_t off_v;       // == off_vseg[0]
+    uint32_t scale_bounds;  // bf16 upper bounds: lo = max K scale (2-bit channels), hi = max V scale (2-bit rows)
     int32_t off_vp;
     int32_t off_vseg[4];
     int32_t off_ids;
@@ -125,7 +125,7 @@ RDKV_HD void tile_layout(TileHeader& h, int32_t d) {
     }
     h.off_vseg[3] = (int32_t)off;
     off = align_up(off + (int64_t)pad4(h.r[3]) * d * 2, 16);
-    h.off_v = h.off_vseg[0];
+    h.scale_bounds = 0;  // filled by the packer once the scales are known
     h.off_vp = (int32_t)off;
     off = align_up(off + (int64_t)8 * h.nslot, 16);
     h.off_ids = (int32_t)off;
@@ -138,6 +138,28 @@ RDKV_HD void tile_layout(TileHeader& h, int32_t d) {
 }
 
 RDKV_HD int32_t chan_table_off() { return kHeaderBytes; }
+
+// K rows are stored slot-transposed: the row of token slot s sits at position
+// (s & 3) * (nslot / 4) + (s >> 2). A tensor-core lane that owns the four
+// consecutive slots 4j..4j+3 (so its softmax weights pack into one 32-bit
+// word per digit) then reads K rows that are 32 B apart across the lanes of a
+// quarter-warp instead of 128 B apart (bank-conflict-free LDS.128).
+RDKV_HD int32_t krow_pos(const TileHeader& h, int32_t s) { return (s & 3) * (h.nslot >> 2) + (s >> 2); }
+RDKV_HD int64_t krow_offset(const TileHeader& h, int32_t s) {
+    return (int64_t)h.off_k + (int64_t)krow_pos(h, s) * h.krow_bytes;
+}
+
+// bf16 bit pattern of a non-negative float, rounded up (an upper bound).
+RDKV_HD uint32_t bf16_bound_bits(float x) {
+    union { float f; uint32_t u; } v;
+    v.f = x;
+    return (v.u & 0xFFFFu) ? (v.u >> 16) + 1u : (v.u >> 16);
+}
+RDKV_HD float bf16_bits_to_float(uint32_t b) {
+    union { float f; uint32_t u; } v;
+    v.u = b << 16;
+    return v.f;
+}
 RDKV_HD int32_t perm_off(const TileHeader& h) { return kHeaderBytes + 8 * h.kslots; }
 
 // First slot of V class i.

@@ -66,7 +66,7 @@ def layout(r, c, d):
         off = align(off + pad4(r[i]) * ref_row_bytes(d, kbits(i)), 16)
     h["off_vseg"].append(off)
     off = align(off + pad4(r[3]) * d * 2, 16)
-    h["off_v"] = h["off_vseg"][0]
+    h["scale_bounds"] = 0
     h["off_vp"] = off
     off = align(off + 8 * h["nslot"], 16)
     h["off_ids"] = off
@@ -81,11 +81,21 @@ def layout(r, c, d):
     return h
 
 
+def krow_pos(h, s):
+    """Slot-transposed K row position (tile_layout.h krow_pos)."""
+    return (s & 3) * (h["nslot"] >> 2) + (s >> 2)
+
+
+def bf16_bound_bits(x):
+    u = int(np.array([abs(x)], np.float32).view(np.uint32)[0])
+    return (u >> 16) + (1 if u & 0xFFFF else 0)
+
+
 def header_bytes(h):
     vals = [MAGIC, h["n"], *h["r"], *h["c"], h["kslots"], h["krow_bytes"], h["nslot"], h["off_k"],
-            h["off_v"], h["off_vp"], *h["off_vseg"], h["off_ids"], h["off_vz"], h["off_kz"],
+            h["scale_bounds"], h["off_vp"], *h["off_vseg"], h["off_ids"], h["off_vz"], h["off_kz"],
             h["total_bytes"], *h["kslot_base"], *h["kbyte_base"]]
-    return np.array(vals, dtype="<i4").view(np.uint8)
+    return np.array(vals, dtype="<i8").astype("<u4").view(np.uint8)
 
 
 def pack_codes(codes, bits):
@@ -170,7 +180,7 @@ def build_tile(canon, v_bits, k_bits, v_src, d):
                 vals[j] = np.float16(canon["kfp"][ki][ch])
             b0 = h["kbyte_base"][3]
             row[b0:b0 + 2 * len(vals)] = vals.view(np.uint8)
-        o = h["off_k"] + sl * h["krow_bytes"]
+        o = h["off_k"] + krow_pos(h, sl) * h["krow_bytes"]
         tile[o:o + h["krow_bytes"]] = row
     # V rows + params
     vp = np.zeros((h["nslot"], 2), "<f4")
@@ -198,4 +208,9 @@ def build_tile(canon, v_bits, k_bits, v_src, d):
         base += cnt
     tile[h["off_vp"]:h["off_vp"] + 8 * h["nslot"]] = vp.reshape(-1).view(np.uint8)
     tile[h["off_vz"]:h["off_vz"] + 8 * h["nslot"]] = vz.view(np.uint8)
+    # scale bounds of the 2-bit class (bf16, rounded up): K channels low, V rows high
+    km = max([abs(float(chan[h["kslot_base"][0] + j][0])) for j in range(h["c"][0])] or [0.0])
+    vm = max([abs(float(vp[j][0])) for j in range(r[0])] or [0.0])
+    h["scale_bounds"] = bf16_bound_bits(km) | (bf16_bound_bits(vm) << 16)
+    tile[:HEADER] = header_bytes(h)
     return tile
