@@ -131,7 +131,7 @@ typedef struct {
     int32_t max_slots;        /* largest token-slot count */
     int32_t max_zone_b_rows;  /* largest Zone B (16-bit V) row count */
     int32_t max_kq_slots;     /* largest quantised-K slot count */
-    int32_t uniform2;         /* every tile: all kept V rows and K channels at 2 bits */
+    int32_t uniform2;         /* every tile: all kept V rows and K channels at 2 bits (2: and all d K channels kept) */
 } rdkv_decode_plan;
 
 typedef struct {

@@ -1300,41 +1300,83 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-template <typename IO, int BPW>
-__device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const IO* __restrict__ qs, int g,
-                                                uint8_t* __restrict__ scr, IO* __restrict__ out, int half,
-                                                int bar) {
-    const int lane = threadIdx.x & 31;
-    const int gid = lane >> 2, tig = lane & 3;
+// Per-lane constants of the u2x body, computed once per warp.
+struct U2xLane {
+    int lane, gid, tig, half;
+    int pshift;      // q~ digit prescale 4^(3 - (gid & 3))
+    int bofs;        // ldmatrix row address of this lane inside a 512-B digit block
+    int qdig_w;      // q~ digit store offset (k-step 0) inside the digit area
+    int pdig_w;      // p~ digit store offset (block 0)
+    uint32_t kmask, vm0, vm1;
+    int jj;          // channel sub-index of this lane's PV rows
+    int vcol;        // V byte offset of this lane inside a 4-token group block (tig group + swizzled column)
+    int ch0;         // first output channel of this lane
+};
+
+__device__ __forceinline__ U2xLane u2x_lane(int half) {
+    U2xLane c;
+    c.lane = threadIdx.x & 31;
+    c.gid = c.lane >> 2;
+    c.tig = c.lane & 3;
+    c.half = half;
+    c.pshift = 2 * (3 - (c.gid & 3));
+    // digit blocks: rows of 32 B (one B column each), the two 16-B halves of
+    // rows 4..7 (mod 8) swapped so ldmatrix phases hit distinct banks
+    const int mat = c.lane >> 3, rr = c.lane & 7;
+    c.bofs = ((mat >> 1) * 8 + rr) * 32 + (((mat & 1) ^ ((rr >> 2) & 1)) * 16);
+    c.qdig_w = 2 * c.tig * 32 + (((c.gid >> 2) ^ ((c.tig >> 1) & 1)) * 16) + 4 * (c.gid & 3);
+    c.pdig_w = c.qdig_w;
+    c.kmask = 0x03030303u << (2 * c.tig);
+    c.jj = c.gid >> 2;
+    c.vm0 = 0x03030303u << (2 * c.jj);
+    c.vm1 = 0x03030303u << (2 * c.jj + 4);
+    c.vcol = c.tig * 128 + (((16 * half + 4 * (c.gid & 3)) ^ (8 * c.tig)) * 4);  // vswz: (G & 3) == tig
+    c.ch0 = 4 * (16 * half + 4 * (c.gid & 3)) + c.jj;
+    return c;
+}
+
+// FULLK: every one of the 128 K channels is kept at 2 bits (channel_perm is
+// the identity, 32-B K rows) — the production shape; otherwise c0 < 128.
+// q rows sit in the ring slot at a padded stride (kXQStride) so the lanes of
+// different heads read different banks.
+template <typename IO>
+__host__ __device__ constexpr int u2x_qstride() { return kD * (int)sizeof(IO) + 16; }
+
+template <typename IO, int BPW, bool FULLK, typename AfterSync1>
+__device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
+                                                uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
+                                                const U2xLane& L, AfterSync1&& after_sync1) {
+    const int gid = L.gid, tig = L.tig, half = L.half;
     const bool hv = tig < g;
     const TileHeader& h = *reinterpret_cast<const TileHeader*>(t);
     PairX& xg = *reinterpret_cast<PairX*>(scr);
     uint8_t* qdig = scr + kXQDig;
     uint8_t* pdig = scr + kXPDig;
     const float2* chan = reinterpret_cast<const float2*>(t + kHeaderBytes);
-    const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
-    const uint8_t* krows = t + h.off_k;
     const int n = h.r[0];
-    const int c0 = h.c[0];
-    const int kmax_slot = h.kslots - 1;
-    const int krb = h.krow_bytes;
-    const int Q = h.nslot >> 2;
+    const int nslot = h.nslot;
+    const int c0 = FULLK ? kD : h.c[0];
+    const int krb = FULLK ? 32 : h.krow_bytes;
+    const int Q = nslot >> 2;
     const uint32_t sbits = h.scale_bounds;
     const float smax = bf16_bits_to_float(sbits & 0xFFFFu), vmax = bf16_bits_to_float(sbits >> 16);
     constexpr float kInvSqrtD = 0.08838834764831845f;
     constexpr float kLog2e = 1.4426950408889634f;
 
-    // ---- q range of head tig (lanes gid cover 16 channels each)
-    float qm = hv ? absmax16<IO>(qs + tig * kD + 16 * gid) : 0.0f;
+    // ---- q range per head: lanes 8h..8h+7 scan head h (16 channels each), then
+    // every lane picks its head tig
+    constexpr int QS = u2x_qstride<IO>();
+    const int hq = L.lane >> 3;
+    float qm = absmax16<IO>(reinterpret_cast<const IO*>(qs + (hq < g ? hq : 0) * QS) + 16 * (L.lane & 7));
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+    for (int o = 1; o < 8; o <<= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+    qm = __shfl_sync(0xffffffffu, qm, 8 * tig);
+    const IO* qh = reinterpret_cast<const IO*>(qs + (hv ? tig : 0) * QS);
     const float bnd = smax * qm;
-    const float sg = bnd > 0.0f ? 8.2e6f * rcp_approx(bnd) : 0.0f;
+    const float sg = (hv && bnd > 0.0f) ? 8.2e6f * rcp_approx(bnd) : 0.0f;  // heads >= g: zero digits
 
     // ---- q~ digits (k-steps half, half + 2) and the bias sum_c q_c * offset_c
     float bpart = 0.0f;
-    const int pshift = 2 * (3 - (gid & 3));
-    const IO* qh = qs + (hv ? tig : 0) * kD;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const int kk = half + 2 * i;
@@ -1342,19 +1384,26 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int j = kk * 32 + 16 * (gid >> 2) + 4 * e + (gid & 3);
-            const bool ok = hv && j < c0;
-            const int js = min(j, kmax_slot);
-            const float2 cs = chan[js];
-            const float qv = ok ? ld_io(qh, perm[js]) : 0.0f;
+            float qv;
+            float2 cs;
+            if constexpr (FULLK) {
+                cs = chan[j];
+                qv = ld_io(qh, j);
+            } else {
+                const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
+                const int js = min(j, h.kslots - 1);
+                cs = chan[js];
+                qv = j < c0 ? ld_io(qh, perm[js]) : 0.0f;
+            }
             bpart = fmaf(qv, cs.y, bpart);
             const int N = __float2int_rn(cs.x * qv * sg);
-            x[e] = ((uint32_t)N << pshift) + 0x80808080u ^ 0x80808080u;
+            x[e] = ((uint32_t)N << L.pshift) + 0x80808080u ^ 0x80808080u;
         }
         const uint32_t w0 = __byte_perm(__byte_perm(x[0], x[1], 0x0040), __byte_perm(x[2], x[3], 0x0040), 0x5410);
         const uint32_t w1 = __byte_perm(__byte_perm(x[0], x[1], 0x0051), __byte_perm(x[2], x[3], 0x0051), 0x5410);
         const uint32_t w2 = __byte_perm(__byte_perm(x[0], x[1], 0x0062), __byte_perm(x[2], x[3], 0x0062), 0x5410);
         const uint32_t w3 = __byte_perm(__byte_perm(x[0], x[1], 0x0073), __byte_perm(x[2], x[3], 0x0073), 0x5410);
-        uint8_t* a0 = qdig + kk * 512 + 2 * tig * 32 + 4 * gid;
+        uint8_t* a0 = qdig + kk * 512 + L.qdig_w;
         *reinterpret_cast<uint32_t*>(a0) = w3;
         *reinterpret_cast<uint32_t*>(a0 + 32) = w2;
         *reinterpret_cast<uint32_t*>(a0 + 256) = w1;
@@ -1364,17 +1413,19 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     for (int o = 4; o < 32; o <<= 1) bpart += __shfl_xor_sync(0xffffffffu, bpart, o);
     if (gid == 0) xg.bias[half][tig] = bpart;
     pair_sync(bar);
-    // l' = log2(e) * (v / (64 sigma) + bias) / sqrt(d)
-    const float bias2 = (xg.bias[0][tig] + xg.bias[1][tig]) * (kInvSqrtD * kLog2e);
+    after_sync1();  // both warps are past the previous tile: its buffer may be refilled
+    // l' = log2(e) * (v / (64 sigma) + bias) / sqrt(d); heads >= g get -inf logits
+    const float bias2 = hv ? (xg.bias[0][tig] + xg.bias[1][tig]) * (kInvSqrtD * kLog2e) : -INFINITY;
     const float qscale2 = bnd * (kInvSqrtD * kLog2e / (64.0f * 8.2e6f));
 
-    // ---- QK
-    const int mat = lane >> 3, rr = lane & 7;
-    const int bofs = ((mat >> 1) * 8 + rr) * 32 + (mat & 1) * 16;
+    // ---- QK over this warp's blocks half, half + 2, ...
     uint32_t bq[4][4];
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) ldsm_x4(bq[kk], qdig + kk * 512 + bofs);
-    const uint32_t kmask = 0x03030303u << (2 * tig);
+    for (int kk = 0; kk < 4; ++kk) ldsm_x4(bq[kk], qdig + kk * 512 + L.bofs);
+    // A rows gid / gid + 8 of m-tile u = slots 32pb + 4gid + 2u / + 1, stored at
+    // positions (2u + r) Q + 8pb + gid (slot-transposed K rows)
+    const uint8_t* kbase = t + h.off_k + (size_t)(8 * half + gid) * krb;
+    const int qstride = Q * krb;
     float lg[BPW][4];
     float mx = -INFINITY;
 #pragma unroll
@@ -1383,9 +1434,8 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
         int acc[2][2][4];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            // A rows gid / gid + 8 = slots 32pb + 4gid + 2u / + 1 (positions (2u + r) Q + 8pb + gid)
-            const uint8_t* r0 = krows + (size_t)((2 * u) * Q + 8 * pb + gid) * krb;
-            const uint8_t* r1 = r0 + (size_t)Q * krb;
+            const uint8_t* r0 = kbase + 2 * u * qstride + 16 * i * krb;
+            const uint8_t* r1 = r0 + qstride;
             const uint4 x0 = lds128(r0), x1 = lds128(r0 + 16), y0 = lds128(r1), y1 = lds128(r1 + 16);
             const uint32_t w0[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
             const uint32_t w1[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
@@ -1393,21 +1443,21 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                const uint32_t a[4] = {w0[2 * kk] & kmask, w1[2 * kk] & kmask, w0[2 * kk + 1] & kmask,
-                                       w1[2 * kk + 1] & kmask};
+                const uint32_t a[4] = {w0[2 * kk] & L.kmask, w1[2 * kk] & L.kmask, w0[2 * kk + 1] & L.kmask,
+                                       w1[2 * kk + 1] & L.kmask};
                 mma_u8s8(acc[u][0], a, bq[kk][0], bq[kk][1]);
                 mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
             }
         }
+        const int sbase = 32 * pb + 4 * gid;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
-                const int s = 32 * pb + 4 * gid + 2 * u + r;
                 const int hi = acc[u][0][2 * r] * 256 + acc[u][0][2 * r + 1];
                 const int lo = acc[u][1][2 * r] * 256 + acc[u][1][2 * r + 1];
                 const float v = fmaf((float)hi, 65536.0f, (float)lo);
-                const float l = (s < n && hv) ? fmaf(v, qscale2, bias2) : -INFINITY;
+                const float l = (sbase + 2 * u + r < n) ? fmaf(v, qscale2, bias2) : -INFINITY;
                 lg[i][2 * u + r] = l;
                 mx = fmaxf(mx, l);
             }
@@ -1429,7 +1479,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
         const int pb = half + 2 * i;
         // slots past the tile (partial / ghost blocks) read the last real group's
         // finite parameters; their weights are exactly zero
-        const float4* vp4 = reinterpret_cast<const float4*>(vparam + min(32 * pb + 4 * gid, h.nslot - 4));
+        const float4* vp4 = reinterpret_cast<const float4*>(vparam + min(32 * pb + 4 * gid, nslot - 4));
         const float4 va = vp4[0], vb = vp4[1];
         const float vs[4] = {va.x, va.z, vb.x, vb.z}, vo[4] = {va.y, va.w, vb.y, vb.w};
         uint32_t N[4];
@@ -1443,7 +1493,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
         const uint32_t d0 = __byte_perm(__byte_perm(N[0], N[1], 0x0040), __byte_perm(N[2], N[3], 0x0040), 0x5410);
         const uint32_t d1 = __byte_perm(__byte_perm(N[0], N[1], 0x0051), __byte_perm(N[2], N[3], 0x0051), 0x5410);
         const uint32_t d2 = __byte_perm(__byte_perm(N[0], N[1], 0x0062), __byte_perm(N[2], N[3], 0x0062), 0x5410);
-        uint8_t* pw = pdig + pb * 512 + 2 * tig * 32 + 4 * gid;
+        uint8_t* pw = pdig + pb * 512 + L.pdig_w;
         *reinterpret_cast<uint32_t*>(pw) = d2;
         *reinterpret_cast<uint32_t*>(pw + 32) = d1;
         *reinterpret_cast<uint32_t*>(pw + 256) = d0;
@@ -1467,188 +1517,178 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     for (int m = 0; m < 4; ++m)
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) acc[m][nt][0] = acc[m][nt][1] = acc[m][nt][2] = acc[m][nt][3] = 0;
-    const int jj = gid >> 2;
-    const uint32_t vm0 = 0x03030303u << (2 * jj), vm1 = 0x03030303u << (2 * jj + 4);
-    const int colb = ((16 * half + 4 * (gid & 3)) ^ (8 * tig)) * 4;  // vswz: (G & 3) == tig
-    const uint8_t* g0b = t + h.off_vseg[0] + (size_t)tig * 128 + colb;
+    const uint8_t* g0b = t + h.off_vseg[0] + L.vcol;
 #pragma unroll
     for (int kk = 0; kk < 2 * BPW; ++kk) {
         uint32_t b[4];
-        ldsm_x4(b, pdig + kk * 512 + bofs);
-        const uint4 x0 = lds128(g0b + (size_t)kk * 1024), x1 = lds128(g0b + (size_t)kk * 1024 + 512);
+        ldsm_x4(b, pdig + kk * 512 + L.bofs);
+        const uint4 x0 = lds128(g0b + kk * 1024), x1 = lds128(g0b + kk * 1024 + 512);
         const uint32_t u0[4] = {x0.x, x0.y, x0.z, x0.w}, u1[4] = {x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const uint32_t a[4] = {u0[m] & vm0, u0[m] & vm1, u1[m] & vm0, u1[m] & vm1};
+            const uint32_t a[4] = {u0[m] & L.vm0, u0[m] & L.vm1, u1[m] & L.vm0, u1[m] & L.vm1};
             mma_u8u8(acc[m][0], a, b[0], b[1]);
             mma_u8u8(acc[m][1], a, b[2], b[3]);
         }
     }
     if (hv) {
         const float inv = rcp_approx(lt);
-        const float s0 = vinv * (jj ? 0.25f : 1.0f), s1 = s0 * 0.0625f;
-        IO* orow = out + tig * kD;
+        const float s0 = vinv * (L.jj ? 0.25f : 1.0f), s1 = s0 * 0.0625f;
+        IO* orow = out + tig * kD + L.ch0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const int ch = 4 * (16 * half + 4 * (gid & 3) + m) + jj;
             const float v0 = fmaf(fmaf((float)acc[m][0][0], 256.0f, (float)acc[m][0][1]), 256.0f, (float)acc[m][1][0]);
             const float v1 = fmaf(fmaf((float)acc[m][0][2], 256.0f, (float)acc[m][0][3]), 256.0f, (float)acc[m][1][2]);
             const float r0 = fmaf(v0, s0, bt) * inv, r1 = fmaf(v1, s1, bt) * inv;
             if constexpr (sizeof(IO) == 2) {
-                orow[ch] = __float2half_rn(r0);
-                orow[ch + 2] = __float2half_rn(r1);
+                orow[4 * m] = __float2half_rn(r0);
+                orow[4 * m + 2] = __float2half_rn(r1);
             } else {
-                orow[ch] = r0;
-                orow[ch + 2] = r1;
+                orow[4 * m] = r0;
+                orow[4 * m + 2] = r1;
             }
         }
     }
 }
 
-template <typename IO, int BPW>
-__global__ void __launch_bounds__(32 * (2 * kPairs + 1), 1) decode_u2x_kernel(const MmaParams p) {
+constexpr int kXPairs = 8;   // <= 16 warps per CTA: up to 128 registers per thread, no spills
+constexpr int kXMaxBuf = 4;  // tile buffers per pair
+
+// Self-fed warp pairs: pair p owns NBUF tile buffers and decodes the CTA's
+// tiles p, p + W, p + 2W, ...; its first lane issues the TMA bulk copies of its
+// own next tiles (a buffer is refilled as soon as both warps are past the
+// previous tile's first barrier), so a slow pair never blocks the others'
+// loads (no shared producer, no head-of-line blocking).
+template <typename IO, int BPW, bool FULLK>
+__global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
-    uint64_t* empty = full + kMaxR;
-    uint8_t* ring = dsm + 2 * kMaxR * sizeof(uint64_t);
-    uint8_t* scratch0 = ring + (size_t)p.R * p.slot_bytes;
+    const int nbuf = p.R;  // buffers per pair
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);  // [W][kXMaxBuf]
+    uint8_t* bufs = dsm + kXPairs * kXMaxBuf * sizeof(uint64_t);
+    uint8_t* scratch0 = bufs + (size_t)p.W * nbuf * p.slot_bytes;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qbytes = p.g * kD * (int)sizeof(IO);
-    const int npairs = p.W;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < p.R; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 2);
-        }
-        fence_barrier_init();
-    }
-    // p~ digit columns that are never written (n-tile 1, odd rows) stay zero
-    for (int i = threadIdx.x; i < npairs * p.scratch_bytes / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(scratch0)[i] = make_uint4(0, 0, 0, 0);
-    __syncthreads();
+    const int pr = warp >> 1, half = warp & 1;
+    const int qrow = kD * (int)sizeof(IO);
+    const int qbytes = p.g * qrow;
     const int ntiles = p.units > (int)blockIdx.x ? (p.units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    if (warp == 0) {
-        for (int base = 0; base < ntiles; base += 32) {
-            const int mj = base + lane;
-            int64_t moff = 0;
-            int msz = 0;
-            if (mj < ntiles) {
-                const int tile = blockIdx.x + mj * gridDim.x;
-                moff = p.offsets[tile];
-                msz = p.dsize[tile];
-            }
-            const int cnt = min(32, ntiles - base);
-            for (int k = 0; k < cnt; ++k) {
-                const int64_t off = __shfl_sync(0xffffffffu, moff, k);
-                const int sz = __shfl_sync(0xffffffffu, msz, k);
-                if (lane == 0) {
-                    const int j = base + k;
-                    const int slot = j % p.R, use = j / p.R;
-                    if (use > 0) mbar_wait(&empty[slot], (uint32_t)((use - 1) & 1));
-                    fence_proxy_async();
-                    uint8_t* dst = ring + (size_t)slot * p.slot_bytes;
-                    const int tile = blockIdx.x + j * gridDim.x;
-                    mbar_expect_tx(&full[slot], (uint32_t)(sz + qbytes));
-                    bulk_g2s(dst, p.arena + off, (uint32_t)sz, &full[slot]);
-                    bulk_g2s(dst + p.slot_bytes - qbytes,
-                             static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &full[slot]);
-                }
-                __syncwarp();
-            }
-        }
-        return;
-    }
-    const int pr = (warp - 1) >> 1, half = (warp - 1) & 1;
+    const int mine = pr < ntiles ? (ntiles - 1 - pr) / p.W + 1 : 0;  // tiles of this pair
+    uint64_t* fb = full + pr * kXMaxBuf;
+    uint8_t* pbuf = bufs + (size_t)pr * nbuf * p.slot_bytes;
     uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
-    int slot = pr % p.R, use = pr / p.R;
-    for (int j = pr; j < ntiles; j += npairs) {
-        mbar_wait(&full[slot], (uint32_t)(use & 1));
+    const bool issuer = half == 0 && lane == 0;
+    // stage the k-th tile of this pair into buffer k % nbuf
+    auto issue = [&](int k) {
+        const int tile = blockIdx.x + (pr + k * p.W) * gridDim.x;
+        uint8_t* dst = pbuf + (size_t)(k % nbuf) * p.slot_bytes;
+        uint64_t* bar = &fb[k % nbuf];
+        const int sz = p.dsize[tile];
+        fence_proxy_async();
+        mbar_expect_tx(bar, (uint32_t)(sz + qbytes));
+        bulk_g2s(dst, p.arena + p.offsets[tile], (uint32_t)sz, bar);
+        uint8_t* qdst = dst + p.slot_bytes - p.g * u2x_qstride<IO>();
+        const uint8_t* qsrc = static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes;
+        for (int hh = 0; hh < p.g; ++hh)
+            bulk_g2s(qdst + hh * u2x_qstride<IO>(), qsrc + hh * qrow, (uint32_t)qrow, bar);
+    };
+    if (issuer) {
+        for (int b = 0; b < nbuf; ++b) mbar_init(&fb[b], 1);
+        fence_barrier_init();
+        for (int k = 0; k < nbuf && k < mine; ++k) issue(k);
+    }
+    // p~ digit rows that are never written (n-tile 1, odd rows) stay zero
+    for (int i = threadIdx.x; i < p.W * p.scratch_bytes / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(scratch0)[i] = make_uint4(0, 0, 0, 0);
+    const U2xLane lc = u2x_lane(half);
+    __syncthreads();
+    for (int k = 0; k < mine; ++k) {
+        mbar_wait(&fb[k % nbuf], (uint32_t)((k / nbuf) & 1));
         __syncwarp();
-        const uint8_t* st = ring + (size_t)slot * p.slot_bytes;
-        const int tile = blockIdx.x + j * gridDim.x;
-        const IO* qs = reinterpret_cast<const IO*>(st + p.slot_bytes - qbytes);
+        const uint8_t* st = pbuf + (size_t)(k % nbuf) * p.slot_bytes;
+        const int tile = blockIdx.x + (pr + k * p.W) * gridDim.x;
+        const uint8_t* qs = st + p.slot_bytes - p.g * u2x_qstride<IO>();
         IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
+        auto refill = [&]() {
+            if (issuer && k >= 1 && k - 1 + nbuf < mine) issue(k - 1 + nbuf);
+        };
         // blocks per warp of THIS tile (warp-uniform via redux): tiles with a few
         // tokens over a 64-token boundary do not pay ghost blocks for the others
         const int bpw = __reduce_max_sync(0xffffffffu, (reinterpret_cast<const TileHeader*>(st)->r[0] + 63) >> 6);
         if (BPW >= 3 && bpw == 3)
-            decode_tile_u2x<IO, (BPW >= 3 ? 3 : BPW)>(st, qs, p.g, scr, o, half, 1 + pr);
+            decode_tile_u2x<IO, (BPW >= 3 ? 3 : BPW), FULLK>(st, qs, p.g, scr, o, 1 + pr, lc, refill);
         else if (BPW >= 2 && bpw == 2)
-            decode_tile_u2x<IO, (BPW >= 2 ? 2 : BPW)>(st, qs, p.g, scr, o, half, 1 + pr);
+            decode_tile_u2x<IO, (BPW >= 2 ? 2 : BPW), FULLK>(st, qs, p.g, scr, o, 1 + pr, lc, refill);
         else
-            decode_tile_u2x<IO, 1>(st, qs, p.g, scr, o, half, 1 + pr);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[slot]);
-        slot += npairs;
-        while (slot >= p.R) {
-            slot -= p.R;
-            ++use;
-        }
+            decode_tile_u2x<IO, 1, FULLK>(st, qs, p.g, scr, o, 1 + pr, lc, refill);
     }
 }
 
-// Pairs per CTA and ring depth. The tiles of a CTA are dealt round-robin to
-// its pairs, so a CTA takes ceil(T / W) tile rounds for its T tiles: W is
-// chosen to waste as few pair-rounds as possible (e.g. 7 pairs for the 27-28
-// tiles per SM of a 4096-tile step rather than 11, which needs 3 rounds for
-// 2.5 tiles of work), then the ring gets every slot that still fits as TMA
-// lookahead.
-static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, int& W, int& R) {
-    const int head = 2 * kMaxR * (int)sizeof(uint64_t);
-    const int slack = 4096;  // ghost-block fragment over-reads past the last ring slot
+// Pairs per CTA and buffers per pair. The tiles of a CTA are dealt
+// round-robin to its pairs, so a CTA takes ceil(T / W) tile rounds for its T
+// tiles: W is chosen to waste as few pair-rounds as possible (e.g. 7 pairs
+// for the 27-28 tiles per SM of a 4096-tile step rather than 8, which needs
+// the same 4 rounds with more warps sharing the SM), then each pair gets as
+// many buffers (>= 2, double buffering) as fit.
+static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, int& W, int& nbuf) {
+    const int head = kXPairs * kXMaxBuf * (int)sizeof(uint64_t);
     const char* env = getenv("RDKV_DECODE_PAIRS");
     const int forced = env ? atoi(env) : 0;
     const int per_sm = (units + nsm - 1) / nsm;
     double best = 1e30;
     W = 0;
-    for (int w = 1; w <= kPairs; ++w) {
+    for (int w = 1; w <= kXPairs; ++w) {
         if (forced && w != forced) continue;
-        if (head + (size_t)(w + 1) * slot + (size_t)w * scratch + slack > (size_t)smem_max) continue;
+        if (head + (size_t)w * (2 * slot + scratch) > (size_t)smem_max) continue;
         const int rounds = (per_sm + w - 1) / w;
-        // time ~ rounds x per-round latency; a round's latency grows with the
-        // warps sharing the SM but not below the ~6-pair latency floor
+        // time ~ rounds x per-round latency, which grows with the warps sharing
+        // the SM but not below the ~6-pair latency floor
         const double cost = rounds * (double)(w > 6 ? w : 6);
-        if (cost < best - 1e-9 || (cost < best + 1e-9 && w > W)) {
+        if (cost < best - 1e-9) {
             best = cost;
             W = w;
         }
     }
     if (W == 0) return false;
-    R = W;
-    while (R < kMaxR && head + (size_t)(R + 1) * slot + (size_t)W * scratch + slack <= (size_t)smem_max) ++R;
+    nbuf = 2;
+    while (nbuf < kXMaxBuf && head + (size_t)W * ((nbuf + 1) * slot + scratch) <= (size_t)smem_max) ++nbuf;
     return true;
 }
 
-template <typename IO, int BPW>
+template <typename IO, int BPW, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
-    const int qbytes = a->group * kD * (int)sizeof(IO);
+    const int qbytes = a->group * u2x_qstride<IO>();
     const int slot = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
     const int scratch = kXPDig + 2 * BPW * 512;
     int dev = 0, smem_max = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int W = 0, R = 0;
-    if (!pick_pairs(a->units, nsm, slot, scratch, smem_max, W, R)) return RDKV_EINVAL;
-    const size_t smem = 2 * kMaxR * sizeof(uint64_t) + (size_t)R * slot + (size_t)W * scratch + 4096;
-    const char* null_env = getenv("RDKV_DECODE_NULL");  // experiment: stream tiles, skip the math
+    // fragment over-reads of partial / ghost blocks stay inside the buffers + scratch
+    const int slack = 4096;
+    int W = 0, nbuf = 0;
+    if (!pick_pairs(a->units, nsm, slot, scratch, smem_max - slack, W, nbuf)) return RDKV_EINVAL;
+    const size_t smem = kXPairs * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
-                a->units, a->group, 0, R, W, slot, scratch, 0, 0, -1, -1,
-                null_env && *null_env == '1' ? 777 : 0};
-    auto kern = decode_u2x_kernel<IO, BPW>;
+                a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0};
+    auto kern = decode_u2x_kernel<IO, BPW, FULLK>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
-    kern<<<blocks, 32 * (2 * W + 1), smem, st>>>(p);
+    kern<<<blocks, 32 * 2 * W, smem, st>>>(p);
     return launch_status();
+}
+
+template <typename IO, bool FULLK>
+static int launch_u2x_k(const rdkv_decode_args* a, cudaStream_t st) {
+    const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
+    if (nb <= 2) return launch_u2x_t<IO, 1, FULLK>(a, st);
+    if (nb <= 4) return launch_u2x_t<IO, 2, FULLK>(a, st);
+    return launch_u2x_t<IO, 3, FULLK>(a, st);
 }
 
 template <typename IO>
 static int launch_u2x(const rdkv_decode_args* a, cudaStream_t st) {
-    const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
-    if (nb <= 2) return launch_u2x_t<IO, 1>(a, st);
-    if (nb <= 4) return launch_u2x_t<IO, 2>(a, st);
-    return launch_u2x_t<IO, 3>(a, st);
+    // plan.uniform2 == 2: every tile also keeps all 128 K channels (identity channel_perm)
+    return a->plan.uniform2 == 2 ? launch_u2x_k<IO, true>(a, st) : launch_u2x_k<IO, false>(a, st);
 }
 
 }  // namespace rdkv_b200
@@ -1747,7 +1787,7 @@ extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int
     for (int u = 0; u < units; ++u)
         cudaMemcpyAsync(&hdrs[u], arena + tile_offsets_host[u], sizeof(TileHeader), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) rc = RDKV_ECUDA;
-    rdkv_decode_plan p{0, 0, 0, 0, 1};
+    rdkv_decode_plan p{0, 0, 0, 0, 2};
     for (int u = 0; u < units && rc == RDKV_OK; ++u) {
         const TileHeader& h = hdrs[u];
         if (h.magic != kTileMagic) {
@@ -1762,6 +1802,7 @@ extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int
         const bool u2 = h.r[1] == 0 && h.r[2] == 0 && h.r[3] == 0 && h.c[1] == 0 && h.c[2] == 0 &&
                         h.c[3] == 0 && h.r[0] > 0 && h.c[0] > 0 && h.nslot <= kU2MaxSlots;
         if (!u2) p.uniform2 = 0;
+        else if (h.c[0] != kD && p.uniform2 == 2) p.uniform2 = 1;
     }
     if (rc == RDKV_OK) {
         if (cudaMemcpyAsync(decode_bytes_dev, ds, sizeof(int32_t) * (size_t)units, cudaMemcpyHostToDevice, st) !=

@@ -81,7 +81,7 @@ def test_mma_all_two_bit_default_budget_shape(cuda, orc):
         kb[:] = 2
         cases.append((k, v, vb, kb, q))
     worst, model = _run_batch(cuda, orc, cases, 4)
-    assert model.plan.max_slots == 128 and model.plan.uniform2 == 1
+    assert model.plan.max_slots == 128 and model.plan.uniform2 == 2  # uniform 2-bit, all K channels kept
     assert worst < FP16_INPUT_TOL, worst
     # the specialised uniform-2-bit body and the general tensor-core body agree
     q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda)
