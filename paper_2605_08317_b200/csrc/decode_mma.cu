@@ -1240,22 +1240,29 @@ static int launch_pair(const rdkv_decode_args* a, cudaStream_t st) {
 }
 
 // ============================================================================
-// Uniform-2-bit warp-pair body, v2 ("u2x"): the same digit arithmetic as
+// Uniform-2-bit warp-pair body, v3 ("u2x"): the digit arithmetic of
 // decode_tile_u2_pair with the instruction count cut for the issue-bound
-// regime (~3.6K -> ~1.5K warp instructions per tile):
-//   * compile-time block loops: BPW 32-token blocks per warp (a ghost block
-//     with zero weights evens out odd block counts), no data-dependent
-//     branches around the mma.sync / ldmatrix / shuffle collectives;
+// regime (~3.6K -> ~1.1K warp instructions per tile):
+//   * block loops bounded by compile-time NBMAX (32-token blocks per tile) with
+//     warp-uniform guards on the tile's own block count: no ghost blocks;
+//     warp `half` owns blocks half, half + 2, ...;
 //   * QK A rows <-> token slots 32b + 4*gid + 2u + r, so every lane ends up
 //     with four CONSECUTIVE slots per block: their V parameters are two
-//     LDS.128 and their p~ digits pack (PRMT) into one 32-bit word per digit
-//     (3 STS.32 instead of 12 STS.U8); K rows are stored slot-transposed
-//     (tile_layout.h krow_pos) so those A-row loads stay conflict-free;
+//     LDS.128 and their p~ digits pack (PRMT) into one 32-bit word per digit;
+//     K rows are stored slot-transposed (tile_layout.h krow_pos) so those
+//     A-row loads stay conflict-free;
+//   * q rows are staged contiguously (one bulk copy) and read in a per-head
+//     staggered channel order that is bank-conflict-free; the stagger is undone
+//     for free by the runtime selector of the digit-transposing PRMT;
+//   * p~ = p * vscale in 16-bit fixed point: two u8 digits, one n-tile, so PV
+//     is 4 MMAs per 32 tokens per warp and one integer combine per output;
 //   * fixed-point ranges from the header's scale bounds (no per-tile scans);
 //   * digit sums combined in integer registers before one I2F pair (QK);
 //   * log2(e) folded into the logit scale: p = ex2(l' - m').
-constexpr int kXQDig = 256;                   // q~ digits: 4 k-steps x 2 n-tiles x 8 rows x 32 B
-constexpr int kXPDig = kXQDig + 4 * 512;      // p~ digits: 2 * BPW blocks x 512 B
+constexpr int kXQDig = 256;                 // q~ digits: 4 k-steps x 512 B (2 n-tiles x 8 rows x 32 B)
+constexpr int kXPDig = kXQDig + 4 * 512;    // p~ digits: one 256-B block (8 rows x 32 B) per 32 tokens
+constexpr int kXNbMax = 5;                  // 32-token blocks per tile on this path (kU2MaxSlots = 160)
+constexpr int kPScale = 65280;              // p~ = p * vscale * kPScale / vmax <= 65280 < 2^16
 
 struct PairX {
     float bias[2][4];
@@ -1300,18 +1307,29 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                 : "=r"(r[0]), "=r"(r[1])
+                 : "r"(smem_u32(p)));
+}
+
 // Per-lane constants of the u2x body, computed once per warp.
 struct U2xLane {
     int lane, gid, tig, half;
     int pshift;      // q~ digit prescale 4^(3 - (gid & 3))
     int bofs;        // ldmatrix row address of this lane inside a 512-B digit block
-    int qdig_w;      // q~ digit store offset (k-step 0) inside the digit area
-    int pdig_w;      // p~ digit store offset (block 0)
+    int bofs2;       // ldmatrix (x2) row address inside a 256-B digit block
+    int qdig_w;      // q~ / p~ digit store offset inside a digit block (rows 2 tig, 2 tig + 1)
+    uint32_t sel_lo, sel_hi;  // stage-2 PRMT selectors of the staggered q~ digit transpose
     uint32_t kmask, vm0, vm1;
     int jj;          // channel sub-index of this lane's PV rows
     int vcol;        // V byte offset of this lane inside a 4-token group block (tig group + swizzled column)
     int ch0;         // first output channel of this lane
 };
+
+__device__ __forceinline__ uint32_t rot_sel(uint32_t s, int t) {  // rotate 4 PRMT nibbles left by t
+    return ((s << (4 * t)) | (s >> (16 - 4 * t))) & 0xFFFFu;
+}
 
 __device__ __forceinline__ U2xLane u2x_lane(int half) {
     U2xLane c;
@@ -1324,8 +1342,10 @@ __device__ __forceinline__ U2xLane u2x_lane(int half) {
     // rows 4..7 (mod 8) swapped so ldmatrix phases hit distinct banks
     const int mat = c.lane >> 3, rr = c.lane & 7;
     c.bofs = ((mat >> 1) * 8 + rr) * 32 + (((mat & 1) ^ ((rr >> 2) & 1)) * 16);
+    c.bofs2 = rr * 32 + ((((c.lane >> 3) & 1) ^ ((rr >> 2) & 1)) * 16);
     c.qdig_w = 2 * c.tig * 32 + (((c.gid >> 2) ^ ((c.tig >> 1) & 1)) * 16) + 4 * (c.gid & 3);
-    c.pdig_w = c.qdig_w;
+    c.sel_lo = rot_sel(0x5410u, c.tig);
+    c.sel_hi = rot_sel(0x7632u, c.tig);
     c.kmask = 0x03030303u << (2 * c.tig);
     c.jj = c.gid >> 2;
     c.vm0 = 0x03030303u << (2 * c.jj);
@@ -1337,15 +1357,12 @@ __device__ __forceinline__ U2xLane u2x_lane(int half) {
 
 // FULLK: every one of the 128 K channels is kept at 2 bits (channel_perm is
 // the identity, 32-B K rows) — the production shape; otherwise c0 < 128.
-// q rows sit in the ring slot at a padded stride (kXQStride) so the lanes of
-// different heads read different banks.
-template <typename IO>
-__host__ __device__ constexpr int u2x_qstride() { return kD * (int)sizeof(IO) + 16; }
-
-template <typename IO, int BPW, bool FULLK, typename AfterSync1>
+// The g query rows sit contiguously (one bulk copy) at the end of the slot.
+template <typename IO, int NBMAX, bool FULLK, typename AfterSync1>
 __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
                                                 uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
                                                 const U2xLane& L, AfterSync1&& after_sync1) {
+    constexpr int NBW = (NBMAX + 1) / 2;  // blocks per warp (upper bound)
     const int gid = L.gid, tig = L.tig, half = L.half;
     const bool hv = tig < g;
     const TileHeader& h = *reinterpret_cast<const TileHeader*>(t);
@@ -1355,6 +1372,8 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     const float2* chan = reinterpret_cast<const float2*>(t + kHeaderBytes);
     const int n = h.r[0];
     const int nslot = h.nslot;
+    const int nb = (n + 31) >> 5;             // 32-token blocks of this tile (warp-uniform)
+    const int mynb = (nb + 1 - half) >> 1;    // blocks of this warp: half, half + 2, ...
     const int c0 = FULLK ? kD : h.c[0];
     const int krb = FULLK ? 32 : h.krow_bytes;
     const int Q = nslot >> 2;
@@ -1362,20 +1381,24 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     const float smax = bf16_bits_to_float(sbits & 0xFFFFu), vmax = bf16_bits_to_float(sbits >> 16);
     constexpr float kInvSqrtD = 0.08838834764831845f;
     constexpr float kLog2e = 1.4426950408889634f;
+    constexpr int QROW = kD * (int)sizeof(IO);
 
     // ---- q range per head: lanes 8h..8h+7 scan head h (16 channels each), then
     // every lane picks its head tig
-    constexpr int QS = u2x_qstride<IO>();
     const int hq = L.lane >> 3;
-    float qm = absmax16<IO>(reinterpret_cast<const IO*>(qs + (hq < g ? hq : 0) * QS) + 16 * (L.lane & 7));
+    float qm = absmax16<IO>(reinterpret_cast<const IO*>(qs + (hq < g ? hq : 0) * QROW) + 16 * (L.lane & 7));
 #pragma unroll
     for (int o = 1; o < 8; o <<= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
     qm = __shfl_sync(0xffffffffu, qm, 8 * tig);
-    const IO* qh = reinterpret_cast<const IO*>(qs + (hv ? tig : 0) * QS);
+    const IO* qh = reinterpret_cast<const IO*>(qs + (hv ? tig : 0) * QROW);
     const float bnd = smax * qm;
     const float sg = (hv && bnd > 0.0f) ? 8.2e6f * rcp_approx(bnd) : 0.0f;  // heads >= g: zero digits
 
-    // ---- q~ digits (k-steps half, half + 2) and the bias sum_c q_c * offset_c
+    // ---- q~ digits (k-steps half, half + 2) and the bias sum_c q_c * offset_c.
+    // Value e of a digit word is channel 4e + (gid & 3) of the lane's 16-channel
+    // group; lanes of head tig visit e in the order (e + tig) & 3 so the four
+    // heads' rows (256 B apart, same banks) are read at distinct banks, and
+    // the final PRMT selectors rotate the bytes back into place.
     float bpart = 0.0f;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -1383,7 +1406,8 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
         uint32_t x[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const int j = kk * 32 + 16 * (gid >> 2) + 4 * e + (gid & 3);
+            const int es = (e + tig) & 3;
+            const int j = kk * 32 + 16 * (gid >> 2) + 4 * es + (gid & 3);
             float qv;
             float2 cs;
             if constexpr (FULLK) {
@@ -1399,10 +1423,11 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             const int N = __float2int_rn(cs.x * qv * sg);
             x[e] = ((uint32_t)N << L.pshift) + 0x80808080u ^ 0x80808080u;
         }
-        const uint32_t w0 = __byte_perm(__byte_perm(x[0], x[1], 0x0040), __byte_perm(x[2], x[3], 0x0040), 0x5410);
-        const uint32_t w1 = __byte_perm(__byte_perm(x[0], x[1], 0x0051), __byte_perm(x[2], x[3], 0x0051), 0x5410);
-        const uint32_t w2 = __byte_perm(__byte_perm(x[0], x[1], 0x0062), __byte_perm(x[2], x[3], 0x0062), 0x5410);
-        const uint32_t w3 = __byte_perm(__byte_perm(x[0], x[1], 0x0073), __byte_perm(x[2], x[3], 0x0073), 0x5410);
+        // 4x4 byte transpose (digit d of value e -> byte e of word d), rotated by tig
+        const uint32_t a01 = __byte_perm(x[0], x[1], 0x5140), b01 = __byte_perm(x[0], x[1], 0x7362);
+        const uint32_t a23 = __byte_perm(x[2], x[3], 0x5140), b23 = __byte_perm(x[2], x[3], 0x7362);
+        const uint32_t w0 = __byte_perm(a01, a23, L.sel_lo), w1 = __byte_perm(a01, a23, L.sel_hi);
+        const uint32_t w2 = __byte_perm(b01, b23, L.sel_lo), w3 = __byte_perm(b01, b23, L.sel_hi);
         uint8_t* a0 = qdig + kk * 512 + L.qdig_w;
         *reinterpret_cast<uint32_t*>(a0) = w3;
         *reinterpret_cast<uint32_t*>(a0 + 32) = w2;
@@ -1426,41 +1451,43 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     // positions (2u + r) Q + 8pb + gid (slot-transposed K rows)
     const uint8_t* kbase = t + h.off_k + (size_t)(8 * half + gid) * krb;
     const int qstride = Q * krb;
-    float lg[BPW][4];
+    float lg[NBW][4];
     float mx = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < BPW; ++i) {
-        const int pb = half + 2 * i;
-        int acc[2][2][4];
+    for (int i = 0; i < NBW; ++i) {
+        if (i < mynb) {
+            const int pb = half + 2 * i;
+            int acc[2][2][4];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const uint8_t* r0 = kbase + 2 * u * qstride + 16 * i * krb;
-            const uint8_t* r1 = r0 + qstride;
-            const uint4 x0 = lds128(r0), x1 = lds128(r0 + 16), y0 = lds128(r1), y1 = lds128(r1 + 16);
-            const uint32_t w0[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-            const uint32_t w1[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+            for (int u = 0; u < 2; ++u) {
+                const uint8_t* r0 = kbase + 2 * u * qstride + 16 * i * krb;
+                const uint8_t* r1 = r0 + qstride;
+                const uint4 x0 = lds128(r0), x1 = lds128(r0 + 16), y0 = lds128(r1), y1 = lds128(r1 + 16);
+                const uint32_t w0[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+                const uint32_t w1[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
+                for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const uint32_t a[4] = {w0[2 * kk] & L.kmask, w1[2 * kk] & L.kmask, w0[2 * kk + 1] & L.kmask,
-                                       w1[2 * kk + 1] & L.kmask};
-                mma_u8s8(acc[u][0], a, bq[kk][0], bq[kk][1]);
-                mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint32_t a[4] = {w0[2 * kk] & L.kmask, w1[2 * kk] & L.kmask, w0[2 * kk + 1] & L.kmask,
+                                           w1[2 * kk + 1] & L.kmask};
+                    mma_u8s8(acc[u][0], a, bq[kk][0], bq[kk][1]);
+                    mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
+                }
             }
+            const int sbase = 32 * pb + 4 * gid;
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const int hi = acc[u][0][2 * r] * 256 + acc[u][0][2 * r + 1];
+                    const int lo = acc[u][1][2 * r] * 256 + acc[u][1][2 * r + 1];
+                    const float v = fmaf((float)hi, 65536.0f, (float)lo);
+                    const float l = (sbase + 2 * u + r < n) ? fmaf(v, qscale2, bias2) : -INFINITY;
+                    lg[i][2 * u + r] = l;
+                    mx = fmaxf(mx, l);
+                }
         }
-        const int sbase = 32 * pb + 4 * gid;
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const int hi = acc[u][0][2 * r] * 256 + acc[u][0][2 * r + 1];
-                const int lo = acc[u][1][2 * r] * 256 + acc[u][1][2 * r + 1];
-                const float v = fmaf((float)hi, 65536.0f, (float)lo);
-                const float l = (sbase + 2 * u + r < n) ? fmaf(v, qscale2, bias2) : -INFINITY;
-                lg[i][2 * u + r] = l;
-                mx = fmaxf(mx, l);
-            }
     }
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -1468,35 +1495,34 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     pair_sync(bar);
     mx = fmaxf(xg.mx[0][tig], xg.mx[1][tig]);
     if (mx == -INFINITY) mx = 0.0f;  // head without tokens (tig >= g)
-    const float psig = vmax > 0.0f ? 1.6e7f * rcp_approx(vmax) : 0.0f;
-    const float vinv = vmax * (1.0f / 1.6e7f);
+    const float psig = vmax > 0.0f ? (float)kPScale * rcp_approx(vmax) : 0.0f;
+    const float vinv = vmax * (1.0f / (float)kPScale);
 
-    // ---- softmax + p~ digits: four consecutive slots per lane and block
+    // ---- softmax + p~ digits (hi, lo bytes): four consecutive slots per lane and block
     float lsum = 0.0f, bv = 0.0f;
     const float2* vparam = reinterpret_cast<const float2*>(t + h.off_vp);
 #pragma unroll
-    for (int i = 0; i < BPW; ++i) {
-        const int pb = half + 2 * i;
-        // slots past the tile (partial / ghost blocks) read the last real group's
-        // finite parameters; their weights are exactly zero
-        const float4* vp4 = reinterpret_cast<const float4*>(vparam + min(32 * pb + 4 * gid, nslot - 4));
-        const float4 va = vp4[0], vb = vp4[1];
-        const float vs[4] = {va.x, va.z, vb.x, vb.z}, vo[4] = {va.y, va.w, vb.y, vb.w};
-        uint32_t N[4];
+    for (int i = 0; i < NBW; ++i) {
+        if (i < mynb) {
+            const int pb = half + 2 * i;
+            // slots past the tile read the last real group's finite parameters;
+            // their weights are exactly zero
+            const float4* vp4 = reinterpret_cast<const float4*>(vparam + min(32 * pb + 4 * gid, nslot - 4));
+            const float4 va = vp4[0], vb = vp4[1];
+            const float vs[4] = {va.x, va.z, vb.x, vb.z}, vo[4] = {va.y, va.w, vb.y, vb.w};
+            uint32_t N[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float p = ex2_approx(lg[i][j] - mx);
-            lsum += p;
-            bv = fmaf(p, vo[j], bv);
-            N[j] = (uint32_t)__float2int_rn(p * (vs[j] * psig));
+            for (int j = 0; j < 4; ++j) {
+                const float p = ex2_approx(lg[i][j] - mx);
+                lsum += p;
+                bv = fmaf(p, vo[j], bv);
+                N[j] = (uint32_t)__float2int_rn(p * (vs[j] * psig));
+            }
+            const uint32_t t01 = __byte_perm(N[0], N[1], 0x5140), t23 = __byte_perm(N[2], N[3], 0x5140);
+            uint8_t* pw = pdig + pb * 256 + L.qdig_w;
+            *reinterpret_cast<uint32_t*>(pw) = __byte_perm(t01, t23, 0x7632);       // hi bytes -> row 2 tig
+            *reinterpret_cast<uint32_t*>(pw + 32) = __byte_perm(t01, t23, 0x5410);  // lo bytes -> row 2 tig + 1
         }
-        const uint32_t d0 = __byte_perm(__byte_perm(N[0], N[1], 0x0040), __byte_perm(N[2], N[3], 0x0040), 0x5410);
-        const uint32_t d1 = __byte_perm(__byte_perm(N[0], N[1], 0x0051), __byte_perm(N[2], N[3], 0x0051), 0x5410);
-        const uint32_t d2 = __byte_perm(__byte_perm(N[0], N[1], 0x0062), __byte_perm(N[2], N[3], 0x0062), 0x5410);
-        uint8_t* pw = pdig + pb * 512 + L.pdig_w;
-        *reinterpret_cast<uint32_t*>(pw) = d2;
-        *reinterpret_cast<uint32_t*>(pw + 32) = d1;
-        *reinterpret_cast<uint32_t*>(pw + 256) = d0;
     }
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
@@ -1511,24 +1537,23 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     const float lt = xg.lsum[0][tig] + xg.lsum[1][tig];
     const float bt = xg.bv[0][tig] + xg.bv[1][tig];
 
-    // ---- PV: this warp's 4 m-tiles (byte columns 16 half + 4 (gid & 3) + m)
-    int acc[4][2][4];
+    // ---- PV: this warp's 4 m-tiles (byte columns 16 half + 4 (gid & 3) + m), one n-tile
+    int acc[4][4];
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) acc[m][nt][0] = acc[m][nt][1] = acc[m][nt][2] = acc[m][nt][3] = 0;
+    for (int m = 0; m < 4; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0;
     const uint8_t* g0b = t + h.off_vseg[0] + L.vcol;
 #pragma unroll
-    for (int kk = 0; kk < 2 * BPW; ++kk) {
-        uint32_t b[4];
-        ldsm_x4(b, pdig + kk * 512 + L.bofs);
-        const uint4 x0 = lds128(g0b + kk * 1024), x1 = lds128(g0b + kk * 1024 + 512);
-        const uint32_t u0[4] = {x0.x, x0.y, x0.z, x0.w}, u1[4] = {x1.x, x1.y, x1.z, x1.w};
+    for (int kk = 0; kk < NBMAX; ++kk) {
+        if (kk < nb) {
+            uint32_t b[2];
+            ldsm_x2(b, pdig + kk * 256 + L.bofs2);
+            const uint4 x0 = lds128(g0b + kk * 1024), x1 = lds128(g0b + kk * 1024 + 512);
+            const uint32_t u0[4] = {x0.x, x0.y, x0.z, x0.w}, u1[4] = {x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const uint32_t a[4] = {u0[m] & L.vm0, u0[m] & L.vm1, u1[m] & L.vm0, u1[m] & L.vm1};
-            mma_u8u8(acc[m][0], a, b[0], b[1]);
-            mma_u8u8(acc[m][1], a, b[2], b[3]);
+            for (int m = 0; m < 4; ++m) {
+                const uint32_t a[4] = {u0[m] & L.vm0, u0[m] & L.vm1, u1[m] & L.vm0, u1[m] & L.vm1};
+                mma_u8u8(acc[m], a, b[0], b[1]);
+            }
         }
     }
     if (hv) {
@@ -1537,8 +1562,8 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
         IO* orow = out + tig * kD + L.ch0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const float v0 = fmaf(fmaf((float)acc[m][0][0], 256.0f, (float)acc[m][0][1]), 256.0f, (float)acc[m][1][0]);
-            const float v1 = fmaf(fmaf((float)acc[m][0][2], 256.0f, (float)acc[m][0][3]), 256.0f, (float)acc[m][1][2]);
+            const float v0 = (float)(acc[m][0] * 256 + acc[m][1]);
+            const float v1 = (float)(acc[m][2] * 256 + acc[m][3]);
             const float r0 = fmaf(v0, s0, bt) * inv, r1 = fmaf(v1, s1, bt) * inv;
             if constexpr (sizeof(IO) == 2) {
                 orow[4 * m] = __float2half_rn(r0);
@@ -1551,15 +1576,19 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     }
 }
 
-constexpr int kXPairs = 8;   // <= 16 warps per CTA: up to 128 registers per thread, no spills
+constexpr int kXPairs = 7;   // <= 14 warps per CTA: up to 144 registers per thread, no spills
 constexpr int kXMaxBuf = 4;  // tile buffers per pair
 
 // Self-fed warp pairs: pair p owns NBUF tile buffers and decodes the CTA's
-// tiles p, p + W, p + 2W, ...; its first lane issues the TMA bulk copies of its
-// own next tiles (a buffer is refilled as soon as both warps are past the
-// previous tile's first barrier), so a slow pair never blocks the others'
-// loads (no shared producer, no head-of-line blocking).
-template <typename IO, int BPW, bool FULLK>
+// tiles p, p + W, p + 2W, ...; one lane of the pair issues the TMA bulk
+// copies of its own next tiles (tile + q rows: two copies), so a slow pair
+// never blocks the others' loads (no shared producer, no head-of-line
+// blocking). At start only the first tile of every pair is requested; the
+// rest of the pair's buffers are filled once it has landed, so the first
+// round's tiles are not queued behind everyone's look-ahead.
+// MODE (timing experiments only, RDKV_DECODE_NULL): 0 decode, 1 loads only
+// (no math), 2 math only (tiles past the first buffers are not reloaded).
+template <typename IO, int NBMAX, bool FULLK, int MODE = 0>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
     const int nbuf = p.R;  // buffers per pair
@@ -1568,57 +1597,58 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     uint8_t* scratch0 = bufs + (size_t)p.W * nbuf * p.slot_bytes;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int pr = warp >> 1, half = warp & 1;
-    const int qrow = kD * (int)sizeof(IO);
-    const int qbytes = p.g * qrow;
+    constexpr int QROW = kD * (int)sizeof(IO);
+    const int qbytes = p.g * QROW;
     const int ntiles = p.units > (int)blockIdx.x ? (p.units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int mine = pr < ntiles ? (ntiles - 1 - pr) / p.W + 1 : 0;  // tiles of this pair
     uint64_t* fb = full + pr * kXMaxBuf;
     uint8_t* pbuf = bufs + (size_t)pr * nbuf * p.slot_bytes;
     uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
-    const bool issuer = half == 0 && lane == 0;
-    // stage the k-th tile of this pair into buffer k % nbuf
-    auto issue = [&](int k) {
-        const int tile = blockIdx.x + (pr + k * p.W) * gridDim.x;
-        uint8_t* dst = pbuf + (size_t)(k % nbuf) * p.slot_bytes;
-        uint64_t* bar = &fb[k % nbuf];
-        const int sz = p.dsize[tile];
+    const int tile0 = blockIdx.x + pr * gridDim.x, tstride = p.W * gridDim.x;
+    const int qoff = p.slot_bytes - qbytes;
+    // stage the k-th tile of this pair into buffer b (one lane)
+    auto issue = [&](int k, int b) {
+        const int tile = tile0 + k * tstride;
+        uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
+        uint64_t* bar = &fb[b];
+        const uint32_t sz = (uint32_t)p.dsize[tile];
         fence_proxy_async();
-        mbar_expect_tx(bar, (uint32_t)(sz + qbytes));
-        bulk_g2s(dst, p.arena + p.offsets[tile], (uint32_t)sz, bar);
-        uint8_t* qdst = dst + p.slot_bytes - p.g * u2x_qstride<IO>();
-        const uint8_t* qsrc = static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes;
-        for (int hh = 0; hh < p.g; ++hh)
-            bulk_g2s(qdst + hh * u2x_qstride<IO>(), qsrc + hh * qrow, (uint32_t)qrow, bar);
+        mbar_expect_tx(bar, sz + (uint32_t)qbytes);
+        bulk_g2s(dst, p.arena + p.offsets[tile], sz, bar);
+        bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, bar);
     };
-    if (issuer) {
+    if (half == 0 && lane == 0) {
         for (int b = 0; b < nbuf; ++b) mbar_init(&fb[b], 1);
         fence_barrier_init();
-        for (int k = 0; k < nbuf && k < mine; ++k) issue(k);
+        if (mine > 0) issue(0, 0);
     }
-    // p~ digit rows that are never written (n-tile 1, odd rows) stay zero
-    for (int i = threadIdx.x; i < p.W * p.scratch_bytes / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(scratch0)[i] = make_uint4(0, 0, 0, 0);
     const U2xLane lc = u2x_lane(half);
     __syncthreads();
+    int b = 0;
+    uint32_t phase = 0;
     for (int k = 0; k < mine; ++k) {
-        mbar_wait(&fb[k % nbuf], (uint32_t)((k / nbuf) & 1));
+        if (MODE != 2 || k < nbuf) mbar_wait(&fb[b], phase);
         __syncwarp();
-        const uint8_t* st = pbuf + (size_t)(k % nbuf) * p.slot_bytes;
-        const int tile = blockIdx.x + (pr + k * p.W) * gridDim.x;
-        const uint8_t* qs = st + p.slot_bytes - p.g * u2x_qstride<IO>();
+        const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
+        const int tile = tile0 + k * tstride;
+        if (k == 0 && half == 1 && lane == 0)  // look-ahead once the first tile is in
+            for (int j = 1; j < nbuf && j < mine; ++j) issue(j, j);
         IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
+        const int bprev = b == 0 ? nbuf - 1 : b - 1;
+        // the buffer of tile k - 1 takes tile k - 1 + nbuf; the two warps take turns issuing
         auto refill = [&]() {
-            if (issuer && k >= 1 && k - 1 + nbuf < mine) issue(k - 1 + nbuf);
+            if (MODE != 2 && half == (k & 1) && lane == 0 && k >= 1 && k - 1 + nbuf < mine) issue(k - 1 + nbuf, bprev);
         };
-        // blocks per warp of THIS tile (warp-uniform via redux): tiles with a few
-        // tokens over a 64-token boundary do not pay ghost blocks for the others
-        const int bpw = __reduce_max_sync(0xffffffffu, (reinterpret_cast<const TileHeader*>(st)->r[0] + 63) >> 6);
-        if (BPW >= 3 && bpw == 3)
-            decode_tile_u2x<IO, (BPW >= 3 ? 3 : BPW), FULLK>(st, qs, p.g, scr, o, 1 + pr, lc, refill);
-        else if (BPW >= 2 && bpw == 2)
-            decode_tile_u2x<IO, (BPW >= 2 ? 2 : BPW), FULLK>(st, qs, p.g, scr, o, 1 + pr, lc, refill);
-        else
-            decode_tile_u2x<IO, 1, FULLK>(st, qs, p.g, scr, o, 1 + pr, lc, refill);
+        if (MODE == 1) {
+            pair_sync(1 + pr);
+            refill();
+        } else {
+            decode_tile_u2x<IO, NBMAX, FULLK>(st, st + qoff, p.g, scr, o, 1 + pr, lc, refill);
+        }
+        if (++b == nbuf) {
+            b = 0;
+            phase ^= 1u;
+        }
     }
 }
 
@@ -1653,23 +1683,26 @@ static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, 
     return true;
 }
 
-template <typename IO, int BPW, bool FULLK>
+template <typename IO, int NBMAX, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
-    const int qbytes = a->group * u2x_qstride<IO>();
+    const int qbytes = a->group * kD * (int)sizeof(IO);
     const int slot = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
-    const int scratch = kXPDig + 2 * BPW * 512;
+    const int scratch = (kXPDig + ((NBMAX + 1) & ~1) * 256 + 127) & ~127;
     int dev = 0, smem_max = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    // fragment over-reads of partial / ghost blocks stay inside the buffers + scratch
+    // fragment over-reads of partial blocks stay inside the buffers + scratch
     const int slack = 4096;
     int W = 0, nbuf = 0;
     if (!pick_pairs(a->units, nsm, slot, scratch, smem_max - slack, W, nbuf)) return RDKV_EINVAL;
     const size_t smem = kXPairs * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
                 a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0};
-    auto kern = decode_u2x_kernel<IO, BPW, FULLK>;
+    const char* nenv = getenv("RDKV_DECODE_NULL");
+    const int mode = nenv ? atoi(nenv) : 0;
+    auto kern = mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
+              : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2> : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
@@ -1680,9 +1713,9 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
 template <typename IO, bool FULLK>
 static int launch_u2x_k(const rdkv_decode_args* a, cudaStream_t st) {
     const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
-    if (nb <= 2) return launch_u2x_t<IO, 1, FULLK>(a, st);
-    if (nb <= 4) return launch_u2x_t<IO, 2, FULLK>(a, st);
-    return launch_u2x_t<IO, 3, FULLK>(a, st);
+    if (nb <= 2) return launch_u2x_t<IO, 2, FULLK>(a, st);
+    if (nb <= 4) return launch_u2x_t<IO, 4, FULLK>(a, st);
+    return launch_u2x_t<IO, kXNbMax, FULLK>(a, st);
 }
 
 template <typename IO>

@@ -159,3 +159,23 @@ def test_mma_large_batch_persistent(cuda, orc):
     err = (a - b).norm(dim=-1) / b.norm(dim=-1)
     assert float(err.max()) < 2 * FP16_INPUT_TOL
     del T
+
+
+@pytest.mark.parametrize("g,fullk,io", [(4, True, torch.float32), (4, True, torch.float16), (4, False, torch.float32),
+                                        (1, True, torch.float32), (2, False, torch.float16), (3, True, torch.float32)])
+def test_mma_uniform_two_bit_ragged(cuda, orc, g, fullk, io):
+    """Uniform 2-bit tiles of every block count (1..160 kept tokens, ragged last
+    block), with all K channels kept (identity channel_perm) or some dropped."""
+    rng = np.random.default_rng(40 + g + 10 * fullk)
+    cases = []
+    for n in (1, 3, 31, 32, 33, 64, 65, 100, 127, 128, 129, 131, 150, 157, 160):
+        k, v, vb, kb, q = _random_case(rng, 400, g)
+        vb[:] = 0
+        vb[np.sort(rng.choice(400, n, replace=False))] = 2
+        kb[:] = 2
+        if not fullk:
+            kb[rng.choice(D, 9, replace=False)] = 0
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, g, io=io)
+    assert model.plan.uniform2 == (2 if fullk else 1)
+    assert worst < (FP16_INPUT_TOL if io == torch.float32 else 1e-3), worst
