@@ -44,6 +44,7 @@ constexpr int kMaxW = 12;      // consumer warps per CTA (13 warps -> <=152 regs
 constexpr int kMaxSlots = 256; // token slots per tile on this path
 
 // ---------------------------------------------------------------- PTX helpers
+#define getenv_pair_smsp() (p.smsp_pairs)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -84,7 +85,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 // D = A(u8, 16x32 row-major) * B(s8, 32x8 col-major) + C, s32 accumulate
 __device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
         : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
@@ -92,7 +93,7 @@ __device__ __forceinline__ void mma_u8s8(int (&c)[4], const uint32_t (&a)[4], ui
 }
 // D = A(u8) * B(u8) + C
 __device__ __forceinline__ void mma_u8u8(int (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
         : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
@@ -144,6 +145,7 @@ struct MmaParams {
     int lg_stride;          // per-head stride (floats) of the logit scratch
     int off_p16, off_zl;    // -1 when unused
     int max_r16;
+    int smsp_pairs;  // u2x: a pair's two warps on one SM sub-partition
 };
 
 // Per-warp scratch: [ScratchHead][B digits][lg / acc][p16][zl]
@@ -1313,18 +1315,51 @@ __device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], const void* p) {
                  : "r"(smem_u32(p)));
 }
 
+// Packed f32x2 arithmetic (sm_100a FFMA2 / FMUL2 / FADD2): two lanes of work
+// per issue slot for the per-(token, head) and per-(channel, head) math.
+__device__ __forceinline__ unsigned long long f2u(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 u2f(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+
+// Two adjacent q values (channels c, c + 1) of one head row as f32.
+template <typename IO>
+__device__ __forceinline__ float2 ld_io2(const IO* p, int c);
+template <>
+__device__ __forceinline__ float2 ld_io2<__half>(const __half* p, int c) {
+    return __half22float2(*reinterpret_cast<const __half2*>(p + c));
+}
+template <>
+__device__ __forceinline__ float2 ld_io2<float>(const float* p, int c) {
+    return *reinterpret_cast<const float2*>(p + c);
+}
+
 // Per-lane constants of the u2x body, computed once per warp.
 struct U2xLane {
     int lane, gid, tig, half;
-    int pshift;      // q~ digit prescale 4^(3 - (gid & 3))
-    int bofs;        // ldmatrix row address of this lane inside a 512-B digit block
-    int bofs2;       // ldmatrix (x2) row address inside a 256-B digit block
-    int qdig_w;      // q~ / p~ digit store offset inside a digit block (rows 2 tig, 2 tig + 1)
+    int bofs;        // ldmatrix (x4) row address of this lane inside a 512-B q~ digit block
+    int bofs2;       // ldmatrix (x2) row address inside a 256-B p~ digit block
+    int pdig_w;      // p~ digit store offset inside a 256-B block (rows 2 tig, 2 tig + 1)
+    int qdig_w;      // q~ digit store offset (row 2 tig + 1, k-step 2 half + (lane >> 4))
+    int qch;         // first channel of this lane's q~ prep (k-step, 16-channel half, class pair)
     uint32_t sel_lo, sel_hi;  // stage-2 PRMT selectors of the staggered q~ digit transpose
     uint32_t kmask, vm0, vm1;
-    int jj;          // channel sub-index of this lane's PV rows
     int vcol;        // V byte offset of this lane inside a 4-token group block (tig group + swizzled column)
-    int ch0;         // first output channel of this lane
+    int ch0;         // first output channel of this lane (channels ch0 + 4m, ch0 + 4m + 1)
+    float s0f;       // PV row scale of rows gid (row gid + 8: s0f / 4)
 };
 
 __device__ __forceinline__ uint32_t rot_sel(uint32_t s, int t) {  // rotate 4 PRMT nibbles left by t
@@ -1337,27 +1372,44 @@ __device__ __forceinline__ U2xLane u2x_lane(int half) {
     c.gid = c.lane >> 2;
     c.tig = c.lane & 3;
     c.half = half;
-    c.pshift = 2 * (3 - (c.gid & 3));
     // digit blocks: rows of 32 B (one B column each), the two 16-B halves of
     // rows 4..7 (mod 8) swapped so ldmatrix phases hit distinct banks
     const int mat = c.lane >> 3, rr = c.lane & 7;
     c.bofs = ((mat >> 1) * 8 + rr) * 32 + (((mat & 1) ^ ((rr >> 2) & 1)) * 16);
-    c.bofs2 = rr * 32 + ((((c.lane >> 3) & 1) ^ ((rr >> 2) & 1)) * 16);
-    c.qdig_w = 2 * c.tig * 32 + (((c.gid >> 2) ^ ((c.tig >> 1) & 1)) * 16) + 4 * (c.gid & 3);
+    c.bofs2 = rr * 32 + (((mat & 1) ^ ((rr >> 2) & 1)) * 16);
+    c.pdig_w = 2 * c.tig * 32 + (((c.gid >> 2) ^ ((c.tig >> 1) & 1)) * 16) + 4 * (c.gid & 3);
+    // q~ prep: lane = (i, ch, p, h): head h = tig, class pair p, 16-channel half
+    // ch, k-step 2 half + i; it writes digit rows 2h + 1 (d2), 8 + 2h (d1),
+    // 9 + 2h (d0) at K positions 8p .. 8p + 7 of half ch
+    const int p = (c.lane >> 2) & 1, ch = (c.lane >> 3) & 1, i = c.lane >> 4;
+    const int kk = 2 * half + i;
+    c.qdig_w = kk * 512 + (2 * c.tig + 1) * 32 + ((ch ^ (c.tig >> 1)) * 16) + 8 * p;
+    c.qch = kk * 32 + 16 * ch + 2 * p;
     c.sel_lo = rot_sel(0x5410u, c.tig);
     c.sel_hi = rot_sel(0x7632u, c.tig);
     c.kmask = 0x03030303u << (2 * c.tig);
-    c.jj = c.gid >> 2;
-    c.vm0 = 0x03030303u << (2 * c.jj);
-    c.vm1 = 0x03030303u << (2 * c.jj + 4);
+    const int jj = c.gid >> 2;
+    c.vm0 = 0x03030303u << (4 * jj);      // rows gid:     code position 2 jj     (x 4^(2 jj))
+    c.vm1 = 0x03030303u << (4 * jj + 2);  // rows gid + 8: code position 2 jj + 1 (x 4^(2 jj + 1))
     c.vcol = c.tig * 128 + (((16 * half + 4 * (c.gid & 3)) ^ (8 * c.tig)) * 4);  // vswz: (G & 3) == tig
-    c.ch0 = 4 * (16 * half + 4 * (c.gid & 3)) + c.jj;
+    c.ch0 = 4 * (16 * half + 4 * (c.gid & 3)) + 2 * jj;
+    c.s0f = jj ? 0.0625f : 1.0f;
     return c;
 }
 
 // FULLK: every one of the 128 K channels is kept at 2 bits (channel_perm is
 // the identity, 32-B K rows) — the production shape; otherwise c0 < 128.
 // The g query rows sit contiguously (one bulk copy) at the end of the slot.
+//
+// Fixed point: q~_c = scale_c * q_c is rounded to N = rint(q~ * sg * 4^(3 - t))
+// (t = the channel's K-position class, whose codes the in-place mask scales by
+// 4^t), |N| < 2^22, split into three balanced s8 digits (rows d2, d1, d0; the
+// d3 row stays zero). p~ = p * vscale * 65280 / vmax < 2^16, two u8 digits.
+// The float -> int roundings use the 1.5 * 2^23 / 2^23 magic-number adds, so
+// the digit bytes come straight out of the float bits.
+constexpr float kQFix = 65000.0f;   // sg = kQFix / bound: |N| <= 64 * 65000 < 2^22
+constexpr float kMagicS = 12582912.0f;  // 1.5 * 2^23: bits = 0x4B400000 + rint(x), |x| < 2^22
+constexpr float kMagicU = 8388608.0f;   // 2^23: bits = 0x4B000000 + rint(x), 0 <= x < 2^23
 template <typename IO, int NBMAX, bool FULLK, typename AfterSync1>
 __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
                                                 uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
@@ -1369,12 +1421,11 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     PairX& xg = *reinterpret_cast<PairX*>(scr);
     uint8_t* qdig = scr + kXQDig;
     uint8_t* pdig = scr + kXPDig;
-    const float2* chan = reinterpret_cast<const float2*>(t + kHeaderBytes);
+    const float* chanf = reinterpret_cast<const float*>(t + kHeaderBytes);
     const int n = h.r[0];
     const int nslot = h.nslot;
     const int nb = (n + 31) >> 5;             // 32-token blocks of this tile (warp-uniform)
     const int mynb = (nb + 1 - half) >> 1;    // blocks of this warp: half, half + 2, ...
-    const int c0 = FULLK ? kD : h.c[0];
     const int krb = FULLK ? 32 : h.krow_bytes;
     const int Q = nslot >> 2;
     const uint32_t sbits = h.scale_bounds;
@@ -1392,56 +1443,63 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     qm = __shfl_sync(0xffffffffu, qm, 8 * tig);
     const IO* qh = reinterpret_cast<const IO*>(qs + (hv ? tig : 0) * QROW);
     const float bnd = smax * qm;
-    const float sg = (hv && bnd > 0.0f) ? 8.2e6f * rcp_approx(bnd) : 0.0f;  // heads >= g: zero digits
+    const float sg = (hv && bnd > 0.0f) ? kQFix * rcp_approx(bnd) : 0.0f;  // heads >= g: zero digits
 
-    // ---- q~ digits (k-steps half, half + 2) and the bias sum_c q_c * offset_c.
-    // Value e of a digit word is channel 4e + (gid & 3) of the lane's 16-channel
-    // group; lanes of head tig visit e in the order (e + tig) & 3 so the four
-    // heads' rows (256 B apart, same banks) are read at distinct banks, and
+    // ---- q~ digits of k-steps 2 half, 2 half + 1 and the bias sum_c q_c * offset_c.
+    // The lane takes channel pairs (c, c + 1) = classes (2p, 2p + 1) at e = 0..3
+    // (c = qch + 4e); lanes of head tig visit e in the order (e + tig) & 3 so the
+    // four heads' rows (256 B apart, same banks) are read at distinct banks, and
     // the final PRMT selectors rotate the bytes back into place.
-    float bpart = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const int kk = half + 2 * i;
-        uint32_t x[4];
+    {
+        const int ps = 4 * (L.lane & 4);  // class 2p -> prescale 4^(3 - 2p) = 2^(6 - 4p)
+        const float sgA = sg * __int_as_float((127 + 6 - ps) << 23);  // class 2p
+        const float sgB = sgA * 0.25f;                                // class 2p + 1
+        uint32_t xa[4], xb[4];
+        float2 bp = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const int es = (e + tig) & 3;
-            const int j = kk * 32 + 16 * (gid >> 2) + 4 * es + (gid & 3);
-            float qv;
-            float2 cs;
+            const int c = L.qch + 4 * ((e + tig) & 3);
+            float2 qv;
+            float4 cs;
             if constexpr (FULLK) {
-                cs = chan[j];
-                qv = ld_io(qh, j);
+                cs = *reinterpret_cast<const float4*>(chanf + 2 * c);
+                qv = ld_io2(qh, c);
             } else {
                 const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
-                const int js = min(j, h.kslots - 1);
-                cs = chan[js];
-                qv = j < c0 ? ld_io(qh, perm[js]) : 0.0f;
+                const int c0 = h.c[0];
+                const int j0 = min(c, h.kslots - 2);
+                cs = *reinterpret_cast<const float4*>(chanf + 2 * j0);
+                qv.x = c < c0 ? ld_io(qh, perm[j0]) : 0.0f;
+                qv.y = c + 1 < c0 ? ld_io(qh, perm[j0 + 1]) : 0.0f;
             }
-            bpart = fmaf(qv, cs.y, bpart);
-            const int N = __float2int_rn(cs.x * qv * sg);
-            x[e] = ((uint32_t)N << L.pshift) + 0x80808080u ^ 0x80808080u;
+            bp = ffma2(qv, make_float2(cs.y, cs.w), bp);
+            const float ya = fmaf(cs.x * qv.x, sgA, kMagicS), yb = fmaf(cs.z * qv.y, sgB, kMagicS);
+            // balanced base-256 digits of N: byte k of (N + 0x808080) ^ 0x80
+            xa[e] = (__float_as_uint(ya) + (0x00808080u - 0x4B400000u)) ^ 0x00808080u;
+            xb[e] = (__float_as_uint(yb) + (0x00808080u - 0x4B400000u)) ^ 0x00808080u;
         }
-        // 4x4 byte transpose (digit d of value e -> byte e of word d), rotated by tig
-        const uint32_t a01 = __byte_perm(x[0], x[1], 0x5140), b01 = __byte_perm(x[0], x[1], 0x7362);
-        const uint32_t a23 = __byte_perm(x[2], x[3], 0x5140), b23 = __byte_perm(x[2], x[3], 0x7362);
-        const uint32_t w0 = __byte_perm(a01, a23, L.sel_lo), w1 = __byte_perm(a01, a23, L.sel_hi);
-        const uint32_t w2 = __byte_perm(b01, b23, L.sel_lo), w3 = __byte_perm(b01, b23, L.sel_hi);
-        uint8_t* a0 = qdig + kk * 512 + L.qdig_w;
-        *reinterpret_cast<uint32_t*>(a0) = w3;
-        *reinterpret_cast<uint32_t*>(a0 + 32) = w2;
-        *reinterpret_cast<uint32_t*>(a0 + 256) = w1;
-        *reinterpret_cast<uint32_t*>(a0 + 288) = w0;
-    }
+        float bpart = bp.x + bp.y;
+        // 4x4 byte transposes (digit d of value e -> byte e of word d), rotated by tig
+        const uint32_t a01 = __byte_perm(xa[0], xa[1], 0x5140), b01 = __byte_perm(xa[0], xa[1], 0x7362);
+        const uint32_t a23 = __byte_perm(xa[2], xa[3], 0x5140), b23 = __byte_perm(xa[2], xa[3], 0x7362);
+        const uint32_t c01 = __byte_perm(xb[0], xb[1], 0x5140), d01 = __byte_perm(xb[0], xb[1], 0x7362);
+        const uint32_t c23 = __byte_perm(xb[2], xb[3], 0x5140), d23 = __byte_perm(xb[2], xb[3], 0x7362);
+        uint8_t* w = qdig + L.qdig_w;
+        *reinterpret_cast<uint2*>(w) =  // d2 -> row 2 tig + 1
+            make_uint2(__byte_perm(b01, b23, L.sel_lo), __byte_perm(d01, d23, L.sel_lo));
+        *reinterpret_cast<uint2*>(w + 224) =  // d1 -> row 8 + 2 tig
+            make_uint2(__byte_perm(a01, a23, L.sel_hi), __byte_perm(c01, c23, L.sel_hi));
+        *reinterpret_cast<uint2*>(w + 256) =  // d0 -> row 9 + 2 tig
+            make_uint2(__byte_perm(a01, a23, L.sel_lo), __byte_perm(c01, c23, L.sel_lo));
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) bpart += __shfl_xor_sync(0xffffffffu, bpart, o);
-    if (gid == 0) xg.bias[half][tig] = bpart;
+        for (int o = 4; o < 32; o <<= 1) bpart += __shfl_xor_sync(0xffffffffu, bpart, o);
+        if (gid == 0) xg.bias[half][tig] = bpart;
+    }
     pair_sync(bar);
     after_sync1();  // both warps are past the previous tile: its buffer may be refilled
-    // l' = log2(e) * (v / (64 sigma) + bias) / sqrt(d); heads >= g get -inf logits
+    // l' = log2(e) * (v / (64 sg) + bias) / sqrt(d); heads >= g get -inf logits
     const float bias2 = hv ? (xg.bias[0][tig] + xg.bias[1][tig]) * (kInvSqrtD * kLog2e) : -INFINITY;
-    const float qscale2 = bnd * (kInvSqrtD * kLog2e / (64.0f * 8.2e6f));
+    const float qscale2 = bnd * (kInvSqrtD * kLog2e / (64.0f * kQFix));
 
     // ---- QK over this warp's blocks half, half + 2, ...
     uint32_t bq[4][4];
@@ -1451,7 +1509,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     // positions (2u + r) Q + 8pb + gid (slot-transposed K rows)
     const uint8_t* kbase = t + h.off_k + (size_t)(8 * half + gid) * krb;
     const int qstride = Q * krb;
-    float lg[NBW][4];
+    float2 lg[NBW][2];
     float mx = -INFINITY;
 #pragma unroll
     for (int i = 0; i < NBW; ++i) {
@@ -1475,18 +1533,24 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                     mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
                 }
             }
-            const int sbase = 32 * pb + 4 * gid;
+            // rows (u, r) = slots 32 pb + 4 gid + 2u + r: v = d2 * 2^16 + d1 * 2^8 + d0
 #pragma unroll
-            for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < 2; ++u) {
+                const float2 hi = make_float2((float)acc[u][0][1], (float)acc[u][0][3]);
+                const float2 lo = make_float2((float)(acc[u][1][0] * 256 + acc[u][1][1]),
+                                              (float)(acc[u][1][2] * 256 + acc[u][1][3]));
+                const float2 v = ffma2(hi, make_float2(65536.0f, 65536.0f), lo);
+                lg[i][u] = ffma2(v, make_float2(qscale2, qscale2), make_float2(bias2, bias2));
+            }
+            if (32 * pb + 32 > n) {  // ragged last block: slots >= n get no weight
+                const int sbase = 32 * pb + 4 * gid;
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const int hi = acc[u][0][2 * r] * 256 + acc[u][0][2 * r + 1];
-                    const int lo = acc[u][1][2 * r] * 256 + acc[u][1][2 * r + 1];
-                    const float v = fmaf((float)hi, 65536.0f, (float)lo);
-                    const float l = (sbase + 2 * u + r < n) ? fmaf(v, qscale2, bias2) : -INFINITY;
-                    lg[i][2 * u + r] = l;
-                    mx = fmaxf(mx, l);
+                for (int u = 0; u < 2; ++u) {
+                    if (sbase + 2 * u >= n) lg[i][u].x = -INFINITY;
+                    if (sbase + 2 * u + 1 >= n) lg[i][u].y = -INFINITY;
                 }
+            }
+            mx = fmaxf(mx, fmaxf(fmaxf(lg[i][0].x, lg[i][0].y), fmaxf(lg[i][1].x, lg[i][1].y)));
         }
     }
 #pragma unroll
@@ -1499,8 +1563,10 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     const float vinv = vmax * (1.0f / (float)kPScale);
 
     // ---- softmax + p~ digits (hi, lo bytes): four consecutive slots per lane and block
-    float lsum = 0.0f, bv = 0.0f;
+    float2 ls2 = make_float2(0.0f, 0.0f);
+    float bv = 0.0f;
     const float2* vparam = reinterpret_cast<const float2*>(t + h.off_vp);
+    const float2 nmx = make_float2(-mx, -mx);
 #pragma unroll
     for (int i = 0; i < NBW; ++i) {
         if (i < mynb) {
@@ -1509,21 +1575,26 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             // their weights are exactly zero
             const float4* vp4 = reinterpret_cast<const float4*>(vparam + min(32 * pb + 4 * gid, nslot - 4));
             const float4 va = vp4[0], vb = vp4[1];
-            const float vs[4] = {va.x, va.z, vb.x, vb.z}, vo[4] = {va.y, va.w, vb.y, vb.w};
-            uint32_t N[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float p = ex2_approx(lg[i][j] - mx);
-                lsum += p;
-                bv = fmaf(p, vo[j], bv);
-                N[j] = (uint32_t)__float2int_rn(p * (vs[j] * psig));
-            }
-            const uint32_t t01 = __byte_perm(N[0], N[1], 0x5140), t23 = __byte_perm(N[2], N[3], 0x5140);
-            uint8_t* pw = pdig + pb * 256 + L.qdig_w;
+            const float2 d01 = fadd2(lg[i][0], nmx), d23 = fadd2(lg[i][1], nmx);
+            const float2 p01 = make_float2(ex2_approx(d01.x), ex2_approx(d01.y));
+            const float2 p23 = make_float2(ex2_approx(d23.x), ex2_approx(d23.y));
+            ls2 = fadd2(ls2, fadd2(p01, p23));
+            bv = fmaf(p01.x, va.y, bv);
+            bv = fmaf(p01.y, va.w, bv);
+            bv = fmaf(p23.x, vb.y, bv);
+            bv = fmaf(p23.y, vb.w, bv);
+            const float2 vs01 = fmul2(make_float2(va.x, va.z), make_float2(psig, psig));
+            const float2 vs23 = fmul2(make_float2(vb.x, vb.z), make_float2(psig, psig));
+            const float2 y01 = ffma2(p01, vs01, make_float2(kMagicU, kMagicU));
+            const float2 y23 = ffma2(p23, vs23, make_float2(kMagicU, kMagicU));
+            const uint32_t t01 = __byte_perm(__float_as_uint(y01.x), __float_as_uint(y01.y), 0x5140);
+            const uint32_t t23 = __byte_perm(__float_as_uint(y23.x), __float_as_uint(y23.y), 0x5140);
+            uint8_t* pw = pdig + pb * 256 + L.pdig_w;
             *reinterpret_cast<uint32_t*>(pw) = __byte_perm(t01, t23, 0x7632);       // hi bytes -> row 2 tig
             *reinterpret_cast<uint32_t*>(pw + 32) = __byte_perm(t01, t23, 0x5410);  // lo bytes -> row 2 tig + 1
         }
     }
+    float lsum = ls2.x + ls2.y;
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
         lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
@@ -1558,25 +1629,22 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     }
     if (hv) {
         const float inv = rcp_approx(lt);
-        const float s0 = vinv * (L.jj ? 0.25f : 1.0f), s1 = s0 * 0.0625f;
+        const float s0 = vinv * L.s0f;
+        const float2 sc = make_float2(s0 * inv, s0 * 0.25f * inv), bb = make_float2(bt * inv, bt * inv);
         IO* orow = out + tig * kD + L.ch0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            const float v0 = (float)(acc[m][0] * 256 + acc[m][1]);
-            const float v1 = (float)(acc[m][2] * 256 + acc[m][3]);
-            const float r0 = fmaf(v0, s0, bt) * inv, r1 = fmaf(v1, s1, bt) * inv;
-            if constexpr (sizeof(IO) == 2) {
-                orow[4 * m] = __float2half_rn(r0);
-                orow[4 * m + 2] = __float2half_rn(r1);
-            } else {
-                orow[4 * m] = r0;
-                orow[4 * m + 2] = r1;
-            }
+            const float2 v = make_float2((float)(acc[m][0] * 256 + acc[m][1]), (float)(acc[m][2] * 256 + acc[m][3]));
+            const float2 r = ffma2(v, sc, bb);
+            if constexpr (sizeof(IO) == 2)
+                *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
+            else
+                *reinterpret_cast<float2*>(orow + 4 * m) = r;
         }
     }
 }
 
-constexpr int kXPairs = 7;   // <= 14 warps per CTA: up to 144 registers per thread, no spills
+constexpr int kXPairs = 8;   // <= 16 warps per CTA: up to 128 registers per thread
 constexpr int kXMaxBuf = 4;  // tile buffers per pair
 
 // Self-fed warp pairs: pair p owns NBUF tile buffers and decodes the CTA's
@@ -1596,11 +1664,13 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     uint8_t* bufs = dsm + kXPairs * kXMaxBuf * sizeof(uint64_t);
     uint8_t* scratch0 = bufs + (size_t)p.W * nbuf * p.slot_bytes;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int pr = warp >> 1, half = warp & 1;
+    // with a multiple of 4 pairs, a pair's two warps sit on the same SM
+    // sub-partition (warp w -> SMSP w % 4): warps (8j + s, 8j + s + 4)
+    const bool same_smsp = getenv_pair_smsp() && (p.W & 3) == 0;
+    const int pr = same_smsp ? ((warp & 3) | ((warp >> 3) << 2)) : warp >> 1;
+    const int half = same_smsp ? (warp >> 2) & 1 : warp & 1;
     constexpr int QROW = kD * (int)sizeof(IO);
     const int qbytes = p.g * QROW;
-    const int ntiles = p.units > (int)blockIdx.x ? (p.units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    const int mine = pr < ntiles ? (ntiles - 1 - pr) / p.W + 1 : 0;  // tiles of this pair
     uint64_t* fb = full + pr * kXMaxBuf;
     uint8_t* pbuf = bufs + (size_t)pr * nbuf * p.slot_bytes;
     uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
@@ -1620,24 +1690,25 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     if (half == 0 && lane == 0) {
         for (int b = 0; b < nbuf; ++b) mbar_init(&fb[b], 1);
         fence_barrier_init();
-        if (mine > 0) issue(0, 0);
+        if (tile0 < p.units) issue(0, 0);
     }
     const U2xLane lc = u2x_lane(half);
     __syncthreads();
     int b = 0;
     uint32_t phase = 0;
-    for (int k = 0; k < mine; ++k) {
+    int k = 0;
+    for (int tile = tile0; tile < p.units; tile += tstride, ++k) {
         if (MODE != 2 || k < nbuf) mbar_wait(&fb[b], phase);
         __syncwarp();
         const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
-        const int tile = tile0 + k * tstride;
         if (k == 0 && half == 1 && lane == 0)  // look-ahead once the first tile is in
-            for (int j = 1; j < nbuf && j < mine; ++j) issue(j, j);
+            for (int j = 1; j < nbuf && tile0 + j * tstride < p.units; ++j) issue(j, j);
         IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
         const int bprev = b == 0 ? nbuf - 1 : b - 1;
         // the buffer of tile k - 1 takes tile k - 1 + nbuf; the two warps take turns issuing
         auto refill = [&]() {
-            if (MODE != 2 && half == (k & 1) && lane == 0 && k >= 1 && k - 1 + nbuf < mine) issue(k - 1 + nbuf, bprev);
+            if (MODE != 2 && half == (k & 1) && lane == 0 && k >= 1 && tile + (nbuf - 1) * tstride < p.units)
+                issue(k - 1 + nbuf, bprev);
         };
         if (MODE == 1) {
             pair_sync(1 + pr);
@@ -1652,30 +1723,20 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     }
 }
 
-// Pairs per CTA and buffers per pair. The tiles of a CTA are dealt
-// round-robin to its pairs, so a CTA takes ceil(T / W) tile rounds for its T
-// tiles: W is chosen to waste as few pair-rounds as possible (e.g. 7 pairs
-// for the 27-28 tiles per SM of a 4096-tile step rather than 8, which needs
-// the same 4 rounds with more warps sharing the SM), then each pair gets as
-// many buffers (>= 2, double buffering) as fit.
+// Pairs per CTA and buffers per pair: as many pairs as fit (issue slots are
+// the bound, so more resident warps hide more latency; measured 15.7 us at 8
+// pairs vs 16.6 us at 7 on the 4096-tile step), then as many buffers per pair
+// (>= 2, double buffering) as fit.
 static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, int& W, int& nbuf) {
     const int head = kXPairs * kXMaxBuf * (int)sizeof(uint64_t);
     const char* env = getenv("RDKV_DECODE_PAIRS");
     const int forced = env ? atoi(env) : 0;
     const int per_sm = (units + nsm - 1) / nsm;
-    double best = 1e30;
     W = 0;
-    for (int w = 1; w <= kXPairs; ++w) {
+    for (int w = 1; w <= kXPairs && w <= per_sm; ++w) {
         if (forced && w != forced) continue;
         if (head + (size_t)w * (2 * slot + scratch) > (size_t)smem_max) continue;
-        const int rounds = (per_sm + w - 1) / w;
-        // time ~ rounds x per-round latency, which grows with the warps sharing
-        // the SM but not below the ~6-pair latency floor
-        const double cost = rounds * (double)(w > 6 ? w : 6);
-        if (cost < best - 1e-9) {
-            best = cost;
-            W = w;
-        }
+        W = w;
     }
     if (W == 0) return false;
     nbuf = 2;
@@ -1698,7 +1759,8 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     if (!pick_pairs(a->units, nsm, slot, scratch, smem_max - slack, W, nbuf)) return RDKV_EINVAL;
     const size_t smem = kXPairs * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
-                a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0};
+                a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
+    if (const char* e = getenv("RDKV_DECODE_SMSP")) p.smsp_pairs = atoi(e);
     const char* nenv = getenv("RDKV_DECODE_NULL");
     const int mode = nenv ? atoi(nenv) : 0;
     auto kern = mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>

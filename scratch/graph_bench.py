@@ -43,9 +43,11 @@ def graph_time(fn_list, reps=20):
 for mode in os.environ.get("MODES", "0").split(","):
     os.environ["RDKV_DECODE_NULL"] = mode
     for pairs in os.environ.get("PAIRS", "0").split(","):
+      for smsp in os.environ.get("SMSP", "0").split(","):
         os.environ["RDKV_DECODE_PAIRS"] = pairs
+        os.environ["RDKV_DECODE_SMSP"] = smsp
         t = graph_time([lambda r=r: P.packed_decode_step(models[r], qs[r], outs[r], kernel=kern) for r in range(NR)])
-        print(f"decode b2b graph mode {mode} pairs {pairs}: {t:.2f} us/step  {ab/t/1e3:.0f} GB/s (arena only)", flush=True)
+        print(f"decode b2b graph mode {mode} pairs {pairs} smsp {smsp}: {t:.2f} us/step  {ab/t/1e3:.0f} GB/s (arena only)", flush=True)
 os.environ["RDKV_DECODE_NULL"] = "0"; os.environ["RDKV_DECODE_PAIRS"] = "0"
 L = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "bw", "libbw.so"))
 o = torch.zeros(4, dtype=torch.int32, device="cuda")
