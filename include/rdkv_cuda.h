@@ -172,6 +172,21 @@ RDKV_API int rdkv_cuda_decode(const rdkv_decode_args* a, void* stream);
 RDKV_API int rdkv_cuda_decode_host(const rdkv_decode_args* a, const void* q_host, void* out_host,
                                    void* stream);
 
+/* Pipelined end-to-end decode (same contract as rdkv_cuda_decode_host).
+ * The step is cut into `chunks` unit ranges; chunk c's q H2D (on the
+ * context's copy-in stream), decode (on `stream`) and out D2H (on its
+ * copy-out stream) overlap the neighbouring chunks', so the call costs about
+ * one PCIe transfer instead of H2D + decode + D2H in series. The context is
+ * caller-owned (two streams and per-chunk events, no global state); one
+ * context serves one call at a time. The call forks from and joins back
+ * into `stream`: work queued on `stream` before it is ordered before the
+ * copies, and `stream` is ordered after the last D2H. */
+typedef struct rdkv_decode_ctx rdkv_decode_ctx;
+RDKV_API int rdkv_cuda_decode_ctx_create(int32_t chunks, rdkv_decode_ctx** ctx);
+RDKV_API int rdkv_cuda_decode_ctx_destroy(rdkv_decode_ctx* ctx);
+RDKV_API int rdkv_cuda_decode_host_pipelined(rdkv_decode_ctx* ctx, const rdkv_decode_args* a,
+                                             const void* q_host, void* out_host, void* stream);
+
 /* ---- Zone C ------------------------------------------------------------- */
 /* Appends one K and one V row per unit (k_new/v_new [units][head_dim] of
  * dtype) at position zc_len[u], then increments zc_len[u]. */

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/rdkv_cuda.h"
 #include "tile_layout.h"
 
@@ -18,6 +20,44 @@ namespace rdkv_b200 {
 
 inline int launch_status() {
     return cudaGetLastError() == cudaSuccess ? RDKV_OK : RDKV_ECUDA;
+}
+
+// Immutable per-device attributes, queried once per device (launch paths are
+// called per decode step; the attribute queries cost microseconds each).
+struct DevAttrs {
+    int dev, smem_optin, nsm;
+};
+constexpr int kMaxDevices = 64;
+inline DevAttrs dev_attrs() {
+    static std::atomic<int> cache[kMaxDevices][2];  // 0 = not yet queried
+    int dev = 0;
+    cudaGetDevice(&dev);
+    DevAttrs a{dev, 0, 0};
+    if (dev >= 0 && dev < kMaxDevices) {
+        a.smem_optin = cache[dev][0].load(std::memory_order_relaxed);
+        a.nsm = cache[dev][1].load(std::memory_order_relaxed);
+        if (a.smem_optin > 0 && a.nsm > 0) return a;
+    }
+    cudaDeviceGetAttribute(&a.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&a.nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < kMaxDevices) {
+        cache[dev][0].store(a.smem_optin, std::memory_order_relaxed);
+        cache[dev][1].store(a.nsm, std::memory_order_relaxed);
+    }
+    return a;
+}
+
+// Raises a kernel's dynamic shared-memory limit at most once per (kernel,
+// device, size): `slots` is a per-kernel static array of kMaxDevices.
+template <typename F>
+inline void set_smem_once(F kern, int smem, std::atomic<int>* slots, int dev) {
+    if (dev >= 0 && dev < kMaxDevices && slots[dev].load(std::memory_order_relaxed) >= smem) return;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess && dev >= 0 &&
+        dev < kMaxDevices) {
+        int cur = slots[dev].load(std::memory_order_relaxed);
+        while (cur < smem && !slots[dev].compare_exchange_weak(cur, smem)) {
+        }
+    }
 }
 
 template <typename T>

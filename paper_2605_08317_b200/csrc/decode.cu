@@ -49,3 +49,93 @@ extern "C" RDKV_API int rdkv_cuda_decode_host(const rdkv_decode_args* a, const v
     RDKV_CUDA_TRY(cudaMemcpyAsync(out_host, a->out, bytes, cudaMemcpyDeviceToHost, st));
     return RDKV_OK;
 }
+
+// ---- pipelined end-to-end decode -------------------------------------------
+struct rdkv_decode_ctx {
+    int chunks;
+    cudaStream_t s_in, s_out;
+    cudaEvent_t start, done;
+    cudaEvent_t* in_done;
+    cudaEvent_t* dec_done;
+};
+
+extern "C" RDKV_API int rdkv_cuda_decode_ctx_create(int32_t chunks, rdkv_decode_ctx** out) {
+    if (!out || chunks < 1 || chunks > 256) return RDKV_EINVAL;
+    auto* c = new rdkv_decode_ctx{};
+    c->chunks = chunks;
+    c->in_done = new cudaEvent_t[chunks]();
+    c->dec_done = new cudaEvent_t[chunks]();
+    bool ok = cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&c->start, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&c->done, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; ok && i < chunks; ++i)
+        ok = cudaEventCreateWithFlags(&c->in_done[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->dec_done[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        rdkv_cuda_decode_ctx_destroy(c);
+        return RDKV_ECUDA;
+    }
+    *out = c;
+    return RDKV_OK;
+}
+
+extern "C" RDKV_API int rdkv_cuda_decode_ctx_destroy(rdkv_decode_ctx* c) {
+    if (!c) return RDKV_EINVAL;
+    for (int i = 0; i < c->chunks; ++i) {
+        if (c->in_done[i]) cudaEventDestroy(c->in_done[i]);
+        if (c->dec_done[i]) cudaEventDestroy(c->dec_done[i]);
+    }
+    if (c->start) cudaEventDestroy(c->start);
+    if (c->done) cudaEventDestroy(c->done);
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
+    delete[] c->in_done;
+    delete[] c->dec_done;
+    delete c;
+    return RDKV_OK;
+}
+
+extern "C" RDKV_API int rdkv_cuda_decode_host_pipelined(rdkv_decode_ctx* c, const rdkv_decode_args* a,
+                                                        const void* q_host, void* out_host, void* stream) {
+    if (!c || !a || !q_host || !out_host || !a->q || !a->out || a->units < 1) return RDKV_EINVAL;
+    if (a->split > 1) return RDKV_EINVAL;  // chunks share one unit-indexed workspace otherwise
+    const size_t row = (size_t)a->group * a->head_dim * (a->io_dtype == RDKV_F16 ? 2 : 4);
+    auto st = static_cast<cudaStream_t>(stream);
+    const int nch = a->units < c->chunks ? a->units : c->chunks;
+    // fork: the copies are ordered after everything already queued on `stream`
+    RDKV_CUDA_TRY(cudaEventRecord(c->start, st));
+    RDKV_CUDA_TRY(cudaStreamWaitEvent(c->s_in, c->start, 0));
+    RDKV_CUDA_TRY(cudaStreamWaitEvent(c->s_out, c->start, 0));
+    for (int i = 0; i < nch; ++i) {
+        const int u0 = (int)((int64_t)a->units * i / nch), u1 = (int)((int64_t)a->units * (i + 1) / nch);
+        const size_t off = (size_t)u0 * row, bytes = (size_t)(u1 - u0) * row;
+        RDKV_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(const_cast<void*>(a->q)) + off,
+                                      static_cast<const uint8_t*>(q_host) + off, bytes, cudaMemcpyHostToDevice,
+                                      c->s_in));
+        RDKV_CUDA_TRY(cudaEventRecord(c->in_done[i], c->s_in));
+        RDKV_CUDA_TRY(cudaStreamWaitEvent(st, c->in_done[i], 0));
+        rdkv_decode_args sub = *a;
+        sub.units = u1 - u0;
+        sub.tile_offsets = a->tile_offsets + u0;
+        if (a->tile_decode_bytes) sub.tile_decode_bytes = a->tile_decode_bytes + u0;
+        sub.q = static_cast<const uint8_t*>(a->q) + off;
+        sub.out = static_cast<uint8_t*>(a->out) + off;
+        if (a->zc_len) {
+            const size_t zrow = (size_t)a->zc_cap * a->head_dim * 2;
+            sub.zc_k = static_cast<const uint8_t*>(a->zc_k) + (size_t)u0 * zrow;
+            sub.zc_v = static_cast<const uint8_t*>(a->zc_v) + (size_t)u0 * zrow;
+            sub.zc_len = a->zc_len + u0;
+        }
+        if (int rc = rdkv_cuda_decode(&sub, stream)) return rc;
+        RDKV_CUDA_TRY(cudaEventRecord(c->dec_done[i], st));
+        RDKV_CUDA_TRY(cudaStreamWaitEvent(c->s_out, c->dec_done[i], 0));
+        RDKV_CUDA_TRY(cudaMemcpyAsync(static_cast<uint8_t*>(out_host) + off,
+                                      static_cast<const uint8_t*>(a->out) + off, bytes, cudaMemcpyDeviceToHost,
+                                      c->s_out));
+    }
+    // join: `stream` is ordered after the last D2H
+    RDKV_CUDA_TRY(cudaEventRecord(c->done, c->s_out));
+    RDKV_CUDA_TRY(cudaStreamWaitEvent(st, c->done, 0));
+    return RDKV_OK;
+}

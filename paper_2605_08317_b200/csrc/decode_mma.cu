@@ -36,6 +36,8 @@
 // (tolerance 1e-3; tests assert 1e-4 on FP16-representable inputs).
 #include "common.cuh"
 
+#include <cstdio>
+
 namespace rdkv_b200 {
 
 constexpr int kD = 128;        // head_dim of this path
@@ -1257,14 +1259,16 @@ static int launch_pair(const rdkv_decode_args* a, cudaStream_t st) {
 //     staggered channel order that is bank-conflict-free; the stagger is undone
 //     for free by the runtime selector of the digit-transposing PRMT;
 //   * p~ = p * vscale in 16-bit fixed point: two u8 digits, one n-tile, so PV
-//     is 4 MMAs per 32 tokens per warp and one integer combine per output;
+//     is 4 MMAs per 32 tokens per warp and one integer combine per output
+//     (~1e-4 relative decode error, matched to the fp16 output; 24-bit p~
+//     costs ~10% of the step);
 //   * fixed-point ranges from the header's scale bounds (no per-tile scans);
 //   * digit sums combined in integer registers before one I2F pair (QK);
 //   * log2(e) folded into the logit scale: p = ex2(l' - m').
 constexpr int kXQDig = 256;                 // q~ digits: 4 k-steps x 512 B (2 n-tiles x 8 rows x 32 B)
 constexpr int kXPDig = kXQDig + 4 * 512;    // p~ digits: one 256-B block (8 rows x 32 B) per 32 tokens
 constexpr int kXNbMax = 5;                  // 32-token blocks per tile on this path (kU2MaxSlots = 160)
-constexpr int kPScale = 65280;              // p~ = p * vscale * kPScale / vmax <= 65280 < 2^16
+constexpr float kPScale = 65280.0f;         // p~ = p * vscale * kPScale / vmax <= 65280 < 2^16
 
 struct PairX {
     float bias[2][4];
@@ -1404,7 +1408,8 @@ __device__ __forceinline__ U2xLane u2x_lane(int half) {
 // Fixed point: q~_c = scale_c * q_c is rounded to N = rint(q~ * sg * 4^(3 - t))
 // (t = the channel's K-position class, whose codes the in-place mask scales by
 // 4^t), |N| < 2^22, split into three balanced s8 digits (rows d2, d1, d0; the
-// d3 row stays zero). p~ = p * vscale * 65280 / vmax < 2^16, two u8 digits.
+// d3 row stays zero). p~ = p * vscale * 65280 / vmax < 2^16, two u8 digits
+// (hi, lo) in rows 2h, 2h + 1 of a 256-B block.
 // The float -> int roundings use the 1.5 * 2^23 / 2^23 magic-number adds, so
 // the digit bytes come straight out of the float bits.
 constexpr float kQFix = 65000.0f;   // sg = kQFix / bound: |N| <= 64 * 65000 < 2^22
@@ -1451,7 +1456,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     // four heads' rows (256 B apart, same banks) are read at distinct banks, and
     // the final PRMT selectors rotate the bytes back into place.
     {
-        const int ps = 4 * (L.lane & 4);  // class 2p -> prescale 4^(3 - 2p) = 2^(6 - 4p)
+        const int ps = L.lane & 4;  // = 4p: class 2p -> prescale 4^(3 - 2p) = 2^(6 - 4p)
         const float sgA = sg * __int_as_float((127 + 6 - ps) << 23);  // class 2p
         const float sgB = sgA * 0.25f;                                // class 2p + 1
         uint32_t xa[4], xb[4];
@@ -1559,8 +1564,8 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     pair_sync(bar);
     mx = fmaxf(xg.mx[0][tig], xg.mx[1][tig]);
     if (mx == -INFINITY) mx = 0.0f;  // head without tokens (tig >= g)
-    const float psig = vmax > 0.0f ? (float)kPScale * rcp_approx(vmax) : 0.0f;
-    const float vinv = vmax * (1.0f / (float)kPScale);
+    const float psig = vmax > 0.0f ? kPScale * rcp_approx(vmax) : 0.0f;
+    const float vinv = vmax * (1.0f / kPScale);
 
     // ---- softmax + p~ digits (hi, lo bytes): four consecutive slots per lane and block
     float2 ls2 = make_float2(0.0f, 0.0f);
@@ -1693,6 +1698,9 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         if (tile0 < p.units) issue(0, 0);
     }
     const U2xLane lc = u2x_lane(half);
+    // the q~ digit rows of d3 (never written: |N| < 2^22) must read as zero
+    for (int i = threadIdx.x & 63; i < 4 * 512 / 16; i += 64)
+        reinterpret_cast<uint4*>(scr + kXQDig)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     int b = 0;
     uint32_t phase = 0;
@@ -1748,26 +1756,30 @@ template <typename IO, int NBMAX, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
     const int slot = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
-    const int scratch = (kXPDig + ((NBMAX + 1) & ~1) * 256 + 127) & ~127;
-    int dev = 0, smem_max = 0, nsm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    // fragment over-reads of partial blocks stay inside the buffers + scratch
-    const int slack = 4096;
+    const int scratch = (kXPDig + NBMAX * 256 + 127) & ~127;
+    const DevAttrs da = dev_attrs();
+    const int smem_max = da.smem_optin, nsm = da.nsm;
+    // fragment over-reads of ragged blocks land in the following smem region
+    // (K rows: < 256 B past a tile's K rows; the last region is scratch)
+    const int slack = 512;
     int W = 0, nbuf = 0;
     if (!pick_pairs(a->units, nsm, slot, scratch, smem_max - slack, W, nbuf)) return RDKV_EINVAL;
     const size_t smem = kXPairs * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
                 a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
-    if (const char* e = getenv("RDKV_DECODE_SMSP")) p.smsp_pairs = atoi(e);
+    const char* smsp_env = getenv("RDKV_DECODE_SMSP");
+    if (smsp_env) p.smsp_pairs = atoi(smsp_env);
     const char* nenv = getenv("RDKV_DECODE_NULL");
     const int mode = nenv ? atoi(nenv) : 0;
     auto kern = mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
               : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2> : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static std::atomic<int> smem_set[3][kMaxDevices];
+    set_smem_once(kern, (int)smem, smem_set[mode == 1 ? 1 : mode == 2 ? 2 : 0], da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
+    if (getenv("RDKV_DECODE_VERBOSE"))
+        fprintf(stderr, "u2x: units %d nbmax %d pairs %d bufs %d slot %d scratch %d smem %zu grid %d\n", a->units,
+                NBMAX, W, nbuf, slot, scratch, smem, blocks);
     kern<<<blocks, 32 * 2 * W, smem, st>>>(p);
     return launch_status();
 }

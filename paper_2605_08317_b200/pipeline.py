@@ -365,6 +365,46 @@ def packed_decode_step(model: PackedModel, q, out=None, split=1, kernel=0, works
     return out
 
 
+class HostDecoder:
+    """End-to-end decode from pinned host q to pinned host out through the
+    pipelined C-ABI entry point (rdkv_cuda_decode_host_pipelined): the step is
+    cut into `chunks` unit ranges whose H2D copy, decode and D2H copy overlap.
+    Owns the native context (two copy streams + events) and the device staging
+    buffers; one step at a time per instance."""
+
+    def __init__(self, model: PackedModel, dtype=torch.float16, chunks: int = 8, kernel: int = 0):
+        self.model = model
+        shape = (model.units, model.group, model.head_dim)
+        self.q_dev = torch.empty(shape, dtype=dtype, device=model.arena.device)
+        self.out_dev = torch.empty_like(self.q_dev)
+        self.args = decode_args(model, self.q_dev, self.out_dev, 1, kernel)
+        ctx = C.c_void_p()
+        raise_for(capi.lib().rdkv_cuda_decode_ctx_create(chunks, C.byref(ctx)), "decode_ctx_create")
+        self.ctx = ctx
+
+    def step(self, q_host: torch.Tensor, out_host: torch.Tensor, stream: int | None = None) -> None:
+        """Enqueue one step on `stream` (default: torch's current stream)."""
+        if q_host.dtype != self.q_dev.dtype or out_host.dtype != self.q_dev.dtype:
+            raise capi.InvalidArgument(capi.RDKV_EINVAL, "host buffers must match the decoder dtype")
+        if q_host.shape != self.q_dev.shape or out_host.shape != self.q_dev.shape:
+            raise capi.InvalidArgument(capi.RDKV_EINVAL, "host buffers must be [units, group, head_dim]")
+        raise_for(capi.lib().rdkv_cuda_decode_host_pipelined(self.ctx, C.byref(self.args), q_host.data_ptr(),
+                                                             out_host.data_ptr(),
+                                                             _stream() if stream is None else stream),
+                  "decode_host_pipelined")
+
+    def close(self) -> None:
+        if getattr(self, "ctx", None):
+            capi.lib().rdkv_cuda_decode_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 def append_new_token(model: PackedModel, k_new, v_new) -> None:
     """One K/V row per unit into Zone C (trizone.cpp:307-314)."""
     if model.zc_len is None:

@@ -15,6 +15,9 @@ pytestmark = pytest.mark.gpu
 
 D = 128
 FP16_INPUT_TOL = 1e-4
+# uniform-2-bit fast path (csrc/decode_mma.cu u2x): 16-bit softmax weights,
+# ~1e-4 relative on random data (contract: 1e-3)
+U2X_TOL = 5e-4
 
 
 def f16r(x):
@@ -39,7 +42,7 @@ def _random_case(rng, T, g, p_bits=(0.2, 0.2, 0.2, 0.2, 0.2), kp=(0.2, 0.2, 0.2,
     return k, v, vb, kb, q
 
 
-def _run_batch(cuda, orc, cases, g, io=torch.float32, appends=0, rng=None):
+def _run_batch(cuda, orc, cases, g, io=torch.float32, appends=0, rng=None, tol=FP16_INPUT_TOL):
     """Pack all cases (same T) as units of one model; decode with both kernels."""
     T = cases[0][0].shape[0]
     K = torch.from_numpy(np.stack([c[0] for c in cases])).to(cuda)
@@ -47,7 +50,7 @@ def _run_batch(cuda, orc, cases, g, io=torch.float32, appends=0, rng=None):
     vb = torch.from_numpy(np.stack([c[2] for c in cases]).astype(np.uint8)).to(cuda)
     kb = torch.from_numpy(np.stack([c[3] for c in cases]).astype(np.uint8)).to(cuda)
     stats = torch.zeros(len(cases) * capi.HEAD_STATS_BYTES, dtype=torch.uint8, device=cuda)
-    model = P.build_packed_model(K, V, P.Allocation(vb, kb, stats), group=g, zc_cap=max(appends, 1))
+    model = P.build_packed_model(K, V, P.Allocation(vb, kb, stats), group=g, zc_cap=appends)
     model.check()
     zk = zv = None
     if appends:
@@ -66,7 +69,7 @@ def _run_batch(cuda, orc, cases, g, io=torch.float32, appends=0, rng=None):
         for j in range(g):
             want = tz.decode(qq[j])
             worst = max(worst, rel(out_mma[u, j], want))
-            assert rel(out_mma[u, j], out_gen[u, j]) < 2 * FP16_INPUT_TOL
+            assert rel(out_mma[u, j], out_gen[u, j]) < (2 * tol if io == torch.float32 else 1e-3)
     return worst, model
 
 
@@ -80,15 +83,15 @@ def test_mma_all_two_bit_default_budget_shape(cuda, orc):
         vb[np.sort(rng.choice(512, 128, replace=False))] = 2
         kb[:] = 2
         cases.append((k, v, vb, kb, q))
-    worst, model = _run_batch(cuda, orc, cases, 4)
+    worst, model = _run_batch(cuda, orc, cases, 4, tol=U2X_TOL)
     assert model.plan.max_slots == 128 and model.plan.uniform2 == 2  # uniform 2-bit, all K channels kept
-    assert worst < FP16_INPUT_TOL, worst
+    assert worst < U2X_TOL, worst
     # the specialised uniform-2-bit body and the general tensor-core body agree
     q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda)
     a = P.packed_decode_step(model, q, kernel=2)
     for k in (3, 4):  # general body, one-warp uniform body (kernel 2 = warp-pair body)
         b = P.packed_decode_step(model, q, kernel=k)
-        assert float(((a - b).norm(dim=-1) / b.norm(dim=-1)).max()) < 2 * FP16_INPUT_TOL, k
+        assert float(((a - b).norm(dim=-1) / b.norm(dim=-1)).max()) < 2 * U2X_TOL, k
 
 
 @pytest.mark.parametrize("g", [1, 2, 4, 7, 8])
@@ -176,6 +179,31 @@ def test_mma_uniform_two_bit_ragged(cuda, orc, g, fullk, io):
         if not fullk:
             kb[rng.choice(D, 9, replace=False)] = 0
         cases.append((k, v, vb, kb, q))
-    worst, model = _run_batch(cuda, orc, cases, g, io=io)
+    worst, model = _run_batch(cuda, orc, cases, g, io=io, tol=U2X_TOL)
     assert model.plan.uniform2 == (2 if fullk else 1)
-    assert worst < (FP16_INPUT_TOL if io == torch.float32 else 1e-3), worst
+    assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_pipelined_host_decode_matches_device(cuda, orc, chunks):
+    """rdkv_cuda_decode_host_pipelined (chunked H2D / decode / D2H overlap) returns
+    exactly the device-path outputs, for chunk counts that do not divide the units."""
+    rng = np.random.default_rng(5 + chunks)
+    cases = []
+    for _ in range(37):
+        k, v, vb, kb, q = _random_case(rng, 300, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(300, int(rng.integers(90, 160)), replace=False))] = 2
+        kb[:] = 2
+        cases.append((k, v, vb, kb, q))
+    _, model = _run_batch(cuda, orc, cases, 4, tol=U2X_TOL)
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).half()
+    want = P.packed_decode_step(model, q).cpu()
+    dec = P.HostDecoder(model, torch.float16, chunks=chunks)
+    qh = q.cpu().pin_memory()
+    oh = torch.full_like(qh, float("nan")).pin_memory()
+    for _ in range(2):  # reuse of the context and staging buffers
+        dec.step(qh, oh)
+        torch.cuda.current_stream().synchronize()
+        assert torch.equal(oh, want)
+    dec.close()
