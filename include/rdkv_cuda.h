@@ -134,6 +134,11 @@ typedef struct {
     int32_t uniform2;         /* every tile: all kept V rows and K channels at 2 bits (2: and all d K channels kept) */
 } rdkv_decode_plan;
 
+/* rdkv_decode_args.flags: `out` lives in mapped host memory — the tensor-core
+ * kernels write each output row with one TMA bulk store (128/256-B PCIe
+ * writes) instead of per-lane stores (set by rdkv_cuda_decode_host). */
+#define RDKV_DECODE_OUT_HOST 1
+
 typedef struct {
     const uint8_t* arena;
     const int64_t* tile_offsets;
@@ -152,7 +157,7 @@ typedef struct {
     size_t workspace_bytes;
     int32_t kernel;     /* 0 = automatic, 1 = generic CUDA-core, 2 = tensor-core (automatic body),
                            3 = tensor-core general body, 4 = tensor-core one-warp uniform-2-bit body */
-    int32_t reserved;
+    int32_t flags;      /* RDKV_DECODE_* bits (0 = default) */
     const int32_t* tile_decode_bytes; /* [units] device, from rdkv_cuda_decode_prepare (NULL: generic) */
     rdkv_decode_plan plan;
 } rdkv_decode_args;
@@ -166,9 +171,11 @@ RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int64_t* tile_
 RDKV_API size_t rdkv_cuda_decode_workspace(int32_t units, int32_t group, int32_t head_dim,
                                            int32_t split);
 RDKV_API int rdkv_cuda_decode(const rdkv_decode_args* a, void* stream);
-/* End-to-end variant: q_host / out_host are pinned host buffers; the H2D and
- * D2H copies are enqueued on `stream` around the decode (q_dev / out_dev are
- * device staging buffers of the same size). */
+/* End-to-end variant: q_host / out_host are host buffers [units][group]
+ * [head_dim]. Pinned (page-locked, UVA-mapped) buffers are used zero-copy:
+ * the decode kernel reads q over PCIe with TMA bulk loads and writes out with
+ * TMA bulk stores, overlapping both transfers with the step. Pageable buffers
+ * are staged through a->q / a->out with cudaMemcpyAsync on `stream`. */
 RDKV_API int rdkv_cuda_decode_host(const rdkv_decode_args* a, const void* q_host, void* out_host,
                                    void* stream);
 

@@ -89,7 +89,7 @@ class DecodeArgs(C.Structure):
         ("q", C.c_void_p), ("out", C.c_void_p), ("zc_k", C.c_void_p), ("zc_v", C.c_void_p),
         ("zc_len", C.c_void_p), ("zc_cap", C.c_int32), ("split", C.c_int32),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("kernel", C.c_int32),
-        ("reserved", C.c_int32), ("tile_decode_bytes", C.c_void_p), ("plan", DecodePlan),
+        ("flags", C.c_int32), ("tile_decode_bytes", C.c_void_p), ("plan", DecodePlan),
     ]
 
 

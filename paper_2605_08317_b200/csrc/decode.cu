@@ -3,6 +3,8 @@
 // workspace; host-buffer (end-to-end) entry point.
 #include "common.cuh"
 
+#include <cstring>
+
 namespace rdkv_b200 {
 template <typename IO>
 int launch_generic(const rdkv_decode_args* a, int split, int max_kslots, cudaStream_t st);
@@ -38,9 +40,31 @@ extern "C" RDKV_API int rdkv_cuda_decode(const rdkv_decode_args* a, void* stream
                                    : launch_generic<__half>(a, split, max_kslots, st);
 }
 
+// Device address of mapped (pinned, UVA) host memory, or nullptr.
+static const void* mapped_device_ptr(const void* host) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 extern "C" RDKV_API int rdkv_cuda_decode_host(const rdkv_decode_args* a, const void* q_host,
                                               void* out_host, void* stream) {
     if (!a || !q_host || !out_host) return RDKV_EINVAL;
+    // pinned (mapped) host buffers: zero-copy — the decode kernel streams q
+    // from host memory with TMA bulk loads and writes out with bulk stores,
+    // so the PCIe traffic in both directions overlaps the step itself
+    const void* qd = mapped_device_ptr(q_host);
+    const void* od = mapped_device_ptr(out_host);
+    if (qd && od) {
+        rdkv_decode_args z = *a;
+        z.q = qd;
+        z.out = const_cast<void*>(od);
+        z.flags |= RDKV_DECODE_OUT_HOST;
+        return rdkv_cuda_decode(&z, stream);
+    }
     const size_t elem = a->io_dtype == RDKV_F16 ? 2 : 4;
     const size_t bytes = (size_t)a->units * a->group * a->head_dim * elem;
     auto st = static_cast<cudaStream_t>(stream);
@@ -57,6 +81,13 @@ struct rdkv_decode_ctx {
     cudaEvent_t start, done;
     cudaEvent_t* in_done;
     cudaEvent_t* dec_done;
+    // the last call's work captured as a CUDA graph, replayed while the
+    // arguments and host buffers stay the same (one launch per step instead
+    // of ~6 enqueues per chunk)
+    cudaGraphExec_t exec;
+    rdkv_decode_args key;
+    const void* key_q;
+    void* key_out;
 };
 
 extern "C" RDKV_API int rdkv_cuda_decode_ctx_create(int32_t chunks, rdkv_decode_ctx** out) {
@@ -90,16 +121,15 @@ extern "C" RDKV_API int rdkv_cuda_decode_ctx_destroy(rdkv_decode_ctx* c) {
     if (c->done) cudaEventDestroy(c->done);
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
+    if (c->exec) cudaGraphExecDestroy(c->exec);
     delete[] c->in_done;
     delete[] c->dec_done;
     delete c;
     return RDKV_OK;
 }
 
-extern "C" RDKV_API int rdkv_cuda_decode_host_pipelined(rdkv_decode_ctx* c, const rdkv_decode_args* a,
-                                                        const void* q_host, void* out_host, void* stream) {
-    if (!c || !a || !q_host || !out_host || !a->q || !a->out || a->units < 1) return RDKV_EINVAL;
-    if (a->split > 1) return RDKV_EINVAL;  // chunks share one unit-indexed workspace otherwise
+static int enqueue_pipelined(rdkv_decode_ctx* c, const rdkv_decode_args* a, const void* q_host, void* out_host,
+                             void* stream) {
     const size_t row = (size_t)a->group * a->head_dim * (a->io_dtype == RDKV_F16 ? 2 : 4);
     auto st = static_cast<cudaStream_t>(stream);
     const int nch = a->units < c->chunks ? a->units : c->chunks;
@@ -137,5 +167,41 @@ extern "C" RDKV_API int rdkv_cuda_decode_host_pipelined(rdkv_decode_ctx* c, cons
     // join: `stream` is ordered after the last D2H
     RDKV_CUDA_TRY(cudaEventRecord(c->done, c->s_out));
     RDKV_CUDA_TRY(cudaStreamWaitEvent(st, c->done, 0));
+    return RDKV_OK;
+}
+
+extern "C" RDKV_API int rdkv_cuda_decode_host_pipelined(rdkv_decode_ctx* c, const rdkv_decode_args* a,
+                                                        const void* q_host, void* out_host, void* stream) {
+    if (!c || !a || !q_host || !out_host || !a->q || !a->out || a->units < 1) return RDKV_EINVAL;
+    if (a->split > 1) return RDKV_EINVAL;  // chunks share one unit-indexed workspace otherwise
+    auto st = static_cast<cudaStream_t>(stream);
+    if (!st) return enqueue_pipelined(c, a, q_host, out_host, stream);  // legacy stream: no capture
+    if (c->exec && c->key_q == q_host && c->key_out == out_host && memcmp(&c->key, a, sizeof(*a)) == 0) {
+        RDKV_CUDA_TRY(cudaGraphLaunch(c->exec, st));
+        return RDKV_OK;
+    }
+    if (c->exec) {
+        cudaGraphExecDestroy(c->exec);
+        c->exec = nullptr;
+    }
+    RDKV_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    const int rc = enqueue_pipelined(c, a, q_host, out_host, stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (rc != RDKV_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (e != cudaSuccess) return RDKV_ECUDA;
+    const cudaError_t ie = cudaGraphInstantiate(&c->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+        c->exec = nullptr;
+        return RDKV_ECUDA;
+    }
+    c->key = *a;
+    c->key_q = q_host;
+    c->key_out = out_host;
+    RDKV_CUDA_TRY(cudaGraphLaunch(c->exec, st));
     return RDKV_OK;
 }

@@ -78,6 +78,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// TMA bulk store smem -> global (bulk async-group completion)
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -1415,7 +1424,7 @@ __device__ __forceinline__ U2xLane u2x_lane(int half) {
 constexpr float kQFix = 65000.0f;   // sg = kQFix / bound: |N| <= 64 * 65000 < 2^22
 constexpr float kMagicS = 12582912.0f;  // 1.5 * 2^23: bits = 0x4B400000 + rint(x), |x| < 2^22
 constexpr float kMagicU = 8388608.0f;   // 2^23: bits = 0x4B000000 + rint(x), 0 <= x < 2^23
-template <typename IO, int NBMAX, bool FULLK, typename AfterSync1>
+template <typename IO, int NBMAX, bool FULLK, bool BULK, typename AfterSync1>
 __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
                                                 uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
                                                 const U2xLane& L, AfterSync1&& after_sync1) {
@@ -1500,6 +1509,9 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
         for (int o = 4; o < 32; o <<= 1) bpart += __shfl_xor_sync(0xffffffffu, bpart, o);
         if (gid == 0) xg.bias[half][tig] = bpart;
     }
+    // BULK: the previous tile's output stores read its buffer's q rows, and
+    // that buffer is refilled right after this barrier
+    if (BULK && L.lane == 0) bulk_wait_read0();
     pair_sync(bar);
     after_sync1();  // both warps are past the previous tile: its buffer may be refilled
     // l' = log2(e) * (v / (64 sg) + bias) / sqrt(d); heads >= g get -inf logits
@@ -1632,11 +1644,16 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             }
         }
     }
+    // BULK (out in mapped host memory): outputs are staged in this tile's q rows
+    // (dead since sync 1: both warps are past the q~ prep) and each head's
+    // 64-channel half row of this warp leaves with one TMA bulk store (128 /
+    // 256-B PCIe writes); otherwise lanes store straight to `out`
+    IO* stage = BULK ? reinterpret_cast<IO*>(const_cast<uint8_t*>(qs)) : out;
     if (hv) {
         const float inv = rcp_approx(lt);
         const float s0 = vinv * L.s0f;
         const float2 sc = make_float2(s0 * inv, s0 * 0.25f * inv), bb = make_float2(bt * inv, bt * inv);
-        IO* orow = out + tig * kD + L.ch0;
+        IO* orow = stage + tig * kD + L.ch0;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
             const float2 v = make_float2((float)(acc[m][0] * 256 + acc[m][1]), (float)(acc[m][2] * 256 + acc[m][3]));
@@ -1645,6 +1662,15 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                 *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
             else
                 *reinterpret_cast<float2*>(orow + 4 * m) = r;
+        }
+    }
+    if constexpr (BULK) {
+        __syncwarp();
+        if (L.lane == 0) {
+            fence_proxy_async();
+            for (int hh = 0; hh < g; ++hh)
+                bulk_s2g(out + hh * kD + 64 * half, stage + hh * kD + 64 * half, 64 * (uint32_t)sizeof(IO));
+            bulk_commit();
         }
     }
 }
@@ -1661,7 +1687,7 @@ constexpr int kXMaxBuf = 4;  // tile buffers per pair
 // round's tiles are not queued behind everyone's look-ahead.
 // MODE (timing experiments only, RDKV_DECODE_NULL): 0 decode, 1 loads only
 // (no math), 2 math only (tiles past the first buffers are not reloaded).
-template <typename IO, int NBMAX, bool FULLK, int MODE = 0>
+template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
     const int nbuf = p.R;  // buffers per pair
@@ -1722,13 +1748,14 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
             pair_sync(1 + pr);
             refill();
         } else {
-            decode_tile_u2x<IO, NBMAX, FULLK>(st, st + qoff, p.g, scr, o, 1 + pr, lc, refill);
+            decode_tile_u2x<IO, NBMAX, FULLK, BULK>(st, st + qoff, p.g, scr, o, 1 + pr, lc, refill);
         }
         if (++b == nbuf) {
             b = 0;
             phase ^= 1u;
         }
     }
+    if (BULK && lane == 0) bulk_wait0();
 }
 
 // Pairs per CTA and buffers per pair: as many pairs as fit (issue slots are
@@ -1737,7 +1764,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
 // (>= 2, double buffering) as fit.
 static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, int& W, int& nbuf) {
     const int head = kXPairs * kXMaxBuf * (int)sizeof(uint64_t);
-    const char* env = getenv("RDKV_DECODE_PAIRS");
+    static const char* env = getenv("RDKV_DECODE_PAIRS");  // experiment knobs: read once per process
     const int forced = env ? atoi(env) : 0;
     const int per_sm = (units + nsm - 1) / nsm;
     W = 0;
@@ -1767,17 +1794,20 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     const size_t smem = kXPairs * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
                 a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
-    const char* smsp_env = getenv("RDKV_DECODE_SMSP");
+    static const char* smsp_env = getenv("RDKV_DECODE_SMSP");
     if (smsp_env) p.smsp_pairs = atoi(smsp_env);
-    const char* nenv = getenv("RDKV_DECODE_NULL");
+    static const char* nenv = getenv("RDKV_DECODE_NULL");
     const int mode = nenv ? atoi(nenv) : 0;
-    auto kern = mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
+    const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
+    auto kern = bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true>
+              : mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
               : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2> : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
-    static std::atomic<int> smem_set[3][kMaxDevices];
-    set_smem_once(kern, (int)smem, smem_set[mode == 1 ? 1 : mode == 2 ? 2 : 0], da.dev);
+    static std::atomic<int> smem_set[4][kMaxDevices];
+    set_smem_once(kern, (int)smem, smem_set[bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0], da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
-    if (getenv("RDKV_DECODE_VERBOSE"))
+    static const bool verbose = getenv("RDKV_DECODE_VERBOSE") != nullptr;
+    if (verbose)
         fprintf(stderr, "u2x: units %d nbmax %d pairs %d bufs %d slot %d scratch %d smem %zu grid %d\n", a->units,
                 NBMAX, W, nbuf, slot, scratch, smem, blocks);
     kern<<<blocks, 32 * 2 * W, smem, st>>>(p);

@@ -40,15 +40,11 @@ def graph_time(fn_list, reps=20):
     for _ in range(reps): gr.replay()
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) * 1e3 / (reps * len(fn_list))
-for mode in os.environ.get("MODES", "0").split(","):
-    os.environ["RDKV_DECODE_NULL"] = mode
-    for pairs in os.environ.get("PAIRS", "0").split(","):
-      for smsp in os.environ.get("SMSP", "0").split(","):
-        os.environ["RDKV_DECODE_PAIRS"] = pairs
-        os.environ["RDKV_DECODE_SMSP"] = smsp
-        t = graph_time([lambda r=r: P.packed_decode_step(models[r], qs[r], outs[r], kernel=kern) for r in range(NR)])
-        print(f"decode b2b graph mode {mode} pairs {pairs} smsp {smsp}: {t:.2f} us/step  {ab/t/1e3:.0f} GB/s (arena only)", flush=True)
-os.environ["RDKV_DECODE_NULL"] = "0"; os.environ["RDKV_DECODE_PAIRS"] = "0"
+knobs = " ".join(f"{k}={os.environ[k]}" for k in ("RDKV_DECODE_NULL", "RDKV_DECODE_PAIRS", "RDKV_DECODE_SMSP") if k in os.environ)
+t = graph_time([lambda r=r: P.packed_decode_step(models[r], qs[r], outs[r], kernel=kern) for r in range(NR)])
+print(f"decode b2b graph [{knobs}]: {t:.2f} us/step  {ab/t/1e3:.0f} GB/s (arena only)", flush=True)
+if os.environ.get("DECODE_ONLY"):
+    sys.exit(0)
 L = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "bw", "libbw.so"))
 o = torch.zeros(4, dtype=torch.int32, device="cuda")
 for blocks, thr in ((148 * 4, 512), (148 * 16, 256)):

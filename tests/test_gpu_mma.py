@@ -207,3 +207,35 @@ def test_pipelined_host_decode_matches_device(cuda, orc, chunks):
         torch.cuda.current_stream().synchronize()
         assert torch.equal(oh, want)
     dec.close()
+
+
+@pytest.mark.parametrize("io", [torch.float16, torch.float32])
+def test_host_decode_zero_copy_and_pageable(cuda, orc, io):
+    """rdkv_cuda_decode_host: pinned buffers go zero-copy (the kernel streams q
+    in and out over PCIe), pageable ones through the staging copies; both equal
+    the device path bit for bit."""
+    import ctypes as C
+
+    rng = np.random.default_rng(77)
+    cases = []
+    for _ in range(21):
+        k, v, vb, kb, q = _random_case(rng, 300, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(300, int(rng.integers(60, 160)), replace=False))] = 2
+        kb[:] = 2
+        cases.append((k, v, vb, kb, q))
+    _, model = _run_batch(cuda, orc, cases, 4, tol=U2X_TOL)
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).to(io)
+    want = P.packed_decode_step(model, q).cpu()
+    qd, od = torch.empty_like(q), torch.empty_like(q)
+    a = P.decode_args(model, qd, od)
+    L = capi.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    for pinned in (True, False):
+        qh = q.cpu()
+        oh = torch.full_like(qh, float("nan"))
+        if pinned:
+            qh, oh = qh.pin_memory(), oh.pin_memory()
+        assert L.rdkv_cuda_decode_host(C.byref(a), qh.data_ptr(), oh.data_ptr(), st) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(oh, want), pinned
