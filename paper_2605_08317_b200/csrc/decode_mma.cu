@@ -1707,8 +1707,9 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
     const int tile0 = blockIdx.x + pr * gridDim.x, tstride = p.W * gridDim.x;
     const int qoff = p.slot_bytes - qbytes;
-    // stage the k-th tile of this pair into buffer b (one lane)
-    auto issue = [&](int k, int b) {
+    // stage the k-th tile of this pair into buffer b (one lane); with_q = false
+    // leaves the q rows to a second call (issue_q) once the grid dependency is met
+    auto issue_kv = [&](int k, int b) {
         const int tile = tile0 + k * tstride;
         uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
         uint64_t* bar = &fb[b];
@@ -1716,13 +1717,30 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         fence_proxy_async();
         mbar_expect_tx(bar, sz + (uint32_t)qbytes);
         bulk_g2s(dst, p.arena + p.offsets[tile], sz, bar);
-        bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, bar);
     };
+    auto issue_q = [&](int k, int b) {
+        const int tile = tile0 + k * tstride;
+        bulk_g2s(pbuf + (size_t)b * p.slot_bytes + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes,
+                 (uint32_t)qbytes, &fb[b]);
+    };
+    auto issue = [&](int k, int b) {
+        issue_kv(k, b);
+        issue_q(k, b);
+    };
+    // Programmatic dependent launch: this grid may start while the previous
+    // kernel on the stream drains. The packed KV tiles are immutable during
+    // decode, so the first tile's KV stream starts at once; q (produced by the
+    // previous kernel in a model) is read and out written only after
+    // griddepcontrol.wait. Dependents of this grid may launch right away: their
+    // CTAs take SMs as ours retire.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (half == 0 && lane == 0) {
         for (int b = 0; b < nbuf; ++b) mbar_init(&fb[b], 1);
         fence_barrier_init();
-        if (tile0 < p.units) issue(0, 0);
+        if (tile0 < p.units) issue_kv(0, 0);
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (half == 0 && lane == 0 && tile0 < p.units) issue_q(0, 0);
     const U2xLane lc = u2x_lane(half);
     // the q~ digit rows of d3 (never written: |N| < 2^22) must read as zero
     for (int i = threadIdx.x & 63; i < 4 * 512 / 16; i += 64)
@@ -1810,7 +1828,17 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     if (verbose)
         fprintf(stderr, "u2x: units %d nbmax %d pairs %d bufs %d slot %d scratch %d smem %zu grid %d\n", a->units,
                 NBMAX, W, nbuf, slot, scratch, smem, blocks);
-    kern<<<blocks, 32 * 2 * W, smem, st>>>(p);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(32 * 2 * W);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return RDKV_ECUDA;
     return launch_status();
 }
 
