@@ -1707,25 +1707,31 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
     const int tile0 = blockIdx.x + pr * gridDim.x, tstride = p.W * gridDim.x;
     const int qoff = p.slot_bytes - qbytes;
-    // stage the k-th tile of this pair into buffer b (one lane); with_q = false
-    // leaves the q rows to a second call (issue_q) once the grid dependency is met
-    auto issue_kv = [&](int k, int b) {
+    // A tile's KV copy needs its arena offset and size from global memory; the
+    // issuing lanes load them one refill AHEAD (into registers) so the ~1 us
+    // of LDG latency never stalls a warp at the refill point.
+    struct Meta {
+        const uint8_t* src;
+        uint32_t sz;
+    };
+    auto meta = [&](int k) {
         const int tile = tile0 + k * tstride;
-        uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
-        uint64_t* bar = &fb[b];
-        const uint32_t sz = (uint32_t)p.dsize[tile];
+        Meta m{nullptr, 0u};
+        if (tile < p.units) {
+            m.src = p.arena + p.offsets[tile];
+            m.sz = (uint32_t)p.dsize[tile];
+        }
+        return m;
+    };
+    auto issue_kv = [&](const Meta& m, int b) {
         fence_proxy_async();
-        mbar_expect_tx(bar, sz + (uint32_t)qbytes);
-        bulk_g2s(dst, p.arena + p.offsets[tile], sz, bar);
+        mbar_expect_tx(&fb[b], m.sz + (uint32_t)qbytes);
+        bulk_g2s(pbuf + (size_t)b * p.slot_bytes, m.src, m.sz, &fb[b]);
     };
     auto issue_q = [&](int k, int b) {
         const int tile = tile0 + k * tstride;
         bulk_g2s(pbuf + (size_t)b * p.slot_bytes + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes,
                  (uint32_t)qbytes, &fb[b]);
-    };
-    auto issue = [&](int k, int b) {
-        issue_kv(k, b);
-        issue_q(k, b);
     };
     // Programmatic dependent launch: this grid may start while the previous
     // kernel on the stream drains. The packed KV tiles are immutable during
@@ -1734,11 +1740,16 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     // griddepcontrol.wait. Dependents of this grid may launch right away: their
     // CTAs take SMs as ours retire.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    Meta ahead[kXMaxBuf - 1];  // half 1, lane 0: tiles 1 .. nbuf - 1 (look-ahead at tile 0)
+    Meta next{nullptr, 0u};    // half 0, lane 0: the next refill target
     if (half == 0 && lane == 0) {
         for (int b = 0; b < nbuf; ++b) mbar_init(&fb[b], 1);
         fence_barrier_init();
-        if (tile0 < p.units) issue_kv(0, 0);
+        if (tile0 < p.units) issue_kv(meta(0), 0);
+        next = meta(nbuf);  // refill at tile 1 -> tile nbuf
     }
+    if (half == 1 && lane == 0)
+        for (int j = 1; j < kXMaxBuf; ++j) ahead[j - 1] = j < nbuf ? meta(j) : Meta{nullptr, 0u};
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (half == 0 && lane == 0 && tile0 < p.units) issue_q(0, 0);
     const U2xLane lc = u2x_lane(half);
@@ -1753,14 +1764,25 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         if (MODE != 2 || k < nbuf) mbar_wait(&fb[b], phase);
         __syncwarp();
         const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
-        if (k == 0 && half == 1 && lane == 0)  // look-ahead once the first tile is in
-            for (int j = 1; j < nbuf && tile0 + j * tstride < p.units; ++j) issue(j, j);
+        if (k == 0 && half == 1 && lane == 0) {  // look-ahead once the first tile is in
+#pragma unroll
+            for (int j = 1; j < kXMaxBuf; ++j)
+                if (j < nbuf && ahead[j - 1].src) {
+                    issue_kv(ahead[j - 1], j);
+                    issue_q(j, j);
+                }
+        }
         IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
         const int bprev = b == 0 ? nbuf - 1 : b - 1;
-        // the buffer of tile k - 1 takes tile k - 1 + nbuf; the two warps take turns issuing
+        // the buffer of tile k - 1 takes tile k - 1 + nbuf
         auto refill = [&]() {
-            if (MODE != 2 && half == (k & 1) && lane == 0 && k >= 1 && tile + (nbuf - 1) * tstride < p.units)
-                issue(k - 1 + nbuf, bprev);
+            if (MODE != 2 && half == 0 && lane == 0 && k >= 1) {
+                if (next.src) {
+                    issue_kv(next, bprev);
+                    issue_q(k - 1 + nbuf, bprev);
+                }
+                next = meta(k + nbuf);
+            }
         };
         if (MODE == 1) {
             pair_sync(1 + pr);
