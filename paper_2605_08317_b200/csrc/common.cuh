@@ -52,6 +52,7 @@ inline DevAttrs dev_attrs() {
 template <typename F>
 inline void set_smem_once(F kern, int smem, std::atomic<int>* slots, int dev) {
     if (dev >= 0 && dev < kMaxDevices && slots[dev].load(std::memory_order_relaxed) >= smem) return;
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);  // all of L1 as smem
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess && dev >= 0 &&
         dev < kMaxDevices) {
         int cur = slots[dev].load(std::memory_order_relaxed);

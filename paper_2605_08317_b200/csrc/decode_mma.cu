@@ -1687,12 +1687,14 @@ constexpr int kXMaxBuf = 4;  // tile buffers per pair
 // round's tiles are not queued behind everyone's look-ahead.
 // MODE (timing experiments only, RDKV_DECODE_NULL): 0 decode, 1 loads only
 // (no math), 2 math only (tiles past the first buffers are not reloaded).
-template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false>
+// PERCTA: one pair per CTA (a compile-time barrier id, so a CTA reserves 2
+// hardware barriers instead of 16 and 8 CTAs fit on an SM).
+template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
     const int nbuf = p.R;  // buffers per pair
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);  // [W][kXMaxBuf]
-    uint8_t* bufs = dsm + kXPairs * kXMaxBuf * sizeof(uint64_t);
+    uint8_t* bufs = dsm + p.W * kXMaxBuf * sizeof(uint64_t);
     uint8_t* scratch0 = bufs + (size_t)p.W * nbuf * p.slot_bytes;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // with a multiple of 4 pairs, a pair's two warps sit on the same SM
@@ -1785,10 +1787,10 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
             }
         };
         if (MODE == 1) {
-            pair_sync(1 + pr);
+            pair_sync(PERCTA ? 1 : 1 + pr);
             refill();
         } else {
-            decode_tile_u2x<IO, NBMAX, FULLK, BULK>(st, st + qoff, p.g, scr, o, 1 + pr, lc, refill);
+            decode_tile_u2x<IO, NBMAX, FULLK, BULK>(st, st + qoff, p.g, scr, o, PERCTA ? 1 : 1 + pr, lc, refill);
         }
         if (++b == nbuf) {
             b = 0;
@@ -1802,8 +1804,13 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
 // the bound, so more resident warps hide more latency; measured 15.7 us at 8
 // pairs vs 16.6 us at 7 on the 4096-tile step), then as many buffers per pair
 // (>= 2, double buffering) as fit.
+static bool verbose_env() {
+    static const bool v = getenv("RDKV_DECODE_VERBOSE") != nullptr;
+    return v;
+}
+
 static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, int& W, int& nbuf) {
-    const int head = kXPairs * kXMaxBuf * (int)sizeof(uint64_t);
+    const int head = kXPairs * kXMaxBuf * (int)sizeof(uint64_t);  // upper bound of W * kXMaxBuf barriers
     static const char* env = getenv("RDKV_DECODE_PAIRS");  // experiment knobs: read once per process
     const int forced = env ? atoi(env) : 0;
     const int per_sm = (units + nsm - 1) / nsm;
@@ -1828,10 +1835,10 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     const int smem_max = da.smem_optin, nsm = da.nsm;
     // fragment over-reads of ragged blocks land in the following smem region
     // (K rows: < 256 B past a tile's K rows; the last region is scratch)
-    const int slack = 512;
+    const int slack = 128;
     int W = 0, nbuf = 0;
     if (!pick_pairs(a->units, nsm, slot, scratch, smem_max - slack, W, nbuf)) return RDKV_EINVAL;
-    const size_t smem = kXPairs * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
+    size_t smem = W * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
                 a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
     static const char* smsp_env = getenv("RDKV_DECODE_SMSP");
@@ -1846,8 +1853,28 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     set_smem_once(kern, (int)smem, smem_set[bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0], da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
-    static const bool verbose = getenv("RDKV_DECODE_VERBOSE") != nullptr;
-    if (verbose)
+    // One pair per CTA (RDKV_DECODE_CTA=1): the same persistent pairs, but each
+    // retires its own CTA, so under programmatic dependent launch the next
+    // kernel's CTAs take a pair's smem / warp slots as soon as it finishes
+    // instead of when the SM's slowest pair does.
+    static const char* cta_env = getenv("RDKV_DECODE_CTA");
+    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0) {
+        const size_t smem1 = kXMaxBuf * sizeof(uint64_t) + (size_t)2 * slot + scratch + slack;
+        auto k1 = bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, true> : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, true>;
+        static std::atomic<int> smem1_set[2][kMaxDevices];
+        set_smem_once(k1, (int)smem1, smem1_set[bulk ? 1 : 0], da.dev);
+        int per_sm = 0;
+        const cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1, 64, smem1);
+        if (verbose_env()) fprintf(stderr, "u2x: per-pair CTAs: smem %zu -> %d per SM (err %d)\n", smem1, per_sm, (int)oe);
+        if (oe == cudaSuccess && per_sm >= W) {
+            kern = k1;
+            p.W = W = 1;
+            p.R = nbuf = 2;
+            smem = smem1;
+            blocks = a->units < nsm * per_sm ? a->units : nsm * per_sm;
+        }
+    }
+    if (verbose_env())
         fprintf(stderr, "u2x: units %d nbmax %d pairs %d bufs %d slot %d scratch %d smem %zu grid %d\n", a->units,
                 NBMAX, W, nbuf, slot, scratch, smem, blocks);
     cudaLaunchConfig_t cfg{};
