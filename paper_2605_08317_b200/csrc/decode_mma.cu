@@ -1519,9 +1519,6 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     const float qscale2 = bnd * (kInvSqrtD * kLog2e / (64.0f * kQFix));
 
     // ---- QK over this warp's blocks half, half + 2, ...
-    uint32_t bq[4][4];
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) ldsm_x4(bq[kk], qdig + kk * 512 + L.bofs);
     // A rows gid / gid + 8 of m-tile u = slots 32pb + 4gid + 2u / + 1, stored at
     // positions (2u + r) Q + 8pb + gid (slot-transposed K rows)
     const uint8_t* kbase = t + h.off_k + (size_t)(8 * half + gid) * krb;
@@ -1532,6 +1529,11 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     for (int i = 0; i < NBW; ++i) {
         if (i < mynb) {
             const int pb = half + 2 * i;
+            // q~ digit fragments re-read per block (4 LDSM) rather than held in 16
+            // registers across the block loop: the register peak is here
+            uint32_t bq[4][4];
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) ldsm_x4(bq[kk], qdig + kk * 512 + L.bofs);
             int acc[2][2][4];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
