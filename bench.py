@@ -442,7 +442,7 @@ def main():
         try:
             with open(prof) as f:
                 pj = json.load(f)
-            if pj.get("units") == U and pj.get("kernel_mode") == args.kernel:
+            if pj.get("units") == U and pj.get("kernel_mode") == args.kernel and pj.get("arena_bytes") == model.arena_bytes:
                 traffic = pj.get("dram_bytes_per_launch")
         except Exception:  # noqa: BLE001
             traffic = None

@@ -1424,10 +1424,27 @@ __device__ __forceinline__ U2xLane u2x_lane(int half) {
 constexpr float kQFix = 65000.0f;   // sg = kQFix / bound: |N| <= 64 * 65000 < 2^22
 constexpr float kMagicS = 12582912.0f;  // 1.5 * 2^23: bits = 0x4B400000 + rint(x), |x| < 2^22
 constexpr float kMagicU = 8388608.0f;   // 2^23: bits = 0x4B000000 + rint(x), 0 <= x < 2^23
-template <typename IO, int NBMAX, bool FULLK, bool BULK, typename AfterSync1>
+// Long tiles (> 160 slots) are decoded in chunks of <= 160 token slots by one
+// pair, with an online softmax across the chunks (U2xRun); a chunk's data sits
+// in the staging buffer at the offsets of U2xChunk, with the tile's header /
+// channel table / q rows present only for the first chunk.
+struct U2xChunk {
+    int n, nslot;                // kept tokens / slots of this chunk
+    int off_k, off_v, off_vp;    // K rows, V groups, V params inside the staging buffer
+    int krb;                     // K row bytes
+    bool first, last;
+};
+struct U2xRun {
+    float vmax, bias2, qscale2;  // tile constants (this lane's head)
+    float m, l;                  // running max (log2 units) and weight sum of this lane's head
+    float2 o[4];                 // running unnormalised outputs (channels ch0 + 4m, + 1)
+};
+
+template <typename IO, int NBMAX, bool FULLK, bool BULK, bool CHUNKED = false, typename AfterSync1>
 __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
                                                 uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
-                                                const U2xLane& L, AfterSync1&& after_sync1) {
+                                                const U2xLane& L, AfterSync1&& after_sync1,
+                                                const U2xChunk* ck = nullptr, U2xRun* run = nullptr) {
     constexpr int NBW = (NBMAX + 1) / 2;  // blocks per warp (upper bound)
     const int gid = L.gid, tig = L.tig, half = L.half;
     const bool hv = tig < g;
@@ -1436,17 +1453,29 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     uint8_t* qdig = scr + kXQDig;
     uint8_t* pdig = scr + kXPDig;
     const float* chanf = reinterpret_cast<const float*>(t + kHeaderBytes);
-    const int n = h.r[0];
-    const int nslot = h.nslot;
+    const bool first = CHUNKED ? ck->first : true;
+    const int n = CHUNKED ? ck->n : h.r[0];
+    const int nslot = CHUNKED ? ck->nslot : h.nslot;
     const int nb = (n + 31) >> 5;             // 32-token blocks of this tile (warp-uniform)
     const int mynb = (nb + 1 - half) >> 1;    // blocks of this warp: half, half + 2, ...
-    const int krb = FULLK ? 32 : h.krow_bytes;
+    const int krb_c = FULLK ? 32 : (CHUNKED ? ck->krb : h.krow_bytes);
     const int Q = nslot >> 2;
-    const uint32_t sbits = h.scale_bounds;
-    const float smax = bf16_bits_to_float(sbits & 0xFFFFu), vmax = bf16_bits_to_float(sbits >> 16);
+    const int off_k = CHUNKED ? ck->off_k : h.off_k;
+    const int off_v = CHUNKED ? ck->off_v : h.off_vseg[0];
+    const int off_vp = CHUNKED ? ck->off_vp : h.off_vp;
+    const uint32_t sbits = first ? h.scale_bounds : 0u;
+    const float smax = bf16_bits_to_float(sbits & 0xFFFFu);
+    const float vmax = (CHUNKED && !first) ? run->vmax : bf16_bits_to_float(sbits >> 16);
     constexpr float kInvSqrtD = 0.08838834764831845f;
     constexpr float kLog2e = 1.4426950408889634f;
     constexpr int QROW = kD * (int)sizeof(IO);
+    float bias2, qscale2;
+    if (CHUNKED && !first) {
+        bias2 = run->bias2;
+        qscale2 = run->qscale2;
+        pair_sync(bar);  // both warps are past the previous chunk: its buffer may be refilled
+        after_sync1();
+    } else {
 
     // ---- q range per head: lanes 8h..8h+7 scan head h (16 channels each), then
     // every lane picks its head tig
@@ -1515,14 +1544,24 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     pair_sync(bar);
     after_sync1();  // both warps are past the previous tile: its buffer may be refilled
     // l' = log2(e) * (v / (64 sg) + bias) / sqrt(d); heads >= g get -inf logits
-    const float bias2 = hv ? (xg.bias[0][tig] + xg.bias[1][tig]) * (kInvSqrtD * kLog2e) : -INFINITY;
-    const float qscale2 = bnd * (kInvSqrtD * kLog2e / (64.0f * kQFix));
+    bias2 = hv ? (xg.bias[0][tig] + xg.bias[1][tig]) * (kInvSqrtD * kLog2e) : -INFINITY;
+    qscale2 = bnd * (kInvSqrtD * kLog2e / (64.0f * kQFix));
+    if constexpr (CHUNKED) {
+        run->vmax = vmax;
+        run->bias2 = bias2;
+        run->qscale2 = qscale2;
+        run->m = -INFINITY;
+        run->l = 0.0f;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) run->o[m] = make_float2(0.0f, 0.0f);
+    }
+    }  // first chunk
 
     // ---- QK over this warp's blocks half, half + 2, ...
     // A rows gid / gid + 8 of m-tile u = slots 32pb + 4gid + 2u / + 1, stored at
     // positions (2u + r) Q + 8pb + gid (slot-transposed K rows)
-    const uint8_t* kbase = t + h.off_k + (size_t)(8 * half + gid) * krb;
-    const int qstride = Q * krb;
+    const uint8_t* kbase = t + off_k + (size_t)(8 * half + gid) * krb_c;
+    const int qstride = Q * krb_c;
     float2 lg[NBW][2];
     float mx = -INFINITY;
 #pragma unroll
@@ -1537,7 +1576,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             int acc[2][2][4];
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
-                const uint8_t* r0 = kbase + 2 * u * qstride + 16 * i * krb;
+                const uint8_t* r0 = kbase + 2 * u * qstride + 16 * i * krb_c;
                 const uint8_t* r1 = r0 + qstride;
                 const uint4 x0 = lds128(r0), x1 = lds128(r0 + 16), y0 = lds128(r1), y1 = lds128(r1 + 16);
                 const uint32_t w0[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
@@ -1584,7 +1623,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     // ---- softmax + p~ digits (hi, lo bytes): four consecutive slots per lane and block
     float2 ls2 = make_float2(0.0f, 0.0f);
     float bv = 0.0f;
-    const float2* vparam = reinterpret_cast<const float2*>(t + h.off_vp);
+    const float2* vparam = reinterpret_cast<const float2*>(t + off_vp);
     const float2 nmx = make_float2(-mx, -mx);
 #pragma unroll
     for (int i = 0; i < NBW; ++i) {
@@ -1631,7 +1670,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     int acc[4][4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0;
-    const uint8_t* g0b = t + h.off_vseg[0] + L.vcol;
+    const uint8_t* g0b = t + off_v + L.vcol;
 #pragma unroll
     for (int kk = 0; kk < NBMAX; ++kk) {
         if (kk < nb) {
@@ -1651,7 +1690,39 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     // 64-channel half row of this warp leaves with one TMA bulk store (128 /
     // 256-B PCIe writes); otherwise lanes store straight to `out`
     IO* stage = BULK ? reinterpret_cast<IO*>(const_cast<uint8_t*>(qs)) : out;
-    if (hv) {
+    if constexpr (CHUNKED) {
+        // online softmax across chunks: fold this chunk (max mx, sum lt,
+        // unnormalised outputs v * s + bt) into the running state
+        if (hv && lt > 0.0f) {
+            const float mnew = fmaxf(run->m, mx);
+            const float a = ex2_approx(run->m - mnew), bw = ex2_approx(mx - mnew);
+            const float s0 = vinv * L.s0f;
+            const float2 sc = make_float2(s0 * bw, s0 * 0.25f * bw), bb = make_float2(bt * bw, bt * bw);
+            const float2 aa = make_float2(a, a);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const float2 v =
+                    make_float2((float)(acc[m][0] * 256 + acc[m][1]), (float)(acc[m][2] * 256 + acc[m][3]));
+                run->o[m] = ffma2(run->o[m], aa, ffma2(v, sc, bb));
+            }
+            run->l = fmaf(run->l, a, lt * bw);
+            run->m = mnew;
+        }
+        if (!ck->last) return;
+        if (hv) {
+            const float inv = rcp_approx(run->l);
+            const float2 iv = make_float2(inv, inv);
+            IO* orow = stage + tig * kD + L.ch0;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const float2 r = fmul2(run->o[m], iv);
+                if constexpr (sizeof(IO) == 2)
+                    *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
+                else
+                    *reinterpret_cast<float2*>(orow + 4 * m) = r;
+            }
+        }
+    } else if (hv) {
         const float inv = rcp_approx(lt);
         const float s0 = vinv * L.s0f;
         const float2 sc = make_float2(s0 * inv, s0 * 0.25f * inv), bb = make_float2(bt * inv, bt * inv);
@@ -1828,6 +1899,187 @@ static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, 
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// Long uniform-2-bit tiles (more than 160 token slots, e.g. the configs[3]
+// budget sweep: 512 .. 2048 FP16-equivalent tokens per layer keep 256 .. 1024
+// tokens per head at 2 bits). A pair walks its tiles chunk by chunk: chunk c of
+// a tile covers slots [c S, c S + ns) (S a multiple of 32, <= 160), staged by
+// TMA as [tile header + channel table | 4 K-row runs | V groups | V params |
+// q rows] (header and q only for c = 0), and folded into an online softmax.
+__device__ __forceinline__ void u2c_geom(int nslot, int c, int& C, int& s0, int& ns) {
+    C = nslot <= 160 ? 1 : (nslot + 159) / 160;
+    const int S = C == 1 ? nslot : (((nslot + C - 1) / C) + 31) & ~31;
+    s0 = c * S;
+    ns = min(S, nslot - s0);
+}
+
+template <typename IO, bool FULLK, bool BULK>
+__global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const MmaParams p) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    const int nbuf = p.R;
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    uint8_t* bufs = dsm + p.W * kXMaxBuf * sizeof(uint64_t);
+    uint8_t* scratch0 = bufs + (size_t)p.W * nbuf * p.slot_bytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pr = warp >> 1, half = warp & 1;
+    constexpr int QROW = kD * (int)sizeof(IO);
+    const int qbytes = p.g * QROW;
+    uint64_t* fb = full + pr * kXMaxBuf;
+    uint8_t* pbuf = bufs + (size_t)pr * nbuf * p.slot_bytes;
+    uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
+    const int tile0 = blockIdx.x + pr * gridDim.x, tstride = p.W * gridDim.x;
+    const int qoff = p.slot_bytes - qbytes;
+    const bool issuer = half == 0 && lane == 0;
+
+    // ---- issuer state (one lane): the next item (tile, chunk) to stage
+    struct TileMeta {
+        const uint8_t* base;
+        int nslot, hk, krb, offv, offvp;
+    };
+    auto load_meta = [&](int tile) {
+        TileMeta m{nullptr, 0, 0, 0, 0, 0};
+        if (tile < p.units) {
+            m.base = p.arena + p.offsets[tile];
+            const TileHeader* th = reinterpret_cast<const TileHeader*>(m.base);
+            m.nslot = th->nslot;
+            m.hk = th->off_k;
+            m.krb = th->krow_bytes;
+            m.offv = th->off_vseg[0];
+            m.offvp = th->off_vp;
+        }
+        return m;
+    };
+    int cur_tile = tile0, cur_c = 0;
+    TileMeta cur{nullptr, 0, 0, 0, 0, 0}, nxt{nullptr, 0, 0, 0, 0, 0};
+    // stage the cursor's item into buffer b (q rows optional: the first item's
+    // q waits for the grid dependency); returns false when the pair is done
+    auto issue_item = [&](int b, bool with_q) {
+        if (cur_tile >= p.units || !cur.base) return false;
+        int C, s0, ns;
+        u2c_geom(cur.nslot, cur_c, C, s0, ns);
+        uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
+        const int rows = ns >> 2, Q = cur.nslot >> 2;
+        const uint32_t kbytes = (uint32_t)(rows * cur.krb), vbytes = (uint32_t)(rows * 128), pbytes = (uint32_t)(ns * 8);
+        const bool c0 = cur_c == 0;
+        uint32_t tx = 4 * kbytes + vbytes + pbytes + (c0 ? (uint32_t)(cur.hk + qbytes) : 0u);
+        fence_proxy_async();
+        mbar_expect_tx(&fb[b], tx);
+        if (c0) bulk_g2s(dst, cur.base, (uint32_t)cur.hk, &fb[b]);
+        const int dk = cur.hk;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            bulk_g2s(dst + dk + r * kbytes, cur.base + cur.hk + (size_t)(r * Q + (s0 >> 2)) * cur.krb, kbytes, &fb[b]);
+        bulk_g2s(dst + dk + ns * cur.krb, cur.base + cur.offv + (size_t)(s0 >> 2) * 128, vbytes, &fb[b]);
+        bulk_g2s(dst + dk + ns * (cur.krb + 32), cur.base + cur.offvp + (size_t)s0 * 8, pbytes, &fb[b]);
+        if (c0 && with_q)
+            bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)cur_tile * qbytes, (uint32_t)qbytes,
+                     &fb[b]);
+        // advance the cursor
+        if (++cur_c == C) {
+            cur_tile += tstride;
+            cur_c = 0;
+            cur = nxt;
+            nxt = load_meta(cur_tile + tstride);
+        }
+        return true;
+    };
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (issuer) {
+        for (int b = 0; b < nbuf; ++b) mbar_init(&fb[b], 1);
+        fence_barrier_init();
+        cur = load_meta(tile0);
+        nxt = load_meta(tile0 + tstride);
+        issue_item(0, false);  // KV of the first chunk before the grid dependency
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (issuer && tile0 < p.units)
+        bulk_g2s(pbuf + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile0 * qbytes, (uint32_t)qbytes, &fb[0]);
+    const U2xLane lc = u2x_lane(half);
+    for (int i = threadIdx.x & 63; i < 4 * 512 / 16; i += 64)
+        reinterpret_cast<uint4*>(scr + kXQDig)[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    int b = 0, k = 0;
+    uint32_t phase = 0;
+    U2xRun run;
+    for (int tile = tile0; tile < p.units; tile += tstride) {
+        int n_t = 0, nslot_t = 0, hk = 0, krb = 0, C = 1;
+        IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
+        for (int c = 0; c < C; ++c, ++k) {
+            mbar_wait(&fb[b], phase);
+            __syncwarp();
+            const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
+            if (c == 0) {
+                const TileHeader& th = *reinterpret_cast<const TileHeader*>(st);
+                n_t = th.r[0];
+                nslot_t = th.nslot;
+                hk = th.off_k;
+                krb = FULLK ? 32 : th.krow_bytes;
+                int s0_, ns_;
+                u2c_geom(nslot_t, 0, C, s0_, ns_);
+            }
+            if (k == 0 && issuer)  // look-ahead once the first item is in
+                for (int j = 1; j < nbuf; ++j) issue_item(j, true);
+            int Cc, s0, ns;
+            u2c_geom(nslot_t, c, Cc, s0, ns);
+            U2xChunk ck;
+            ck.n = max(0, min(n_t - s0, ns));
+            ck.nslot = ns;
+            ck.off_k = hk;
+            ck.off_v = hk + ns * krb;
+            ck.off_vp = hk + ns * (krb + 32);
+            ck.krb = krb;
+            ck.first = c == 0;
+            ck.last = c == C - 1;
+            const int bprev = b == 0 ? nbuf - 1 : b - 1;
+            auto refill = [&]() {
+                if (issuer && k >= 1) issue_item(bprev, true);
+            };
+            decode_tile_u2x<IO, kXNbMax, FULLK, BULK, true>(st, st + qoff, p.g, scr, o, 1 + pr, lc, refill, &ck, &run);
+            if (++b == nbuf) {
+                b = 0;
+                phase ^= 1u;
+            }
+        }
+    }
+    if (BULK && lane == 0) bulk_wait0();
+}
+
+template <typename IO, bool FULLK>
+static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st) {
+    const int qbytes = a->group * kD * (int)sizeof(IO);
+    const int slot = (kHeaderBytes + 10 * kD + 160 * (32 + 32 + 8) + qbytes + 127) & ~127;  // header+chan+perm, <=160 slots
+    const int scratch = (kXPDig + kXNbMax * 256 + 127) & ~127;
+    const DevAttrs da = dev_attrs();
+    const int slack = 128;
+    int W = 0, nbuf = 0;
+    if (!pick_pairs(a->units, da.nsm, slot, scratch, da.smem_optin - slack, W, nbuf)) return RDKV_EINVAL;
+    const size_t smem = W * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
+    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
+                a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
+    const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
+    auto kern = bulk ? decode_u2c_kernel<IO, FULLK, true> : decode_u2c_kernel<IO, FULLK, false>;
+    static std::atomic<int> smem_set[2][kMaxDevices];
+    set_smem_once(kern, (int)smem, smem_set[bulk ? 1 : 0], da.dev);
+    int blocks = (a->units + W - 1) / W;
+    if (blocks > da.nsm) blocks = da.nsm;
+    if (verbose_env())
+        fprintf(stderr, "u2c: units %d pairs %d bufs %d slot %d scratch %d smem %zu grid %d\n", a->units, W, nbuf,
+                slot, scratch, smem, blocks);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(32 * 2 * W);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return RDKV_ECUDA;
+    return launch_status();
+}
+
 template <typename IO, int NBMAX, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
@@ -1895,6 +2147,7 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
 
 template <typename IO, bool FULLK>
 static int launch_u2x_k(const rdkv_decode_args* a, cudaStream_t st) {
+    if (a->plan.max_slots > kU2MaxSlots) return launch_u2c<IO, FULLK>(a, st);  // long tiles: chunked
     const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
     if (nb <= 2) return launch_u2x_t<IO, 2, FULLK>(a, st);
     if (nb <= 4) return launch_u2x_t<IO, 4, FULLK>(a, st);
@@ -1917,6 +2170,8 @@ bool mma_supported(const rdkv_decode_args* a) {
     if (a->head_dim != kD || a->group > 8 || !a->tile_decode_bytes) return false;
     if (a->zc_len && a->zc_cap > 1024) return false;
     const rdkv_decode_plan& p = a->plan;
+    // uniform 2-bit tiles of any length: u2x (<= 160 slots) or its chunked variant
+    if (p.uniform2 && a->group <= 4 && !a->zc_len && p.max_decode_bytes > 0) return true;
     return p.max_decode_bytes > 0 && p.max_slots <= kMaxSlots && p.max_zone_b_rows <= kMaxSlots;
 }
 
@@ -1979,9 +2234,11 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     // uniform 2-bit tiles (the n=128 production shape) take the specialised body
     // uniform 2-bit tiles (the n=128 production shape): warp-pair body by default,
     // kernel 4 selects the one-warp body, kernel 3 the general body
-    const bool u2 = a->plan.uniform2 && a->group <= 4 && !a->zc_len && a->kernel != 3;
-    if (u2 && a->kernel == 4) return f16 ? launch_t<1, __half, true>(a, st) : launch_t<1, float, true>(a, st);
-    if (u2 && a->kernel == 5) return f16 ? launch_pair<__half>(a, st) : launch_pair<float>(a, st);
+    const bool u2 = a->plan.uniform2 && a->group <= 4 && !a->zc_len &&
+                    (a->kernel != 3 || a->plan.max_slots > kMaxSlots);  // the general body stops at 256 slots
+    const bool short_u2 = u2 && a->plan.max_slots <= kU2MaxSlots;
+    if (short_u2 && a->kernel == 4) return f16 ? launch_t<1, __half, true>(a, st) : launch_t<1, float, true>(a, st);
+    if (short_u2 && a->kernel == 5) return f16 ? launch_pair<__half>(a, st) : launch_pair<float>(a, st);
     if (u2) return f16 ? launch_u2x<__half>(a, st) : launch_u2x<float>(a, st);
     if (a->group <= 4) return f16 ? launch_t<1, __half, false>(a, st) : launch_t<1, float, false>(a, st);
     return f16 ? launch_t<2, __half, false>(a, st) : launch_t<2, float, false>(a, st);
@@ -2016,7 +2273,7 @@ extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int
         p.max_zone_b_rows = h.r[3] > p.max_zone_b_rows ? h.r[3] : p.max_zone_b_rows;
         p.max_kq_slots = h.kslot_base[3] > p.max_kq_slots ? h.kslot_base[3] : p.max_kq_slots;
         const bool u2 = h.r[1] == 0 && h.r[2] == 0 && h.r[3] == 0 && h.c[1] == 0 && h.c[2] == 0 &&
-                        h.c[3] == 0 && h.r[0] > 0 && h.c[0] > 0 && h.nslot <= kU2MaxSlots;
+                        h.c[3] == 0 && h.r[0] > 0 && h.c[0] > 0;
         if (!u2) p.uniform2 = 0;
         else if (h.c[0] != kD && p.uniform2 == 2) p.uniform2 = 1;
     }

@@ -239,3 +239,23 @@ def test_host_decode_zero_copy_and_pageable(cuda, orc, io):
         assert L.rdkv_cuda_decode_host(C.byref(a), qh.data_ptr(), oh.data_ptr(), st) == 0
         torch.cuda.synchronize()
         assert torch.equal(oh, want), pinned
+
+
+@pytest.mark.parametrize("g,fullk,io", [(4, True, torch.float16), (4, False, torch.float32), (2, True, torch.float32)])
+def test_mma_uniform_two_bit_long_tiles(cuda, orc, g, fullk, io):
+    """Uniform 2-bit tiles longer than 160 slots (the configs[3] budget sweep):
+    the chunked u2x kernel with an online softmax across <= 160-slot chunks,
+    mixed with short tiles in the same launch."""
+    rng = np.random.default_rng(60 + g + 10 * fullk)
+    cases = []
+    for n in (5, 128, 161, 200, 333, 512, 700, 1100):
+        k, v, vb, kb, q = _random_case(rng, 1200, g)
+        vb[:] = 0
+        vb[np.sort(rng.choice(1200, n, replace=False))] = 2
+        kb[:] = 2
+        if not fullk:
+            kb[rng.choice(D, 5, replace=False)] = 0
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, g, io=io, tol=U2X_TOL)
+    assert model.plan.max_slots > 1000 and model.plan.uniform2 == (2 if fullk else 1)
+    assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
