@@ -1360,6 +1360,18 @@ __device__ __forceinline__ float2 ld_io2<float>(const float* p, int c) {
     return *reinterpret_cast<const float2*>(p + c);
 }
 
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+// D = A(f16, 16x16 row) * B(f16, 16x8 col) + D, f32 accumulate
+__device__ __forceinline__ void hmma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
 // Per-lane constants of the u2x body, computed once per warp.
 struct U2xLane {
     int lane, gid, tig, half;
@@ -1913,7 +1925,142 @@ __device__ __forceinline__ void u2c_geom(int nslot, int c, int& C, int& s0, int&
     ns = min(S, nslot - s0);
 }
 
-template <typename IO, bool FULLK, bool BULK>
+// ---- Zone C (appended fp16 K/V rows, trizone.cpp:307-314) on the fast path.
+// After a tile's packed chunks its Zone C rows are decoded in chunks of 16
+// tokens with fp16 tensor-core MMAs (m16n8k16, f32 accumulate), q and the
+// softmax weights split hi + lo into two fp16 columns each so the products
+// keep ~22 bits, and folded into the same online softmax.
+constexpr int kZcChunk = 16;
+constexpr int kQ16Row = 272;              // bytes per row of the fp16 q table (8 rows, padded)
+constexpr int kQ16Bytes = 8 * kQ16Row;
+constexpr int kZcAuxWarp = 256 + 4 * 64 * 4;  // per warp: P tile (8 x 16 fp16) + output exchange (4 x 64 f32)
+
+// Rows 2h / 2h + 1 = hi / lo fp16 parts of q_h (zero for h >= g); warp `half`
+// writes channels 64 half .. 64 half + 63 (visible to the pair after sync 1).
+template <typename IO>
+__device__ __forceinline__ void build_q16(const uint8_t* qs, int g, uint8_t* q16, const U2xLane& L) {
+    const int r = L.lane >> 2, hq = r >> 1, lo = r & 1;
+    const int c0 = 64 * L.half + 16 * (L.lane & 3);
+    const IO* qh = reinterpret_cast<const IO*>(qs + (hq < g ? hq : 0) * kD * (int)sizeof(IO));
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        __half v2[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const float qv = hq < g ? ld_io(qh, c0 + 2 * i + j) : 0.0f;
+            const __half hi = __float2half_rn(qv);
+            v2[j] = lo ? __float2half_rn(qv - __half2float(hi)) : hi;
+        }
+        w[i] = *reinterpret_cast<uint32_t*>(v2);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(q16 + r * kQ16Row + 2 * c0);
+    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+// One Zone C chunk: K rows [16][d] fp16 at st, V rows at st + 16 * 256, cnt
+// valid tokens; each warp's spare (P tile, output exchange) follows the V rows.
+template <typename IO, bool BULK, typename AfterSync1>
+__device__ __forceinline__ void zc_chunk_u2x(const uint8_t* __restrict__ st, int cnt, const uint8_t* __restrict__ q16,
+                                             int g, int bar, const U2xLane& L, U2xRun& run, bool last,
+                                             IO* __restrict__ out, IO* __restrict__ stage, AfterSync1&& after_sync1) {
+    constexpr float kScale = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(d)
+    const int lane = L.lane, gid = L.gid, tig = L.tig, half = L.half;
+    const bool hv = tig < g;
+    pair_sync(bar);  // both warps are past the previous item: its buffer may be refilled
+    after_sync1();
+    uint8_t* vrows = const_cast<uint8_t*>(st) + kZcChunk * 256;
+    uint8_t* aux = const_cast<uint8_t*>(st) + 2 * kZcChunk * 256 + half * kZcAuxWarp;  // this warp's spare
+    // rows past cnt hold stale bytes: zero this warp's channel half of the V rows
+    for (int r = cnt + (lane >> 3); r < kZcChunk; r += 4)
+        *reinterpret_cast<uint4*>(vrows + r * 256 + 128 * half + 16 * (lane & 7)) = make_uint4(0u, 0u, 0u, 0u);
+    // ---- QK (every warp, all 16 tokens): A = K rows, B = q table
+    float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    const uint8_t* abase = st + (lane & 15) * 256 + (lane >> 4) * 16;
+    const uint8_t* bbase = q16 + (lane & 7) * kQ16Row + ((lane >> 3) & 1) * 16;
+#pragma unroll
+    for (int ks = 0; ks < kD / 16; ++ks) {
+        uint32_t a[4], b[2];
+        ldsm_x4(a, abase + ks * 32);
+        ldsm_x2(b, bbase + ks * 32);
+        hmma16816(c, a, b[0], b[1]);
+    }
+    // rows gid, gid + 8 = tokens; columns 2 tig (hi), 2 tig + 1 (lo) = head tig
+    float l0 = (c[0] + c[1]) * kScale, l1 = (c[2] + c[3]) * kScale;
+    if (!hv || gid >= cnt) l0 = -INFINITY;
+    if (!hv || gid + 8 >= cnt) l1 = -INFINITY;
+    float m = fmaxf(l0, l1);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (m == -INFINITY) m = 0.0f;
+    const float p0 = ex2_approx(l0 - m), p1 = ex2_approx(l1 - m);
+    float ls = p0 + p1;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
+    // ---- P as the PV B operand: rows 2 tig (hi) / 2 tig + 1 (lo), 16 tokens of fp16
+    __half* pt = reinterpret_cast<__half*>(aux);
+    const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
+    pt[(2 * tig) * 16 + gid] = h0;
+    pt[(2 * tig + 1) * 16 + gid] = __float2half_rn(p0 - __half2float(h0));
+    pt[(2 * tig) * 16 + gid + 8] = h1;
+    pt[(2 * tig + 1) * 16 + gid + 8] = __float2half_rn(p1 - __half2float(h1));
+    __syncwarp();
+    uint32_t bp[2];
+    ldsm_x2(bp, aux + (lane & 7) * 32 + ((lane >> 3) & 1) * 16);
+    // ---- PV: this warp's channels 64 half .. + 63 as 4 m-tiles (A = V^T via ldmatrix.trans)
+    float* xo = reinterpret_cast<float*>(aux + 256);  // [4 heads][64 channels]
+    const uint8_t* vbase = vrows + ((lane & 7) + 8 * ((lane >> 4) & 1)) * 256 + (64 * half + 8 * ((lane >> 3) & 1)) * 2;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        uint32_t a[4];
+        ldsm_x4_t(a, vbase + mt * 32);
+        float o[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        hmma16816(o, a, bp[0], bp[1]);
+        xo[tig * 64 + 16 * mt + gid] = o[0] + o[1];
+        xo[tig * 64 + 16 * mt + gid + 8] = o[2] + o[3];
+    }
+    __syncwarp();
+    // ---- fold into the running state in the u2x lane mapping (channels ch0 + 4m, + 1)
+    if (hv && ls > 0.0f) {
+        const float mnew = fmaxf(run.m, m);
+        const float a = ex2_approx(run.m - mnew), bw = ex2_approx(m - mnew);
+        const float2 aa = make_float2(a, a), bb = make_float2(bw, bw);
+        const float* xr = xo + tig * 64 + (L.ch0 - 64 * half);
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) {
+            const float2 z = *reinterpret_cast<const float2*>(xr + 4 * mm);
+            run.o[mm] = ffma2(run.o[mm], aa, fmul2(z, bb));
+        }
+        run.l = fmaf(run.l, a, ls * bw);
+        run.m = mnew;
+    }
+    if (!last) return;
+    if (hv) {
+        const float inv = rcp_approx(run.l);
+        const float2 iv = make_float2(inv, inv);
+        IO* orow = stage + tig * kD + L.ch0;
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm) {
+            const float2 r = fmul2(run.o[mm], iv);
+            if constexpr (sizeof(IO) == 2)
+                *reinterpret_cast<__half2*>(orow + 4 * mm) = __float22half2_rn(r);
+            else
+                *reinterpret_cast<float2*>(orow + 4 * mm) = r;
+        }
+    }
+    if constexpr (BULK) {
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async();
+            for (int hh = 0; hh < g; ++hh)
+                bulk_s2g(out + hh * kD + 64 * half, stage + hh * kD + 64 * half, 64 * (uint32_t)sizeof(IO));
+            bulk_commit();
+        }
+    }
+}
+
+template <typename IO, bool FULLK, bool BULK, bool ZC = false>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
     const int nbuf = p.R;
@@ -1927,6 +2074,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
     uint64_t* fb = full + pr * kXMaxBuf;
     uint8_t* pbuf = bufs + (size_t)pr * nbuf * p.slot_bytes;
     uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
+    uint8_t* q16 = scr + p.scratch_bytes - kQ16Bytes;  // ZC only
     const int tile0 = blockIdx.x + pr * gridDim.x, tstride = p.W * gridDim.x;
     const int qoff = p.slot_bytes - qbytes;
     const bool issuer = half == 0 && lane == 0;
@@ -1949,38 +2097,63 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
         }
         return m;
     };
-    int cur_tile = tile0, cur_c = 0;
+    int cur_tile = tile0, cur_c = 0, cur_zc = 0;
     TileMeta cur{nullptr, 0, 0, 0, 0, 0}, nxt{nullptr, 0, 0, 0, 0, 0};
+    // Zone C lengths are written by the previous kernel (append): read only
+    // after griddepcontrol.wait
+    auto zc_of = [&](int tile) { return (ZC && tile < p.units) ? p.zc_len[tile] : 0; };
     // stage the cursor's item into buffer b (q rows optional: the first item's
     // q waits for the grid dependency); returns false when the pair is done
-    auto issue_item = [&](int b, bool with_q) {
-        if (cur_tile >= p.units || !cur.base) return false;
+    auto advance = [&]() {
         int C, s0, ns;
-        u2c_geom(cur.nslot, cur_c, C, s0, ns);
-        uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
-        const int rows = ns >> 2, Q = cur.nslot >> 2;
-        const uint32_t kbytes = (uint32_t)(rows * cur.krb), vbytes = (uint32_t)(rows * 128), pbytes = (uint32_t)(ns * 8);
-        const bool c0 = cur_c == 0;
-        uint32_t tx = 4 * kbytes + vbytes + pbytes + (c0 ? (uint32_t)(cur.hk + qbytes) : 0u);
-        fence_proxy_async();
-        mbar_expect_tx(&fb[b], tx);
-        if (c0) bulk_g2s(dst, cur.base, (uint32_t)cur.hk, &fb[b]);
-        const int dk = cur.hk;
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-            bulk_g2s(dst + dk + r * kbytes, cur.base + cur.hk + (size_t)(r * Q + (s0 >> 2)) * cur.krb, kbytes, &fb[b]);
-        bulk_g2s(dst + dk + ns * cur.krb, cur.base + cur.offv + (size_t)(s0 >> 2) * 128, vbytes, &fb[b]);
-        bulk_g2s(dst + dk + ns * (cur.krb + 32), cur.base + cur.offvp + (size_t)s0 * 8, pbytes, &fb[b]);
-        if (c0 && with_q)
-            bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)cur_tile * qbytes, (uint32_t)qbytes,
-                     &fb[b]);
-        // advance the cursor
-        if (++cur_c == C) {
+        u2c_geom(cur.nslot, 0, C, s0, ns);
+        if (++cur_c == C + (cur_zc + kZcChunk - 1) / kZcChunk) {
             cur_tile += tstride;
             cur_c = 0;
             cur = nxt;
             nxt = load_meta(cur_tile + tstride);
+            cur_zc = zc_of(cur_tile);
         }
+    };
+    auto stage_item = [&](int b, bool with_q) {
+        if (cur_tile >= p.units || !cur.base) return false;
+        int C, s0, ns;
+        u2c_geom(cur.nslot, cur_c, C, s0, ns);
+        uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
+        if (ZC && cur_c >= C) {  // Zone C chunk (cur_c - C) of this tile
+            const int j = cur_c - C;
+            const int rows = min(kZcChunk, cur_zc - kZcChunk * j);
+            const size_t row0 = (size_t)cur_tile * p.zc_cap + (size_t)kZcChunk * j;
+            fence_proxy_async();
+            mbar_expect_tx(&fb[b], (uint32_t)(2 * rows * 256));
+            bulk_g2s(dst, reinterpret_cast<const uint8_t*>(p.zc_k + row0 * kD), (uint32_t)(rows * 256), &fb[b]);
+            bulk_g2s(dst + kZcChunk * 256, reinterpret_cast<const uint8_t*>(p.zc_v + row0 * kD), (uint32_t)(rows * 256),
+                     &fb[b]);
+        } else {
+            const int rows = ns >> 2, Q = cur.nslot >> 2;
+            const uint32_t kbytes = (uint32_t)(rows * cur.krb), vbytes = (uint32_t)(rows * 128),
+                           pbytes = (uint32_t)(ns * 8);
+            const bool c0 = cur_c == 0;
+            const uint32_t tx = 4 * kbytes + vbytes + pbytes + (c0 ? (uint32_t)(cur.hk + qbytes) : 0u);
+            fence_proxy_async();
+            mbar_expect_tx(&fb[b], tx);
+            if (c0) bulk_g2s(dst, cur.base, (uint32_t)cur.hk, &fb[b]);
+            const int dk = cur.hk;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+                bulk_g2s(dst + dk + r * kbytes, cur.base + cur.hk + (size_t)(r * Q + (s0 >> 2)) * cur.krb, kbytes,
+                         &fb[b]);
+            bulk_g2s(dst + dk + ns * cur.krb, cur.base + cur.offv + (size_t)(s0 >> 2) * 128, vbytes, &fb[b]);
+            bulk_g2s(dst + dk + ns * (cur.krb + 32), cur.base + cur.offvp + (size_t)s0 * 8, pbytes, &fb[b]);
+            if (c0 && with_q)
+                bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)cur_tile * qbytes,
+                         (uint32_t)qbytes, &fb[b]);
+        }
+        return true;
+    };
+    auto issue_item = [&](int b, bool with_q) {
+        if (!stage_item(b, with_q)) return false;
+        advance();
         return true;
     };
 
@@ -1990,11 +2163,14 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
         fence_barrier_init();
         cur = load_meta(tile0);
         nxt = load_meta(tile0 + tstride);
-        issue_item(0, false);  // KV of the first chunk before the grid dependency
+        stage_item(0, false);  // KV of the first (packed) chunk before the grid dependency
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (issuer && tile0 < p.units)
+    if (issuer && tile0 < p.units) {
         bulk_g2s(pbuf + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile0 * qbytes, (uint32_t)qbytes, &fb[0]);
+        cur_zc = zc_of(tile0);  // known now: the cursor may move past tile0's packed chunks
+        advance();
+    }
     const U2xLane lc = u2x_lane(half);
     for (int i = threadIdx.x & 63; i < 4 * 512 / 16; i += 64)
         reinterpret_cast<uint4*>(scr + kXQDig)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -2002,8 +2178,11 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
     int b = 0, k = 0;
     uint32_t phase = 0;
     U2xRun run;
+    int zcl_next = zc_of(tile0);
     for (int tile = tile0; tile < p.units; tile += tstride) {
-        int n_t = 0, nslot_t = 0, hk = 0, krb = 0, C = 1;
+        int n_t = 0, nslot_t = 0, hk = 0, krb = 0, Cp = 1, C = 1;
+        const int zcl = zcl_next;
+        zcl_next = zc_of(tile + tstride);
         IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
         for (int c = 0; c < C; ++c, ++k) {
             mbar_wait(&fb[b], phase);
@@ -2016,26 +2195,35 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
                 hk = th.off_k;
                 krb = FULLK ? 32 : th.krow_bytes;
                 int s0_, ns_;
-                u2c_geom(nslot_t, 0, C, s0_, ns_);
+                u2c_geom(nslot_t, 0, Cp, s0_, ns_);
+                C = Cp + (zcl + kZcChunk - 1) / kZcChunk;
+                if (ZC) build_q16<IO>(st + qoff, p.g, q16, lc);
             }
             if (k == 0 && issuer)  // look-ahead once the first item is in
                 for (int j = 1; j < nbuf; ++j) issue_item(j, true);
-            int Cc, s0, ns;
-            u2c_geom(nslot_t, c, Cc, s0, ns);
-            U2xChunk ck;
-            ck.n = max(0, min(n_t - s0, ns));
-            ck.nslot = ns;
-            ck.off_k = hk;
-            ck.off_v = hk + ns * krb;
-            ck.off_vp = hk + ns * (krb + 32);
-            ck.krb = krb;
-            ck.first = c == 0;
-            ck.last = c == C - 1;
             const int bprev = b == 0 ? nbuf - 1 : b - 1;
             auto refill = [&]() {
                 if (issuer && k >= 1) issue_item(bprev, true);
             };
-            decode_tile_u2x<IO, kXNbMax, FULLK, BULK, true>(st, st + qoff, p.g, scr, o, 1 + pr, lc, refill, &ck, &run);
+            if (ZC && c >= Cp) {
+                const int j = c - Cp;
+                zc_chunk_u2x<IO, BULK>(st, min(kZcChunk, zcl - kZcChunk * j), q16, p.g, 1 + pr, lc, run, c == C - 1, o,
+                                       BULK ? reinterpret_cast<IO*>(const_cast<uint8_t*>(st) + qoff) : o, refill);
+            } else {
+                int Cc, s0, ns;
+                u2c_geom(nslot_t, c, Cc, s0, ns);
+                U2xChunk ck;
+                ck.n = max(0, min(n_t - s0, ns));
+                ck.nslot = ns;
+                ck.off_k = hk;
+                ck.off_v = hk + ns * krb;
+                ck.off_vp = hk + ns * (krb + 32);
+                ck.krb = krb;
+                ck.first = c == 0;
+                ck.last = c == C - 1;
+                decode_tile_u2x<IO, kXNbMax, FULLK, BULK, true>(st, st + qoff, p.g, scr, o, 1 + pr, lc, refill, &ck,
+                                                                 &run);
+            }
             if (++b == nbuf) {
                 b = 0;
                 phase ^= 1u;
@@ -2047,25 +2235,33 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
 
 template <typename IO, bool FULLK>
 static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st) {
+    const bool zc = a->zc_len != nullptr;
     const int qbytes = a->group * kD * (int)sizeof(IO);
-    const int slot = (kHeaderBytes + 10 * kD + 160 * (32 + 32 + 8) + qbytes + 127) & ~127;  // header+chan+perm, <=160 slots
-    const int scratch = (kXPDig + kXNbMax * 256 + 127) & ~127;
+    // header + channel table + perm, then <= 160 slots of K / V / params (a
+    // Zone C chunk: 16 K + 16 V rows + 8 KB of spare), q rows at the end
+    const int cslots = a->plan.max_slots < kU2MaxSlots ? ((a->plan.max_slots + 3) & ~3) : kU2MaxSlots;
+    int body = 10 * kD + cslots * (32 + 32 + 8);
+    const int zbody = 2 * kZcChunk * 256 + 2 * kZcAuxWarp;  // Zone C chunk: K + V rows + both warps' spare
+    const int slot = ((zc && zbody > kHeaderBytes + body ? zbody : kHeaderBytes + body) + qbytes + 127) & ~127;
+    const int scratch = (kXPDig + kXNbMax * 256 + (zc ? kQ16Bytes : 0) + 127) & ~127;
     const DevAttrs da = dev_attrs();
     const int slack = 128;
     int W = 0, nbuf = 0;
     if (!pick_pairs(a->units, da.nsm, slot, scratch, da.smem_optin - slack, W, nbuf)) return RDKV_EINVAL;
     const size_t smem = W * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
-    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
-                a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
+    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
+                static_cast<const __half*>(a->zc_k), static_cast<const __half*>(a->zc_v), a->zc_len,
+                a->units, a->group, a->zc_cap, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
     const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
-    auto kern = bulk ? decode_u2c_kernel<IO, FULLK, true> : decode_u2c_kernel<IO, FULLK, false>;
-    static std::atomic<int> smem_set[2][kMaxDevices];
-    set_smem_once(kern, (int)smem, smem_set[bulk ? 1 : 0], da.dev);
+    auto kern = zc ? (bulk ? decode_u2c_kernel<IO, FULLK, true, true> : decode_u2c_kernel<IO, FULLK, false, true>)
+                   : (bulk ? decode_u2c_kernel<IO, FULLK, true, false> : decode_u2c_kernel<IO, FULLK, false, false>);
+    static std::atomic<int> smem_set[4][kMaxDevices];
+    set_smem_once(kern, (int)smem, smem_set[(zc ? 2 : 0) + (bulk ? 1 : 0)], da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > da.nsm) blocks = da.nsm;
     if (verbose_env())
-        fprintf(stderr, "u2c: units %d pairs %d bufs %d slot %d scratch %d smem %zu grid %d\n", a->units, W, nbuf,
-                slot, scratch, smem, blocks);
+        fprintf(stderr, "u2c: units %d zc %d pairs %d bufs %d slot %d scratch %d smem %zu grid %d\n", a->units, (int)zc,
+                W, nbuf, slot, scratch, smem, blocks);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(32 * 2 * W);
@@ -2147,7 +2343,8 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
 
 template <typename IO, bool FULLK>
 static int launch_u2x_k(const rdkv_decode_args* a, cudaStream_t st) {
-    if (a->plan.max_slots > kU2MaxSlots) return launch_u2c<IO, FULLK>(a, st);  // long tiles: chunked
+    // long tiles or Zone C rows: the chunked kernel
+    if (a->plan.max_slots > kU2MaxSlots || a->zc_len) return launch_u2c<IO, FULLK>(a, st);
     const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
     if (nb <= 2) return launch_u2x_t<IO, 2, FULLK>(a, st);
     if (nb <= 4) return launch_u2x_t<IO, 4, FULLK>(a, st);
@@ -2171,7 +2368,7 @@ bool mma_supported(const rdkv_decode_args* a) {
     if (a->zc_len && a->zc_cap > 1024) return false;
     const rdkv_decode_plan& p = a->plan;
     // uniform 2-bit tiles of any length: u2x (<= 160 slots) or its chunked variant
-    if (p.uniform2 && a->group <= 4 && !a->zc_len && p.max_decode_bytes > 0) return true;
+    if (p.uniform2 && a->group <= 4 && p.max_decode_bytes > 0) return true;
     return p.max_decode_bytes > 0 && p.max_slots <= kMaxSlots && p.max_zone_b_rows <= kMaxSlots;
 }
 
@@ -2234,9 +2431,9 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     // uniform 2-bit tiles (the n=128 production shape) take the specialised body
     // uniform 2-bit tiles (the n=128 production shape): warp-pair body by default,
     // kernel 4 selects the one-warp body, kernel 3 the general body
-    const bool u2 = a->plan.uniform2 && a->group <= 4 && !a->zc_len &&
+    const bool u2 = a->plan.uniform2 && a->group <= 4 &&
                     (a->kernel != 3 || a->plan.max_slots > kMaxSlots);  // the general body stops at 256 slots
-    const bool short_u2 = u2 && a->plan.max_slots <= kU2MaxSlots;
+    const bool short_u2 = u2 && a->plan.max_slots <= kU2MaxSlots && !a->zc_len;
     if (short_u2 && a->kernel == 4) return f16 ? launch_t<1, __half, true>(a, st) : launch_t<1, float, true>(a, st);
     if (short_u2 && a->kernel == 5) return f16 ? launch_pair<__half>(a, st) : launch_pair<float>(a, st);
     if (u2) return f16 ? launch_u2x<__half>(a, st) : launch_u2x<float>(a, st);

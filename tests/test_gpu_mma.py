@@ -259,3 +259,22 @@ def test_mma_uniform_two_bit_long_tiles(cuda, orc, g, fullk, io):
     worst, model = _run_batch(cuda, orc, cases, g, io=io, tol=U2X_TOL)
     assert model.plan.max_slots > 1000 and model.plan.uniform2 == (2 if fullk else 1)
     assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
+
+
+@pytest.mark.parametrize("n_max,appends,io", [(150, 1, torch.float16), (150, 17, torch.float32), (600, 40, torch.float16),
+                                              (130, 5, torch.float32)])
+def test_mma_uniform_two_bit_zone_c(cuda, orc, n_max, appends, io):
+    """Zone C (appended fp16 K/V rows) on the uniform-2-bit fast path: 16-token
+    fp16 tensor-core chunks folded into the online softmax, after short or
+    chunked long packed tiles."""
+    rng = np.random.default_rng(80 + appends)
+    cases = []
+    for n in (3, 64, 100, n_max):
+        k, v, vb, kb, q = _random_case(rng, 700, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(700, n, replace=False))] = 2
+        kb[:] = 2
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, 4, io=io, appends=appends, rng=rng, tol=U2X_TOL)
+    assert model.plan.uniform2 == 2
+    assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
