@@ -45,6 +45,7 @@ def parse():
     p.add_argument("--no-fp16-baseline", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-pipeline", action="store_true")
+    p.add_argument("--no-secondary", action="store_true", help="skip the Zone C / budget-512 secondary lines")
     p.add_argument("--cpu-budget-s", type=float, default=8.0)
     return p.parse_args()
 
@@ -306,6 +307,80 @@ def pipeline_config2(P, steps):
             "note": "allocate/pack timed per (layer) chunk incl. host syncs; decode back-to-back (L2-warm)"}
 
 
+def graph_step_us(P, model, q, steps, kernel=0):
+    """Back-to-back decode steps from one CUDA graph over rotation copies of the
+    arena (>= 3x L2), one event pair: the same method as the headline number."""
+    import torch
+
+    l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
+    per_copy = model.arena_bytes + 2 * q.numel() * q.element_size()
+    n_rot = max(1, -(-3 * l2 // per_copy))
+    rot = []
+    for r in range(n_rot):
+        m = P.PackedModel(model.arena if r == 0 else model.arena.clone(), model.offsets, model.offsets_host,
+                          model.units, model.group, model.head_dim, model.zc_k, model.zc_v, model.zc_len, model.zc_cap)
+        m.decode_sizes, m.plan = model.decode_sizes, model.plan
+        rot.append((m, q if r == 0 else q.clone(), torch.empty_like(q)))
+    for i in range(3):
+        m, qq, oo = rot[i % n_rot]
+        P.packed_decode_step(m, qq, oo, kernel=kernel)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(g, stream=side):
+        for i in range(steps):
+            m, qq, oo = rot[i % n_rot]
+            P.packed_decode_step(m, qq, oo, kernel=kernel)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(side):
+        e0.record(side)
+        g.replay()
+        e1.record(side)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps * 1e3, n_rot
+
+
+def secondary_configs(P, spec0, model, q, args):
+    """Other BASELINE shapes on the same GPU (secondary lines, not the headline):
+    the decode step with the new token already appended to Zone C, and a
+    configs[3]-style budget point (512 FP16-equivalent tokens per layer)."""
+    import torch
+    from paper_2605_08317_b200.workload import WorkloadSpec, build
+
+    out = {}
+    U, d = model.units, spec0.head_dim
+    peak, _ = load_peaks()
+    # (1) Zone C: the step's own token appended (append_new_token, trizone.cpp:307-314)
+    model.zc_cap = 16
+    model.zc_k = torch.zeros((U, 16, d), dtype=torch.float16, device="cuda")
+    model.zc_v = torch.zeros_like(model.zc_k)
+    model.zc_len = torch.zeros(U, dtype=torch.int32, device="cuda")
+    kn = P.generate((U, d), torch.float16, seed=77, tensor=1)
+    P.append_new_token(model, kn, kn)
+    us, _ = graph_step_us(P, model, q, min(args.steps, 100))
+    byts = model.decode_bytes(io_bytes=2)
+    out["zone_c_1"] = {"config": "configs[2] step with the new token in Zone C (1 fp16 K/V row per tile)",
+                       "us_per_step": us, "tok_s": spec0.batch / (us / 1e6),
+                       "roofline_frac": byts / (us / 1e6) / 1e9 / peak}
+    model.zc_cap, model.zc_k, model.zc_v, model.zc_len = 0, None, None, None
+    # (2) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
+    spec = WorkloadSpec(batch=spec0.batch, layers=spec0.layers, ctx=spec0.ctx, n_tokens=512, seed=3)
+    m2, _, st2, _ = build(spec)
+    q2 = P.generate((m2.units, spec.group, d), torch.float16, seed=QSEED, tensor=2)
+    us, _ = graph_step_us(P, m2, q2, min(args.steps, 100))
+    byts = m2.decode_bytes(io_bytes=2)
+    out["budget_512"] = {"config": "LLaMA-3.1-8B KV shape, 128K ctx, n=512 tokens/layer (configs[3] budget point), "
+                                   f"batch {spec.batch}, kept tokens/head {float(np.mean([s['n_kept'].mean() for s in st2])):.1f}",
+                         "us_per_step": us, "tok_s": spec.batch / (us / 1e6),
+                         "roofline_frac": byts / (us / 1e6) / 1e9 / peak, "bytes_per_step": byts}
+    del m2, q2
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup()
@@ -513,6 +588,11 @@ def main():
                               "tolerance": 1e-3}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
+    if rank == 0 and world == 1 and not args.no_secondary:
+        try:
+            line["secondary"] = secondary_configs(P, spec, model, q, args)
+        except Exception as e:  # noqa: BLE001
+            line["secondary"] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if rank == 0 and world == 1 and not args.no_pipeline:
