@@ -365,8 +365,49 @@ def secondary_configs(P, spec0, model, q, args):
     out["zone_c_1"] = {"config": "configs[2] step with the new token in Zone C (1 fp16 K/V row per tile)",
                        "us_per_step": us, "tok_s": spec0.batch / (us / 1e6),
                        "roofline_frac": byts / (us / 1e6) / 1e9 / peak}
+    # (2) a generation loop on the device: per step append the new token's K/V
+    # to Zone C (rdkv_cuda_append) and decode, 16 steps replayed from one CUDA
+    # graph (Zone C reset at the start of each replay)
+    nsteps = 16
+    model.zc_cap = nsteps
+    model.zc_k = torch.zeros((U, nsteps, d), dtype=torch.float16, device="cuda")
+    model.zc_v = torch.zeros_like(model.zc_k)
+    model.zc_len = torch.zeros(U, dtype=torch.int32, device="cuda")
+    kv = [P.generate((U, d), torch.float16, seed=900 + i, tensor=1) for i in range(nsteps)]
+    qs = [P.generate(tuple(q.shape), torch.float16, seed=700 + i, tensor=2) for i in range(nsteps)]
+    o = torch.empty_like(q)
+
+    def loop():
+        model.zc_len.zero_()
+        for i in range(nsteps):
+            P.append_new_token(model, kv[i], kv[i])
+            P.packed_decode_step(model, qs[i], o)
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        loop()
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        loop()
+    g.replay()
+    torch.cuda.synchronize()
+    reps = 10
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(side):
+        e0.record(side)
+        for _ in range(reps):
+            g.replay()
+        e1.record(side)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / (reps * nsteps) * 1e3
+    out["decode_loop_16"] = {"config": "16 generated tokens: append (Zone C) + decode per step, one CUDA graph; "
+                                       "Zone C grows 1..16 rows per tile (L2-warm: the step re-reads one arena)",
+                             "us_per_token_step": us, "tok_s": spec0.batch / (us / 1e6)}
     model.zc_cap, model.zc_k, model.zc_v, model.zc_len = 0, None, None, None
-    # (2) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
+    # (3) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
     spec = WorkloadSpec(batch=spec0.batch, layers=spec0.layers, ctx=spec0.ctx, n_tokens=512, seed=3)
     m2, _, st2, _ = build(spec)
     q2 = P.generate((m2.units, spec.group, d), torch.float16, seed=QSEED, tensor=2)

@@ -9,7 +9,7 @@ K = (torch.randn((U, T, D), device="cuda", generator=g)).half().float()
 V = (torch.randn((U, T, D), device="cuda", generator=g)).half().float()
 q = torch.randn((U, 4, D), device="cuda", generator=g).half()
 def ev(): return torch.cuda.Event(enable_timing=True)
-for counts in ([128], [127, 128, 129], [129], [160], [96]):
+for counts in [[int(x) for x in c.split("+")] for c in os.environ.get("COUNTS", "128,127+128+129,129,160,96").split(",")]:
     rng = np.random.default_rng(1)
     vb = np.zeros((U, T), np.uint8)
     for u in range(U):
