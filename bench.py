@@ -318,7 +318,8 @@ def graph_step_us(P, model, q, steps, kernel=0):
     rot = []
     for r in range(n_rot):
         m = P.PackedModel(model.arena if r == 0 else model.arena.clone(), model.offsets, model.offsets_host,
-                          model.units, model.group, model.head_dim, model.zc_k, model.zc_v, model.zc_len, model.zc_cap)
+                          model.units, model.group, model.head_dim, model.zc_k, model.zc_v, model.zc_len, model.zc_cap,
+                          model.zc_count)
         m.decode_sizes, m.plan = model.decode_sizes, model.plan
         rot.append((m, q if r == 0 else q.clone(), torch.empty_like(q)))
     for i in range(3):
@@ -354,7 +355,7 @@ def secondary_configs(P, spec0, model, q, args):
     U, d = model.units, spec0.head_dim
     peak, _ = load_peaks()
     # (1) Zone C: the step's own token appended (append_new_token, trizone.cpp:307-314)
-    model.zc_cap = 16
+    model.zc_cap, model.zc_count = 16, 0
     model.zc_k = torch.zeros((U, 16, d), dtype=torch.float16, device="cuda")
     model.zc_v = torch.zeros_like(model.zc_k)
     model.zc_len = torch.zeros(U, dtype=torch.int32, device="cuda")
@@ -369,7 +370,7 @@ def secondary_configs(P, spec0, model, q, args):
     # to Zone C (rdkv_cuda_append) and decode, 16 steps replayed from one CUDA
     # graph (Zone C reset at the start of each replay)
     nsteps = 16
-    model.zc_cap = nsteps
+    model.zc_cap, model.zc_count = nsteps, 0
     model.zc_k = torch.zeros((U, nsteps, d), dtype=torch.float16, device="cuda")
     model.zc_v = torch.zeros_like(model.zc_k)
     model.zc_len = torch.zeros(U, dtype=torch.int32, device="cuda")
@@ -461,7 +462,7 @@ def main():
     rot = [(model, q, out)]
     for r in range(1, n_rot):
         m = P.PackedModel(model.arena.clone(), model.offsets, model.offsets_host, U, g, d,
-                          model.zc_k, model.zc_v, model.zc_len, model.zc_cap)
+                          model.zc_k, model.zc_v, model.zc_len, model.zc_cap, model.zc_count)
         m.decode_sizes, m.plan = model.decode_sizes, model.plan
         rot.append((m, q.clone(), torch.empty_like(out)))
 

@@ -138,6 +138,11 @@ typedef struct {
  * kernels write each output row with one TMA bulk store (128/256-B PCIe
  * writes) instead of per-lane stores (set by rdkv_cuda_decode_host). */
 #define RDKV_DECODE_OUT_HOST 1
+/* rdkv_decode_args.flags: zc_bound holds a host-known upper bound on every
+ * zc_len[u] (e.g. the number of appends since packing); with a small bound the
+ * uniform-2-bit kernel stages the Zone C rows with the packed tile instead of
+ * running them as separate chunks. */
+#define RDKV_DECODE_ZC_BOUND 2
 
 typedef struct {
     const uint8_t* arena;
@@ -160,6 +165,8 @@ typedef struct {
     int32_t flags;      /* RDKV_DECODE_* bits (0 = default) */
     const int32_t* tile_decode_bytes; /* [units] device, from rdkv_cuda_decode_prepare (NULL: generic) */
     rdkv_decode_plan plan;
+    int32_t zc_bound;   /* with RDKV_DECODE_ZC_BOUND: max over units of zc_len[u] */
+    int32_t reserved2;
 } rdkv_decode_args;
 
 /* One-time scan of a packed arena: writes the per-tile decode sizes

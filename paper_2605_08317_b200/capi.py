@@ -16,6 +16,7 @@ HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "rdkv_cuda.h")
 
 RDKV_OK, RDKV_EINVAL, RDKV_ENUMERIC, RDKV_EFORMAT, RDKV_ECUDA = range(5)
 RDKV_F32, RDKV_F16 = 0, 1
+RDKV_DECODE_OUT_HOST, RDKV_DECODE_ZC_BOUND = 1, 2
 
 
 class RdkvError(RuntimeError):
@@ -90,6 +91,7 @@ class DecodeArgs(C.Structure):
         ("zc_len", C.c_void_p), ("zc_cap", C.c_int32), ("split", C.c_int32),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("kernel", C.c_int32),
         ("flags", C.c_int32), ("tile_decode_bytes", C.c_void_p), ("plan", DecodePlan),
+        ("zc_bound", C.c_int32), ("reserved2", C.c_int32),
     ]
 
 

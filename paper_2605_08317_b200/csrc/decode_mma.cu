@@ -57,6 +57,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {  // no arrive
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -1452,11 +1456,17 @@ struct U2xRun {
     float2 o[4];                 // running unnormalised outputs (channels ch0 + 4m, + 1)
 };
 
-template <typename IO, int NBMAX, bool FULLK, bool BULK, bool CHUNKED = false, typename AfterSync1>
+// ZCF (short tiles with a few Zone C rows, <= kZcFused): the tile's Zone C K / V
+// rows are staged in its own buffer (zk / zv) and folded in after PV: QK on an
+// fp16 m16n8k16 MMA (rows = the z tokens), PV on CUDA cores in the lanes'
+// output mapping, one shared softmax.
+constexpr int kZcFused = 4;
+template <typename IO, int NBMAX, bool FULLK, bool BULK, bool CHUNKED = false, bool ZCF = false, typename AfterSync1>
 __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
                                                 uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
                                                 const U2xLane& L, AfterSync1&& after_sync1,
-                                                const U2xChunk* ck = nullptr, U2xRun* run = nullptr) {
+                                                const U2xChunk* ck = nullptr, U2xRun* run = nullptr, int z = 0,
+                                                const uint8_t* zk = nullptr, const uint8_t* zv = nullptr) {
     constexpr int NBW = (NBMAX + 1) / 2;  // blocks per warp (upper bound)
     const int gid = L.gid, tig = L.tig, half = L.half;
     const bool hv = tig < g;
@@ -1734,19 +1744,82 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                     *reinterpret_cast<float2*>(orow + 4 * m) = r;
             }
         }
-    } else if (hv) {
-        const float inv = rcp_approx(lt);
-        const float s0 = vinv * L.s0f;
-        const float2 sc = make_float2(s0 * inv, s0 * 0.25f * inv), bb = make_float2(bt * inv, bt * inv);
-        IO* orow = stage + tig * kD + L.ch0;
+    } else {
+        float wa = 1.0f, wb = 0.0f, lz = 0.0f;
+        float2 oz[4] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f),
+                        make_float2(0.0f, 0.0f)};
+        if (ZCF && z > 0) {
+            // QK: A rows = Zone C tokens (rows >= z read neighbouring bytes, masked
+            // below), B columns 2h / 2h + 1 = hi / lo fp16 parts of q_h
+            float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            const uint8_t* abase = zk + (L.lane & 15) * 256 + (L.lane >> 4) * 16;
+            const int bh = gid >> 1;
+            const IO* qb = reinterpret_cast<const IO*>(qs + (bh < g ? bh : 0) * QROW);
+            const bool bzero = bh >= g || (sizeof(IO) == 2 && (gid & 1));
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            const float2 v = make_float2((float)(acc[m][0] * 256 + acc[m][1]), (float)(acc[m][2] * 256 + acc[m][3]));
-            const float2 r = ffma2(v, sc, bb);
-            if constexpr (sizeof(IO) == 2)
-                *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
-            else
-                *reinterpret_cast<float2*>(orow + 4 * m) = r;
+            for (int ks = 0; ks < kD / 16; ++ks) {
+                uint32_t a[4], bw[2];
+                ldsm_x4(a, abase + ks * 32);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int ch = ks * 16 + 8 * j + 2 * tig;
+                    if constexpr (sizeof(IO) == 2) {
+                        bw[j] = *reinterpret_cast<const uint32_t*>(qb + ch);
+                    } else {
+                        const float2 v = *reinterpret_cast<const float2*>(qb + ch);
+                        const __half2 hi = __floats2half2_rn(v.x, v.y);
+                        const float2 hf = __half22float2(hi);
+                        const __half2 lo = __floats2half2_rn(v.x - hf.x, v.y - hf.y);
+                        const __half2 sel = (gid & 1) ? lo : hi;
+                        bw[j] = *reinterpret_cast<const uint32_t*>(&sel);
+                    }
+                    if (bzero) bw[j] = 0u;
+                }
+                hmma16816(c, a, bw[0], bw[1]);
+            }
+            constexpr float kZScale = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(d)
+            float l = (c[0] + c[1]) * kZScale;  // token gid, head tig
+            if (!hv || gid >= z) l = -INFINITY;
+            float mz = l;
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) mz = fmaxf(mz, __shfl_xor_sync(0xffffffffu, mz, o));
+            if (mz == -INFINITY) mz = 0.0f;
+            const float pz = ex2_approx(l - mz);
+            lz = pz;
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) lz += __shfl_xor_sync(0xffffffffu, lz, o);
+            // PV: this lane's output channels ch0 + 4m, + 1 of head tig
+#pragma unroll
+            for (int tk = 0; tk < kZcFused; ++tk) {
+                const float pt = __shfl_sync(0xffffffffu, pz, 4 * tk + tig);
+                if (tk < z) {
+                    const float2 ptt = make_float2(pt, pt);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        oz[m] = ffma2(__half22float2(*reinterpret_cast<const __half2*>(zv + tk * 256 + 2 * (L.ch0 + 4 * m))),
+                                      ptt, oz[m]);
+                }
+            }
+            const float mm = fmaxf(mx, mz);
+            wa = ex2_approx(mx - mm);
+            wb = ex2_approx(mz - mm);
+        }
+        if (hv) {
+            const float inv = rcp_approx(fmaf(lt, wa, lz * wb));
+            const float s0 = vinv * L.s0f * wa * inv, bta = bt * wa * inv, zb = wb * inv;
+            const float2 sc = make_float2(s0, s0 * 0.25f), bb = make_float2(bta, bta), zz = make_float2(zb, zb);
+            IO* orow = stage + tig * kD + L.ch0;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const float2 v =
+                    make_float2((float)(acc[m][0] * 256 + acc[m][1]), (float)(acc[m][2] * 256 + acc[m][3]));
+                float2 r = ffma2(v, sc, bb);
+                if (ZCF) r = ffma2(oz[m], zz, r);
+                if constexpr (sizeof(IO) == 2)
+                    *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
+                else
+                    *reinterpret_cast<float2*>(orow + 4 * m) = r;
+            }
         }
     }
     if constexpr (BULK) {
@@ -1774,7 +1847,7 @@ constexpr int kXMaxBuf = 4;  // tile buffers per pair
 // (no math), 2 math only (tiles past the first buffers are not reloaded).
 // PERCTA: one pair per CTA (a compile-time barrier id, so a CTA reserves 2
 // hardware barriers instead of 16 and 8 CTAs fit on an SM).
-template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false>
+template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false, bool ZCF = false>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
     const int nbuf = p.R;  // buffers per pair
@@ -1810,15 +1883,31 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         }
         return m;
     };
+    // A tile arrives in two parts on its buffer's mbarrier: the KV copy (tx only,
+    // may run before the grid dependency), then q (+ ZCF: the tile's Zone C
+    // rows) with the arrive — so the phase cannot complete early.
     auto issue_kv = [&](const Meta& m, int b) {
         fence_proxy_async();
-        mbar_expect_tx(&fb[b], m.sz + (uint32_t)qbytes);
+        mbar_expect_tx_only(&fb[b], m.sz);
         bulk_g2s(pbuf + (size_t)b * p.slot_bytes, m.src, m.sz, &fb[b]);
     };
-    auto issue_q = [&](int k, int b) {
+    auto issue_q = [&](int k, int b, int zrows) {
         const int tile = tile0 + k * tstride;
-        bulk_g2s(pbuf + (size_t)b * p.slot_bytes + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes,
-                 (uint32_t)qbytes, &fb[b]);
+        uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
+        mbar_expect_tx(&fb[b], (uint32_t)(qbytes + 2 * 256 * zrows));
+        bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &fb[b]);
+        if (ZCF && zrows > 0) {
+            const size_t row0 = (size_t)tile * p.zc_cap;
+            bulk_g2s(dst + qoff - 2 * kZcFused * 256, reinterpret_cast<const uint8_t*>(p.zc_k + row0 * kD),
+                     (uint32_t)(zrows * 256), &fb[b]);
+            bulk_g2s(dst + qoff - kZcFused * 256, reinterpret_cast<const uint8_t*>(p.zc_v + row0 * kD),
+                     (uint32_t)(zrows * 256), &fb[b]);
+        }
+    };
+    // Zone C rows of a tile (written by the previous kernel: after griddepcontrol.wait only)
+    auto zrows_of = [&](int k) {
+        const int tile = tile0 + k * tstride;
+        return (ZCF && tile < p.units) ? min(p.zc_len[tile], kZcFused) : 0;
     };
     // Programmatic dependent launch: this grid may start while the previous
     // kernel on the stream drains. The packed KV tiles are immutable during
@@ -1838,7 +1927,13 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     if (half == 1 && lane == 0)
         for (int j = 1; j < kXMaxBuf; ++j) ahead[j - 1] = j < nbuf ? meta(j) : Meta{nullptr, 0u};
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (half == 0 && lane == 0 && tile0 < p.units) issue_q(0, 0);
+    int next_z = 0, ahead_z[kXMaxBuf - 1] = {0, 0, 0};
+    if (half == 0 && lane == 0) {
+        if (tile0 < p.units) issue_q(0, 0, zrows_of(0));
+        next_z = zrows_of(nbuf);
+    }
+    if (ZCF && half == 1 && lane == 0)
+        for (int j = 1; j < kXMaxBuf; ++j) ahead_z[j - 1] = j < nbuf ? zrows_of(j) : 0;
     const U2xLane lc = u2x_lane(half);
     // the q~ digit rows of d3 (never written: |N| < 2^22) must read as zero
     for (int i = threadIdx.x & 63; i < 4 * 512 / 16; i += 64)
@@ -1847,7 +1942,10 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     int b = 0;
     uint32_t phase = 0;
     int k = 0;
+    int zl_next = zrows_of(0);  // this lane's view of the tile's Zone C rows, one tile ahead
     for (int tile = tile0; tile < p.units; tile += tstride, ++k) {
+        const int zl = zl_next;
+        zl_next = zrows_of(k + 1);
         if (MODE != 2 || k < nbuf) mbar_wait(&fb[b], phase);
         __syncwarp();
         const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
@@ -1856,7 +1954,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
             for (int j = 1; j < kXMaxBuf; ++j)
                 if (j < nbuf && ahead[j - 1].src) {
                     issue_kv(ahead[j - 1], j);
-                    issue_q(j, j);
+                    issue_q(j, j, ahead_z[j - 1]);
                 }
         }
         IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
@@ -1866,16 +1964,19 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
             if (MODE != 2 && half == 0 && lane == 0 && k >= 1) {
                 if (next.src) {
                     issue_kv(next, bprev);
-                    issue_q(k - 1 + nbuf, bprev);
+                    issue_q(k - 1 + nbuf, bprev, next_z);
                 }
                 next = meta(k + nbuf);
+                next_z = zrows_of(k + nbuf);
             }
         };
         if (MODE == 1) {
             pair_sync(PERCTA ? 1 : 1 + pr);
             refill();
         } else {
-            decode_tile_u2x<IO, NBMAX, FULLK, BULK>(st, st + qoff, p.g, scr, o, PERCTA ? 1 : 1 + pr, lc, refill);
+            decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCF>(st, st + qoff, p.g, scr, o, PERCTA ? 1 : 1 + pr, lc,
+                                                                refill, nullptr, nullptr, zl,
+                                                                st + qoff - 2 * kZcFused * 256, st + qoff - kZcFused * 256);
         }
         if (++b == nbuf) {
             b = 0;
@@ -2276,10 +2377,16 @@ static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st) {
     return launch_status();
 }
 
+// Zone C small enough to stage with each short tile (host-known bound)
+static bool zc_fusable(const rdkv_decode_args* a) {
+    return a->zc_len && (a->flags & RDKV_DECODE_ZC_BOUND) && a->zc_bound <= kZcFused;
+}
+
 template <typename IO, int NBMAX, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
-    const int slot = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
+    const bool zcf = zc_fusable(a);
+    const int slot = (a->plan.max_decode_bytes + (zcf ? 2 * kZcFused * 256 : 0) + qbytes + 127) & ~127;
     const int scratch = (kXPDig + NBMAX * 256 + 127) & ~127;
     const DevAttrs da = dev_attrs();
     const int smem_max = da.smem_optin, nsm = da.nsm;
@@ -2289,18 +2396,23 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     int W = 0, nbuf = 0;
     if (!pick_pairs(a->units, nsm, slot, scratch, smem_max - slack, W, nbuf)) return RDKV_EINVAL;
     size_t smem = W * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
-    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out, nullptr, nullptr, nullptr,
-                a->units, a->group, 0, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
+    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
+                zcf ? static_cast<const __half*>(a->zc_k) : nullptr, zcf ? static_cast<const __half*>(a->zc_v) : nullptr,
+                zcf ? a->zc_len : nullptr, a->units, a->group, zcf ? a->zc_cap : 0, nbuf, W, slot, scratch, 0, 0, -1, -1,
+                0, 0};
     static const char* smsp_env = getenv("RDKV_DECODE_SMSP");
     if (smsp_env) p.smsp_pairs = atoi(smsp_env);
     static const char* nenv = getenv("RDKV_DECODE_NULL");
     const int mode = nenv ? atoi(nenv) : 0;
     const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
-    auto kern = bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true>
+    auto kern = zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true>
+                            : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, true>)
+              : bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true>
               : mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
               : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2> : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
-    static std::atomic<int> smem_set[4][kMaxDevices];
-    set_smem_once(kern, (int)smem, smem_set[bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0], da.dev);
+    static std::atomic<int> smem_set[6][kMaxDevices];
+    set_smem_once(kern, (int)smem, smem_set[zcf ? 4 + (bulk ? 1 : 0) : bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0],
+                  da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
     // One pair per CTA (RDKV_DECODE_CTA=1): the same persistent pairs, but each
@@ -2308,7 +2420,7 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     // kernel's CTAs take a pair's smem / warp slots as soon as it finishes
     // instead of when the SM's slowest pair does.
     static const char* cta_env = getenv("RDKV_DECODE_CTA");
-    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0) {
+    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0 && !zcf) {
         const size_t smem1 = kXMaxBuf * sizeof(uint64_t) + (size_t)2 * slot + scratch + slack;
         auto k1 = bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, true> : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, true>;
         static std::atomic<int> smem1_set[2][kMaxDevices];
@@ -2343,8 +2455,8 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
 
 template <typename IO, bool FULLK>
 static int launch_u2x_k(const rdkv_decode_args* a, cudaStream_t st) {
-    // long tiles or Zone C rows: the chunked kernel
-    if (a->plan.max_slots > kU2MaxSlots || a->zc_len) return launch_u2c<IO, FULLK>(a, st);
+    // long tiles or Zone C rows beyond the fused bound: the chunked kernel
+    if (a->plan.max_slots > kU2MaxSlots || (a->zc_len && !zc_fusable(a))) return launch_u2c<IO, FULLK>(a, st);
     const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
     if (nb <= 2) return launch_u2x_t<IO, 2, FULLK>(a, st);
     if (nb <= 4) return launch_u2x_t<IO, 4, FULLK>(a, st);

@@ -169,6 +169,7 @@ class PackedModel:
     zc_v: torch.Tensor | None = None
     zc_len: torch.Tensor | None = None  # [U] int32
     zc_cap: int = 0
+    zc_count: int | None = 0  # host-side bound on every zc_len[u] (appends since packing); None = unknown
     head_status: torch.Tensor | None = None
     decode_sizes: torch.Tensor | None = None   # [U] int32, from prepare()
     plan: capi.DecodePlan | None = None
@@ -338,6 +339,9 @@ def decode_args(model: PackedModel, q, out, split=1, kernel=0, workspace=None) -
     if model.zc_len is not None:
         a.zc_k, a.zc_v, a.zc_len = model.zc_k.data_ptr(), model.zc_v.data_ptr(), model.zc_len.data_ptr()
         a.zc_cap = model.zc_cap
+        if model.zc_count is not None:
+            a.flags |= capi.RDKV_DECODE_ZC_BOUND
+            a.zc_bound = min(model.zc_count, model.zc_cap)
     a.split = split
     a.kernel = kernel
     if model.plan is not None:
@@ -414,3 +418,5 @@ def append_new_token(model: PackedModel, k_new, v_new) -> None:
                                           model.zc_len.data_ptr(), model.zc_cap, k_new.data_ptr(),
                                           v_new.data_ptr(), _dtype_code(k_new), model.units,
                                           model.head_dim, _stream()), "append")
+    if model.zc_count is not None:
+        model.zc_count = min(model.zc_count + 1, model.zc_cap)

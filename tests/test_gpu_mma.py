@@ -16,8 +16,9 @@ pytestmark = pytest.mark.gpu
 D = 128
 FP16_INPUT_TOL = 1e-4
 # uniform-2-bit fast path (csrc/decode_mma.cu u2x): 16-bit softmax weights,
-# ~1e-4 relative on random data (contract: 1e-3)
-U2X_TOL = 5e-4
+# typically 1e-5 .. 3e-4 relative on random data, worst seen 5.4e-4; the
+# contract is 1e-3 (DECODE_TOL in test_gpu_parity.py)
+U2X_TOL = 1e-3
 
 
 def f16r(x):
@@ -262,11 +263,13 @@ def test_mma_uniform_two_bit_long_tiles(cuda, orc, g, fullk, io):
 
 
 @pytest.mark.parametrize("n_max,appends,io", [(150, 1, torch.float16), (150, 17, torch.float32), (600, 40, torch.float16),
-                                              (130, 5, torch.float32)])
+                                              (130, 5, torch.float32), (128, 3, torch.float32), (160, 4, torch.float16),
+                                              (600, 2, torch.float32)])
 def test_mma_uniform_two_bit_zone_c(cuda, orc, n_max, appends, io):
-    """Zone C (appended fp16 K/V rows) on the uniform-2-bit fast path: 16-token
-    fp16 tensor-core chunks folded into the online softmax, after short or
-    chunked long packed tiles."""
+    """Zone C (appended fp16 K/V rows) on the uniform-2-bit fast path: up to 4
+    rows staged with each short tile (fused), more as 16-token fp16
+    tensor-core chunks folded into the online softmax, after short or chunked
+    long packed tiles."""
     rng = np.random.default_rng(80 + appends)
     cases = []
     for n in (3, 64, 100, n_max):
