@@ -281,3 +281,32 @@ def test_mma_uniform_two_bit_zone_c(cuda, orc, n_max, appends, io):
     worst, model = _run_batch(cuda, orc, cases, 4, io=io, appends=appends, rng=rng, tol=U2X_TOL)
     assert model.plan.uniform2 == 2
     assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
+
+
+@pytest.mark.parametrize("appends,known", [(2, True), (6, True), (2, False)])
+def test_host_decode_zero_copy_zone_c(cuda, orc, appends, known):
+    """Zero-copy host decode (TMA bulk stores to mapped host memory) with Zone C
+    rows: fused (host-known bound <= 4) and chunked paths equal the device path."""
+    import ctypes as C
+
+    rng = np.random.default_rng(90 + appends)
+    cases = []
+    for n in (2, 90, 128, 150):
+        k, v, vb, kb, q = _random_case(rng, 400, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(400, n, replace=False))] = 2
+        kb[:] = 2
+        cases.append((k, v, vb, kb, q))
+    _, model = _run_batch(cuda, orc, cases, 4, appends=appends, rng=rng, tol=U2X_TOL)
+    if not known:
+        model.zc_count = None
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).half()
+    want = P.packed_decode_step(model, q).cpu()
+    qd, od = torch.empty_like(q), torch.empty_like(q)
+    a = P.decode_args(model, qd, od)
+    qh = q.cpu().pin_memory()
+    oh = torch.full_like(qh, float("nan")).pin_memory()
+    assert capi.lib().rdkv_cuda_decode_host(C.byref(a), qh.data_ptr(), oh.data_ptr(),
+                                            torch.cuda.current_stream().cuda_stream) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(oh, want)
