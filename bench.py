@@ -408,7 +408,18 @@ def secondary_configs(P, spec0, model, q, args):
                                        "Zone C grows 1..16 rows per tile (L2-warm: the step re-reads one arena)",
                              "us_per_token_step": us, "tok_s": spec0.batch / (us / 1e6)}
     model.zc_cap, model.zc_k, model.zc_v, model.zc_len = 0, None, None, None
-    # (3) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
+    # (3) batch sweep (configs[2] is "batch 1-16"): the first b sequences of the
+    # packed arena (a prefix of the units), same timing method
+    sweep = {}
+    for b in (1, 2, 4, 8):
+        ub = b * spec0.layers * spec0.kv_heads
+        sub = P.PackedModel(model.arena, model.offsets[: ub + 1], model.offsets_host[: ub + 1], ub, model.group,
+                            model.head_dim)
+        sub.prepare()
+        us, _ = graph_step_us(P, sub, q[:ub].contiguous(), min(args.steps, 100))
+        sweep[str(b)] = {"us_per_step": us, "tok_s": b / (us / 1e6)}
+    out["batch_sweep"] = sweep
+    # (4) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
     spec = WorkloadSpec(batch=spec0.batch, layers=spec0.layers, ctx=spec0.ctx, n_tokens=512, seed=3)
     m2, _, st2, _ = build(spec)
     q2 = P.generate((m2.units, spec.group, d), torch.float16, seed=QSEED, tensor=2)
