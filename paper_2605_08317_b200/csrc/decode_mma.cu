@@ -1461,6 +1461,8 @@ struct U2xRun {
 // fp16 m16n8k16 MMA (rows = the z tokens), PV on CUDA cores in the lanes'
 // output mapping, one shared softmax.
 constexpr int kZcFused = 4;
+constexpr int kZcKStride = 272;                        // padded K-row stride: conflict-free ldmatrix
+constexpr int kZcStage = kZcFused * (kZcKStride + 256);  // fused Zone C staging bytes (K rows + V rows)
 template <typename IO, int NBMAX, bool FULLK, bool BULK, bool CHUNKED = false, bool ZCF = false, typename AfterSync1>
 __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
                                                 uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
@@ -1752,7 +1754,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             // QK: A rows = Zone C tokens (rows >= z read neighbouring bytes, masked
             // below), B columns 2h / 2h + 1 = hi / lo fp16 parts of q_h
             float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-            const uint8_t* abase = zk + (L.lane & 15) * 256 + (L.lane >> 4) * 16;
+            const uint8_t* abase = zk + (L.lane & 15) * kZcKStride + (L.lane >> 4) * 16;
             const int bh = gid >> 1;
             const IO* qb = reinterpret_cast<const IO*>(qs + (bh < g ? bh : 0) * QROW);
             const bool bzero = bh >= g || (sizeof(IO) == 2 && (gid & 1));
@@ -1898,8 +1900,9 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &fb[b]);
         if (ZCF && zrows > 0) {
             const size_t row0 = (size_t)tile * p.zc_cap;
-            bulk_g2s(dst + qoff - 2 * kZcFused * 256, reinterpret_cast<const uint8_t*>(p.zc_k + row0 * kD),
-                     (uint32_t)(zrows * 256), &fb[b]);
+            for (int r = 0; r < zrows; ++r)  // K rows at a padded stride
+                bulk_g2s(dst + qoff - kZcStage + r * kZcKStride,
+                         reinterpret_cast<const uint8_t*>(p.zc_k + (row0 + r) * kD), 256u, &fb[b]);
             bulk_g2s(dst + qoff - kZcFused * 256, reinterpret_cast<const uint8_t*>(p.zc_v + row0 * kD),
                      (uint32_t)(zrows * 256), &fb[b]);
         }
@@ -1976,7 +1979,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         } else {
             decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCF>(st, st + qoff, p.g, scr, o, PERCTA ? 1 : 1 + pr, lc,
                                                                 refill, nullptr, nullptr, zl,
-                                                                st + qoff - 2 * kZcFused * 256, st + qoff - kZcFused * 256);
+                                                                st + qoff - kZcStage, st + qoff - kZcFused * 256);
         }
         if (++b == nbuf) {
             b = 0;
@@ -2386,7 +2389,7 @@ template <typename IO, int NBMAX, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
     const bool zcf = zc_fusable(a);
-    const int slot = (a->plan.max_decode_bytes + (zcf ? 2 * kZcFused * 256 : 0) + qbytes + 127) & ~127;
+    const int slot = (a->plan.max_decode_bytes + (zcf ? kZcStage : 0) + qbytes + 127) & ~127;
     const int scratch = (kXPDig + NBMAX * 256 + 127) & ~127;
     const DevAttrs da = dev_attrs();
     const int smem_max = da.smem_optin, nsm = da.nsm;
