@@ -2074,14 +2074,14 @@ __device__ __forceinline__ void zc_chunk_u2x(const uint8_t* __restrict__ st, int
     const bool hv = tig < g;
     pair_sync(bar);  // both warps are past the previous item: its buffer may be refilled
     after_sync1();
-    uint8_t* vrows = const_cast<uint8_t*>(st) + kZcChunk * 256;
-    uint8_t* aux = const_cast<uint8_t*>(st) + 2 * kZcChunk * 256 + half * kZcAuxWarp;  // this warp's spare
+    uint8_t* vrows = const_cast<uint8_t*>(st) + kZcChunk * kZcKStride;
+    uint8_t* aux = const_cast<uint8_t*>(st) + 2 * kZcChunk * kZcKStride + half * kZcAuxWarp;  // this warp's spare
     // rows past cnt hold stale bytes: zero this warp's channel half of the V rows
     for (int r = cnt + (lane >> 3); r < kZcChunk; r += 4)
-        *reinterpret_cast<uint4*>(vrows + r * 256 + 128 * half + 16 * (lane & 7)) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(vrows + r * kZcKStride + 128 * half + 16 * (lane & 7)) = make_uint4(0u, 0u, 0u, 0u);
     // ---- QK (every warp, all 16 tokens): A = K rows, B = q table
     float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    const uint8_t* abase = st + (lane & 15) * 256 + (lane >> 4) * 16;
+    const uint8_t* abase = st + (lane & 15) * kZcKStride + (lane >> 4) * 16;
     const uint8_t* bbase = q16 + (lane & 7) * kQ16Row + ((lane >> 3) & 1) * 16;
 #pragma unroll
     for (int ks = 0; ks < kD / 16; ++ks) {
@@ -2114,7 +2114,8 @@ __device__ __forceinline__ void zc_chunk_u2x(const uint8_t* __restrict__ st, int
     ldsm_x2(bp, aux + (lane & 7) * 32 + ((lane >> 3) & 1) * 16);
     // ---- PV: this warp's channels 64 half .. + 63 as 4 m-tiles (A = V^T via ldmatrix.trans)
     float* xo = reinterpret_cast<float*>(aux + 256);  // [4 heads][64 channels]
-    const uint8_t* vbase = vrows + ((lane & 7) + 8 * ((lane >> 4) & 1)) * 256 + (64 * half + 8 * ((lane >> 3) & 1)) * 2;
+    const uint8_t* vbase =
+        vrows + ((lane & 7) + 8 * ((lane >> 4) & 1)) * kZcKStride + (64 * half + 8 * ((lane >> 3) & 1)) * 2;
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
         uint32_t a[4];
@@ -2230,9 +2231,12 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
             const size_t row0 = (size_t)cur_tile * p.zc_cap + (size_t)kZcChunk * j;
             fence_proxy_async();
             mbar_expect_tx(&fb[b], (uint32_t)(2 * rows * 256));
-            bulk_g2s(dst, reinterpret_cast<const uint8_t*>(p.zc_k + row0 * kD), (uint32_t)(rows * 256), &fb[b]);
-            bulk_g2s(dst + kZcChunk * 256, reinterpret_cast<const uint8_t*>(p.zc_v + row0 * kD), (uint32_t)(rows * 256),
-                     &fb[b]);
+            // one copy per row into padded (272-B) rows: conflict-free ldmatrix
+            for (int r = 0; r < rows; ++r) {
+                bulk_g2s(dst + r * kZcKStride, reinterpret_cast<const uint8_t*>(p.zc_k + (row0 + r) * kD), 256u, &fb[b]);
+                bulk_g2s(dst + (kZcChunk + r) * kZcKStride, reinterpret_cast<const uint8_t*>(p.zc_v + (row0 + r) * kD),
+                         256u, &fb[b]);
+            }
         } else {
             const int rows = ns >> 2, Q = cur.nslot >> 2;
             const uint32_t kbytes = (uint32_t)(rows * cur.krb), vbytes = (uint32_t)(rows * 128),
@@ -2345,7 +2349,7 @@ static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st) {
     // Zone C chunk: 16 K + 16 V rows + 8 KB of spare), q rows at the end
     const int cslots = a->plan.max_slots < kU2MaxSlots ? ((a->plan.max_slots + 3) & ~3) : kU2MaxSlots;
     int body = 10 * kD + cslots * (32 + 32 + 8);
-    const int zbody = 2 * kZcChunk * 256 + 2 * kZcAuxWarp;  // Zone C chunk: K + V rows + both warps' spare
+    const int zbody = 2 * kZcChunk * kZcKStride + 2 * kZcAuxWarp;  // Zone C chunk: K + V rows + both warps' spare
     const int slot = ((zc && zbody > kHeaderBytes + body ? zbody : kHeaderBytes + body) + qbytes + 127) & ~127;
     const int scratch = (kXPDig + kXNbMax * 256 + (zc ? kQ16Bytes : 0) + 127) & ~127;
     const DevAttrs da = dev_attrs();
