@@ -320,7 +320,7 @@ def graph_step_us(P, model, q, steps, kernel=0):
         m = P.PackedModel(model.arena if r == 0 else model.arena.clone(), model.offsets, model.offsets_host,
                           model.units, model.group, model.head_dim, model.zc_k, model.zc_v, model.zc_len, model.zc_cap,
                           model.zc_count)
-        m.decode_sizes, m.plan = model.decode_sizes, model.plan
+        m.share_plan(model)
         rot.append((m, q if r == 0 else q.clone(), torch.empty_like(q)))
     for i in range(3):
         m, qq, oo = rot[i % n_rot]
@@ -474,7 +474,7 @@ def main():
     for r in range(1, n_rot):
         m = P.PackedModel(model.arena.clone(), model.offsets, model.offsets_host, U, g, d,
                           model.zc_k, model.zc_v, model.zc_len, model.zc_cap, model.zc_count)
-        m.decode_sizes, m.plan = model.decode_sizes, model.plan
+        m.share_plan(model)
         rot.append((m, q.clone(), torch.empty_like(out)))
 
     def step(i):
@@ -632,7 +632,8 @@ def main():
                         for h in range(spec.kv_heads))
             q0 = torch.from_numpy(info["q"][0].reshape(spec.kv_heads, g, d)).cuda().half()
             sub = P.PackedModel(model.arena, model.offsets, model.offsets_host, spec.kv_heads, g, d)
-            sub.decode_sizes, sub.plan = model.decode_sizes, model.plan
+            sub.share_plan(model)
+            sub.unit_ids = None  # a prefix of the units: no split lists
             o0 = P.packed_decode_step(sub, q0).float().cpu().numpy().reshape(-1, d)
             want = info["out"][0]
             err = float(max(np.linalg.norm(o0[j] - want[j]) / np.linalg.norm(want[j]) for j in range(len(want))))

@@ -132,6 +132,8 @@ typedef struct {
     int32_t max_zone_b_rows;  /* largest Zone B (16-bit V) row count */
     int32_t max_kq_slots;     /* largest quantised-K slot count */
     int32_t uniform2;         /* every tile: all kept V rows and K channels at 2 bits (2: and all d K channels kept) */
+    int32_t n_uniform;        /* rdkv_cuda_decode_prepare_split: tiles of the uniform class (listed first in unit_ids) */
+    int32_t uniform2_split;   /* the uniform2 value of that subset */
 } rdkv_decode_plan;
 
 /* rdkv_decode_args.flags: `out` lives in mapped host memory — the tensor-core
@@ -167,6 +169,7 @@ typedef struct {
     rdkv_decode_plan plan;
     int32_t zc_bound;   /* with RDKV_DECODE_ZC_BOUND: max over units of zc_len[u] */
     int32_t reserved2;
+    const int32_t* unit_ids; /* [units] device, from rdkv_cuda_decode_prepare_split (NULL: no split) */
 } rdkv_decode_args;
 
 /* One-time scan of a packed arena: writes the per-tile decode sizes
@@ -174,6 +177,15 @@ typedef struct {
 RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int64_t* tile_offsets_host,
                                       int32_t units, int32_t* tile_decode_bytes,
                                       rdkv_decode_plan* plan, void* stream);
+/* Same, and also writes unit_ids [units] (device): the units whose tiles are
+ * uniform 2-bit (every kept V row and K channel at 2 bits, <= 160 slots)
+ * first, then the rest (plan->n_uniform, plan->uniform2_split). With
+ * rdkv_decode_args.unit_ids set, a step over a mixed arena runs the mixed
+ * tiles on the general tensor-core body and the uniform ones on the fast
+ * uniform-2-bit kernel (two launches) instead of everything on the former. */
+RDKV_API int rdkv_cuda_decode_prepare_split(const uint8_t* arena, const int64_t* tile_offsets_host,
+                                            int32_t units, int32_t* tile_decode_bytes, int32_t* unit_ids,
+                                            rdkv_decode_plan* plan, void* stream);
 
 RDKV_API size_t rdkv_cuda_decode_workspace(int32_t units, int32_t group, int32_t head_dim,
                                            int32_t split);

@@ -80,7 +80,8 @@ HEAD_STATS_BYTES = C.sizeof(HeadStats)
 
 class DecodePlan(C.Structure):
     _fields_ = [("max_decode_bytes", C.c_int32), ("max_slots", C.c_int32),
-                ("max_zone_b_rows", C.c_int32), ("max_kq_slots", C.c_int32), ("uniform2", C.c_int32)]
+                ("max_zone_b_rows", C.c_int32), ("max_kq_slots", C.c_int32), ("uniform2", C.c_int32),
+                ("n_uniform", C.c_int32), ("uniform2_split", C.c_int32)]
 
 
 class DecodeArgs(C.Structure):
@@ -91,7 +92,7 @@ class DecodeArgs(C.Structure):
         ("zc_len", C.c_void_p), ("zc_cap", C.c_int32), ("split", C.c_int32),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t), ("kernel", C.c_int32),
         ("flags", C.c_int32), ("tile_decode_bytes", C.c_void_p), ("plan", DecodePlan),
-        ("zc_bound", C.c_int32), ("reserved2", C.c_int32),
+        ("zc_bound", C.c_int32), ("reserved2", C.c_int32), ("unit_ids", C.c_void_p),
     ]
 
 
@@ -119,6 +120,7 @@ _SIGS = {
     "rdkv_cuda_decode_workspace": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "rdkv_cuda_decode": (C.c_int, [C.POINTER(DecodeArgs), _VP]),
     "rdkv_cuda_decode_prepare": (C.c_int, [_VP, _VP, C.c_int32, _VP, C.POINTER(DecodePlan), _VP]),
+    "rdkv_cuda_decode_prepare_split": (C.c_int, [_VP, _VP, C.c_int32, _VP, _VP, C.POINTER(DecodePlan), _VP]),
     "rdkv_cuda_decode_host": (C.c_int, [C.POINTER(DecodeArgs), _VP, _VP, _VP]),
     "rdkv_cuda_decode_ctx_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "rdkv_cuda_decode_ctx_destroy": (C.c_int, [C.c_void_p]),

@@ -161,7 +161,9 @@ struct MmaParams {
     int off_p16, off_zl;    // -1 when unused
     int max_r16;
     int smsp_pairs;  // u2x: a pair's two warps on one SM sub-partition
+    const int32_t* ids;  // launch tile -> unit (NULL: identity), a split step's subset
 };
+__device__ __forceinline__ int unit_of(const MmaParams& p, int tile) { return p.ids ? p.ids[tile] : tile; }
 
 // Per-warp scratch: [ScratchHead][B digits][lg / acc][p16][zl]
 struct ScratchHead {
@@ -802,6 +804,7 @@ __device__ __noinline__ void decode_tile_u2(const uint8_t* __restrict__ t, const
 template <int NT, typename IO, bool U2>
 __global__ void __launch_bounds__(32 * (kMaxW + 1), 1) decode_mma_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
     uint64_t* empty = full + kMaxR;
     uint8_t* ring = dsm + 2 * kMaxR * sizeof(uint64_t);  // 512 B, 128-aligned
@@ -823,26 +826,28 @@ __global__ void __launch_bounds__(32 * (kMaxW + 1), 1) decode_mma_kernel(const M
             const int mj = base + lane;
             int64_t moff = 0;
             int msz = 0;
+            int munit = 0;
             if (mj < ntiles) {
                 const int tile = blockIdx.x + mj * gridDim.x;
-                moff = p.offsets[tile];
-                msz = p.dsize[tile];
+                munit = unit_of(p, tile);
+                moff = p.offsets[munit];
+                msz = p.dsize[munit];
             }
             const int cnt = min(32, ntiles - base);
             for (int k = 0; k < cnt; ++k) {
                 const int64_t off = __shfl_sync(0xffffffffu, moff, k);
                 const int sz = __shfl_sync(0xffffffffu, msz, k);
+                const int unit = __shfl_sync(0xffffffffu, munit, k);
                 if (lane == 0) {
                     const int j = base + k;
                     const int slot = j % p.R, use = j / p.R;
                     if (use > 0) mbar_wait(&empty[slot], (uint32_t)((use - 1) & 1));
                     fence_proxy_async();
                     uint8_t* dst = ring + (size_t)slot * p.slot_bytes;
-                    const int tile = blockIdx.x + j * gridDim.x;
                     mbar_expect_tx(&full[slot], (uint32_t)(sz + qbytes));
                     bulk_g2s(dst, p.arena + off, (uint32_t)sz, &full[slot]);
                     bulk_g2s(dst + p.slot_bytes - qbytes,
-                             static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &full[slot]);
+                             static_cast<const uint8_t*>(p.q) + (size_t)unit * qbytes, (uint32_t)qbytes, &full[slot]);
                 }
                 __syncwarp();
             }
@@ -856,7 +861,7 @@ __global__ void __launch_bounds__(32 * (kMaxW + 1), 1) decode_mma_kernel(const M
         const int slot = j % p.R, use = j / p.R;
         mbar_wait(&full[slot], (uint32_t)(use & 1));
         const uint8_t* st = ring + (size_t)slot * p.slot_bytes;
-        const int tile = blockIdx.x + j * gridDim.x;
+        const int tile = unit_of(p, blockIdx.x + j * gridDim.x);  // the unit this tile belongs to
         const IO* qs = reinterpret_cast<const IO*>(st + p.slot_bytes - qbytes);
         const int nzc = p.zc_len ? min(p.zc_len[tile], p.zc_cap) : 0;
         if constexpr (U2) {
@@ -1174,26 +1179,28 @@ __global__ void __launch_bounds__(32 * (2 * kPairs + 1), 1) decode_u2_pair_kerne
             const int mj = base + lane;
             int64_t moff = 0;
             int msz = 0;
+            int munit = 0;
             if (mj < ntiles) {
                 const int tile = blockIdx.x + mj * gridDim.x;
-                moff = p.offsets[tile];
-                msz = p.dsize[tile];
+                munit = unit_of(p, tile);
+                moff = p.offsets[munit];
+                msz = p.dsize[munit];
             }
             const int cnt = min(32, ntiles - base);
             for (int k = 0; k < cnt; ++k) {
                 const int64_t off = __shfl_sync(0xffffffffu, moff, k);
                 const int sz = __shfl_sync(0xffffffffu, msz, k);
+                const int unit = __shfl_sync(0xffffffffu, munit, k);
                 if (lane == 0) {
                     const int j = base + k;
                     const int slot = j % p.R, use = j / p.R;
                     if (use > 0) mbar_wait(&empty[slot], (uint32_t)((use - 1) & 1));
                     fence_proxy_async();
                     uint8_t* dst = ring + (size_t)slot * p.slot_bytes;
-                    const int tile = blockIdx.x + j * gridDim.x;
                     mbar_expect_tx(&full[slot], (uint32_t)(sz + qbytes));
                     bulk_g2s(dst, p.arena + off, (uint32_t)sz, &full[slot]);
                     bulk_g2s(dst + p.slot_bytes - qbytes,
-                             static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &full[slot]);
+                             static_cast<const uint8_t*>(p.q) + (size_t)unit * qbytes, (uint32_t)qbytes, &full[slot]);
                 }
                 __syncwarp();
             }
@@ -1880,8 +1887,9 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         const int tile = tile0 + k * tstride;
         Meta m{nullptr, 0u};
         if (tile < p.units) {
-            m.src = p.arena + p.offsets[tile];
-            m.sz = (uint32_t)p.dsize[tile];
+            const int u = unit_of(p, tile);
+            m.src = p.arena + p.offsets[u];
+            m.sz = (uint32_t)p.dsize[u];
         }
         return m;
     };
@@ -1894,7 +1902,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         bulk_g2s(pbuf + (size_t)b * p.slot_bytes, m.src, m.sz, &fb[b]);
     };
     auto issue_q = [&](int k, int b, int zrows) {
-        const int tile = tile0 + k * tstride;
+        const int tile = unit_of(p, tile0 + k * tstride);
         uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
         mbar_expect_tx(&fb[b], (uint32_t)(qbytes + 2 * 256 * zrows));
         bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &fb[b]);
@@ -1910,7 +1918,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     // Zone C rows of a tile (written by the previous kernel: after griddepcontrol.wait only)
     auto zrows_of = [&](int k) {
         const int tile = tile0 + k * tstride;
-        return (ZCF && tile < p.units) ? min(p.zc_len[tile], kZcFused) : 0;
+        return (ZCF && tile < p.units) ? min(p.zc_len[unit_of(p, tile)], kZcFused) : 0;
     };
     // Programmatic dependent launch: this grid may start while the previous
     // kernel on the stream drains. The packed KV tiles are immutable during
@@ -1960,7 +1968,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
                     issue_q(j, j, ahead_z[j - 1]);
                 }
         }
-        IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
+        IO* o = static_cast<IO*>(p.out) + (size_t)unit_of(p, tile) * p.g * kD;
         const int bprev = b == 0 ? nbuf - 1 : b - 1;
         // the buffer of tile k - 1 takes tile k - 1 + nbuf
         auto refill = [&]() {
@@ -2406,7 +2414,7 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
                 zcf ? static_cast<const __half*>(a->zc_k) : nullptr, zcf ? static_cast<const __half*>(a->zc_v) : nullptr,
                 zcf ? a->zc_len : nullptr, a->units, a->group, zcf ? a->zc_cap : 0, nbuf, W, slot, scratch, 0, 0, -1, -1,
-                0, 0};
+                0, 0, a->unit_ids};
     static const char* smsp_env = getenv("RDKV_DECODE_SMSP");
     if (smsp_env) p.smsp_pairs = atoi(smsp_env);
     static const char* nenv = getenv("RDKV_DECODE_NULL");
@@ -2536,7 +2544,8 @@ static int launch_t(const rdkv_decode_args* a, cudaStream_t st) {
     const size_t smem = head + (size_t)R * slot + (size_t)W * scratch + slack;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
                 static_cast<const __half*>(a->zc_k), static_cast<const __half*>(a->zc_v), a->zc_len,
-                a->units, a->group, a->zc_cap, R, W, slot, scratch, off_lg, lg_stride, off_p16, off_zl, max_r16};
+                a->units, a->group, a->zc_cap, R, W, slot, scratch, off_lg, lg_stride, off_p16, off_zl, max_r16, 0,
+                a->unit_ids};
     auto kern = decode_mma_kernel<NT, IO, U2>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = (a->units + W - 1) / W;
@@ -2547,6 +2556,27 @@ static int launch_t(const rdkv_decode_args* a, cudaStream_t st) {
 
 int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     const bool f16 = a->io_dtype == RDKV_F16;
+    // split step (rdkv_cuda_decode_prepare_split): mixed tiles on the general
+    // body, then the uniform-2-bit ones on u2x (PDL: its prologue and KV
+    // prefetch overlap the general kernel's tail)
+    const rdkv_decode_plan& pl = a->plan;
+    if (a->unit_ids && !pl.uniform2 && pl.n_uniform > 0 && pl.n_uniform < a->units && a->group <= 4 &&
+        a->kernel == 0 && (!a->zc_len || zc_fusable(a))) {
+        rdkv_decode_args gm = *a;
+        gm.units = a->units - pl.n_uniform;
+        gm.unit_ids = a->unit_ids + pl.n_uniform;
+        const int rc = a->group <= 4 ? (f16 ? launch_t<1, __half, false>(&gm, st) : launch_t<1, float, false>(&gm, st))
+                                     : (f16 ? launch_t<2, __half, false>(&gm, st) : launch_t<2, float, false>(&gm, st));
+        if (rc) return rc;
+        rdkv_decode_args um = *a;
+        um.units = pl.n_uniform;
+        um.plan.uniform2 = pl.uniform2_split;
+        return f16 ? launch_u2x<__half>(&um, st) : launch_u2x<float>(&um, st);
+    }
+    // not split: every launch walks the units in order (unit_ids only name subsets)
+    rdkv_decode_args plain = *a;
+    plain.unit_ids = nullptr;
+    a = &plain;
     // uniform 2-bit tiles (the n=128 production shape) take the specialised body
     // uniform 2-bit tiles (the n=128 production shape): warp-pair body by default,
     // kernel 4 selects the one-warp body, kernel 3 the general body
@@ -2565,9 +2595,27 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
 // Scans every tile header once (one small D2H copy per tile) and writes the
 // per-tile decode sizes the persistent kernel stages with cp.async.bulk, plus
 // the maxima that select the kernel variant and size its smem ring.
+static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets_host, int32_t units,
+                               int32_t* decode_bytes_dev, int32_t* unit_ids_dev, rdkv_decode_plan* plan,
+                               void* stream);
+
 extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int64_t* tile_offsets_host,
                                                  int32_t units, int32_t* decode_bytes_dev,
                                                  rdkv_decode_plan* plan, void* stream) {
+    return decode_prepare_impl(arena, tile_offsets_host, units, decode_bytes_dev, nullptr, plan, stream);
+}
+
+extern "C" RDKV_API int rdkv_cuda_decode_prepare_split(const uint8_t* arena, const int64_t* tile_offsets_host,
+                                                       int32_t units, int32_t* decode_bytes_dev,
+                                                       int32_t* unit_ids_dev, rdkv_decode_plan* plan,
+                                                       void* stream) {
+    if (!unit_ids_dev) return RDKV_EINVAL;
+    return decode_prepare_impl(arena, tile_offsets_host, units, decode_bytes_dev, unit_ids_dev, plan, stream);
+}
+
+static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets_host, int32_t units,
+                               int32_t* decode_bytes_dev, int32_t* unit_ids_dev, rdkv_decode_plan* plan,
+                               void* stream) {
     if (!arena || !tile_offsets_host || !decode_bytes_dev || !plan || units < 1) return RDKV_EINVAL;
     auto st = static_cast<cudaStream_t>(stream);
     TileHeader* hdrs = static_cast<TileHeader*>(malloc(sizeof(TileHeader) * (size_t)units));
@@ -2576,7 +2624,9 @@ extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int
     for (int u = 0; u < units; ++u)
         cudaMemcpyAsync(&hdrs[u], arena + tile_offsets_host[u], sizeof(TileHeader), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) rc = RDKV_ECUDA;
-    rdkv_decode_plan p{0, 0, 0, 0, 2};
+    rdkv_decode_plan p{0, 0, 0, 0, 2, 0, 2};
+    int32_t* ids = unit_ids_dev ? static_cast<int32_t*>(malloc(sizeof(int32_t) * (size_t)units)) : nullptr;
+    int nmixed = 0;
     for (int u = 0; u < units && rc == RDKV_OK; ++u) {
         const TileHeader& h = hdrs[u];
         if (h.magic != kTileMagic) {
@@ -2592,15 +2642,34 @@ extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int
                         h.c[3] == 0 && h.r[0] > 0 && h.c[0] > 0;
         if (!u2) p.uniform2 = 0;
         else if (h.c[0] != kD && p.uniform2 == 2) p.uniform2 = 1;
+        if (ids) {  // split lists: short uniform tiles first (in order), the rest from the back
+            if (u2 && h.nslot <= kU2MaxSlots) {
+                ids[p.n_uniform++] = u;
+                if (h.c[0] != kD) p.uniform2_split = 1;
+            } else {
+                ids[units - 1 - nmixed++] = u;
+            }
+        }
+    }
+    if (ids) {  // the mixed tail back in unit order
+        for (int i = p.n_uniform, j = units - 1; i < j; ++i, --j) {
+            const int32_t t = ids[i];
+            ids[i] = ids[j];
+            ids[j] = t;
+        }
+        if (p.n_uniform == 0) p.uniform2_split = 0;
     }
     if (rc == RDKV_OK) {
         if (cudaMemcpyAsync(decode_bytes_dev, ds, sizeof(int32_t) * (size_t)units, cudaMemcpyHostToDevice, st) !=
                 cudaSuccess ||
+            (ids && cudaMemcpyAsync(unit_ids_dev, ids, sizeof(int32_t) * (size_t)units, cudaMemcpyHostToDevice, st) !=
+                        cudaSuccess) ||
             cudaStreamSynchronize(st) != cudaSuccess)
             rc = RDKV_ECUDA;
         *plan = p;
     }
     free(hdrs);
     free(ds);
+    free(ids);
     return rc;
 }

@@ -173,18 +173,25 @@ class PackedModel:
     head_status: torch.Tensor | None = None
     decode_sizes: torch.Tensor | None = None   # [U] int32, from prepare()
     plan: capi.DecodePlan | None = None
+    unit_ids: torch.Tensor | None = None       # [U] int32: uniform-2-bit tiles first (split dispatch)
     _infos: list = field(default_factory=list)
 
     def prepare(self) -> capi.DecodePlan:
         """One-time tile scan enabling the tensor-core decode (rdkv_cuda_decode_prepare)."""
         offs = np.ascontiguousarray(self.offsets_host, np.int64)
         self.decode_sizes = torch.empty(self.units, dtype=torch.int32, device=self.arena.device)
+        self.unit_ids = torch.empty(self.units, dtype=torch.int32, device=self.arena.device)
         plan = capi.DecodePlan()
-        raise_for(capi.lib().rdkv_cuda_decode_prepare(self.arena.data_ptr(), offs.ctypes.data, self.units,
-                                                      self.decode_sizes.data_ptr(), C.byref(plan),
-                                                      _stream()), "decode_prepare")
+        raise_for(capi.lib().rdkv_cuda_decode_prepare_split(self.arena.data_ptr(), offs.ctypes.data, self.units,
+                                                            self.decode_sizes.data_ptr(), self.unit_ids.data_ptr(),
+                                                            C.byref(plan), _stream()), "decode_prepare")
         self.plan = plan
         return plan
+
+    def share_plan(self, other: "PackedModel") -> "PackedModel":
+        """Reuse another model's prepare() results (same tiles, e.g. an arena copy)."""
+        self.decode_sizes, self.plan, self.unit_ids = other.decode_sizes, other.plan, other.unit_ids
+        return self
 
     @property
     def arena_bytes(self) -> int:
@@ -347,6 +354,8 @@ def decode_args(model: PackedModel, q, out, split=1, kernel=0, workspace=None) -
     if model.plan is not None:
         a.tile_decode_bytes = model.decode_sizes.data_ptr()
         a.plan = model.plan
+        if model.unit_ids is not None:
+            a.unit_ids = model.unit_ids.data_ptr()
     if workspace is not None:
         a.workspace, a.workspace_bytes = workspace.data_ptr(), workspace.numel()
     return a

@@ -14,7 +14,7 @@ models, qs, outs = [], [], []
 for r in range(NR):
     a = model.arena.clone()
     m = P.PackedModel(a, model.offsets, model.offsets_host, U, g, d)
-    m.decode_sizes, m.plan = model.decode_sizes, model.plan
+    m.share_plan(model)
     models.append(m)
     qs.append(P.generate((U, g, d), torch.float16, seed=0xD15C0 + r, tensor=2))
     outs.append(torch.empty_like(qs[-1]))

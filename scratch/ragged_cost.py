@@ -22,7 +22,7 @@ for counts in [[int(x) for x in c.split("+")] for c in os.environ.get("COUNTS", 
     rot = [(model.arena.clone(), q.clone(), torch.empty_like(q)) for _ in range(NR)]
     ms = []
     for a, qq, oo in rot:
-        m = P.PackedModel(a, model.offsets, model.offsets_host, U, 4, D); m.decode_sizes, m.plan = model.decode_sizes, model.plan
+        m = P.PackedModel(a, model.offsets, model.offsets_host, U, 4, D); m.share_plan(model)
         ms.append((m, qq, oo))
     s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):

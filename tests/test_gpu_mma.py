@@ -310,3 +310,32 @@ def test_host_decode_zero_copy_zone_c(cuda, orc, appends, known):
                                             torch.cuda.current_stream().cuda_stream) == 0
     torch.cuda.synchronize()
     assert torch.equal(oh, want)
+
+
+@pytest.mark.parametrize("io", [torch.float16, torch.float32])
+def test_split_dispatch_mixed_arena(cuda, orc, io):
+    """An arena of mostly uniform-2-bit tiles plus a few mixed ones (the heavy-
+    hitter shape): the split step (mixed tiles on the general body, uniform ones
+    on u2x through unit_ids) equals the all-general step and the oracle."""
+    rng = np.random.default_rng(123)
+    cases = []
+    for i in range(40):
+        k, v, vb, kb, q = _random_case(rng, 300, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(300, int(rng.integers(100, 150)), replace=False))] = 2
+        kb[:] = 2
+        if i % 7 == 3:  # a few 4-bit rows / channels
+            vb[np.nonzero(vb)[0][:3]] = 4
+            kb[rng.choice(D, 3, replace=False)] = 4
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, 4, io=io)
+    plan = model.plan
+    assert plan.uniform2 == 0 and 0 < plan.n_uniform < len(cases)
+    assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).to(io)
+    split = P.packed_decode_step(model, q)
+    ids, model.unit_ids = model.unit_ids, None
+    general = P.packed_decode_step(model, q)
+    model.unit_ids = ids
+    err = (split.float() - general.float()).norm(dim=-1) / general.float().norm(dim=-1)
+    assert float(err.max()) < (2 * U2X_TOL if io == torch.float32 else 2e-3)
