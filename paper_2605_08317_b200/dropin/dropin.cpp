@@ -513,15 +513,16 @@ std::vector<__half> to_half(const float* x, std::size_t n) {
 
 // One decode launch over device tiles.
 struct DecodeState {
-    DevBuf arena, offsets, decode_sizes, zc_k, zc_v, zc_len;
+    DevBuf arena, offsets, decode_sizes, unit_ids, zc_k, zc_v, zc_len;
     std::vector<int64_t> offsets_host;
     rdkv_decode_plan plan{};
     int units = 0, zc_cap = 0;
 
     void prepare() {
         decode_sizes = DevBuf(units * sizeof(int32_t));
-        check(rdkv_cuda_decode_prepare(arena.as<uint8_t>(), offsets_host.data(), units, decode_sizes.as<int32_t>(),
-                                       &plan, nullptr),
+        unit_ids = DevBuf(units * sizeof(int32_t));
+        check(rdkv_cuda_decode_prepare_split(arena.as<uint8_t>(), offsets_host.data(), units,
+                                             decode_sizes.as<int32_t>(), unit_ids.as<int32_t>(), &plan, nullptr),
               "decode prepare");
         sync();
     }
@@ -546,6 +547,7 @@ struct DecodeState {
         a.kernel = 0;
         a.tile_decode_bytes = decode_sizes.as<int32_t>();
         a.plan = plan;
+        a.unit_ids = unit_ids.as<int32_t>();
         check(rdkv_cuda_decode(&a, nullptr), "packed_decode_step");
         sync();
     }
