@@ -162,6 +162,7 @@ struct MmaParams {
     int max_r16;
     int smsp_pairs;  // u2x: a pair's two warps on one SM sub-partition
     const int32_t* ids;  // launch tile -> unit (NULL: identity), a split step's subset
+    int concurrent;      // u2x of a split step: runs beside the general kernel (see launch_mma)
 };
 __device__ __forceinline__ int unit_of(const MmaParams& p, int tile) { return p.ids ? p.ids[tile] : tile; }
 
@@ -1937,7 +1938,11 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     }
     if (half == 1 && lane == 0)
         for (int j = 1; j < kXMaxBuf; ++j) ahead[j - 1] = j < nbuf ? meta(j) : Meta{nullptr, 0u};
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // concurrent (split step): the predecessor is the general kernel, which only
+    // triggers this launch after its own grid dependency resolved, so q is
+    // ready now; this grid waits for it at exit instead, so kernels after this
+    // one still see both halves of the step done
+    if (!p.concurrent) asm volatile("griddepcontrol.wait;" ::: "memory");
     int next_z = 0, ahead_z[kXMaxBuf - 1] = {0, 0, 0};
     if (half == 0 && lane == 0) {
         if (tile0 < p.units) issue_q(0, 0, zrows_of(0));
@@ -1994,6 +1999,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
             phase ^= 1u;
         }
     }
+    if (p.concurrent && threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (BULK && lane == 0) bulk_wait0();
 }
 
@@ -2398,7 +2404,7 @@ static bool zc_fusable(const rdkv_decode_args* a) {
 }
 
 template <typename IO, int NBMAX, bool FULLK>
-static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
+static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_blocks = 0) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
     const bool zcf = zc_fusable(a);
     const int slot = (a->plan.max_decode_bytes + (zcf ? kZcStage : 0) + qbytes + 127) & ~127;
@@ -2430,12 +2436,16 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
                   da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
+    if (max_blocks > 0) {  // split step: the SMs the general kernel leaves free
+        p.concurrent = 1;
+        if (blocks > max_blocks) blocks = max_blocks;
+    }
     // One pair per CTA (RDKV_DECODE_CTA=1): the same persistent pairs, but each
     // retires its own CTA, so under programmatic dependent launch the next
     // kernel's CTAs take a pair's smem / warp slots as soon as it finishes
     // instead of when the SM's slowest pair does.
     static const char* cta_env = getenv("RDKV_DECODE_CTA");
-    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0 && !zcf) {
+    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0 && !zcf && max_blocks == 0) {
         const size_t smem1 = kXMaxBuf * sizeof(uint64_t) + (size_t)2 * slot + scratch + slack;
         auto k1 = bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, true> : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, true>;
         static std::atomic<int> smem1_set[2][kMaxDevices];
@@ -2469,19 +2479,20 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st) {
 }
 
 template <typename IO, bool FULLK>
-static int launch_u2x_k(const rdkv_decode_args* a, cudaStream_t st) {
+static int launch_u2x_k(const rdkv_decode_args* a, cudaStream_t st, int max_blocks) {
     // long tiles or Zone C rows beyond the fused bound: the chunked kernel
     if (a->plan.max_slots > kU2MaxSlots || (a->zc_len && !zc_fusable(a))) return launch_u2c<IO, FULLK>(a, st);
     const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
-    if (nb <= 2) return launch_u2x_t<IO, 2, FULLK>(a, st);
-    if (nb <= 4) return launch_u2x_t<IO, 4, FULLK>(a, st);
-    return launch_u2x_t<IO, kXNbMax, FULLK>(a, st);
+    if (nb <= 2) return launch_u2x_t<IO, 2, FULLK>(a, st, max_blocks);
+    if (nb <= 4) return launch_u2x_t<IO, 4, FULLK>(a, st, max_blocks);
+    return launch_u2x_t<IO, kXNbMax, FULLK>(a, st, max_blocks);
 }
 
 template <typename IO>
-static int launch_u2x(const rdkv_decode_args* a, cudaStream_t st) {
+static int launch_u2x(const rdkv_decode_args* a, cudaStream_t st, int max_blocks = 0) {
     // plan.uniform2 == 2: every tile also keeps all 128 K channels (identity channel_perm)
-    return a->plan.uniform2 == 2 ? launch_u2x_k<IO, true>(a, st) : launch_u2x_k<IO, false>(a, st);
+    return a->plan.uniform2 == 2 ? launch_u2x_k<IO, true>(a, st, max_blocks)
+                                 : launch_u2x_k<IO, false>(a, st, max_blocks);
 }
 
 }  // namespace rdkv_b200
@@ -2500,7 +2511,7 @@ bool mma_supported(const rdkv_decode_args* a) {
 }
 
 template <int NT, typename IO, bool U2>
-static int launch_t(const rdkv_decode_args* a, cudaStream_t st) {
+static int launch_t(const rdkv_decode_args* a, cudaStream_t st, int* grid_out = nullptr) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
     const int slot = (a->plan.max_decode_bytes + qbytes + 127) & ~127;
     // per-warp scratch: head | digits | logits (aliased by the PV accumulators) | p16 | zl
@@ -2550,6 +2561,7 @@ static int launch_t(const rdkv_decode_args* a, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
+    if (grid_out) *grid_out = blocks;
     kern<<<blocks, 32 * (W + 1), smem, st>>>(p);
     return launch_status();
 }
@@ -2565,13 +2577,17 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
         rdkv_decode_args gm = *a;
         gm.units = a->units - pl.n_uniform;
         gm.unit_ids = a->unit_ids + pl.n_uniform;
-        const int rc = a->group <= 4 ? (f16 ? launch_t<1, __half, false>(&gm, st) : launch_t<1, float, false>(&gm, st))
-                                     : (f16 ? launch_t<2, __half, false>(&gm, st) : launch_t<2, float, false>(&gm, st));
+        int gblocks = 0;
+        const int rc = f16 ? launch_t<1, __half, false>(&gm, st, &gblocks) : launch_t<1, float, false>(&gm, st, &gblocks);
         if (rc) return rc;
+        // the uniform tiles run beside it on the SMs it leaves free (u2x is
+        // issue-bound: the mixed tiles are few but slow, latency-bound per tile)
         rdkv_decode_args um = *a;
         um.units = pl.n_uniform;
         um.plan.uniform2 = pl.uniform2_split;
-        return f16 ? launch_u2x<__half>(&um, st) : launch_u2x<float>(&um, st);
+        const int free_sms = dev_attrs().nsm - gblocks;
+        return f16 ? launch_u2x<__half>(&um, st, free_sms > 0 ? free_sms : 1)
+                   : launch_u2x<float>(&um, st, free_sms > 0 ? free_sms : 1);
     }
     // not split: every launch walks the units in order (unit_ids only name subsets)
     rdkv_decode_args plain = *a;
