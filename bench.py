@@ -419,7 +419,19 @@ def secondary_configs(P, spec0, model, q, args):
         us, _ = graph_step_us(P, sub, q[:ub].contiguous(), min(args.steps, 100))
         sweep[str(b)] = {"us_per_step": us, "tok_s": b / (us / 1e6)}
     out["batch_sweep"] = sweep
-    # (4) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
+    # (4) configs[4]: LLaMA-3.1-70B shape (80 layers, 64 q / 8 kv heads: GQA group 8),
+    # 128K ctx; batch 8 over 8 GPUs = one sequence per GPU
+    spec70 = WorkloadSpec(batch=1, layers=80, q_heads=64, kv_heads=8, ctx=spec0.ctx, n_tokens=128, seed=5)
+    m70, _, _, _ = build(spec70)
+    q70 = P.generate((m70.units, spec70.group, d), torch.float16, seed=QSEED, tensor=2)
+    us, _ = graph_step_us(P, m70, q70, min(args.steps, 100))
+    byts = m70.decode_bytes(io_bytes=2)
+    out["llama70b_1seq_per_gpu"] = {"config": "configs[4]: LLaMA-3.1-70B KV shape (80 layers, 64 q / 8 kv heads), "
+                                              "128K ctx, n=128, one sequence per GPU (batch 8 over 8 GPUs)",
+                                    "us_per_step": us, "tok_s_per_gpu": 1 / (us / 1e6),
+                                    "roofline_frac": byts / (us / 1e6) / 1e9 / peak}
+    del m70, q70
+    # (5) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
     spec = WorkloadSpec(batch=spec0.batch, layers=spec0.layers, ctx=spec0.ctx, n_tokens=512, seed=3)
     m2, _, st2, _ = build(spec)
     q2 = P.generate((m2.units, spec.group, d), torch.float16, seed=QSEED, tensor=2)

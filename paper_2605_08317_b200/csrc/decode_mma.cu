@@ -1857,7 +1857,8 @@ constexpr int kXMaxBuf = 4;  // tile buffers per pair
 // (no math), 2 math only (tiles past the first buffers are not reloaded).
 // PERCTA: one pair per CTA (a compile-time barrier id, so a CTA reserves 2
 // hardware barriers instead of 16 and 8 CTAs fit on an SM).
-template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false, bool ZCF = false>
+template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false, bool ZCF = false,
+          bool G8 = false>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
     const int nbuf = p.R;  // buffers per pair
@@ -1990,9 +1991,17 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
             pair_sync(PERCTA ? 1 : 1 + pr);
             refill();
         } else {
-            decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCF>(st, st + qoff, p.g, scr, o, PERCTA ? 1 : 1 + pr, lc,
-                                                                refill, nullptr, nullptr, zl,
-                                                                st + qoff - kZcStage, st + qoff - kZcFused * 256);
+            // GQA groups of up to 8 heads: one pass per 4 heads over the same staged
+            // tile (the buffer refill is issued once, in the first pass)
+#pragma unroll 1
+            for (int hp = 0; hp < (G8 ? 2 : 1) && 4 * hp < p.g; ++hp) {
+                auto rf = [&]() {
+                    if (hp == 0) refill();
+                };
+                decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCF>(
+                    st, st + qoff + 4 * hp * QROW, G8 ? min(4, p.g - 4 * hp) : p.g, scr, o + 4 * hp * kD,
+                    PERCTA ? 1 : 1 + pr, lc, rf, nullptr, nullptr, zl, st + qoff - kZcStage, st + qoff - kZcFused * 256);
+            }
         }
         if (++b == nbuf) {
             b = 0;
@@ -2402,6 +2411,12 @@ static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st) {
 static bool zc_fusable(const rdkv_decode_args* a) {
     return a->zc_len && (a->flags & RDKV_DECODE_ZC_BOUND) && a->zc_bound <= kZcFused;
 }
+// groups of 5..8 heads run as two 4-head passes in the short-tile kernel only
+// (the chunked kernel's running softmax state is per 4-head lane group)
+static bool u2x_group_ok(const rdkv_decode_args* a) {
+    if (a->group <= 4) return true;
+    return a->group <= 8 && a->plan.max_slots <= kU2MaxSlots && (!a->zc_len || zc_fusable(a));
+}
 
 template <typename IO, int NBMAX, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_blocks = 0) {
@@ -2426,13 +2441,20 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
     static const char* nenv = getenv("RDKV_DECODE_NULL");
     const int mode = nenv ? atoi(nenv) : 0;
     const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
-    auto kern = zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true>
+    const bool g8 = a->group > 4;
+    auto kern = g8 ? (zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true, true>
+                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, true, true>)
+                          : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, false, true>
+                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, false, true>))
+              : zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true>
                             : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, true>)
               : bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true>
               : mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
               : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2> : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
-    static std::atomic<int> smem_set[6][kMaxDevices];
-    set_smem_once(kern, (int)smem, smem_set[zcf ? 4 + (bulk ? 1 : 0) : bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0],
+    static std::atomic<int> smem_set[10][kMaxDevices];
+    set_smem_once(kern, (int)smem,
+                  smem_set[g8 ? 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0)
+                              : zcf ? 4 + (bulk ? 1 : 0) : bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0],
                   da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
@@ -2445,7 +2467,7 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
     // kernel's CTAs take a pair's smem / warp slots as soon as it finishes
     // instead of when the SM's slowest pair does.
     static const char* cta_env = getenv("RDKV_DECODE_CTA");
-    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0 && !zcf && max_blocks == 0) {
+    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0 && !zcf && !g8 && max_blocks == 0) {
         const size_t smem1 = kXMaxBuf * sizeof(uint64_t) + (size_t)2 * slot + scratch + slack;
         auto k1 = bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, true> : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, true>;
         static std::atomic<int> smem1_set[2][kMaxDevices];
@@ -2506,7 +2528,7 @@ bool mma_supported(const rdkv_decode_args* a) {
     if (a->zc_len && a->zc_cap > 1024) return false;
     const rdkv_decode_plan& p = a->plan;
     // uniform 2-bit tiles of any length: u2x (<= 160 slots) or its chunked variant
-    if (p.uniform2 && a->group <= 4 && p.max_decode_bytes > 0) return true;
+    if (p.uniform2 && p.max_decode_bytes > 0 && u2x_group_ok(a)) return true;
     return p.max_decode_bytes > 0 && p.max_slots <= kMaxSlots && p.max_zone_b_rows <= kMaxSlots;
 }
 
@@ -2572,8 +2594,9 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     // body, then the uniform-2-bit ones on u2x (PDL: its prologue and KV
     // prefetch overlap the general kernel's tail)
     const rdkv_decode_plan& pl = a->plan;
-    if (a->unit_ids && !pl.uniform2 && pl.n_uniform > 0 && pl.n_uniform < a->units && a->group <= 4 &&
-        a->kernel == 0 && (!a->zc_len || zc_fusable(a))) {
+    if (a->unit_ids && !pl.uniform2 && pl.n_uniform > 0 && pl.n_uniform < a->units &&
+        (a->group <= 4 || (a->group <= 8 && pl.max_slots <= kU2MaxSlots)) && a->kernel == 0 &&
+        (!a->zc_len || zc_fusable(a))) {
         rdkv_decode_args gm = *a;
         gm.units = a->units - pl.n_uniform;
         gm.unit_ids = a->unit_ids + pl.n_uniform;
@@ -2596,7 +2619,7 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     // uniform 2-bit tiles (the n=128 production shape) take the specialised body
     // uniform 2-bit tiles (the n=128 production shape): warp-pair body by default,
     // kernel 4 selects the one-warp body, kernel 3 the general body
-    const bool u2 = a->plan.uniform2 && a->group <= 4 &&
+    const bool u2 = a->plan.uniform2 && u2x_group_ok(a) &&
                     (a->kernel != 3 || a->plan.max_slots > kMaxSlots);  // the general body stops at 256 slots
     const bool short_u2 = u2 && a->plan.max_slots <= kU2MaxSlots && !a->zc_len;
     if (short_u2 && a->kernel == 4) return f16 ? launch_t<1, __half, true>(a, st) : launch_t<1, float, true>(a, st);

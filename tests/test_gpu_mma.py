@@ -166,10 +166,12 @@ def test_mma_large_batch_persistent(cuda, orc):
 
 
 @pytest.mark.parametrize("g,fullk,io", [(4, True, torch.float32), (4, True, torch.float16), (4, False, torch.float32),
-                                        (1, True, torch.float32), (2, False, torch.float16), (3, True, torch.float32)])
+                                        (1, True, torch.float32), (2, False, torch.float16), (3, True, torch.float32),
+                                        (8, True, torch.float16), (7, False, torch.float32), (5, True, torch.float32)])
 def test_mma_uniform_two_bit_ragged(cuda, orc, g, fullk, io):
     """Uniform 2-bit tiles of every block count (1..160 kept tokens, ragged last
-    block), with all K channels kept (identity channel_perm) or some dropped."""
+    block), with all K channels kept (identity channel_perm) or some dropped;
+    GQA groups of 5..8 heads run as two 4-head passes over each staged tile."""
     rng = np.random.default_rng(40 + g + 10 * fullk)
     cases = []
     for n in (1, 3, 31, 32, 33, 64, 65, 100, 127, 128, 129, 131, 150, 157, 160):
