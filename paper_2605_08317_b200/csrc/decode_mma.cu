@@ -2594,9 +2594,10 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     // body, then the uniform-2-bit ones on u2x (PDL: its prologue and KV
     // prefetch overlap the general kernel's tail)
     const rdkv_decode_plan& pl = a->plan;
-    if (a->unit_ids && !pl.uniform2 && pl.n_uniform > 0 && pl.n_uniform < a->units &&
-        (a->group <= 4 || (a->group <= 8 && pl.max_slots <= kU2MaxSlots)) && a->kernel == 0 &&
-        (!a->zc_len || zc_fusable(a))) {
+    // (the uniform subset goes to the short-tile kernel, which is the one that
+    // reads unit_ids: every tile of the step must fit it)
+    if (a->unit_ids && !pl.uniform2 && pl.n_uniform > 0 && pl.n_uniform < a->units && a->group <= 8 &&
+        pl.max_slots <= kU2MaxSlots && a->kernel == 0 && (!a->zc_len || zc_fusable(a))) {
         rdkv_decode_args gm = *a;
         gm.units = a->units - pl.n_uniform;
         gm.unit_ids = a->unit_ids + pl.n_uniform;
