@@ -2602,7 +2602,9 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
         gm.units = a->units - pl.n_uniform;
         gm.unit_ids = a->unit_ids + pl.n_uniform;
         int gblocks = 0;
-        const int rc = f16 ? launch_t<1, __half, false>(&gm, st, &gblocks) : launch_t<1, float, false>(&gm, st, &gblocks);
+        const int rc = a->group <= 4
+                           ? (f16 ? launch_t<1, __half, false>(&gm, st, &gblocks) : launch_t<1, float, false>(&gm, st, &gblocks))
+                           : (f16 ? launch_t<2, __half, false>(&gm, st, &gblocks) : launch_t<2, float, false>(&gm, st, &gblocks));
         if (rc) return rc;
         // the uniform tiles run beside it on the SMs it leaves free (u2x is
         // issue-bound: the mixed tiles are few but slow, latency-bound per tile)

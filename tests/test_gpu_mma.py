@@ -314,15 +314,15 @@ def test_host_decode_zero_copy_zone_c(cuda, orc, appends, known):
     assert torch.equal(oh, want)
 
 
-@pytest.mark.parametrize("io", [torch.float16, torch.float32])
-def test_split_dispatch_mixed_arena(cuda, orc, io):
+@pytest.mark.parametrize("io,g", [(torch.float16, 4), (torch.float32, 4), (torch.float16, 8), (torch.float32, 6)])
+def test_split_dispatch_mixed_arena(cuda, orc, io, g):
     """An arena of mostly uniform-2-bit tiles plus a few mixed ones (the heavy-
     hitter shape): the split step (mixed tiles on the general body, uniform ones
     on u2x through unit_ids) equals the all-general step and the oracle."""
     rng = np.random.default_rng(123)
     cases = []
     for i in range(40):
-        k, v, vb, kb, q = _random_case(rng, 300, 4)
+        k, v, vb, kb, q = _random_case(rng, 300, g)
         vb[:] = 0
         vb[np.sort(rng.choice(300, int(rng.integers(100, 150)), replace=False))] = 2
         kb[:] = 2
@@ -330,7 +330,7 @@ def test_split_dispatch_mixed_arena(cuda, orc, io):
             vb[np.nonzero(vb)[0][:3]] = 4
             kb[rng.choice(D, 3, replace=False)] = 4
         cases.append((k, v, vb, kb, q))
-    worst, model = _run_batch(cuda, orc, cases, 4, io=io)
+    worst, model = _run_batch(cuda, orc, cases, g, io=io)
     plan = model.plan
     assert plan.uniform2 == 0 and 0 < plan.n_uniform < len(cases)
     assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
