@@ -213,6 +213,18 @@ RDKV_API int rdkv_cuda_decode_ctx_destroy(rdkv_decode_ctx* ctx);
 RDKV_API int rdkv_cuda_decode_host_pipelined(rdkv_decode_ctx* ctx, const rdkv_decode_args* a,
                                              const void* q_host, void* out_host, void* stream);
 
+/* Sequence split across ranks (the optional cross-GPU merge): every rank
+ * decodes its share of each uniform-2-bit tile — token chunks c with
+ * c % world == rank (chunks of <= 160 slots, then 16-row Zone C chunks) — into
+ * unnormalised partials [units][group][head_dim + 2] f32 (o, running max in
+ * log2 units, weight sum). The caller gathers the world partials (e.g. NCCL
+ * all-gather into [world][units][group][head_dim + 2]) and merges them with
+ * rdkv_cuda_decode_merge into out [units][group][head_dim] (io_dtype). */
+RDKV_API int rdkv_cuda_decode_partial(const rdkv_decode_args* a, int32_t rank, int32_t world, float* partial,
+                                      void* stream);
+RDKV_API int rdkv_cuda_decode_merge(const float* partials, int32_t nparts, int32_t units, int32_t group,
+                                    int32_t head_dim, void* out, int32_t io_dtype, void* stream);
+
 /* ---- Zone C ------------------------------------------------------------- */
 /* Appends one K and one V row per unit (k_new/v_new [units][head_dim] of
  * dtype) at position zc_len[u], then increments zc_len[u]. */

@@ -122,6 +122,8 @@ _SIGS = {
     "rdkv_cuda_decode_prepare": (C.c_int, [_VP, _VP, C.c_int32, _VP, C.POINTER(DecodePlan), _VP]),
     "rdkv_cuda_decode_prepare_split": (C.c_int, [_VP, _VP, C.c_int32, _VP, _VP, C.POINTER(DecodePlan), _VP]),
     "rdkv_cuda_decode_host": (C.c_int, [C.POINTER(DecodeArgs), _VP, _VP, _VP]),
+    "rdkv_cuda_decode_partial": (C.c_int, [C.POINTER(DecodeArgs), C.c_int32, C.c_int32, _VP, _VP]),
+    "rdkv_cuda_decode_merge": (C.c_int, [_VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _VP, C.c_int32, _VP]),
     "rdkv_cuda_decode_ctx_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "rdkv_cuda_decode_ctx_destroy": (C.c_int, [C.c_void_p]),
     "rdkv_cuda_decode_host_pipelined": (C.c_int, [C.c_void_p, C.POINTER(DecodeArgs), _VP, _VP, _VP]),

@@ -10,6 +10,8 @@ template <typename IO>
 int launch_generic(const rdkv_decode_args* a, int split, int max_kslots, cudaStream_t st);
 int launch_mma(const rdkv_decode_args* a, cudaStream_t st);  // decode_mma.cu
 bool mma_supported(const rdkv_decode_args* a);
+int launch_partial(const rdkv_decode_args* a, int rank, int world, float* partial, cudaStream_t st);
+int launch_merge(const float* part, int nparts, int rows, int d, void* out, int io, cudaStream_t st);
 }  // namespace rdkv_b200
 
 using namespace rdkv_b200;
@@ -204,4 +206,18 @@ extern "C" RDKV_API int rdkv_cuda_decode_host_pipelined(rdkv_decode_ctx* c, cons
     c->key_out = out_host;
     RDKV_CUDA_TRY(cudaGraphLaunch(c->exec, st));
     return RDKV_OK;
+}
+
+// ---- sequence split across ranks (optional merge) ----------
+extern "C" RDKV_API int rdkv_cuda_decode_partial(const rdkv_decode_args* a, int32_t rank, int32_t world,
+                                                 float* partial, void* stream) {
+    if (!a || !partial || world < 1 || rank < 0 || rank >= world || !a->arena || !a->q) return RDKV_EINVAL;
+    return launch_partial(a, rank, world, partial, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" RDKV_API int rdkv_cuda_decode_merge(const float* partials, int32_t nparts, int32_t units, int32_t group,
+                                               int32_t head_dim, void* out, int32_t io_dtype, void* stream) {
+    if (!partials || !out || nparts < 1 || units < 1 || group < 1 || head_dim < 1) return RDKV_EINVAL;
+    if (io_dtype != RDKV_F32 && io_dtype != RDKV_F16) return RDKV_EINVAL;
+    return launch_merge(partials, nparts, units * group, head_dim, out, io_dtype, static_cast<cudaStream_t>(stream));
 }

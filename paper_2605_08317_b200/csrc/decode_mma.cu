@@ -163,6 +163,8 @@ struct MmaParams {
     int smsp_pairs;  // u2x: a pair's two warps on one SM sub-partition
     const int32_t* ids;  // launch tile -> unit (NULL: identity), a split step's subset
     int concurrent;      // u2x of a split step: runs beside the general kernel (see launch_mma)
+    float* partial;      // u2c sequence split: [units][g][d + 2] (o, max, sum) of this rank's chunks
+    int split_rank, split_world;
 };
 __device__ __forceinline__ int unit_of(const MmaParams& p, int tile) { return p.ids ? p.ids[tile] : tile; }
 
@@ -2226,6 +2228,10 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
         return m;
     };
     int cur_tile = tile0, cur_c = 0, cur_zc = 0;
+    // sequence split (p.partial): this rank decodes chunks c % world == rank of
+    // every tile (chunk 0 is always staged: header, channel table and q)
+    const bool psplit = p.partial != nullptr;
+    auto owned = [&](int c) { return !psplit || c % p.split_world == p.split_rank; };
     TileMeta cur{nullptr, 0, 0, 0, 0, 0}, nxt{nullptr, 0, 0, 0, 0, 0};
     // Zone C lengths are written by the previous kernel (append): read only
     // after griddepcontrol.wait
@@ -2235,7 +2241,11 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
     auto advance = [&]() {
         int C, s0, ns;
         u2c_geom(cur.nslot, 0, C, s0, ns);
-        if (++cur_c == C + (cur_zc + kZcChunk - 1) / kZcChunk) {
+        const int total = C + (cur_zc + kZcChunk - 1) / kZcChunk;
+        do {
+            ++cur_c;
+        } while (cur_c < total && !owned(cur_c));
+        if (cur_c >= total) {
             cur_tile += tstride;
             cur_c = 0;
             cur = nxt;
@@ -2261,21 +2271,24 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
                          256u, &fb[b]);
             }
         } else {
-            const int rows = ns >> 2, Q = cur.nslot >> 2;
+            const bool own = owned(cur_c);  // a chunk 0 another rank owns: header + q only
+            const int rows = own ? ns >> 2 : 0, Q = cur.nslot >> 2;
             const uint32_t kbytes = (uint32_t)(rows * cur.krb), vbytes = (uint32_t)(rows * 128),
-                           pbytes = (uint32_t)(ns * 8);
+                           pbytes = (uint32_t)(rows * 4 * 8);
             const bool c0 = cur_c == 0;
             const uint32_t tx = 4 * kbytes + vbytes + pbytes + (c0 ? (uint32_t)(cur.hk + qbytes) : 0u);
             fence_proxy_async();
             mbar_expect_tx(&fb[b], tx);
             if (c0) bulk_g2s(dst, cur.base, (uint32_t)cur.hk, &fb[b]);
             const int dk = cur.hk;
+            if (rows > 0) {
 #pragma unroll
-            for (int r = 0; r < 4; ++r)
-                bulk_g2s(dst + dk + r * kbytes, cur.base + cur.hk + (size_t)(r * Q + (s0 >> 2)) * cur.krb, kbytes,
-                         &fb[b]);
-            bulk_g2s(dst + dk + ns * cur.krb, cur.base + cur.offv + (size_t)(s0 >> 2) * 128, vbytes, &fb[b]);
-            bulk_g2s(dst + dk + ns * (cur.krb + 32), cur.base + cur.offvp + (size_t)s0 * 8, pbytes, &fb[b]);
+                for (int r = 0; r < 4; ++r)
+                    bulk_g2s(dst + dk + r * kbytes, cur.base + cur.hk + (size_t)(r * Q + (s0 >> 2)) * cur.krb, kbytes,
+                             &fb[b]);
+                bulk_g2s(dst + dk + ns * cur.krb, cur.base + cur.offv + (size_t)(s0 >> 2) * 128, vbytes, &fb[b]);
+                bulk_g2s(dst + dk + ns * (cur.krb + 32), cur.base + cur.offvp + (size_t)s0 * 8, pbytes, &fb[b]);
+            }
             if (c0 && with_q)
                 bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)cur_tile * qbytes,
                          (uint32_t)qbytes, &fb[b]);
@@ -2315,7 +2328,8 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
         const int zcl = zcl_next;
         zcl_next = zc_of(tile + tstride);
         IO* o = static_cast<IO*>(p.out) + (size_t)tile * p.g * kD;
-        for (int c = 0; c < C; ++c, ++k) {
+        for (int c = 0; c < C; ++c) {
+            if (c > 0 && !owned(c)) continue;
             mbar_wait(&fb[b], phase);
             __syncwarp();
             const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
@@ -2338,20 +2352,22 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
             };
             if (ZC && c >= Cp) {
                 const int j = c - Cp;
-                zc_chunk_u2x<IO, BULK>(st, min(kZcChunk, zcl - kZcChunk * j), q16, p.g, 1 + pr, lc, run, c == C - 1, o,
+                zc_chunk_u2x<IO, BULK>(st, min(kZcChunk, zcl - kZcChunk * j), q16, p.g, 1 + pr, lc, run,
+                                       !psplit && c == C - 1, o,
                                        BULK ? reinterpret_cast<IO*>(const_cast<uint8_t*>(st) + qoff) : o, refill);
             } else {
                 int Cc, s0, ns;
                 u2c_geom(nslot_t, c, Cc, s0, ns);
                 U2xChunk ck;
-                ck.n = max(0, min(n_t - s0, ns));
-                ck.nslot = ns;
+                const bool own = owned(c);
+                ck.n = own ? max(0, min(n_t - s0, ns)) : 0;
+                ck.nslot = own ? ns : 0;
                 ck.off_k = hk;
                 ck.off_v = hk + ns * krb;
                 ck.off_vp = hk + ns * (krb + 32);
                 ck.krb = krb;
                 ck.first = c == 0;
-                ck.last = c == C - 1;
+                ck.last = !psplit && c == C - 1;
                 decode_tile_u2x<IO, kXNbMax, FULLK, BULK, true>(st, st + qoff, p.g, scr, o, 1 + pr, lc, refill, &ck,
                                                                  &run);
             }
@@ -2359,13 +2375,24 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2c_kernel(const M
                 b = 0;
                 phase ^= 1u;
             }
+            ++k;
+        }
+        if (psplit && lc.tig < p.g) {  // this rank's (o, max, sum) of the tile
+            float* pr_row = p.partial + ((size_t)tile * p.g + lc.tig) * (kD + 2);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) *reinterpret_cast<float2*>(pr_row + lc.ch0 + 4 * m) = run.o[m];
+            if (half == 0 && lc.gid == 0) {
+                pr_row[kD] = run.m;
+                pr_row[kD + 1] = run.l;
+            }
         }
     }
     if (BULK && lane == 0) bulk_wait0();
 }
 
 template <typename IO, bool FULLK>
-static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st) {
+static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st, float* partial = nullptr, int split_rank = 0,
+                      int split_world = 1) {
     const bool zc = a->zc_len != nullptr;
     const int qbytes = a->group * kD * (int)sizeof(IO);
     // header + channel table + perm, then <= 160 slots of K / V / params (a
@@ -2383,7 +2410,10 @@ static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st) {
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
                 static_cast<const __half*>(a->zc_k), static_cast<const __half*>(a->zc_v), a->zc_len,
                 a->units, a->group, a->zc_cap, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
-    const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
+    p.partial = partial;
+    p.split_rank = split_rank;
+    p.split_world = split_world;
+    const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0 && !partial;
     auto kern = zc ? (bulk ? decode_u2c_kernel<IO, FULLK, true, true> : decode_u2c_kernel<IO, FULLK, false, true>)
                    : (bulk ? decode_u2c_kernel<IO, FULLK, true, false> : decode_u2c_kernel<IO, FULLK, false, false>);
     static std::atomic<int> smem_set[4][kMaxDevices];
@@ -2585,6 +2615,52 @@ static int launch_t(const rdkv_decode_args* a, cudaStream_t st, int* grid_out = 
     if (blocks > nsm) blocks = nsm;
     if (grid_out) *grid_out = blocks;
     kern<<<blocks, 32 * (W + 1), smem, st>>>(p);
+    return launch_status();
+}
+
+// Sequence split (SURVEY.md §8(e) optional merge): this rank's share of every
+// uniform-2-bit tile (its chunks c % world == rank) as unnormalised partials.
+int launch_partial(const rdkv_decode_args* a, int rank, int world, float* partial, cudaStream_t st) {
+    if (!a->plan.uniform2 || a->group > 4 || !a->tile_decode_bytes || a->head_dim != kD) return RDKV_EINVAL;
+    if (a->zc_len && a->zc_cap > 1 << 20) return RDKV_EINVAL;
+    const bool f16 = a->io_dtype == RDKV_F16;
+    rdkv_decode_args b = *a;
+    b.unit_ids = nullptr;
+    if (a->plan.uniform2 == 2)
+        return f16 ? launch_u2c<__half, true>(&b, st, partial, rank, world) : launch_u2c<float, true>(&b, st, partial, rank, world);
+    return f16 ? launch_u2c<__half, false>(&b, st, partial, rank, world) : launch_u2c<float, false>(&b, st, partial, rank, world);
+}
+
+// out = sum_r 2^(m_r - M) o_r / sum_r 2^(m_r - M) l_r over nparts partials
+// [nparts][units * g][d + 2] (m in log2 units, as the kernels keep it)
+template <typename IO>
+__global__ void merge_partials_kernel(const float* __restrict__ part, int nparts, int rows, int d, IO* __restrict__ out) {
+    const int row = blockIdx.x;
+    if (row >= rows) return;
+    const size_t stride = (size_t)rows * (d + 2);
+    float M = -INFINITY;
+    for (int r = 0; r < nparts; ++r) M = fmaxf(M, part[r * stride + (size_t)row * (d + 2) + d]);
+    float L = 0.0f;
+    for (int r = 0; r < nparts; ++r) {
+        const float* pr = part + r * stride + (size_t)row * (d + 2);
+        if (pr[d + 1] > 0.0f) L += exp2f(pr[d] - M) * pr[d + 1];
+    }
+    const float inv = L > 0.0f ? 1.0f / L : 0.0f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        float acc = 0.0f;
+        for (int r = 0; r < nparts; ++r) {
+            const float* pr = part + r * stride + (size_t)row * (d + 2);
+            if (pr[d + 1] > 0.0f) acc += exp2f(pr[d] - M) * pr[c];
+        }
+        out[(size_t)row * d + c] = (IO)(acc * inv);
+    }
+}
+
+int launch_merge(const float* part, int nparts, int rows, int d, void* out, int io, cudaStream_t st) {
+    if (io == RDKV_F16)
+        merge_partials_kernel<__half><<<rows, 128, 0, st>>>(part, nparts, rows, d, static_cast<__half*>(out));
+    else
+        merge_partials_kernel<float><<<rows, 128, 0, st>>>(part, nparts, rows, d, static_cast<float*>(out));
     return launch_status();
 }
 

@@ -112,6 +112,34 @@ def sum_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def gather_partials(partial, world: int):
+    """All-gather every rank's decode partials [U, g, d + 2] into [world, U, g, d + 2]
+    (NCCL over NVLink on the box, gloo on CPU): the one data-path collective,
+    used only by the optional sequence split."""
+    import torch
+
+    if world == 1:
+        return partial.unsqueeze(0)
+    import torch.distributed as dist
+
+    out = torch.empty((world * partial.shape[0],) + tuple(partial.shape[1:]), dtype=partial.dtype,
+                      device=partial.device)
+    dist.all_gather_into_tensor(out, partial.contiguous())
+    return out.view((world,) + tuple(partial.shape))
+
+
+def sequence_split_decode(model, q, world: int, rank: int, dtype=None):
+    """Optional cross-GPU merge: every rank decodes its token
+    chunks of every tile (each rank holds the whole packed model), the partials
+    are all-gathered and merged with a log-sum-exp combine — the strong-scaling
+    path for one sequence whose tiles are long."""
+    from . import pipeline as P
+
+    part = P.decode_partial(model, q, rank, world)
+    parts = gather_partials(part, world)
+    return P.merge_partials(parts, dtype or q.dtype)
+
+
 def finalize(world: int) -> None:
     if world > 1:
         import torch.distributed as dist

@@ -378,6 +378,47 @@ def packed_decode_step(model: PackedModel, q, out=None, split=1, kernel=0, works
     return out
 
 
+def chunk_ranges(nslot: int) -> list[tuple[int, int]]:
+    """Token-slot chunks of a tile in the chunked / sequence-split decode
+    (u2c_geom in csrc/decode_mma.cu): <= 160 slots each, starts 32-aligned."""
+    C = 1 if nslot <= 160 else (nslot + 159) // 160
+    S = nslot if C == 1 else ((nslot + C - 1) // C + 31) & ~31
+    return [(c * S, min(S, nslot - c * S)) for c in range(C)]
+
+
+def decode_partial(model: PackedModel, q, rank: int, world: int, partial=None):
+    """This rank's share of a sequence-split step (rdkv_cuda_decode_partial):
+    token chunks c % world == rank of every tile -> [U, g, d + 2] f32
+    (unnormalised o, running max in log2 units, weight sum)."""
+    _check_cuda(q)
+    U, g, d = model.units, model.group, model.head_dim
+    if partial is None:
+        partial = torch.empty((U, g, d + 2), dtype=torch.float32, device=q.device)
+    a = decode_args(model, q, q, 1, 0)
+    raise_for(capi.lib().rdkv_cuda_decode_partial(C.byref(a), rank, world, partial.data_ptr(), _stream()),
+              "decode_partial")
+    return partial
+
+
+def merge_partials(parts, dtype=torch.float16, out=None):
+    """[R, U, g, d + 2] partials -> out [U, g, d] (rdkv_cuda_decode_merge)."""
+    _check_cuda(parts)
+    R, U, g, d2 = parts.shape
+    if out is None:
+        out = torch.empty((U, g, d2 - 2), dtype=dtype, device=parts.device)
+    raise_for(capi.lib().rdkv_cuda_decode_merge(parts.contiguous().data_ptr(), R, U, g, d2 - 2, out.data_ptr(),
+                                                _dtype_code(out), _stream()), "decode_merge")
+    return out
+
+
+def merge_partials_reference(parts):
+    """The merge in plain torch (any device): sum_r 2^(m_r - M) o_r / sum_r 2^(m_r - M) l_r."""
+    o, m, l = parts[..., :-2].double(), parts[..., -2].double(), parts[..., -1].double()
+    M = m.max(dim=0).values
+    w = torch.where(l > 0, torch.exp2(m - M), torch.zeros_like(m))
+    return (w.unsqueeze(-1) * o).sum(0) / (w * l).sum(0).unsqueeze(-1)
+
+
 class HostDecoder:
     """End-to-end decode from pinned host q to pinned host out through the
     pipelined C-ABI entry point (rdkv_cuda_decode_host_pipelined): the step is

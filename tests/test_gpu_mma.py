@@ -341,3 +341,28 @@ def test_split_dispatch_mixed_arena(cuda, orc, io, g):
     model.unit_ids = ids
     err = (split.float() - general.float()).norm(dim=-1) / general.float().norm(dim=-1)
     assert float(err.max()) < (2 * U2X_TOL if io == torch.float32 else 2e-3)
+
+
+@pytest.mark.parametrize("world,appends,io", [(2, 0, torch.float16), (3, 0, torch.float32), (2, 20, torch.float32),
+                                              (4, 3, torch.float16)])
+def test_sequence_split_partials_merge(cuda, orc, world, appends, io):
+    """Optional cross-GPU merge, simulated in one process: each of `world` ranks
+    decodes its token chunks (rdkv_cuda_decode_partial), the stacked partials
+    are merged (rdkv_cuda_decode_merge) — equal to the one-rank decode."""
+    rng = np.random.default_rng(200 + world + appends)
+    cases = []
+    for n in (20, 128, 161, 400, 900):
+        k, v, vb, kb, q = _random_case(rng, 1000, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(1000, n, replace=False))] = 2
+        kb[:] = 2
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, 4, io=io, appends=appends, rng=rng, tol=U2X_TOL)
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).to(io)
+    want = P.packed_decode_step(model, q).float()
+    parts = torch.stack([P.decode_partial(model, q, r, world) for r in range(world)])
+    got = P.merge_partials(parts, io).float()
+    ref = P.merge_partials_reference(parts).float()
+    assert float(((got - ref).norm(dim=-1) / ref.norm(dim=-1)).max()) < (1e-5 if io == torch.float32 else 1e-3)
+    err = (got - want).norm(dim=-1) / want.norm(dim=-1)
+    assert float(err.max()) < (2 * U2X_TOL if io == torch.float32 else 2e-3), float(err.max())
