@@ -1473,7 +1473,14 @@ struct U2xRun {
 constexpr int kZcFused = 4;
 constexpr int kZcKStride = 272;                        // padded K-row stride: conflict-free ldmatrix
 constexpr int kZcStage = kZcFused * (kZcKStride + 256);  // fused Zone C staging bytes (K rows + V rows)
-template <typename IO, int NBMAX, bool FULLK, bool BULK, bool CHUNKED = false, bool ZCF = false, typename AfterSync1>
+// MIX ("mostly 2-bit" tiles, heavy-hitter caches): besides the 2-bit V rows
+// and K channels, up to 32 K channels at 4 bits (one extra QK k-step, class-1
+// digit block 4) and up to 8 V rows at 4 bits (their logits come from QK like
+// any slot; their PV terms are added on CUDA cores after the 2-bit PV, whose
+// p~ digits for those slots are zero).
+constexpr int kMixMaxRows = 16;  // 4-bit V rows per MIX tile (the pt1 weight table)
+template <typename IO, int NBMAX, bool FULLK, bool BULK, bool CHUNKED = false, bool ZCF = false, bool MIX = false,
+          typename AfterSync1>
 __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
                                                 uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
                                                 const U2xLane& L, AfterSync1&& after_sync1,
@@ -1485,11 +1492,15 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     const TileHeader& h = *reinterpret_cast<const TileHeader*>(t);
     PairX& xg = *reinterpret_cast<PairX*>(scr);
     uint8_t* qdig = scr + kXQDig;
-    uint8_t* pdig = scr + kXPDig;
+    // MIX scratch: q~ digit block 4 (class-1 K) at kXPDig, then the 4-bit rows' weights
+    float* pt1 = reinterpret_cast<float*>(scr + kXPDig + 512);  // [kMixMaxRows][4] (MIX only)
+    uint8_t* pdig = scr + kXPDig + (MIX ? 512 + kMixMaxRows * 16 : 0);
     const float* chanf = reinterpret_cast<const float*>(t + kHeaderBytes);
     const bool first = CHUNKED ? ck->first : true;
-    const int n = CHUNKED ? ck->n : h.r[0];
     const int nslot = CHUNKED ? ck->nslot : h.nslot;
+    // MIX: 2-bit rows are slots [0, r0), 4-bit rows [P0, P0 + r1) (P0 = pad4(r0))
+    const int r1 = MIX ? h.r[1] : 0, c1 = MIX ? h.c[1] : 0, P0 = MIX ? ((h.r[0] + 3) & ~3) : 0;
+    const int n = CHUNKED ? ck->n : (MIX && r1 > 0 ? P0 + r1 : h.r[0]);  // slots up to the last kept token
     const int nb = (n + 31) >> 5;             // 32-token blocks of this tile (warp-uniform)
     const int mynb = (nb + 1 - half) >> 1;    // blocks of this warp: half, half + 2, ...
     const int krb_c = FULLK ? 32 : (CHUNKED ? ck->krb : h.krow_bytes);
@@ -1519,7 +1530,14 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     for (int o = 1; o < 8; o <<= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
     qm = __shfl_sync(0xffffffffu, qm, 8 * tig);
     const IO* qh = reinterpret_cast<const IO*>(qs + (hv ? tig : 0) * QROW);
-    const float bnd = smax * qm;
+    float smx = smax;
+    if (MIX && c1 > 0) {  // the 4-bit channels' scale bound (not in the header)
+        float s1 = L.lane < c1 ? fabsf(chanf[2 * (128 + L.lane)]) : 0.0f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s1 = fmaxf(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+        smx = fmaxf(smx, s1);
+    }
+    const float bnd = smx * qm;
     const float sg = (hv && bnd > 0.0f) ? kQFix * rcp_approx(bnd) : 0.0f;  // heads >= g: zero digits
 
     // ---- q~ digits of k-steps 2 half, 2 half + 1 and the bias sum_c q_c * offset_c.
@@ -1556,6 +1574,37 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             xb[e] = (__float_as_uint(yb) + (0x00808080u - 0x4B400000u)) ^ 0x00808080u;
         }
         float bpart = bp.x + bp.y;
+        if (MIX && c1 > 0 && half == 0) {
+            // class-1 (4-bit) channels: K positions 4j .. 4j + 3 of head h = lane & 3
+            // (j = lane >> 2), slot of K position p per the 4-bit in-place masks;
+            // prescale 4 * 16^(1 - t'), so every product carries 64 like class 0
+            const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
+            const int hh1 = tig, j = L.lane >> 2;  // (lane & 3 == tig: sg is already this head's scale)
+            const IO* q1 = qh;
+            const float sg1 = sg;
+            uint32_t x1[4];
+            float b1 = 0.0f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int pk = 4 * j + e, rr = pk & 15, tt = rr >> 2;
+                const int sl = 16 * (pk >> 4) + 8 * (tt >> 1) + 2 * (rr & 3) + (tt & 1);
+                const float2 cs = reinterpret_cast<const float2*>(chanf)[128 + sl];
+                const float qv = (sl < c1 && hh1 < g) ? ld_io(q1, perm[128 + sl]) : 0.0f;
+                b1 = fmaf(qv, cs.y, b1);
+                const float y = fmaf(cs.x * qv, sg1 * ((tt & 1) ? 4.0f : 64.0f), kMagicS);
+                x1[e] = (__float_as_uint(y) + (0x00808080u - 0x4B400000u)) ^ 0x00808080u;
+            }
+            // this lane's bias share is for head hh1 = lane & 3 == tig
+            bpart += b1;
+            const uint32_t a01 = __byte_perm(x1[0], x1[1], 0x5140), b01 = __byte_perm(x1[0], x1[1], 0x7362);
+            const uint32_t a23 = __byte_perm(x1[2], x1[3], 0x5140), b23 = __byte_perm(x1[2], x1[3], 0x7362);
+            uint8_t* w1p = qdig + 4 * 512 + 4 * (j & 3);
+            const int hsel = j >> 2;  // 16-B half of the 32 K positions
+            // rows 2h+1 (d2), 8+2h (d1), 9+2h (d0); halves of rows 4..7 (mod 8) swapped
+            *reinterpret_cast<uint32_t*>(w1p + (2 * hh1 + 1) * 32 + ((hsel ^ (hh1 >> 1)) * 16)) = __byte_perm(b01, b23, 0x5410);
+            *reinterpret_cast<uint32_t*>(w1p + (8 + 2 * hh1) * 32 + ((hsel ^ (hh1 >> 1)) * 16)) = __byte_perm(a01, a23, 0x7632);
+            *reinterpret_cast<uint32_t*>(w1p + (9 + 2 * hh1) * 32 + ((hsel ^ (hh1 >> 1)) * 16)) = __byte_perm(a01, a23, 0x5410);
+        }
         // 4x4 byte transposes (digit d of value e -> byte e of word d), rotated by tig
         const uint32_t a01 = __byte_perm(xa[0], xa[1], 0x5140), b01 = __byte_perm(xa[0], xa[1], 0x7362);
         const uint32_t a23 = __byte_perm(xa[2], xa[3], 0x5140), b23 = __byte_perm(xa[2], xa[3], 0x7362);
@@ -1624,6 +1673,17 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                     mma_u8s8(acc[u][0], a, bq[kk][0], bq[kk][1]);
                     mma_u8s8(acc[u][1], a, bq[kk][2], bq[kk][3]);
                 }
+                if (MIX && c1 > 0) {  // 4-bit K channels: bytes 32..47 of the row, 8 codes per word
+                    uint32_t b4[4];
+                    ldsm_x4(b4, qdig + 4 * 512 + L.bofs);
+                    const uint4 z0 = lds128(r0 + 32), z1 = lds128(r1 + 32);
+                    const uint32_t zw0[4] = {z0.x, z0.y, z0.z, z0.w}, zw1[4] = {z1.x, z1.y, z1.z, z1.w};
+                    const uint32_t m4 = 0x0F0F0F0Fu << (4 * (tig & 1));
+                    const uint32_t a[4] = {zw0[tig >> 1] & m4, zw1[tig >> 1] & m4, zw0[2 + (tig >> 1)] & m4,
+                                           zw1[2 + (tig >> 1)] & m4};
+                    mma_u8s8(acc[u][0], a, b4[0], b4[1]);
+                    mma_u8s8(acc[u][1], a, b4[2], b4[3]);
+                }
             }
             // rows (u, r) = slots 32 pb + 4 gid + 2u + r: v = d2 * 2^16 + d1 * 2^8 + d0
 #pragma unroll
@@ -1634,7 +1694,15 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                 const float2 v = ffma2(hi, make_float2(65536.0f, 65536.0f), lo);
                 lg[i][u] = ffma2(v, make_float2(qscale2, qscale2), make_float2(bias2, bias2));
             }
-            if (32 * pb + 32 > n) {  // ragged last block: slots >= n get no weight
+            if (MIX && 32 * pb + 32 > h.r[0]) {  // slots between the 2-bit rows and the 4-bit rows
+                const int sbase = 32 * pb + 4 * gid;
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int s0 = sbase + 2 * u, s1 = s0 + 1;
+                    if (!(s0 < h.r[0] || (s0 >= P0 && s0 < P0 + r1))) lg[i][u].x = -INFINITY;
+                    if (!(s1 < h.r[0] || (s1 >= P0 && s1 < P0 + r1))) lg[i][u].y = -INFINITY;
+                }
+            } else if (32 * pb + 32 > n) {  // ragged last block: slots >= n get no weight
                 const int sbase = 32 * pb + 4 * gid;
 #pragma unroll
                 for (int u = 0; u < 2; ++u) {
@@ -1677,8 +1745,21 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             bv = fmaf(p23.y, vb.w, bv);
             const float2 vs01 = fmul2(make_float2(va.x, va.z), make_float2(psig, psig));
             const float2 vs23 = fmul2(make_float2(vb.x, vb.z), make_float2(psig, psig));
-            const float2 y01 = ffma2(p01, vs01, make_float2(kMagicU, kMagicU));
-            const float2 y23 = ffma2(p23, vs23, make_float2(kMagicU, kMagicU));
+            float2 y01 = ffma2(p01, vs01, make_float2(kMagicU, kMagicU));
+            float2 y23 = ffma2(p23, vs23, make_float2(kMagicU, kMagicU));
+            if (MIX && r1 > 0 && 32 * pb + 32 > P0) {  // 4-bit rows: weight to the CUDA-core PV, digits 0
+                const int sb = 32 * pb + 4 * gid;
+                const float pp[4] = {p01.x, p01.y, p23.x, p23.y};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int t1 = sb + jj - P0;
+                    if (t1 >= 0 && t1 < r1 && hv) pt1[t1 * 4 + tig] = pp[jj];
+                }
+                if (sb + 0 >= P0) y01.x = kMagicU;
+                if (sb + 1 >= P0) y01.y = kMagicU;
+                if (sb + 2 >= P0) y23.x = kMagicU;
+                if (sb + 3 >= P0) y23.y = kMagicU;
+            }
             const uint32_t t01 = __byte_perm(__float_as_uint(y01.x), __float_as_uint(y01.y), 0x5140);
             const uint32_t t23 = __byte_perm(__float_as_uint(y23.x), __float_as_uint(y23.y), 0x5140);
             uint8_t* pw = pdig + pb * 256 + L.pdig_w;
@@ -1705,9 +1786,10 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
 #pragma unroll
     for (int m = 0; m < 4; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0;
     const uint8_t* g0b = t + off_v + L.vcol;
+    const int nbv = MIX ? (P0 + 31) >> 5 : nb;  // 4-bit rows are not in the 2-bit PV
 #pragma unroll
     for (int kk = 0; kk < NBMAX; ++kk) {
-        if (kk < nb) {
+        if (kk < nbv) {
             uint32_t b[2];
             ldsm_x2(b, pdig + kk * 256 + L.bofs2);
             const uint4 x0 = lds128(g0b + kk * 1024), x1 = lds128(g0b + kk * 1024 + 512);
@@ -1760,6 +1842,27 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
         float wa = 1.0f, wb = 0.0f, lz = 0.0f;
         float2 oz[4] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f),
                         make_float2(0.0f, 0.0f)};
+        float2 o4[4] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f),
+                        make_float2(0.0f, 0.0f)};
+        if (MIX && r1 > 0 && hv) {
+            // 4-bit V rows on CUDA cores: sum_t p_t * vscale_t * code_t for this
+            // lane's channels ch0 + 4m (lo nibble) and + 1 (hi nibble); the
+            // offsets are already in bt (they entered through the softmax)
+            const float2* vparam4 = reinterpret_cast<const float2*>(t + h.off_vp);
+            const uint8_t* v4 = t + h.off_vseg[1];
+#pragma unroll 1
+            for (int t1 = 0; t1 < r1; ++t1) {
+                const float w = pt1[t1 * 4 + tig] * vparam4[P0 + t1].x;
+                const int grp = t1 >> 2;
+                const uint8_t* gb = v4 + grp * 256 + (t1 & 3);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int mc = (L.ch0 + 4 * m) >> 1;  // byte column (two 4-bit channels)
+                    const uint32_t byte = gb[((mc ^ (8 * (grp & 3))) * 4)];
+                    o4[m] = ffma2(make_float2((float)(byte & 15u), (float)(byte >> 4)), make_float2(w, w), o4[m]);
+                }
+            }
+        }
         if (ZCF && z > 0) {
             // QK: A rows = Zone C tokens (rows >= z read neighbouring bytes, masked
             // below), B columns 2h / 2h + 1 = hi / lo fp16 parts of q_h
@@ -1820,6 +1923,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
             const float inv = rcp_approx(fmaf(lt, wa, lz * wb));
             const float s0 = vinv * L.s0f * wa * inv, bta = bt * wa * inv, zb = wb * inv;
             const float2 sc = make_float2(s0, s0 * 0.25f), bb = make_float2(bta, bta), zz = make_float2(zb, zb);
+            const float2 ww = make_float2(wa * inv, wa * inv);
             IO* orow = stage + tig * kD + L.ch0;
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -1827,6 +1931,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                     make_float2((float)(acc[m][0] * 256 + acc[m][1]), (float)(acc[m][2] * 256 + acc[m][3]));
                 float2 r = ffma2(v, sc, bb);
                 if (ZCF) r = ffma2(oz[m], zz, r);
+                if (MIX) r = ffma2(o4[m], ww, r);
                 if constexpr (sizeof(IO) == 2)
                     *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
                 else
@@ -1860,7 +1965,7 @@ constexpr int kXMaxBuf = 4;  // tile buffers per pair
 // PERCTA: one pair per CTA (a compile-time barrier id, so a CTA reserves 2
 // hardware barriers instead of 16 and 8 CTAs fit on an SM).
 template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false, bool ZCF = false,
-          bool G8 = false>
+          bool G8 = false, bool MIX = false>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
     const int nbuf = p.R;  // buffers per pair
@@ -1955,7 +2060,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         for (int j = 1; j < kXMaxBuf; ++j) ahead_z[j - 1] = j < nbuf ? zrows_of(j) : 0;
     const U2xLane lc = u2x_lane(half);
     // the q~ digit rows of d3 (never written: |N| < 2^22) must read as zero
-    for (int i = threadIdx.x & 63; i < 4 * 512 / 16; i += 64)
+    for (int i = threadIdx.x & 63; i < (MIX ? 5 : 4) * 512 / 16; i += 64)
         reinterpret_cast<uint4*>(scr + kXQDig)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     int b = 0;
@@ -2000,7 +2105,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
                 auto rf = [&]() {
                     if (hp == 0) refill();
                 };
-                decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCF>(
+                decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCF, MIX>(
                     st, st + qoff + 4 * hp * QROW, G8 ? min(4, p.g - 4 * hp) : p.g, scr, o + 4 * hp * kD,
                     PERCTA ? 1 : 1 + pr, lc, rf, nullptr, nullptr, zl, st + qoff - kZcStage, st + qoff - kZcFused * 256);
             }
@@ -2444,6 +2549,8 @@ static bool zc_fusable(const rdkv_decode_args* a) {
 // groups of 5..8 heads run as two 4-head passes in the short-tile kernel only
 // (the chunked kernel's running softmax state is per 4-head lane group)
 static bool u2x_group_ok(const rdkv_decode_args* a) {
+    if (a->plan.uniform2 == 3)  // MIX tiles: short-tile kernel only, no Zone C
+        return a->group <= 8 && a->plan.max_slots <= kU2MaxSlots && !a->zc_len;
     if (a->group <= 4) return true;
     return a->group <= 8 && a->plan.max_slots <= kU2MaxSlots && (!a->zc_len || zc_fusable(a));
 }
@@ -2453,7 +2560,8 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
     const int qbytes = a->group * kD * (int)sizeof(IO);
     const bool zcf = zc_fusable(a);
     const int slot = (a->plan.max_decode_bytes + (zcf ? kZcStage : 0) + qbytes + 127) & ~127;
-    const int scratch = (kXPDig + NBMAX * 256 + 127) & ~127;
+    const bool mix = a->plan.uniform2 == 3;  // some tiles carry a few 4-bit rows / channels
+    const int scratch = (kXPDig + (mix ? 512 + kMixMaxRows * 16 : 0) + NBMAX * 256 + 127) & ~127;
     const DevAttrs da = dev_attrs();
     const int smem_max = da.smem_optin, nsm = da.nsm;
     // fragment over-reads of ragged blocks land in the following smem region
@@ -2472,7 +2580,11 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
     const int mode = nenv ? atoi(nenv) : 0;
     const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
     const bool g8 = a->group > 4;
-    auto kern = g8 ? (zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true, true>
+    auto kern = mix ? (g8 ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, false, true, true>
+                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, false, true, true>)
+                          : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, false, false, true>
+                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, false, false, true>))
+              : g8 ? (zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true, true>
                                   : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, true, true>)
                           : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, false, true>
                                   : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, false, true>))
@@ -2481,9 +2593,9 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
               : bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true>
               : mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
               : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2> : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
-    static std::atomic<int> smem_set[10][kMaxDevices];
+    static std::atomic<int> smem_set[12][kMaxDevices];
     set_smem_once(kern, (int)smem,
-                  smem_set[g8 ? 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0)
+                  smem_set[mix ? 10 + (bulk ? 1 : 0) : g8 ? 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0)
                               : zcf ? 4 + (bulk ? 1 : 0) : bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0],
                   da.dev);
     int blocks = (a->units + W - 1) / W;
@@ -2497,7 +2609,7 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
     // kernel's CTAs take a pair's smem / warp slots as soon as it finishes
     // instead of when the SM's slowest pair does.
     static const char* cta_env = getenv("RDKV_DECODE_CTA");
-    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0 && !zcf && !g8 && max_blocks == 0) {
+    if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0 && !zcf && !g8 && !mix && max_blocks == 0) {
         const size_t smem1 = kXMaxBuf * sizeof(uint64_t) + (size_t)2 * slot + scratch + slack;
         auto k1 = bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, true> : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, true>;
         static std::atomic<int> smem1_set[2][kMaxDevices];
@@ -2621,7 +2733,8 @@ static int launch_t(const rdkv_decode_args* a, cudaStream_t st, int* grid_out = 
 // Sequence split (SURVEY.md §8(e) optional merge): this rank's share of every
 // uniform-2-bit tile (its chunks c % world == rank) as unnormalised partials.
 int launch_partial(const rdkv_decode_args* a, int rank, int world, float* partial, cudaStream_t st) {
-    if (!a->plan.uniform2 || a->group > 4 || !a->tile_decode_bytes || a->head_dim != kD) return RDKV_EINVAL;
+    if (!a->plan.uniform2 || a->plan.uniform2 == 3 || a->group > 4 || !a->tile_decode_bytes || a->head_dim != kD)
+        return RDKV_EINVAL;
     if (a->zc_len && a->zc_cap > 1 << 20) return RDKV_EINVAL;
     const bool f16 = a->io_dtype == RDKV_F16;
     rdkv_decode_args b = *a;
@@ -2703,7 +2816,7 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     // kernel 4 selects the one-warp body, kernel 3 the general body
     const bool u2 = a->plan.uniform2 && u2x_group_ok(a) &&
                     (a->kernel != 3 || a->plan.max_slots > kMaxSlots);  // the general body stops at 256 slots
-    const bool short_u2 = u2 && a->plan.max_slots <= kU2MaxSlots && !a->zc_len;
+    const bool short_u2 = u2 && a->plan.max_slots <= kU2MaxSlots && !a->zc_len && a->plan.uniform2 != 3;
     if (short_u2 && a->kernel == 4) return f16 ? launch_t<1, __half, true>(a, st) : launch_t<1, float, true>(a, st);
     if (short_u2 && a->kernel == 5) return f16 ? launch_pair<__half>(a, st) : launch_pair<float>(a, st);
     if (u2) return f16 ? launch_u2x<__half>(a, st) : launch_u2x<float>(a, st);
@@ -2747,7 +2860,8 @@ static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets
     if (cudaStreamSynchronize(st) != cudaSuccess) rc = RDKV_ECUDA;
     rdkv_decode_plan p{0, 0, 0, 0, 2, 0, 2};
     int32_t* ids = unit_ids_dev ? static_cast<int32_t*>(malloc(sizeof(int32_t) * (size_t)units)) : nullptr;
-    int nmixed = 0;
+    int nmixed = 0, n_u = 0, n_m = 0;
+    bool any_notfull = false, any_long = false, split_mix = false, split_notfull = false;
     for (int u = 0; u < units && rc == RDKV_OK; ++u) {
         const TileHeader& h = hdrs[u];
         if (h.magic != kTileMagic) {
@@ -2761,17 +2875,29 @@ static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets
         p.max_kq_slots = h.kslot_base[3] > p.max_kq_slots ? h.kslot_base[3] : p.max_kq_slots;
         const bool u2 = h.r[1] == 0 && h.r[2] == 0 && h.r[3] == 0 && h.c[1] == 0 && h.c[2] == 0 &&
                         h.c[3] == 0 && h.r[0] > 0 && h.c[0] > 0;
-        if (!u2) p.uniform2 = 0;
-        else if (h.c[0] != kD && p.uniform2 == 2) p.uniform2 = 1;
-        if (ids) {  // split lists: short uniform tiles first (in order), the rest from the back
-            if (u2 && h.nslot <= kU2MaxSlots) {
+        // "mostly 2-bit" (heavy-hitter shape): the 2-bit K channels fill the first
+        // 128 K slots, plus <= 32 4-bit channels and <= 8 4-bit V rows, short
+        const bool m2 = !u2 && h.r[2] == 0 && h.r[3] == 0 && h.c[2] == 0 && h.c[3] == 0 && h.r[0] > 0 &&
+                        h.c[0] > 96 && h.r[1] <= kMixMaxRows && h.nslot <= kU2MaxSlots &&
+                        h.kslot_base[1] == 128 && h.kbyte_base[1] == 32;
+        n_u += u2;
+        n_m += m2;
+        if (u2 && h.c[0] != kD) any_notfull = true;
+        if (u2 && h.nslot > kU2MaxSlots) any_long = true;
+        if (ids) {  // split lists: short uniform / mostly-2-bit tiles first (in order), the rest from the back
+            if ((u2 || m2) && h.nslot <= kU2MaxSlots) {
                 ids[p.n_uniform++] = u;
-                if (h.c[0] != kD) p.uniform2_split = 1;
+                if (m2) split_mix = true;
+                else if (h.c[0] != kD) split_notfull = true;
             } else {
                 ids[units - 1 - nmixed++] = u;
             }
         }
     }
+    // 2: all tiles uniform 2-bit with all d K channels; 1: uniform 2-bit; 3: every
+    // tile uniform or mostly 2-bit and short (the MIX kernel); 0: anything else
+    p.uniform2 = n_u == units ? (any_notfull ? 1 : 2) : (n_u + n_m == units && !any_long ? 3 : 0);
+    p.uniform2_split = split_mix ? 3 : split_notfull ? 1 : 2;
     if (ids) {  // the mixed tail back in unit order
         for (int i = p.n_uniform, j = units - 1; i < j; ++i, --j) {
             const int32_t t = ids[i];

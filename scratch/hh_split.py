@@ -33,3 +33,6 @@ if os.environ.get("PROF_MIXED"):
     torch.cuda.synchronize()
     P.packed_decode_step(mm, qm, om)
     torch.cuda.synchronize()
+print("plan uniform2", model.plan.uniform2, "n_uniform", model.plan.n_uniform, "split", model.plan.uniform2_split)
+r1 = np.array([i.rows[1] for i in infos]); c1 = np.array([i.chans[1] for i in infos]); c0 = np.array([i.chans[0] for i in infos])
+print("r1 max", r1.max(), "tiles r1>8", (r1 > 8).sum(), "c0 min", c0.min(), "c1 max", c1.max())

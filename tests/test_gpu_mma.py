@@ -326,7 +326,10 @@ def test_split_dispatch_mixed_arena(cuda, orc, io, g):
         vb[:] = 0
         vb[np.sort(rng.choice(300, int(rng.integers(100, 150)), replace=False))] = 2
         kb[:] = 2
-        if i % 7 == 3:  # a few 4-bit rows / channels
+        if i % 7 == 3:  # an 8-bit row (not "mostly 2-bit": the general body)
+            vb[np.nonzero(vb)[0][:3]] = 8
+            kb[rng.choice(D, 3, replace=False)] = 4
+        elif i % 7 == 5:  # a few 4-bit rows / channels (the MIX kernel)
             vb[np.nonzero(vb)[0][:3]] = 4
             kb[rng.choice(D, 3, replace=False)] = 4
         cases.append((k, v, vb, kb, q))
@@ -366,3 +369,27 @@ def test_sequence_split_partials_merge(cuda, orc, world, appends, io):
     assert float(((got - ref).norm(dim=-1) / ref.norm(dim=-1)).max()) < (1e-5 if io == torch.float32 else 1e-3)
     err = (got - want).norm(dim=-1) / want.norm(dim=-1)
     assert float(err.max()) < (2 * U2X_TOL if io == torch.float32 else 2e-3), float(err.max())
+
+
+
+@pytest.mark.parametrize("g,io", [(4, torch.float32), (4, torch.float16), (8, torch.float32), (2, torch.float16)])
+def test_mix_mostly_two_bit_tiles(cuda, orc, g, io):
+    """Heavy-hitter shape on the fast kernel (MIX): tiles with up to 8 4-bit V
+    rows and up to 28 4-bit K channels next to uniform 2-bit tiles."""
+    rng = np.random.default_rng(300 + g)
+    cases = []
+    for i, n in enumerate((5, 40, 97, 128, 133, 150, 60, 128)):
+        k, v, vb, kb, q = _random_case(rng, 400, g)
+        vb[:] = 0
+        kept = np.sort(rng.choice(400, n, replace=False))
+        vb[kept] = 2
+        kb[:] = 2
+        if i % 2 == 1:
+            r4 = min(n - 1, int(rng.integers(1, 17)))
+            vb[kept[rng.choice(n, r4, replace=False)]] = 4
+        if i % 3 != 2:
+            kb[rng.choice(D, int(rng.integers(1, 29)), replace=False)] = 4
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, g, io=io, tol=U2X_TOL)
+    assert model.plan.uniform2 == 3, model.plan.uniform2
+    assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
