@@ -431,7 +431,21 @@ def secondary_configs(P, spec0, model, q, args):
                                     "us_per_step": us, "tok_s_per_gpu": 1 / (us / 1e6),
                                     "roofline_frac": byts / (us / 1e6) / 1e9 / peak}
     del m70, q70
-    # (5) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
+    # (5) heavy-hitter caches (the realistic attention shape: a few 4-bit rows / channels
+    # in ~16% of the tiles): configs[2] shape with heavy-hitter injection
+    spec_hh = WorkloadSpec(batch=spec0.batch, layers=spec0.layers, ctx=spec0.ctx, n_tokens=128, seed=1,
+                           hh_stride=64, hh_boost=1.0)
+    mhh, _, sthh, _ = build(spec_hh)
+    qhh = P.generate((mhh.units, spec_hh.group, d), torch.float16, seed=QSEED, tensor=2)
+    us, _ = graph_step_us(P, mhh, qhh, min(args.steps, 100))
+    byts = mhh.decode_bytes(io_bytes=2)
+    out["heavy_hitters"] = {"config": "configs[2] shape with heavy-hitter injection (every 64th key boosted): "
+                                      "mixed 2/4-bit tiles", "us_per_step": us, "tok_s": spec_hh.batch / (us / 1e6),
+                            "roofline_frac": byts / (us / 1e6) / 1e9 / peak,
+                            "plan_uniform2": int(mhh.plan.uniform2),
+                            "v4_rows": int(sum(s["n_kept"].sum() for s in sthh))}
+    del mhh, qhh
+    # (6) budget sweep point: 512 FP16-equivalent tokens per layer (~512 kept tokens per head)
     spec = WorkloadSpec(batch=spec0.batch, layers=spec0.layers, ctx=spec0.ctx, n_tokens=512, seed=3)
     m2, _, st2, _ = build(spec)
     q2 = P.generate((m2.units, spec.group, d), torch.float16, seed=QSEED, tensor=2)
