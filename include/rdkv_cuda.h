@@ -339,6 +339,35 @@ RDKV_API int rdkv_tile_import(int32_t d, int32_t n, const int32_t* kept, const u
                               const float* kscale, const int64_t* kzero, const float* kfp,
                               uint8_t* tile, size_t tile_bytes);
 
+/* ---- RDKVC001 cache container straight to device (cache.cpp:228-287) ------ */
+/* Header of a container written by save_cache (cache.cpp:205-226): magic
+ * "RDKVC001", u32le header length, JSON header, then f32 K, V, probe_Q payload
+ * in layer-major, head-major, row-major order — which is already the device
+ * unit order: K/V [L*H_kv][T][d], probe_Q [L*H_kv][g][S_w][d] (unit = l*H_kv+h). */
+typedef struct {
+    int32_t layers, q_heads, kv_heads, head_dim, seq_len, probe_window;
+    int64_t payload_offset; /* byte offset of the K payload */
+    int64_t payload_bytes;  /* 4 * (2*L*H_kv*T*d + L*H_q*S_w*d) */
+} rdkv_cache_header;
+
+/* Host only. Replaces the header half of load_cache (cache.cpp:228-267) with
+ * its error behaviour: RDKV_EFORMAT for a bad magic, implausible/truncated
+ * header, invalid JSON, missing/mistyped fields, dtype != "f32", S_w out of
+ * range, or a file whose size is not header + payload (truncated / trailing
+ * bytes, cache.cpp:275-283); RDKV_EINVAL when CacheShape::validate rejects the
+ * shape (cache.cpp:95-105). */
+RDKV_API int rdkv_cache_read_header(const char* path, rdkv_cache_header* header);
+
+/* Streams the payload of `path` (header from rdkv_cache_read_header) into
+ * device k, v [L*H_kv][T][d] and probe_q [L*H_kv][g][S_w][d] as `dtype`
+ * (RDKV_F32 bit-exact, RDKV_F16 round-to-nearest), through pinned double
+ * buffers overlapping the file reads with the H2D copies. Returns
+ * RDKV_ENUMERIC when an entry is non-finite (KVCache::validate,
+ * cache.cpp:114-130) or overflows fp16. Returns after `stream` has finished
+ * the copies. */
+RDKV_API int rdkv_cuda_cache_load(const char* path, const rdkv_cache_header* header, void* k,
+                                  void* v, void* probe_q, int32_t dtype, void* stream);
+
 RDKV_API const char* rdkv_status_string(int status);
 RDKV_API int rdkv_version(void);
 

@@ -221,6 +221,8 @@ class OracleLib:
             L.ref_model_trizone.argtypes = [C.c_void_p, C.c_int, C.c_int]
             L.ref_model_trizone.restype = C.c_void_p
             L.ref_model_decode.argtypes = [C.c_void_p, F32, F64, F64]
+            L.ref_save_cache.argtypes = [C.c_uint64] + [C.c_int] * 6 + [C.c_char_p]
+            L.ref_load_cache.argtypes = [C.c_char_p, I32]
         else:
             L.orc_normal_stream.argtypes = [C.c_uint64, F32, C.c_size_t]
             L.orc_normal_stream.restype = None
@@ -242,6 +244,17 @@ class OracleLib:
                                               outlier_channels, outlier_scale, _p(k, C.c_float),
                                               _p(v, C.c_float), _p(q, C.c_float)), "gen_synthetic")
         return k, v, q
+
+    def save_cache(self, seed, layers, q_heads, kv_heads, d, t_len, probe_window, path):
+        """save_cache_file(gen_synthetic_cache(...)) (cache.cpp:205-226); reference only."""
+        self._check(self.lib.ref_save_cache(seed, layers, q_heads, kv_heads, d, t_len, probe_window,
+                                            path.encode()), "save_cache")
+
+    def load_cache_status(self, path):
+        """(status, dims) of load_cache_file (cache.cpp:228-287); reference only."""
+        dims = np.zeros(6, np.int32)
+        code = self.lib.ref_load_cache(path.encode(), _p(dims, C.c_int32))
+        return code, dims
 
     def attention_probe(self, q, k, offsets):
         q = np.ascontiguousarray(q, np.float32)

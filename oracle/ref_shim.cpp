@@ -229,6 +229,30 @@ REF_API int ref_gen_synthetic(uint64_t seed, int layers, int q_heads, int kv_hea
     });
 }
 
+// RDKVC001 cache container (cache.cpp:205-287): writes gen_synthetic_cache(seed, shape) with
+// save_cache_file; ref_load_cache runs load_cache_file and returns its status + dims
+// (L, H_q, H_kv, d, T, S_w) — the golden behaviour for the device loader.
+REF_API int ref_save_cache(uint64_t seed, int layers, int q_heads, int kv_heads, int d, int t_len,
+                           int probe_window, const char* path) {
+    return guarded([&] {
+        auto c = rdkv::gen_synthetic_cache(seed, rdkv::CacheShape{layers, q_heads, kv_heads, d, t_len},
+                                           probe_window, 0, 1.0);
+        rdkv::save_cache_file(c, path);
+    });
+}
+
+REF_API int ref_load_cache(const char* path, int* dims) {
+    return guarded([&] {
+        auto c = rdkv::load_cache_file(path);
+        dims[0] = c.shape.layers;
+        dims[1] = c.shape.q_heads;
+        dims[2] = c.shape.kv_heads;
+        dims[3] = c.shape.head_dim;
+        dims[4] = c.shape.seq_len;
+        dims[5] = c.probe_window;
+    });
+}
+
 REF_API int ref_attention_probe(const float* q, int rows, const float* k, int t_len, int d,
                                 const int* offsets, double* a) {
     return guarded([&] {

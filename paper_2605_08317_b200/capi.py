@@ -35,6 +35,10 @@ class NumericError(RdkvError, ArithmeticError):
     pass
 
 
+class FormatError(RdkvError):
+    """rdkv::FormatError (errors.hpp:9-11): malformed containers."""
+
+
 STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "numeric error", 3: "format error", 4: "CUDA error"}
 
 
@@ -45,6 +49,8 @@ def raise_for(code: int, what: str) -> None:
         raise InvalidArgument(code, what)
     if code == RDKV_ENUMERIC:
         raise NumericError(code, what)
+    if code == RDKV_EFORMAT:
+        raise FormatError(code, what)
     raise RdkvError(code, what)
 
 
@@ -107,8 +113,16 @@ class BisectResult(C.Structure):
                 ("converged", C.c_int32), ("status", C.c_int32)]
 
 
+class CacheHeader(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("q_heads", C.c_int32), ("kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("seq_len", C.c_int32), ("probe_window", C.c_int32),
+                ("payload_offset", C.c_int64), ("payload_bytes", C.c_int64)]
+
+
 _VP = C.c_void_p
 _SIGS = {
+    "rdkv_cache_read_header": (C.c_int, [C.c_char_p, C.POINTER(CacheHeader)]),
+    "rdkv_cuda_cache_load": (C.c_int, [C.c_char_p, C.POINTER(CacheHeader), _VP, _VP, _VP, C.c_int32, _VP]),
     "rdkv_cuda_weights_workspace": (C.c_size_t, [C.POINTER(Shape), C.c_int32]),
     "rdkv_cuda_weights": (C.c_int, [_VP, _VP, C.c_int32, C.POINTER(Shape), C.c_int32, C.c_int32,
                                     _VP, _VP, _VP, C.c_size_t, _VP]),

@@ -16,6 +16,7 @@ the native sm_100a kernels of _lib/librdkv_b200.so.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -89,6 +90,47 @@ def generate(shape, dtype=torch.float16, seed=1, tensor=0, first_index=0, seq_le
         out.data_ptr(), _dtype_code(out), seed, tensor, first_index, out.numel(), d, t_len,
         outlier_channels, float(outlier_scale), hh_stride, float(hh_boost), _stream()), "generate")
     return out
+
+
+# ---- RDKVC001 containers -------------------------------------------------------
+@dataclass
+class DeviceCache:
+    """KVCache (cache.hpp:90-107) resident on the device in unit order (unit = l*H_kv + h):
+    k, v [U, T, d]; probe_q [U, g, S_w, d]."""
+
+    k: torch.Tensor
+    v: torch.Tensor
+    probe_q: torch.Tensor
+    layers: int
+    q_heads: int
+    kv_heads: int
+    probe_window: int
+
+    @property
+    def group(self) -> int:
+        return self.q_heads // self.kv_heads
+
+
+def read_cache_header(path: str) -> capi.CacheHeader:
+    """Header of an RDKVC001 container, load_cache's checks (cache.cpp:228-287); host only."""
+    h = capi.CacheHeader()
+    raise_for(capi.lib().rdkv_cache_read_header(os.fsencode(path), C.byref(h)), f"load_cache_file({path})")
+    return h
+
+
+def load_cache_file(path: str, dtype=torch.float16, device="cuda") -> DeviceCache:
+    """load_cache_file (cache.cpp:289-295) straight to device memory: the payload is streamed
+    into k / v / probe_q in the container's own order (no host KVCache)."""
+    h = read_cache_header(path)
+    U, T, d = h.layers * h.kv_heads, h.seq_len, h.head_dim
+    g = h.q_heads // h.kv_heads
+    k = torch.empty((U, T, d), dtype=dtype, device=device)
+    v = torch.empty_like(k)
+    q = torch.empty((U, g, h.probe_window, d), dtype=dtype, device=device)
+    raise_for(capi.lib().rdkv_cuda_cache_load(os.fsencode(path), C.byref(h), k.data_ptr(), v.data_ptr(),
+                                              q.data_ptr(), _dtype_code(k), _stream()),
+              f"load_cache_file({path})")
+    return DeviceCache(k, v, q, h.layers, h.q_heads, h.kv_heads, h.probe_window)
 
 
 # ---- K1 / K2 ----------------------------------------------------------------

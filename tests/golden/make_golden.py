@@ -144,6 +144,79 @@ def make_mckp():
     np.savez_compressed(os.path.join(HERE, "mckp.npz"), **out)
 
 
+def make_cache_io():
+    """RDKVC001 containers (cache.cpp:205-287): one written by the reference's save_cache_file
+    plus byte-level variants, each with the status + dims of the reference's load_cache_file."""
+    import json
+    import struct
+    import tempfile
+    tmp = tempfile.mkdtemp()
+    base_path = os.path.join(tmp, "base.rdkvc")
+    ref.save_cache(3, 2, 4, 2, 8, 16, 4, base_path)
+    base = open(base_path, "rb").read()
+    hlen = struct.unpack("<I", base[8:12])[0]
+    htext = base[12:12 + hlen].decode()
+    payload = base[12 + hlen:]
+    hdr = json.loads(htext)
+
+    def with_header(text, pl=payload):
+        t = text.encode()
+        return b"RDKVC001" + struct.pack("<I", len(t)) + t + pl
+
+    def edit(**kw):
+        h = dict(hdr)
+        for k, v in kw.items():
+            if v is None:
+                h.pop(k)
+            else:
+                h[k] = v
+        return with_header(json.dumps(h, separators=(",", ":")))
+
+    nan_pl = bytearray(payload)
+    kv_bytes = 2 * 2 * 16 * 8 * 4
+    nan_pl[kv_bytes + 40:kv_bytes + 44] = struct.pack("<f", float("nan"))
+    inf_pl = bytearray(payload)
+    inf_pl[-4:] = struct.pack("<f", float("inf"))
+    big_pl = bytearray(payload)
+    big_pl[4:8] = struct.pack("<f", 1.0e6)
+    variants = {
+        "ok": base,
+        "pretty_extra_keys": with_header(json.dumps(dict(hdr, note={"a": [1, 2.5, None, True]}), indent=2)),
+        "float_dim": with_header(htext.replace('"d":8', '"d":8.0')),
+        "bad_magic": b"RDKVC002" + base[8:],
+        "short_file": base[:5],
+        "no_length": base[:10],
+        "hlen_zero": b"RDKVC001" + struct.pack("<I", 0) + base[12:],
+        "hlen_huge": b"RDKVC001" + struct.pack("<I", (1 << 20) + 1) + base[12:],
+        "header_truncated": base[:12 + hlen - 3],
+        "bad_json": with_header("{\"L\":2,"),
+        "json_trailing": with_header(htext + " x"),
+        "not_object": with_header("[1,2]"),
+        "missing_T": edit(T=None),
+        "string_L": edit(L="2"),
+        "dtype_f16": edit(dtype="f16"),
+        "dtype_missing": edit(dtype=None),
+        "q_not_multiple": edit(H_q=3),
+        "zero_layers": edit(L=0),
+        "sw_too_large": edit(S_w=17),
+        "sw_zero": edit(S_w=0),
+        "payload_truncated": base[:-4],
+        "payload_trailing": base + b"\0",
+        "nan_in_v": with_header(htext, bytes(nan_pl)),
+        "inf_in_q": with_header(htext, bytes(inf_pl)),
+        "fp16_overflow": with_header(htext, bytes(big_pl)),
+    }
+    out = {"names": np.array(list(variants))}
+    for i, (name, data) in enumerate(variants.items()):
+        p = os.path.join(tmp, f"v{i}.rdkvc")
+        open(p, "wb").write(data)
+        code, dims = ref.load_cache_status(p)
+        out[f"bytes_{name}"] = np.frombuffer(data, np.uint8)
+        out[f"status_{name}"] = np.int32(code)
+        out[f"dims_{name}"] = dims
+    np.savez_compressed(os.path.join(HERE, "cache_io.npz"), **out)
+
+
 def make_c1():
     """BASELINE configs[0]: 1 layer, 32 q / 8 kv heads, d=128, T=4096, n=128."""
     L, Hq, Hkv, d, T, Sw = 1, 32, 8, 128, 4096, 32
@@ -183,6 +256,7 @@ if __name__ == "__main__":
     make_trizone()
     make_mckp()
     make_c1()
+    make_cache_io()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
