@@ -368,6 +368,30 @@ RDKV_API int rdkv_cache_read_header(const char* path, rdkv_cache_header* header)
 RDKV_API int rdkv_cuda_cache_load(const char* path, const rdkv_cache_header* header, void* k,
                                   void* v, void* probe_q, int32_t dtype, void* stream);
 
+/* ---- ε calibration (calibrate_epsilon, quantizer.cpp:200-284) ------------ */
+/* Per-job partials for one cache: values = V (granularity 0, token units =
+ * rows of d) or K (granularity 1, channel units = columns of seq_len), device
+ * [jobs][seq_len][head_dim] with job = l*H_kv + h (a cache's job order).
+ * widths [n_widths]: the BitSet (validate_relaxed rules, else RDKV_EINVAL).
+ * err_sum [jobs][max(1, #finite widths)] f64 and count [jobs] i64 (device):
+ * per job, the sum of unit NMSEs in unit order for each finite width
+ * (ascending) and the number of nonzero-energy units. RDKV_ENUMERIC when a
+ * value is non-finite. Synchronizes `stream`. */
+RDKV_API size_t rdkv_cuda_calibrate_workspace(int32_t jobs, int32_t seq_len, int32_t head_dim,
+                                              int32_t granularity, int32_t n_widths);
+RDKV_API int rdkv_cuda_calibrate_partials(const void* values, int32_t dtype, int32_t jobs,
+                                          int32_t seq_len, int32_t head_dim, int32_t granularity,
+                                          const int32_t* widths, int32_t n_widths, double* err_sum,
+                                          int64_t* count, void* workspace, size_t workspace_bytes,
+                                          void* stream);
+/* Host: merges host copies of the partials of every job of every cache (in
+ * cache, then job order) into eps [n_widths] (eps(0) = 1, eps(16) = 0) and the
+ * unit count. RDKV_EINVAL for an empty sample or a table that fails
+ * DistortionTable::validate; RDKV_ENUMERIC when every unit has zero norm. */
+RDKV_API int rdkv_calibrate_finalize(const double* err_sum, const int64_t* count, int32_t jobs,
+                                     const int32_t* widths, int32_t n_widths, double* eps,
+                                     int64_t* unit_count);
+
 RDKV_API const char* rdkv_status_string(int status);
 RDKV_API int rdkv_version(void);
 

@@ -221,6 +221,8 @@ class OracleLib:
             L.ref_model_trizone.argtypes = [C.c_void_p, C.c_int, C.c_int]
             L.ref_model_trizone.restype = C.c_void_p
             L.ref_model_decode.argtypes = [C.c_void_p, F32, F64, F64]
+            L.ref_calibrate.argtypes = [F32, F32, F32] + [C.c_int] * 8 + [I32, C.c_int, F64,
+                                                                        C.POINTER(C.c_longlong)]
             L.ref_save_cache.argtypes = [C.c_uint64] + [C.c_int] * 6 + [C.c_char_p]
             L.ref_load_cache.argtypes = [C.c_char_p, I32]
         else:
@@ -249,6 +251,22 @@ class OracleLib:
         """save_cache_file(gen_synthetic_cache(...)) (cache.cpp:205-226); reference only."""
         self._check(self.lib.ref_save_cache(seed, layers, q_heads, kv_heads, d, t_len, probe_window,
                                             path.encode()), "save_cache")
+
+    def calibrate(self, k, v, q, granularity, widths):
+        """calibrate_epsilon (quantizer.cpp:200-284) over caches k, v [n][L][H_kv][T][d],
+        q [n][L][H_q][S_w][d]; returns (eps [n_widths], unit_count). Reference only."""
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        q = np.ascontiguousarray(q, np.float32)
+        n, L, Hkv, T, d = k.shape
+        Hq, Sw = q.shape[2], q.shape[3]
+        w = np.ascontiguousarray(widths, np.int32)
+        eps = np.zeros(len(w), np.float64)
+        units = C.c_longlong(0)
+        self._check(self.lib.ref_calibrate(_p(k, C.c_float), _p(v, C.c_float), _p(q, C.c_float), n, L, Hq,
+                                           Hkv, d, T, Sw, granularity, _p(w, C.c_int), len(w),
+                                           _p(eps, C.c_double), C.byref(units)), "calibrate")
+        return eps, units.value
 
     def load_cache_status(self, path):
         """(status, dims) of load_cache_file (cache.cpp:228-287); reference only."""

@@ -402,6 +402,28 @@ REF_API int ref_tz_canon(const void* tz, int* kept, uint8_t* vcodes, float* vsca
                     kscale, kzero, vfp, kfp, payload, segtab, nseg, perm, nperm);
 }
 
+// ---- calibrate_epsilon (quantizer.cpp:200-284) over n_caches caches of one shape, stored
+// back to back (k, v [n][L][H_kv][T][d], q [n][L][H_q][S_w][d]); eps_out [n_widths].
+REF_API int ref_calibrate(const float* k, const float* v, const float* q, int n_caches, int layers,
+                          int q_heads, int kv_heads, int d, int t_len, int probe_rows, int granularity,
+                          const int* widths, int n_widths, double* eps_out, long long* units_out) {
+    return guarded([&] {
+        std::vector<rdkv::KVCache> caches;
+        const std::size_t kv_n = std::size_t(layers) * kv_heads * t_len * d;
+        const std::size_t q_n = std::size_t(layers) * q_heads * probe_rows * d;
+        for (int c = 0; c < n_caches; ++c)
+            caches.push_back(cache_from(k + c * kv_n, v + c * kv_n, q + c * q_n, layers, q_heads, kv_heads,
+                                        d, t_len, probe_rows));
+        rdkv::BitSet bits;
+        bits.widths.assign(widths, widths + n_widths);
+        auto t = rdkv::calibrate_epsilon(caches, granularity == 0 ? rdkv::Granularity::token
+                                                                  : rdkv::Granularity::channel,
+                                         bits);
+        for (int i = 0; i < n_widths; ++i) eps_out[i] = t.eps[i].second;
+        *units_out = std::stoll(t.provenance.substr(t.provenance.find("), ") + 3));
+    });
+}
+
 // ---- whole-model driver (CPU baseline) -----------------------------------
 
 REF_API void* ref_model_build(const float* k, const float* v, const float* q, int layers, int q_heads,

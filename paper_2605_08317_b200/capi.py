@@ -121,6 +121,10 @@ class CacheHeader(C.Structure):
 
 _VP = C.c_void_p
 _SIGS = {
+    "rdkv_cuda_calibrate_workspace": (C.c_size_t, [C.c_int32] * 5),
+    "rdkv_cuda_calibrate_partials": (C.c_int, [_VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                               _VP, C.c_int32, _VP, _VP, _VP, C.c_size_t, _VP]),
+    "rdkv_calibrate_finalize": (C.c_int, [_VP, _VP, C.c_int32, _VP, C.c_int32, _VP, _VP]),
     "rdkv_cache_read_header": (C.c_int, [C.c_char_p, C.POINTER(CacheHeader)]),
     "rdkv_cuda_cache_load": (C.c_int, [C.c_char_p, C.POINTER(CacheHeader), _VP, _VP, _VP, C.c_int32, _VP]),
     "rdkv_cuda_weights_workspace": (C.c_size_t, [C.POINTER(Shape), C.c_int32]),

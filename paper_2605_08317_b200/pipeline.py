@@ -133,6 +133,46 @@ def load_cache_file(path: str, dtype=torch.float16, device="cuda") -> DeviceCach
     return DeviceCache(k, v, q, h.layers, h.q_heads, h.kv_heads, h.probe_window)
 
 
+# ---- ε calibration -------------------------------------------------------------
+GRANULARITY = {"token": 0, "channel": 1}
+
+
+def calibrate_epsilon(caches, granularity="token", widths=(0, 2, 4, 8, 16)):
+    """calibrate_epsilon (quantizer.cpp:200-284) on the device: `caches` is a list of
+    DeviceCache (or (k, v) pairs of [L*H_kv, T, d] device tensors). Token granularity
+    calibrates on V rows, channel granularity on K columns. Returns (eps [n_widths] as a
+    {width: eps} dict, unit_count); bit-identical to the reference for f32 inputs."""
+    if not caches:
+        raise capi.InvalidArgument(capi.RDKV_EINVAL, "calibrate_epsilon: empty sample")
+    gran = GRANULARITY[granularity] if isinstance(granularity, str) else int(granularity)
+    w = np.ascontiguousarray(widths, np.int32)
+    nq = max(1, int(np.isin(w, (2, 4, 8)).sum()))
+    L = capi.lib()
+    sums, counts = [], []
+    for c in caches:
+        k, v = (c.k, c.v) if isinstance(c, DeviceCache) else c
+        x = v if gran == 0 else k
+        _check_cuda(x)
+        x = x.contiguous()
+        jobs, T, d = x.shape
+        ws_bytes = L.rdkv_cuda_calibrate_workspace(jobs, T, d, gran, nq)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=x.device)
+        err = torch.empty((jobs, nq), dtype=torch.float64, device=x.device)
+        cnt = torch.empty(jobs, dtype=torch.int64, device=x.device)
+        raise_for(L.rdkv_cuda_calibrate_partials(x.data_ptr(), _dtype_code(x), jobs, T, d, gran,
+                                                 w.ctypes.data, len(w), err.data_ptr(), cnt.data_ptr(),
+                                                 ws.data_ptr(), ws_bytes, _stream()), "calibrate_epsilon")
+        sums.append(err.cpu().numpy())
+        counts.append(cnt.cpu().numpy())
+    err_h = np.ascontiguousarray(np.concatenate(sums), np.float64)
+    cnt_h = np.ascontiguousarray(np.concatenate(counts), np.int64)
+    eps = np.zeros(len(w), np.float64)
+    units = C.c_int64(0)
+    raise_for(L.rdkv_calibrate_finalize(err_h.ctypes.data, cnt_h.ctypes.data, len(cnt_h), w.ctypes.data,
+                                        len(w), eps.ctypes.data, C.byref(units)), "calibrate_epsilon")
+    return {int(b): float(e) for b, e in zip(w, eps)}, int(units.value)
+
+
 # ---- K1 / K2 ----------------------------------------------------------------
 def compute_weights(k: torch.Tensor, probe_q: torch.Tensor, window=32, pool_kernel=5,
                     kv_heads=1):

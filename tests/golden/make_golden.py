@@ -217,6 +217,62 @@ def make_cache_io():
     np.savez_compressed(os.path.join(HERE, "cache_io.npz"), **out)
 
 
+CALIB_CASES = [
+    # (name, seeds, (L, Hq, Hkv, d, T), S_w, outliers, scale, widths, edit)
+    ("basic", [1], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 2, 4, 8, 16], None),
+    ("two_caches", [1, 2], (2, 4, 2, 16, 64), 16, 0, 1.0, [0, 2, 4, 8, 16], None),
+    ("outliers", [7], (1, 2, 2, 32, 128), 32, 3, 100.0, [0, 2, 4, 8, 16], None),
+    ("zero_units", [4], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 2, 4, 8, 16], "zero_some"),
+    ("widths_0_4_16", [5], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 4, 16], None),
+    ("widths_0_16", [5], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 16], None),
+    ("widths_2_8", [6], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 2, 8, 16], None),
+    ("fp16_values", [8], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 2, 4, 8, 16], "fp16"),
+    ("all_zero", [1], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 2, 4, 8, 16], "zero_all"),
+    ("non_finite", [1], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 2, 4, 8, 16], "nan"),
+    ("constant_units", [1], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 2, 4, 8, 16], "const"),
+    ("bad_widths", [1], (1, 4, 2, 16, 64), 16, 0, 1.0, [0, 3, 16], None),
+]
+
+
+def make_calib():
+    """calibrate_epsilon (quantizer.cpp:200-284) on the reference, both granularities."""
+    out = {"names": np.array([c[0] for c in CALIB_CASES])}
+    for name, seeds, (L, Hq, Hkv, d, T), sw, oc, osc, widths, ed in CALIB_CASES:
+        ks, vs, qs = [], [], []
+        for s in seeds:
+            k, v, q = ref.gen_synthetic(s, L, Hq, Hkv, d, T, sw, oc, osc)
+            ks.append(k), vs.append(v), qs.append(q)
+        k, v, q = np.stack(ks), np.stack(vs), np.stack(qs)
+        if ed == "zero_some":
+            v[0, 0, 0, 3:9] = 0.0
+            v[0, 0, 1, 60] = 0.0
+            k[0, 0, 1, :, 5] = 0.0
+            k[0, 0, 0, :, 0] = 0.0
+        elif ed == "fp16":
+            k, v = k.astype(np.float16).astype(np.float32), v.astype(np.float16).astype(np.float32)
+        elif ed == "zero_all":
+            k[:] = 0.0
+            v[:] = 0.0
+        elif ed == "nan":
+            k[0, 0, 1, 7, 3] = np.nan
+            v[0, 0, 0, 9, 2] = np.inf
+        elif ed == "const":
+            k[:] = 1.5
+            v[:] = -0.25
+        out[f"k_{name}"], out[f"v_{name}"] = k, v
+        out[f"widths_{name}"] = np.array(widths, np.int32)
+        for gran in (0, 1):
+            try:
+                eps, units = ref.calibrate(k, v, q, gran, widths)
+                st = 0
+            except RuntimeError as e:  # OracleError
+                eps, units, st = np.zeros(len(widths)), 0, e.code
+            out[f"eps_{name}_{gran}"] = eps
+            out[f"units_{name}_{gran}"] = np.int64(units)
+            out[f"status_{name}_{gran}"] = np.int32(st)
+    np.savez_compressed(os.path.join(HERE, "calib.npz"), **out)
+
+
 def make_c1():
     """BASELINE configs[0]: 1 layer, 32 q / 8 kv heads, d=128, T=4096, n=128."""
     L, Hq, Hkv, d, T, Sw = 1, 32, 8, 128, 4096, 32
@@ -257,6 +313,7 @@ if __name__ == "__main__":
     make_mckp()
     make_c1()
     make_cache_io()
+    make_calib()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
