@@ -298,6 +298,24 @@ RDKV_API int rdkv_cuda_tile_logits(const uint8_t* arena, const int64_t* tile_off
                                    int32_t group, int32_t head_dim, const float* q, int32_t max_slots,
                                    int32_t max_kslots, float* logits, void* stream);
 
+/* dual_bound (allocator.cpp:218-246) for every instance of a batched
+ * rdkv_cuda_mckp_bisect, at that instance's final lambda (solved[i].lambda,
+ * device): weights [instances][n] f32, total_budget = target · n (the
+ * run_sweep budget, sweep.cpp:95-101), out [instances] (device). status
+ * RDKV_EINVAL per instance for a negative / non-finite weight or lambda. */
+typedef struct {
+    double g_lambda;
+    double primal;
+    double gap;
+    int32_t feasible;
+    int32_t status;
+} rdkv_dual_bound_result;
+
+RDKV_API int rdkv_cuda_dual_bound(const float* weights, int32_t instances, int32_t n,
+                                  const int32_t* widths, const double* eps, int32_t n_widths,
+                                  const rdkv_bisect_result* solved, double total_budget,
+                                  rdkv_dual_bound_result* out, void* stream);
+
 /* ---- Host-side tile inspection ----------------------------------------- */
 /* Tile header fields. */
 typedef struct {

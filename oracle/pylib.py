@@ -223,6 +223,7 @@ class OracleLib:
             L.ref_model_decode.argtypes = [C.c_void_p, F32, F64, F64]
             L.ref_calibrate.argtypes = [F32, F32, F32] + [C.c_int] * 8 + [I32, C.c_int, F64,
                                                                         C.POINTER(C.c_longlong)]
+            L.ref_run_sweep.argtypes = [F32, F32, F32] + [C.c_int] * 7 + [F64, C.c_int, C.POINTER(Config), F64]
             L.ref_save_cache.argtypes = [C.c_uint64] + [C.c_int] * 6 + [C.c_char_p]
             L.ref_load_cache.argtypes = [C.c_char_p, I32]
         else:
@@ -267,6 +268,23 @@ class OracleLib:
                                            Hkv, d, T, Sw, granularity, _p(w, C.c_int), len(w),
                                            _p(eps, C.c_double), C.byref(units)), "calibrate")
         return eps, units.value
+
+    def run_sweep(self, k, v, q, grid, cfg):
+        """run_sweep (sweep.cpp:40-114) over caches k, v [n][L][H_kv][T][d], q [n][L][H_q][S_w][d];
+        rows [n*len(grid)][5] = (seq_id, avg_bits, primal, dual, feasible). Reference only."""
+        k = np.ascontiguousarray(k, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        q = np.ascontiguousarray(q, np.float32)
+        n, L, Hkv, T, d = k.shape
+        Hq, Sw = q.shape[2], q.shape[3]
+        g = np.ascontiguousarray(grid, np.float64)
+        if not isinstance(cfg, Config):
+            cfg = Config.from_buffer_copy(bytes(cfg))  # same layout (test_struct_layouts_match_oracle)
+        rows = np.zeros((n * len(g), 5), np.float64)
+        self._check(self.lib.ref_run_sweep(_p(k, C.c_float), _p(v, C.c_float), _p(q, C.c_float), n, L, Hq, Hkv,
+                                           d, T, Sw, _p(g, C.c_double), len(g), C.byref(cfg),
+                                           _p(rows, C.c_double)), "run_sweep")
+        return rows
 
     def load_cache_status(self, path):
         """(status, dims) of load_cache_file (cache.cpp:228-287); reference only."""

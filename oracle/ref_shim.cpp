@@ -23,6 +23,7 @@
 #include "rdkv/parallel.hpp"
 #include "rdkv/pipeline.hpp"
 #include "rdkv/quantizer.hpp"
+#include "rdkv/sweep.hpp"
 #include "rdkv/trizone.hpp"
 #include "rdkv/weights.hpp"
 
@@ -421,6 +422,31 @@ REF_API int ref_calibrate(const float* k, const float* v, const float* q, int n_
                                          bits);
         for (int i = 0; i < n_widths; ++i) eps_out[i] = t.eps[i].second;
         *units_out = std::stoll(t.provenance.substr(t.provenance.find("), ") + 3));
+    });
+}
+
+// ---- run_sweep (sweep.cpp:40-114) over n_caches caches of one shape; rows [n_rows][5] =
+// (seq_id, avg_bits, primal, dual, feasible) in the reference's (avg_bits, seq_id) order.
+REF_API int ref_run_sweep(const float* k, const float* v, const float* q, int n_caches, int layers,
+                          int q_heads, int kv_heads, int d, int t_len, int probe_rows, const double* grid,
+                          int n_grid, const Cfg* cfg, double* rows) {
+    return guarded([&] {
+        std::vector<rdkv::KVCache> caches;
+        const std::size_t kv_n = std::size_t(layers) * kv_heads * t_len * d;
+        const std::size_t q_n = std::size_t(layers) * q_heads * probe_rows * d;
+        for (int c = 0; c < n_caches; ++c)
+            caches.push_back(cache_from(k + c * kv_n, v + c * kv_n, q + c * q_n, layers, q_heads, kv_heads,
+                                        d, t_len, probe_rows));
+        const auto p = pipeline_of(*cfg);
+        auto r = rdkv::run_sweep(caches, std::span<const double>(grid, n_grid), table_of(*cfg, true),
+                                 table_of(*cfg, false), bitset_of(*cfg), p.solver, p.probe);
+        for (std::size_t i = 0; i < r.rows.size(); ++i) {
+            rows[5 * i + 0] = r.rows[i].seq_id;
+            rows[5 * i + 1] = r.rows[i].avg_bits;
+            rows[5 * i + 2] = r.rows[i].primal;
+            rows[5 * i + 3] = r.rows[i].dual;
+            rows[5 * i + 4] = r.rows[i].feasible ? 1.0 : 0.0;
+        }
     });
 }
 

@@ -119,8 +119,14 @@ class CacheHeader(C.Structure):
                 ("payload_offset", C.c_int64), ("payload_bytes", C.c_int64)]
 
 
+class DualBoundResult(C.Structure):
+    _fields_ = [("g_lambda", C.c_double), ("primal", C.c_double), ("gap", C.c_double),
+                ("feasible", C.c_int32), ("status", C.c_int32)]
+
+
 _VP = C.c_void_p
 _SIGS = {
+    "rdkv_cuda_dual_bound": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP, _VP, C.c_int32, _VP, C.c_double, _VP, _VP]),
     "rdkv_cuda_calibrate_workspace": (C.c_size_t, [C.c_int32] * 5),
     "rdkv_cuda_calibrate_partials": (C.c_int, [_VP, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                                _VP, C.c_int32, _VP, _VP, _VP, C.c_size_t, _VP]),

@@ -173,6 +173,81 @@ def calibrate_epsilon(caches, granularity="token", widths=(0, 2, 4, 8, 16)):
     return {int(b): float(e) for b, e in zip(w, eps)}, int(units.value)
 
 
+# ---- rate sweep with duality bounds -------------------------------------------
+def mckp_bisect_batched(weights, widths, eps, target, tolerance=1e-2, max_iterations=64, strict=True):
+    """mckp_bisect (allocator.cpp:135-216) over every row of weights [I, n] (device);
+    returns (bits [I, n] u8, results [I] rdkv_bisect_result bytes, device)."""
+    _check_cuda(weights)
+    inst, n = weights.shape
+    w = np.ascontiguousarray(widths, np.int32)
+    e = np.ascontiguousarray(eps, np.float64)
+    bits = torch.empty((inst, n), dtype=torch.uint8, device=weights.device)
+    res = torch.empty(inst * C.sizeof(capi.BisectResult), dtype=torch.uint8, device=weights.device)
+    raise_for(capi.lib().rdkv_cuda_mckp_bisect(weights.data_ptr(), inst, n, w.ctypes.data, e.ctypes.data, len(w),
+                                               float(target), float(tolerance), int(max_iterations), int(strict),
+                                               bits.data_ptr(), res.data_ptr(), _stream()), "mckp_bisect")
+    return bits, res
+
+
+def dual_bound_batched(weights, widths, eps, solved, total_budget):
+    """dual_bound (allocator.cpp:218-246) of every row at its solved lambda (device)."""
+    inst, n = weights.shape
+    w = np.ascontiguousarray(widths, np.int32)
+    e = np.ascontiguousarray(eps, np.float64)
+    out = torch.empty(inst * C.sizeof(capi.DualBoundResult), dtype=torch.uint8, device=weights.device)
+    raise_for(capi.lib().rdkv_cuda_dual_bound(weights.data_ptr(), inst, n, w.ctypes.data, e.ctypes.data, len(w),
+                                              solved.data_ptr(), float(total_budget), out.data_ptr(), _stream()),
+              "dual_bound")
+    return out
+
+
+def _structs(buf: torch.Tensor, ctype):
+    raw = buf.cpu().numpy().tobytes()
+    size = C.sizeof(ctype)
+    return [ctype.from_buffer_copy(raw, i * size) for i in range(len(raw) // size)]
+
+
+def run_sweep(caches, grid, cfg):
+    """run_sweep (sweep.cpp:40-114) on the device: stage-1 weights once per cache, then per
+    grid value a strict-budget bisection of every (layer, KV head) on both sides plus the dual
+    bound at each final lambda; sums merge in head order on the host. `caches`: DeviceCache
+    list. Returns rows (seq_id, avg_bits, primal, dual, feasible) ordered by (avg_bits, seq_id)."""
+    grid = [float(b) for b in grid]
+    if not grid:
+        raise capi.InvalidArgument(capi.RDKV_EINVAL, "run_sweep: empty grid")
+    if any(not (b > 0.0) or b > 16.0 for b in grid):
+        raise capi.InvalidArgument(capi.RDKV_EINVAL, "run_sweep: grid values must be in (0, 16]")
+    if cfg.window < 1 or cfg.pool_kernel < 1 or cfg.pool_kernel % 2 == 0:
+        raise capi.InvalidArgument(capi.RDKV_EINVAL, "run_sweep: ProbeConfig")
+    widths = [cfg.widths[i] for i in range(cfg.n_widths)]
+    eps_v = [cfg.eps_v[i] for i in range(cfg.n_widths)]
+    eps_k = [cfg.eps_k[i] for i in range(cfg.n_widths)]
+    rows = []
+    for seq, c in enumerate(caches):
+        window = min(cfg.window, c.probe_window)
+        w_t, w_c = compute_weights(c.k, c.probe_q, window=window, pool_kernel=cfg.pool_kernel,
+                                   kv_heads=c.kv_heads)
+        T, d = w_t.shape[1], w_c.shape[1]
+        for target in grid:
+            side = []
+            for w, eps, n in ((w_t, eps_v, T), (w_c, eps_k, d)):
+                _, res = mckp_bisect_batched(w, widths, eps, target, cfg.tolerance, cfg.max_iterations, True)
+                db = dual_bound_batched(w, widths, eps, res, target * float(n))
+                side.append((_structs(res, capi.BisectResult), _structs(db, capi.DualBoundResult)))
+            primal = dual = 0.0
+            feasible = True
+            for (vr, vb), (kr, kb) in [((side[0][0][i], side[0][1][i]), (side[1][0][i], side[1][1][i]))
+                                       for i in range(w_t.shape[0])]:
+                for r in (vr, kr, vb, kb):
+                    raise_for(r.status, "run_sweep")
+                primal += vr.objective + kr.objective
+                dual += vb.g_lambda + kb.g_lambda
+                feasible = feasible and bool(vb.feasible) and bool(kb.feasible)
+            rows.append((seq, target, primal, dual, feasible))
+    rows.sort(key=lambda r: (r[1], r[0]))  # stable, like std::stable_sort
+    return rows
+
+
 # ---- K1 / K2 ----------------------------------------------------------------
 def compute_weights(k: torch.Tensor, probe_q: torch.Tensor, window=32, pool_kernel=5,
                     kv_heads=1):

@@ -273,6 +273,40 @@ def make_calib():
     np.savez_compressed(os.path.join(HERE, "calib.npz"), **out)
 
 
+SWEEP_CASES = [
+    # (name, seeds, (L, Hq, Hkv, d, T), S_w, outliers, scale, grid, cfg kwargs)
+    ("basic", [1], (1, 4, 2, 16, 64), 16, 0, 1.0, [0.25, 0.5, 1.0, 2.0, 4.0, 8.0, 16.0], {}),
+    ("two_caches", [2, 3], (2, 4, 2, 16, 64), 16, 0, 1.0, [2.0, 0.5, 1.0], {}),
+    ("outliers_window", [7], (1, 2, 2, 32, 128), 32, 3, 100.0, [1.0, 3.0], dict(window=8, pool_kernel=3)),
+    ("widths_0_4_16", [5], (1, 4, 2, 16, 64), 16, 0, 1.0, [0.5, 2.0, 6.0], dict(widths=(0, 4, 16))),
+    ("bad_grid_zero", [1], (1, 4, 2, 16, 64), 16, 0, 1.0, [0.0], {}),
+    ("bad_grid_big", [1], (1, 4, 2, 16, 64), 16, 0, 1.0, [1.0, 17.0], {}),
+]
+
+
+def make_sweep():
+    """run_sweep (sweep.cpp:40-114) + dual_bound (allocator.cpp:218-246) on the reference."""
+    from paper_2605_08317_b200.pipeline import default_config
+    out = {"names": np.array([c[0] for c in SWEEP_CASES])}
+    for name, seeds, (L, Hq, Hkv, d, T), sw, oc, osc, grid, kw in SWEEP_CASES:
+        ks, vs, qs = [], [], []
+        for s in seeds:
+            k, v, q = ref.gen_synthetic(s, L, Hq, Hkv, d, T, sw, oc, osc)
+            ks.append(k), vs.append(v), qs.append(q)
+        k, v, q = np.stack(ks), np.stack(vs), np.stack(qs)
+        cfg = default_config(**kw)
+        try:
+            rows, st = ref.run_sweep(k, v, q, grid, cfg), 0
+        except RuntimeError as e:  # OracleError
+            rows, st = np.zeros((0, 5)), e.code
+        out[f"k_{name}"], out[f"v_{name}"], out[f"q_{name}"] = k, v, q
+        out[f"grid_{name}"] = np.array(grid, np.float64)
+        out[f"cfg_{name}"] = np.frombuffer(bytes(cfg), np.uint8)
+        out[f"rows_{name}"] = rows
+        out[f"status_{name}"] = np.int32(st)
+    np.savez_compressed(os.path.join(HERE, "sweep.npz"), **out)
+
+
 def make_c1():
     """BASELINE configs[0]: 1 layer, 32 q / 8 kv heads, d=128, T=4096, n=128."""
     L, Hq, Hkv, d, T, Sw = 1, 32, 8, 128, 4096, 32
@@ -314,6 +348,7 @@ if __name__ == "__main__":
     make_c1()
     make_cache_io()
     make_calib()
+    make_sweep()
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))
