@@ -3,7 +3,7 @@
 // Replaces load_cache / load_cache_file (reference proj/core/src/cache.cpp:228-295) for the
 // device path: the container's payload order (K, V, probe_Q; layer-major, head-major,
 // row-major, cache.cpp:205-226) is already the device unit order, so the payload is
-// streamed with large sequential reads into pinned buffers and copied to its final place —
+// streamed with large parallel reads into a persistent pinned double buffer and copied to its final place —
 // no host re-layout, no host-side KVCache. Reads overlap the H2D copies of the previous
 // chunk (two buffers); fp16 targets are converted on the device, where the finiteness check
 // of KVCache::validate (cache.cpp:114-130) also runs.
@@ -11,7 +11,10 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <atomic>
 #include <cctype>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -344,23 +347,54 @@ extern "C" RDKV_API int rdkv_cuda_cache_load(const char* path, const rdkv_cache_
     } segs[3] = {{static_cast<char*>(k), kv_n}, {static_cast<char*>(v), kv_n}, {static_cast<char*>(probe_q), q_n}};
 
     auto st = static_cast<cudaStream_t>(stream);
-    float* pinned[2] = {nullptr, nullptr};
+    // one process-wide pinned double buffer (allocated on first use, kept): pinned allocation
+    // costs more than reading a small container; loads serialise on it
+    static std::mutex pool_mu;
+    static float* pool[2] = {nullptr, nullptr};
+    std::lock_guard<std::mutex> lock(pool_mu);
+    for (int b = 0; b < 2; ++b)
+        if (!pool[b] && cudaHostAlloc((void**)&pool[b], kChunkBytes, cudaHostAllocDefault) != cudaSuccess) {
+            pool[b] = nullptr;
+            return RDKV_ECUDA;
+        }
     float* stage[2] = {nullptr, nullptr};
     cudaEvent_t done[2] = {nullptr, nullptr};
     int* bad = nullptr;
     int bad_h = 0;
     rc = RDKV_OK;
     const size_t chunk_n = kChunkBytes / 4;
+    const size_t total_n = 2 * kv_n + q_n;
+    const size_t stage_bytes = (total_n < chunk_n ? total_n : chunk_n) * 4;
     auto fail = [&](int code) {
         if (rc == RDKV_OK) rc = code;
     };
     for (int b = 0; b < 2 && rc == RDKV_OK; ++b) {
-        if (cudaHostAlloc((void**)&pinned[b], kChunkBytes, cudaHostAllocDefault) != cudaSuccess) fail(RDKV_ECUDA);
-        else if (cudaMalloc((void**)&stage[b], kChunkBytes) != cudaSuccess) fail(RDKV_ECUDA);
+        if (cudaMallocAsync((void**)&stage[b], stage_bytes, st) != cudaSuccess) fail(RDKV_ECUDA);
         else if (cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming) != cudaSuccess) fail(RDKV_ECUDA);
     }
-    if (rc == RDKV_OK && cudaMalloc((void**)&bad, sizeof(int)) != cudaSuccess) fail(RDKV_ECUDA);
+    if (rc == RDKV_OK && cudaMallocAsync((void**)&bad, sizeof(int), st) != cudaSuccess) fail(RDKV_ECUDA);
     if (rc == RDKV_OK && cudaMemsetAsync(bad, 0, sizeof(int), st) != cudaSuccess) fail(RDKV_ECUDA);
+
+    // page-cache copies are memcpy-bound per thread: a chunk is read by up to kReaders threads
+    constexpr int kReaders = 4;
+    auto read_chunk = [&](float* dst, size_t n, off_t off) {
+        const size_t bytes = n * 4;
+        if (bytes < (size_t(4) << 20)) return read_all(f.fd, dst, bytes, off);
+        std::atomic<bool> ok{true};
+        std::thread th[kReaders];
+        const size_t part = (bytes / kReaders + 4095) & ~size_t(4095);
+        for (int r = 0; r < kReaders; ++r) {
+            const size_t b0 = (size_t)r * part;
+            if (b0 >= bytes) break;
+            const size_t nb = bytes - b0 < part ? bytes - b0 : part;
+            th[r] = std::thread([&, b0, nb] {
+                if (!read_all(f.fd, reinterpret_cast<char*>(dst) + b0, nb, off + (off_t)b0)) ok = false;
+            });
+        }
+        for (auto& t : th)
+            if (t.joinable()) t.join();
+        return ok.load();
+    };
 
     off_t off = (off_t)h->payload_offset;
     int buf = 0;
@@ -372,13 +406,12 @@ extern "C" RDKV_API int rdkv_cuda_cache_load(const char* path, const rdkv_cache_
                 fail(RDKV_ECUDA);
                 break;
             }
-            if (!read_all(f.fd, pinned[buf], n * 4, off)) {
+            if (!read_chunk(pool[buf], n, off)) {
                 fail(RDKV_EFORMAT);  // file changed under us
                 break;
             }
             off += (off_t)(n * 4);
-            // f32: stage then verify in place (the convert kernel copies); f16: convert
-            if (cudaMemcpyAsync(stage[buf], pinned[buf], n * 4, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            if (cudaMemcpyAsync(stage[buf], pool[buf], n * 4, cudaMemcpyHostToDevice, st) != cudaSuccess) {
                 fail(RDKV_ECUDA);
                 break;
             }
@@ -399,13 +432,12 @@ extern "C" RDKV_API int rdkv_cuda_cache_load(const char* path, const rdkv_cache_
         }
     }
     if (bad && cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) fail(RDKV_ECUDA);
-    if (cudaStreamSynchronize(st) != cudaSuccess) fail(RDKV_ECUDA);
-    for (int b = 0; b < 2; ++b) {
-        if (pinned[b]) cudaFreeHost(pinned[b]);
-        if (stage[b]) cudaFree(stage[b]);
+    for (int b = 0; b < 2; ++b)
+        if (stage[b]) cudaFreeAsync(stage[b], st);
+    if (bad) cudaFreeAsync(bad, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) fail(RDKV_ECUDA);  // pool buffers free for the next load
+    for (int b = 0; b < 2; ++b)
         if (done[b]) cudaEventDestroy(done[b]);
-    }
-    if (bad) cudaFree(bad);
     if (rc == RDKV_OK && bad_h) rc = RDKV_ENUMERIC;
     return rc;
 }
