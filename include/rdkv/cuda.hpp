@@ -29,6 +29,7 @@
 #include "rdkv/errors.hpp"
 #include "rdkv/pipeline.hpp"
 #include "rdkv/quantizer.hpp"
+#include "rdkv/sweep.hpp"
 #include "rdkv/trizone.hpp"
 #include "rdkv/weights.hpp"
 
@@ -74,6 +75,18 @@ std::vector<double> fused_k_logits(std::span<const float> q, const TriZoneCache&
 std::vector<double> packed_decode_step(std::span<const float> q, const TriZoneCache& cache);
 // trizone.hpp:91 / trizone.cpp:307-314 (host container: same as the reference)
 void append_new_token(TriZoneCache& cache, std::span<const float> k, std::span<const float> v);
+
+// ---- §8(f): rate sweep, dual bound, ε calibration ----------------------------
+// allocator.hpp:68-69 / allocator.cpp:218-246
+DualBound dual_bound(std::span<const float> weights, const DistortionTable& eps, double lambda,
+                     double total_budget, const BitSet& bits = {});
+// sweep.hpp:31-34 / sweep.cpp:40-114 (weights once per cache, batched strict
+// bisection + dual bound of every (layer, KV head) per grid value)
+SweepResult run_sweep(std::span<const KVCache> sequences, std::span<const double> grid, const DistortionTable& eps_v,
+                      const DistortionTable& eps_k, const BitSet& bits, const SolverConfig& solver,
+                      const ProbeConfig& probe);
+// quantizer.hpp:69-70 / quantizer.cpp:200-284
+DistortionTable calibrate_epsilon(std::span<const KVCache> caches, Granularity granularity, const BitSet& bits = {});
 
 // ---- Device-resident performance API ---------------------------------------
 // All (layer, KV head) tiles of a PackedModel in one device arena, plus a

@@ -999,4 +999,170 @@ PackedModel DevicePackedModel::download() const {
     return m;
 }
 
+
+// ---- §8(f): dual bound, rate sweep, ε calibration ------------------------------
+DualBound dual_bound(std::span<const float> weights, const DistortionTable& eps, double lambda,
+                     double total_budget, const BitSet& bits) {
+    require(lambda >= 0.0 && std::isfinite(lambda), "dual_bound: lambda must be >= 0");  // allocator.cpp:220-222
+    for (float w : weights)
+        require(std::isfinite(w) && w >= 0.0f, "dual_bound: weights must be finite and >= 0");
+    validate_bits_relaxed(bits);
+    require(bits.widths.size() <= 8, "BitSet: too many widths");
+    int32_t widths[8];
+    double e[8];
+    int missing;
+    argmin_table(eps, bits, widths, e, &missing);
+    if (missing >= 0) throw_missing_width(missing);
+    rdkv_bisect_result solved{};
+    solved.lambda = lambda;
+    const int n = static_cast<int>(weights.size());
+    DevBuf w = to_device(weights.data(), std::max<std::size_t>(weights.size(), 1)), sv = to_device(&solved, 1),
+           r(sizeof(rdkv_dual_bound_result));
+    check(rdkv_cuda_dual_bound(w.as<float>(), 1, n, widths, e, static_cast<int32_t>(bits.widths.size()),
+                               sv.as<rdkv_bisect_result>(), total_budget, r.as<rdkv_dual_bound_result>(), nullptr),
+          "dual_bound");
+    sync();
+    const auto res = to_host<rdkv_dual_bound_result>(r.get(), 1)[0];
+    check(res.status, "dual_bound");
+    DualBound out;
+    out.g_lambda = res.g_lambda;
+    out.primal = res.primal;
+    out.feasible = res.feasible != 0;
+    out.gap = res.gap;
+    return out;
+}
+
+SweepResult run_sweep(std::span<const KVCache> sequences, std::span<const double> grid, const DistortionTable& eps_v,
+                      const DistortionTable& eps_k, const BitSet& bits, const SolverConfig& solver,
+                      const ProbeConfig& probe) {
+    require(!grid.empty(), "run_sweep: empty grid");  // sweep.cpp:43-49
+    for (double b : grid) require(b > 0.0 && b <= 16.0, "run_sweep: grid values must be in (0, 16]");
+    require(probe.window >= 1, "ProbeConfig: window must be >= 1");
+    require(probe.pool_kernel >= 1 && probe.pool_kernel % 2 == 1, "ProbeConfig: pool_kernel must be odd and >= 1");
+    validate_bits_relaxed(bits);
+    require(bits.widths.size() <= 8, "BitSet: too many widths");
+    validate_solver(solver);
+    int32_t widths[8];
+    double ev[8], ek[8];
+    int miss_v, miss_k;
+    argmin_table(eps_v, bits, widths, ev, &miss_v);
+    argmin_table(eps_k, bits, widths, ek, &miss_k);
+    const int nw = static_cast<int>(bits.widths.size());
+
+    SweepResult result;
+    for (int seq = 0; seq < static_cast<int>(sequences.size()); ++seq) {
+        const KVCache& cache = sequences[seq];
+        const auto& s = cache.shape;
+        const int L = s.layers, Hkv = s.kv_heads, g = s.q_heads / s.kv_heads, T = s.seq_len, d = s.head_dim;
+        const int Sw = cache.probe_window, U = L * Hkv;
+        for (int l = 0; l < L; ++l) {  // cache.validate(): shapes + finiteness
+            check_finite(MatrixView{cache.k[l].data().data(), Hkv * T, d}, "KVCache");
+            check_finite(MatrixView{cache.v[l].data().data(), Hkv * T, d}, "KVCache");
+            check_finite(MatrixView{cache.probe_q[l].data().data(), s.q_heads * Sw, d}, "KVCache");
+        }
+        const int window = std::min(probe.window, Sw);
+        const std::size_t kn = static_cast<std::size_t>(T) * d, qn = static_cast<std::size_t>(g) * Sw * d;
+        DevBuf k_dev(U * kn * sizeof(float)), q_dev(U * qn * sizeof(float));
+        for (int l = 0; l < L; ++l) {  // unit order l * H_kv + h is the containers' own order
+            cuda_check(cudaMemcpy(k_dev.as<float>() + l * Hkv * kn, cache.k[l].data().data(), Hkv * kn * sizeof(float),
+                                  cudaMemcpyHostToDevice), "H2D");
+            cuda_check(cudaMemcpy(q_dev.as<float>() + l * Hkv * qn, cache.probe_q[l].data().data(),
+                                  Hkv * qn * sizeof(float), cudaMemcpyHostToDevice), "H2D");
+        }
+        rdkv_shape sh{U, T, d, g, Sw, Hkv};
+        const std::size_t ws_bytes = rdkv_cuda_weights_workspace(&sh, window);
+        DevBuf ws(ws_bytes), w_t(U * kn / d * sizeof(float) * 1), w_c(U * static_cast<std::size_t>(d) * sizeof(float));
+        check(rdkv_cuda_weights(k_dev.get(), q_dev.get(), RDKV_F32, &sh, window, probe.pool_kernel, w_t.as<float>(),
+                                w_c.as<float>(), ws.get(), ws_bytes, nullptr),
+              "run_sweep");
+        DevBuf bits_v(U * static_cast<std::size_t>(T)), bits_k(U * static_cast<std::size_t>(d));
+        DevBuf rv(U * sizeof(rdkv_bisect_result)), rk(U * sizeof(rdkv_bisect_result));
+        DevBuf dv(U * sizeof(rdkv_dual_bound_result)), dk(U * sizeof(rdkv_dual_bound_result));
+        for (double target : grid) {
+            if (miss_v >= 0) throw_missing_width(miss_v);
+            if (miss_k >= 0) throw_missing_width(miss_k);
+            check(rdkv_cuda_mckp_bisect(w_t.as<float>(), U, T, widths, ev, nw, target, solver.tolerance,
+                                        solver.max_iterations, 1, bits_v.as<uint8_t>(), rv.as<rdkv_bisect_result>(),
+                                        nullptr),
+                  "mckp_bisect");
+            check(rdkv_cuda_dual_bound(w_t.as<float>(), U, T, widths, ev, nw, rv.as<rdkv_bisect_result>(),
+                                       target * static_cast<double>(T), dv.as<rdkv_dual_bound_result>(), nullptr),
+                  "dual_bound");
+            check(rdkv_cuda_mckp_bisect(w_c.as<float>(), U, d, widths, ek, nw, target, solver.tolerance,
+                                        solver.max_iterations, 1, bits_k.as<uint8_t>(), rk.as<rdkv_bisect_result>(),
+                                        nullptr),
+                  "mckp_bisect");
+            check(rdkv_cuda_dual_bound(w_c.as<float>(), U, d, widths, ek, nw, rk.as<rdkv_bisect_result>(),
+                                       target * static_cast<double>(d), dk.as<rdkv_dual_bound_result>(), nullptr),
+                  "dual_bound");
+            sync();
+            const auto av = to_host<rdkv_bisect_result>(rv.get(), U), ak = to_host<rdkv_bisect_result>(rk.get(), U);
+            const auto bv = to_host<rdkv_dual_bound_result>(dv.get(), U),
+                       bk = to_host<rdkv_dual_bound_result>(dk.get(), U);
+            double primal = 0.0, dual = 0.0;
+            bool feasible = true;
+            for (int u = 0; u < U; ++u) {  // head order (sweep.cpp:94-106)
+                check(av[u].status, "mckp_bisect");
+                check(ak[u].status, "mckp_bisect");
+                check(bv[u].status, "dual_bound");
+                check(bk[u].status, "dual_bound");
+                primal += av[u].objective + ak[u].objective;
+                dual += bv[u].g_lambda + bk[u].g_lambda;
+                feasible = feasible && bv[u].feasible && bk[u].feasible;
+            }
+            result.rows.push_back({seq, target, primal, dual, feasible});
+        }
+    }
+    std::stable_sort(result.rows.begin(), result.rows.end(), [](const SweepPoint& a, const SweepPoint& b) {
+        if (a.avg_bits != b.avg_bits) return a.avg_bits < b.avg_bits;
+        return a.seq_id < b.seq_id;
+    });
+    return result;
+}
+
+DistortionTable calibrate_epsilon(std::span<const KVCache> caches, Granularity granularity, const BitSet& bits) {
+    require(!caches.empty(), "calibrate_epsilon: empty sample");
+    validate_bits_relaxed(bits);
+    require(bits.widths.size() <= 8, "BitSet: too many widths");
+    const std::vector<int32_t> w(bits.widths.begin(), bits.widths.end());
+    int nq = 0;
+    for (int b : w) nq += is_quant_width(b);
+    nq = std::max(nq, 1);
+    const int gran = granularity == Granularity::token ? 0 : 1;
+    std::vector<double> err;
+    std::vector<int64_t> cnt;
+    for (const auto& cache : caches) {
+        const auto& s = cache.shape;
+        const int U = s.layers * s.kv_heads, T = s.seq_len, d = s.head_dim;
+        const std::size_t per_layer = static_cast<std::size_t>(s.kv_heads) * T * d;
+        DevBuf x(std::max<std::size_t>(U * static_cast<std::size_t>(T) * d, 1) * sizeof(float));
+        const auto& src = gran == 0 ? cache.v : cache.k;  // token units: V rows; channel units: K columns
+        for (int l = 0; l < s.layers; ++l)
+            cuda_check(cudaMemcpy(x.as<float>() + l * per_layer, src[l].data().data(), per_layer * sizeof(float),
+                                  cudaMemcpyHostToDevice), "H2D");
+        const std::size_t ws_bytes = rdkv_cuda_calibrate_workspace(U, T, d, gran, nq);
+        DevBuf ws(ws_bytes), e(std::max(U * nq, 1) * sizeof(double)), c(std::max(U, 1) * sizeof(int64_t));
+        check(rdkv_cuda_calibrate_partials(x.get(), RDKV_F32, U, T, d, gran, w.data(), static_cast<int32_t>(w.size()),
+                                           e.as<double>(), c.as<int64_t>(), ws.get(), ws_bytes, nullptr),
+              "quantize_unit");
+        const auto eh = to_host<double>(e.get(), static_cast<std::size_t>(U) * nq);
+        const auto ch = to_host<int64_t>(c.get(), U);
+        err.insert(err.end(), eh.begin(), eh.end());
+        cnt.insert(cnt.end(), ch.begin(), ch.end());
+    }
+    std::vector<double> eps(w.size());
+    int64_t units = 0;
+    const int st = rdkv_calibrate_finalize(err.data(), cnt.data(), static_cast<int32_t>(cnt.size()), w.data(),
+                                           static_cast<int32_t>(w.size()), eps.data(), &units);
+    if (st == RDKV_ENUMERIC) throw NumericError("calibrate_epsilon: all units have zero norm");
+    if (st == RDKV_EINVAL) throw std::invalid_argument("DistortionTable: eps must be strictly decreasing");
+    check(st, "calibrate_epsilon");
+    DistortionTable table;
+    table.granularity = granularity;
+    table.provenance = "calibrated on " + std::to_string(caches.size()) + " cache(s), " + std::to_string(units) + " " +
+                       (gran == 0 ? "token" : "channel") + " units";
+    for (std::size_t i = 0; i < w.size(); ++i) table.eps.emplace_back(w[i], eps[i]);
+    return table;
+}
+
 }  // namespace rdkv::cuda

@@ -18,12 +18,14 @@
 // Prints one line per check and exits non-zero on any failure.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <functional>
 #include <random>
 #include <string>
 #include <vector>
 
 #include "rdkv/cuda.hpp"
+#include "rdkv/sweep.hpp"
 
 namespace {
 
@@ -601,6 +603,72 @@ void pipeline() {
     }
 }
 
+// ---- §8(f): dual bound, rate sweep, ε calibration ---------------------------------
+bool same_bits(double a, double b) { return std::memcmp(&a, &b, sizeof(double)) == 0; }
+
+void rows() {
+    std::vector<rdkv::KVCache> caches;
+    caches.push_back(rdkv::gen_synthetic_cache(31, {2, 8, 2, 64, 512}, 32, 3, 50.0));
+    caches.push_back(rdkv::gen_synthetic_cache(32, {2, 8, 2, 64, 512}, 32, 0, 1.0));
+    for (auto gran : {rdkv::Granularity::token, rdkv::Granularity::channel}) {
+        const char* gname = gran == rdkv::Granularity::token ? "token" : "channel";
+        run(std::string("calibrate_epsilon ") + gname + " 2 caches", [&](std::string& d) {
+            const auto want = rdkv::calibrate_epsilon(caches, gran);
+            const auto got = rdkv::cuda::calibrate_epsilon(caches, gran);
+            bool ok = got.eps.size() == want.eps.size() && got.provenance == want.provenance &&
+                      got.granularity == want.granularity;
+            for (size_t i = 0; ok && i < want.eps.size(); ++i)
+                ok = got.eps[i].first == want.eps[i].first && same_bits(got.eps[i].second, want.eps[i].second);
+            d = got.provenance;
+            return ok;
+        });
+    }
+    run("calibrate_epsilon errors", [&](std::string&) {
+        std::vector<rdkv::KVCache> none;
+        auto zero = rdkv::gen_synthetic_cache(1, {1, 2, 1, 8, 16}, 4, 0, 1.0);
+        for (auto& t : zero.v) std::fill(t.data().begin(), t.data().end(), 0.0f);
+        std::vector<rdkv::KVCache> zs{zero};
+        return throws<std::invalid_argument>([&] { rdkv::cuda::calibrate_epsilon(none, rdkv::Granularity::token); }) &&
+               throws<rdkv::NumericError>([&] { rdkv::calibrate_epsilon(zs, rdkv::Granularity::token); }) &&
+               throws<rdkv::NumericError>([&] { rdkv::cuda::calibrate_epsilon(zs, rdkv::Granularity::token); });
+    });
+    run("dual_bound at 5 lambdas", [&](std::string& d) {
+        Gen g(77);
+        std::vector<float> w(3000);
+        for (auto& x : w) x = std::fabs(g.gauss()) * (g.uni() < 0.05 ? 1000.0f : 1.0f);
+        const auto eps = eps_table(true);
+        bool ok = true;
+        for (double lam : {0.0, 1e-4, 0.01, 0.5, 30.0}) {
+            const auto a = rdkv::dual_bound(w, eps, lam, 2.0 * w.size());
+            const auto b = rdkv::cuda::dual_bound(w, eps, lam, 2.0 * w.size());
+            ok = ok && same_bits(a.g_lambda, b.g_lambda) && same_bits(a.primal, b.primal) && a.feasible == b.feasible &&
+                 same_bits(a.gap, b.gap);
+            if (!ok) d = "lambda " + std::to_string(lam);
+        }
+        return ok && throws<std::invalid_argument>([&] { rdkv::cuda::dual_bound(w, eps, -1.0, 1.0); });
+    });
+    run("run_sweep 2 caches x 5 grid points", [&](std::string& d) {
+        const std::vector<double> grid{2.0, 0.25, 1.0, 4.0, 0.5};
+        const auto ev = eps_table(true), ek = eps_table(false);
+        rdkv::BitSet bits;
+        rdkv::SolverConfig solver;
+        rdkv::ProbeConfig probe;
+        probe.window = 16;
+        const auto want = rdkv::run_sweep(caches, grid, ev, ek, bits, solver, probe);
+        const auto got = rdkv::cuda::run_sweep(caches, grid, ev, ek, bits, solver, probe);
+        bool ok = got.rows.size() == want.rows.size();
+        for (size_t i = 0; ok && i < want.rows.size(); ++i) {
+            const auto &a = want.rows[i], &b = got.rows[i];
+            ok = a.seq_id == b.seq_id && same_bits(a.avg_bits, b.avg_bits) && same_bits(a.primal, b.primal) &&
+                 same_bits(a.dual, b.dual) && a.feasible == b.feasible;
+            if (!ok) d = "row " + std::to_string(i);
+        }
+        return ok && throws<std::invalid_argument>([&] {
+                   rdkv::cuda::run_sweep(caches, std::vector<double>{}, ev, ek, bits, solver, probe);
+               });
+    });
+}
+
 }  // namespace
 
 int main() {
@@ -609,6 +677,7 @@ int main() {
     functions();
     trizone();
     pipeline();
+    rows();
     std::printf("%d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
