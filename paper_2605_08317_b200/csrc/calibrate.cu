@@ -3,7 +3,7 @@
 // The reference walks every (cache, layer, KV head) job, and inside it every unit — a V row
 // (token granularity) or a K column (channel granularity) — quantizes it at each finite width,
 // dequantizes, and adds the unit's NMSE to the job's running sum; jobs merge in job order.
-// Here one thread owns one unit (all widths, fp64, the reference's element order, compiled
+// Here one thread owns a unit (channel units: a (unit, width) pair) (fp64, the reference's element order, compiled
 // with -fmad=false so every multiply-add rounds like the reference's non-FMA x86 build), a
 // second kernel sums the per-unit NMSEs of each job in unit order, and the host merges jobs in
 // order — so the table is bit-identical to the reference's. Channel units are read with
@@ -40,13 +40,21 @@ __device__ __forceinline__ float ld(const T* p) {
 }
 
 // nmse [unit][qw.n] for every unit of every job; NaN marks a zero-energy unit (skipped).
+// Channel units (few and long) run one thread per (unit, width) — the energy / range pass is
+// repeated per width — for qw.n× the parallelism; token units (many and short) run one
+// thread per unit over all widths.
 template <typename T>
 __global__ void __launch_bounds__(256) calib_unit_kernel(const T* __restrict__ values, int jobs, int t_len, int d,
                                                          int channel, QWidths qw, double* __restrict__ nmse,
                                                          int* __restrict__ bad) {
     const long long per_job = channel ? d : t_len;
-    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= (long long)jobs * per_job) return;
+    const long long n_units = (long long)jobs * per_job;
+    const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int split = channel ? qw.n : 1;
+    if (gid >= n_units * split) return;
+    // width-major thread order keeps consecutive threads on consecutive units (coalesced K rows)
+    const int b0 = channel ? (int)(gid / n_units) : 0, b1 = channel ? b0 + 1 : qw.n;
+    const long long g = gid % n_units;
     const long long job = g / per_job, i = g % per_job;
     const T* base;
     long long stride;
@@ -72,20 +80,20 @@ __global__ void __launch_bounds__(256) calib_unit_kernel(const T* __restrict__ v
     }
     double* out = nmse + g * qw.n;
     if (energy == 0.0) {  // account_unit: NMSE undefined, the unit carries no weight
-        for (int b = 0; b < qw.n; ++b) out[b] = __longlong_as_double(0x7ff8000000000000ll);
+        for (int b = b0; b < b1; ++b) out[b] = __longlong_as_double(0x7ff8000000000000ll);
         return;
     }
     if (!finite) {  // quantize_unit: NumericError
         atomicOr(bad, 1);
         return;
     }
-    for (int b = 0; b < qw.n; ++b) {
+    for (int b = b0; b < b1; ++b) {
         const int bits = qw.w[b];
         const double max_code = (double)((1 << bits) - 1);
         double scale, zd;
         calib_params(lo, hi, bits, scale, zd);
-        const double sf = (double)(float)scale;               // stored params.scale
-        const double zp = (double)(long long)zd;               // stored params.zero_point
+        const double sf = (double)(float)scale;  // stored params.scale
+        const double zp = (double)(long long)zd;  // stored params.zero_point
         double err = 0.0;
         for (int j = 0; j < len; ++j) {
             const float x = ld(base + j * stride);
@@ -168,7 +176,7 @@ extern "C" RDKV_API int rdkv_cuda_calibrate_partials(const void* values, int32_t
     RDKV_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), st));
     const long long per_job = granularity ? head_dim : seq_len;
     const long long n_units = (long long)jobs * per_job;
-    const unsigned blocks = (unsigned)((n_units + 255) / 256);
+    const unsigned blocks = (unsigned)((n_units * (granularity ? qw.n : 1) + 255) / 256);
     if (dtype == RDKV_F16)
         calib_unit_kernel<__half><<<blocks, 256, 0, st>>>(static_cast<const __half*>(values), jobs, seq_len,
                                                           head_dim, granularity, qw, nmse, bad);
