@@ -456,6 +456,26 @@ def secondary_configs(P, spec0, model, q, args):
                          "us_per_step": us, "tok_s": spec.batch / (us / 1e6),
                          "roofline_frac": byts / (us / 1e6) / 1e9 / peak, "bytes_per_step": byts}
     del m2, q2
+    # (7) configs[3]: Mistral-7B / Qwen2.5-7B GQA shapes at 64K, budget sweep, with heavy hitters
+    # and 4 outlier K channels (x8) so the V and K tiers span 2/4/8 bits
+    c4 = {}
+    for model, (L, Hq, Hkv), budgets in (("qwen2.5-7b", (28, 28, 4), (64, 256, 1024, 2048)),
+                                         ("mistral-7b", (32, 32, 8), (64, 2048))):
+        for n in budgets:
+            spec = WorkloadSpec(batch=4, layers=L, q_heads=Hq, kv_heads=Hkv, ctx=65536, n_tokens=n, seed=11,
+                                hh_stride=64, hh_boost=1.0, outlier_channels=4, outlier_scale=8.0)
+            m4, _, st4, _ = build(spec)
+            q4 = P.generate((m4.units, spec.group, d), torch.float16, seed=QSEED, tensor=2)
+            us, _ = graph_step_us(P, m4, q4, min(args.steps, 50))
+            byts = m4.decode_bytes(io_bytes=2)
+            c4[f"{model}_n{n}"] = {"us_per_step": us, "tok_s": spec.batch / (us / 1e6),
+                                   "roofline_frac": byts / (us / 1e6) / 1e9 / peak, "bytes_per_step": byts,
+                                   "plan_uniform2": int(m4.plan.uniform2),
+                                   "kept_per_head": float(np.mean([s["n_kept"].mean() for s in st4]))}
+            del m4, q4
+    out["configs3_gqa_64k_budget_sweep"] = {"config": "configs[3]: Qwen2.5-7B (28 layers, 28 q / 4 kv, g=7) and "
+                                                      "Mistral-7B (32 layers, 32 q / 8 kv) KV shapes, 64K ctx, batch 4, "
+                                                      "heavy hitters + 4 outlier K channels x8", "points": c4}
     torch.cuda.empty_cache()
     return out
 

@@ -43,7 +43,7 @@ namespace rdkv_b200 {
 constexpr int kD = 128;        // head_dim of this path
 constexpr int kMaxR = 32;      // ring slots per CTA
 constexpr int kMaxW = 12;      // consumer warps per CTA (13 warps -> <=152 regs)
-constexpr int kMaxSlots = 256; // token slots per tile on this path
+constexpr int kMaxSlots = 4096; // token slots per tile on this path (smem permitting, general_min_smem)
 
 // ---------------------------------------------------------------- PTX helpers
 #define getenv_pair_smsp() (p.smsp_pairs)
@@ -2593,9 +2593,9 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
               : bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true>
               : mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
               : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2> : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
-    static std::atomic<int> smem_set[12][kMaxDevices];
+    static std::atomic<int> smem_set[14][kMaxDevices];  // one slot per instantiation above
     set_smem_once(kern, (int)smem,
-                  smem_set[mix ? 10 + (bulk ? 1 : 0) : g8 ? 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0)
+                  smem_set[mix ? 10 + (g8 ? 2 : 0) + (bulk ? 1 : 0) : g8 ? 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0)
                               : zcf ? 4 + (bulk ? 1 : 0) : bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0],
                   da.dev);
     int blocks = (a->units + W - 1) / W;
@@ -2665,13 +2665,33 @@ using namespace rdkv_b200;
 
 namespace rdkv_b200 {
 
+// Shared-memory footprint of the general body (launch_t) with one consumer warp and
+// one ring slot: the whole tile is staged at once, so long or wide tiles may not fit.
+static size_t general_min_smem(const rdkv_decode_args* a) {
+    const int NT = a->group <= 4 ? 1 : 2;
+    const int qbytes = a->group * kD * (a->io_dtype == RDKV_F16 ? 2 : 4);
+    const size_t slot = (size_t)(a->plan.max_decode_bytes + qbytes + 127) & ~(size_t)127;
+    const int qsteps = (a->plan.max_kq_slots + 31) / 32;
+    const int vsteps = (a->plan.max_slots + 31) / 32 + 2;
+    const int steps = qsteps > vsteps ? qsteps : vsteps;
+    size_t scratch = kDigitBytesOff + (size_t)steps * 2 * NT * 8 * 32;
+    const int s32 = ((a->plan.max_slots + 31) / 32) * 32;
+    const int lg_stride = (s32 > kD ? s32 : kD) + 32 / (4 * NT);
+    scratch += (size_t)4 * NT * lg_stride * 4;
+    if (a->plan.max_zone_b_rows > 0) scratch += (size_t)4 * NT * a->plan.max_zone_b_rows * 4;
+    if (a->zc_len) scratch += (size_t)4 * NT * a->zc_cap * 4;
+    scratch = (scratch + 127) & ~(size_t)127;
+    return 2 * kMaxR * sizeof(uint64_t) + slot + scratch + 4096;
+}
+
 bool mma_supported(const rdkv_decode_args* a) {
     if (a->head_dim != kD || a->group > 8 || !a->tile_decode_bytes) return false;
     if (a->zc_len && a->zc_cap > 1024) return false;
     const rdkv_decode_plan& p = a->plan;
     // uniform 2-bit tiles of any length: u2x (<= 160 slots) or its chunked variant
     if (p.uniform2 && p.max_decode_bytes > 0 && u2x_group_ok(a)) return true;
-    return p.max_decode_bytes > 0 && p.max_slots <= kMaxSlots && p.max_zone_b_rows <= kMaxSlots;
+    if (p.max_decode_bytes <= 0 || p.max_slots > kMaxSlots || p.max_zone_b_rows > kMaxSlots) return false;
+    return general_min_smem(a) <= (size_t)dev_attrs().smem_optin;  // else the CUDA-core kernel
 }
 
 template <int NT, typename IO, bool U2>
@@ -2815,7 +2835,8 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     // uniform 2-bit tiles (the n=128 production shape): warp-pair body by default,
     // kernel 4 selects the one-warp body, kernel 3 the general body
     const bool u2 = a->plan.uniform2 && u2x_group_ok(a) &&
-                    (a->kernel != 3 || a->plan.max_slots > kMaxSlots);  // the general body stops at 256 slots
+                    (a->kernel != 3 || a->plan.max_slots > kMaxSlots ||
+                     general_min_smem(a) > (size_t)dev_attrs().smem_optin);  // general body: tile in smem
     const bool short_u2 = u2 && a->plan.max_slots <= kU2MaxSlots && !a->zc_len && a->plan.uniform2 != 3;
     if (short_u2 && a->kernel == 4) return f16 ? launch_t<1, __half, true>(a, st) : launch_t<1, float, true>(a, st);
     if (short_u2 && a->kernel == 5) return f16 ? launch_pair<__half>(a, st) : launch_pair<float>(a, st);

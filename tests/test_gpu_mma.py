@@ -104,6 +104,37 @@ def test_mma_mixed_classes(cuda, orc, g):
     assert worst < FP16_INPUT_TOL, worst
 
 
+@pytest.mark.parametrize("g", [4, 7])
+def test_mma_long_mixed_tiles(cuda, orc, g):
+    """Mixed-bit tiles well past 256 slots (configs[3] budgets n >= 256) stay on the
+    tensor-core general body while the whole tile fits in shared memory."""
+    rng = np.random.default_rng(500 + g)
+    T = 900 if g <= 4 else 540  # g > 4 runs two 4-head passes with twice the scratch
+    cases = [_random_case(rng, T, g, p_bits=(0.15, 0.35, 0.3, 0.15, 0.05)) for _ in range(6)]
+    worst, model = _run_batch(cuda, orc, cases, g)
+    assert model.plan.max_slots > 400 and model.plan.uniform2 == 0
+    assert worst < FP16_INPUT_TOL, worst
+
+
+def test_mma_tile_too_big_for_smem_falls_back(cuda):
+    """A tile whose packed bytes exceed shared memory: automatic dispatch runs the
+    CUDA-core kernel, forcing the tensor-core path is an invalid argument."""
+    rng = np.random.default_rng(9)
+    cases = [_random_case(rng, 3000, 4, p_bits=(0.05, 0.05, 0.1, 0.8, 0.0)) for _ in range(2)]
+    K = torch.from_numpy(np.stack([c[0] for c in cases])).to(cuda)
+    V = torch.from_numpy(np.stack([c[1] for c in cases])).to(cuda)
+    vb = torch.from_numpy(np.stack([c[2] for c in cases]).astype(np.uint8)).to(cuda)
+    kb = torch.from_numpy(np.stack([c[3] for c in cases]).astype(np.uint8)).to(cuda)
+    stats = torch.zeros(len(cases) * capi.HEAD_STATS_BYTES, dtype=torch.uint8, device=cuda)
+    model = P.build_packed_model(K, V, P.Allocation(vb, kb, stats), group=4)
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda)
+    a = P.packed_decode_step(model, q)
+    b = P.packed_decode_step(model, q, kernel=1)
+    assert torch.equal(a, b)
+    with pytest.raises(capi.InvalidArgument):
+        P.packed_decode_step(model, q, kernel=2)
+
+
 def test_mma_zone_c_and_fp16_io(cuda, orc):
     rng = np.random.default_rng(7)
     cases = [_random_case(rng, 200, 4) for _ in range(9)]
@@ -372,7 +403,8 @@ def test_sequence_split_partials_merge(cuda, orc, world, appends, io):
 
 
 
-@pytest.mark.parametrize("g,io", [(4, torch.float32), (4, torch.float16), (8, torch.float32), (2, torch.float16)])
+@pytest.mark.parametrize("g,io", [(4, torch.float32), (4, torch.float16), (8, torch.float32), (2, torch.float16),
+                                  (8, torch.float16), (6, torch.float32)])
 def test_mix_mostly_two_bit_tiles(cuda, orc, g, io):
     """Heavy-hitter shape on the fast kernel (MIX): tiles with up to 8 4-bit V
     rows and up to 28 4-bit K channels next to uniform 2-bit tiles."""
