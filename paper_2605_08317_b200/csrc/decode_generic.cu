@@ -14,6 +14,8 @@
 //   out[h][c] = sum_i p[h][i] (vscale_i code[i][c] + voffset_i) + Zone B/C rows
 // The tensor-core path (decode_mma.cu) handles the common d = 128 layouts;
 // this kernel is the reference-shaped fallback and the parity baseline.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace rdkv_b200 {
@@ -113,22 +115,28 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(
                 pad = li >= h.r[cls];
                 const uint8_t* row = krows + (size_t)krow_pos(h, i) * h.krow_bytes;
                 if (!pad) {
-                    for (int kc = 0; kc < 3; ++kc) {
-                        const int bits = kBits(kc);
-                        const int per_b = 8 / bits;
+                    // one K byte holds per_b codes of a class: compile-time unpacking per class
+                    auto kclass = [&](auto bits_c, int kc) {
+                        constexpr int bits = decltype(bits_c)::value;
+                        constexpr int per_b = 8 / bits;
                         const int b0 = h.kbyte_base[kc];
                         const int nb = (h.c[kc] + per_b - 1) / per_b;
+                        const float* qk = qt + h.kslot_base[kc];
                         for (int b = 0; b < nb; ++b) {
                             const uint32_t byte = row[b0 + b];
+#pragma unroll
                             for (int j = 0; j < per_b; ++j) {
-                                const int ks = h.kslot_base[kc] + b * per_b + j;
                                 const float code = (float)((byte >> (j * bits)) & ((1u << bits) - 1u));
+                                const int ks = b * per_b + j;
 #pragma unroll
                                 for (int hh = 0; hh < kMaxG; ++hh)
-                                    if (hh < g) acc[hh] = fmaf(qt[hh * kslots + ks], code, acc[hh]);
+                                    if (hh < g) acc[hh] = fmaf(qk[hh * kslots + ks], code, acc[hh]);
                             }
                         }
-                    }
+                    };
+                    kclass(std::integral_constant<int, 2>{}, 0);
+                    kclass(std::integral_constant<int, 4>{}, 1);
+                    kclass(std::integral_constant<int, 8>{}, 2);
                     const __half* k16 = reinterpret_cast<const __half*>(row + h.kbyte_base[3]);
                     for (int j = 0; j < h.c[3]; ++j) {
                         const float x = __half2float(k16[j]);
