@@ -222,19 +222,24 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(
                     if (tid < d) v0 = __half2float(vr[tid]);
                     if (tid + kGenThreads < d) v1 = __half2float(vr[tid + kGenThreads]);
                 } else {
-                    const int bits = kBits(cls);
-                    const int per_b = 8 / bits;
                     const float2 vp = vparam[i];
-                    if (tid < d) {
-                        const int c = tid;
-                        const uint32_t byte = tile[vbyte_offset(h, cls, li, c / per_b, d)];
-                        v0 = fmaf(vp.x, (float)((byte >> ((c % per_b) * bits)) & ((1u << bits) - 1u)), vp.y);
-                    }
-                    if (tid + kGenThreads < d) {
-                        const int c = tid + kGenThreads;
-                        const uint32_t byte = tile[vbyte_offset(h, cls, li, c / per_b, d)];
-                        v1 = fmaf(vp.x, (float)((byte >> ((c % per_b) * bits)) & ((1u << bits) - 1u)), vp.y);
-                    }
+                    auto vrow = [&](auto bits_c) {  // the class is block-uniform: compile-time unpacking
+                        constexpr int bits = decltype(bits_c)::value;
+                        constexpr int per_b = 8 / bits;
+                        if (tid < d) {
+                            const int c = tid;
+                            const uint32_t byte = tile[vbyte_offset(h, cls, li, c / per_b, d)];
+                            v0 = fmaf(vp.x, (float)((byte >> ((c % per_b) * bits)) & ((1u << bits) - 1u)), vp.y);
+                        }
+                        if (tid + kGenThreads < d) {
+                            const int c = tid + kGenThreads;
+                            const uint32_t byte = tile[vbyte_offset(h, cls, li, c / per_b, d)];
+                            v1 = fmaf(vp.x, (float)((byte >> ((c % per_b) * bits)) & ((1u << bits) - 1u)), vp.y);
+                        }
+                    };
+                    if (cls == 0) vrow(std::integral_constant<int, 2>{});
+                    else if (cls == 1) vrow(std::integral_constant<int, 4>{});
+                    else vrow(std::integral_constant<int, 8>{});
                 }
             } else {
                 const __half* vr = zc_v + ((size_t)unit * zc_cap + (i - h.nslot)) * d;
