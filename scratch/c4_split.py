@@ -5,7 +5,7 @@ sys.path.insert(0, ".")
 from paper_2605_08317_b200 import pipeline as P
 from paper_2605_08317_b200.workload import WorkloadSpec, build
 
-for model, n in (("qwen", 256), ("qwen", 2048), ("mistral", 2048)):
+for model, n in (("qwen", 1024), ("qwen", 2048), ("mistral", 2048)):
     L, Hq, Hkv = {"qwen": (28, 28, 4), "mistral": (32, 32, 8)}[model]
     spec = WorkloadSpec(batch=4, layers=L, q_heads=Hq, kv_heads=Hkv, ctx=65536, n_tokens=n, seed=11,
                         hh_stride=64, hh_boost=1.0, outlier_channels=4, outlier_scale=8.0)
@@ -13,7 +13,7 @@ for model, n in (("qwen", 256), ("qwen", 2048), ("mistral", 2048)):
     q = P.generate((m.units, spec.group, spec.head_dim), torch.float16, seed=7, tensor=2)
     ref = P.packed_decode_step(m, q, kernel=1).float()
     res = []
-    for split in (1, 2, 4, 8, 16, 32):
+    for split in (1, 2, 3, 4, 8):
         ws = P.decode_workspace(m, split) if split > 1 else None
         out = torch.empty_like(q)
         for _ in range(3):
