@@ -66,16 +66,17 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(
     __syncthreads();
     const int kslots = h.kslots;
     float* qs = smem;                       // [g][d]
-    float* qt = qs + g * d;                 // [g][kslots]
-    float* lg = qt + g * kslots;            // [g][chunk]
+    const int gp = (g + 3) & ~3;            // heads padded to a float4
+    float* qt = qs + ((g * d + 3) & ~3);    // [kslots][gp], 16-B aligned: one float4 load feeds 4 heads
+    float* lg = qt + gp * kslots;           // [g][chunk]
     const size_t qrow = (size_t)unit * g * d;
     for (int i = tid; i < g * d; i += blockDim.x) qs[i] = io_load(q_all, qrow + i);
     __syncthreads();
     const float2* chan = reinterpret_cast<const float2*>(tile + chan_table_off());
     const uint16_t* perm = reinterpret_cast<const uint16_t*>(tile + perm_off(h));
-    for (int i = tid; i < g * kslots; i += blockDim.x) {
-        const int hh = i / kslots, sl = i % kslots;
-        qt[i] = chan[sl].x * qs[hh * d + perm[sl]];
+    for (int i = tid; i < gp * kslots; i += blockDim.x) {
+        const int sl = i / gp, hh = i % gp;
+        qt[i] = hh < g ? chan[sl].x * qs[hh * d + perm[sl]] : 0.0f;
     }
     if (tid < g) {
         float b = 0.0f;
@@ -121,16 +122,23 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(
                         constexpr int per_b = 8 / bits;
                         const int b0 = h.kbyte_base[kc];
                         const int nb = (h.c[kc] + per_b - 1) / per_b;
-                        const float* qk = qt + h.kslot_base[kc];
+                        const float* qk = qt + (size_t)h.kslot_base[kc] * gp;
                         for (int b = 0; b < nb; ++b) {
                             const uint32_t byte = row[b0 + b];
 #pragma unroll
                             for (int j = 0; j < per_b; ++j) {
                                 const float code = (float)((byte >> (j * bits)) & ((1u << bits) - 1u));
-                                const int ks = b * per_b + j;
+                                const float4* q4 = reinterpret_cast<const float4*>(qk + (b * per_b + j) * gp);
 #pragma unroll
-                                for (int hh = 0; hh < kMaxG; ++hh)
-                                    if (hh < g) acc[hh] = fmaf(qk[hh * kslots + ks], code, acc[hh]);
+                                for (int h4 = 0; h4 < kMaxG / 4; ++h4) {
+                                    if (4 * h4 < g) {
+                                        const float4 w = q4[h4];
+                                        acc[4 * h4 + 0] = fmaf(w.x, code, acc[4 * h4 + 0]);
+                                        acc[4 * h4 + 1] = fmaf(w.y, code, acc[4 * h4 + 1]);
+                                        acc[4 * h4 + 2] = fmaf(w.z, code, acc[4 * h4 + 2]);
+                                        acc[4 * h4 + 3] = fmaf(w.w, code, acc[4 * h4 + 3]);
+                                    }
+                                }
                             }
                         }
                     };
@@ -143,7 +151,7 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic_kernel(
                         const int ks = h.kslot_base[3] + j;
 #pragma unroll
                         for (int hh = 0; hh < kMaxG; ++hh)
-                            if (hh < g) acc[hh] = fmaf(qt[hh * kslots + ks], x, acc[hh]);
+                            if (hh < g) acc[hh] = fmaf(qt[(size_t)ks * gp + hh], x, acc[hh]);
                     }
 #pragma unroll
                     for (int hh = 0; hh < kMaxG; ++hh) acc[hh] += bias[hh < g ? hh : 0];
@@ -322,7 +330,7 @@ __global__ void append_kernel(__half* __restrict__ zc_k, __half* __restrict__ zc
 }
 
 size_t generic_smem_bytes(int g, int d, int kslots) {
-    return sizeof(float) * ((size_t)g * d + (size_t)g * kslots + (size_t)g * kGenChunk);
+    return sizeof(float) * ((size_t)((g * d + 3) & ~3) + (size_t)((g + 3) & ~3) * kslots + (size_t)g * kGenChunk);
 }
 
 template <typename IO>
