@@ -51,6 +51,33 @@ def parse():
 
 
 # ---------------------------------------------------------------------------------
+def check_env():
+    """The product library reads no environment knobs; a debug build's timing
+    knobs (RDKV_DECODE_NULL etc., csrc/Makefile EXPERIMENTS=1) must not be set
+    for a bench run, whatever library is loaded."""
+    bad = sorted(k for k in os.environ if k.startswith("RDKV_DECODE_"))
+    if bad:
+        raise SystemExit(f"bench.py: unset the decode experiment knobs {bad} before timing")
+
+
+def host_cpu():
+    """CPU model and usable core count of the box."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count()
+    return {"cpu_model": model, "nproc": n}
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -210,7 +237,7 @@ def run_reference_arm(args, world, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (K0 counter-based generator, FP16-representable)",
         "impl": "reference",
         "config": workload_config(spec, args),
-        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": info["cores"], "kind": info["kind"],
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": info["cores"], "kind": info["kind"], **host_cpu(),
                          "sample": f"1 of {int(scale)} (sequence, layer) slices (8 KV heads x 4 q-heads, T={spec.ctx}) timed "
                                    f"{info['sample_step_s'] * 1e3:.3f} ms/step via parallel_for; step = x{int(scale)}"},
         "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -362,7 +389,7 @@ def secondary_configs(P, spec0, model, q, args):
     kn = P.generate((U, d), torch.float16, seed=77, tensor=1)
     P.append_new_token(model, kn, kn)
     us, _ = graph_step_us(P, model, q, min(args.steps, 100))
-    byts = model.decode_bytes(io_bytes=2)
+    byts = model.survey_bytes(io_bytes=2)
     out["zone_c_1"] = {"config": "configs[2] step with the new token in Zone C (1 fp16 K/V row per tile)",
                        "us_per_step": us, "tok_s": spec0.batch / (us / 1e6),
                        "roofline_frac": byts / (us / 1e6) / 1e9 / peak}
@@ -425,7 +452,7 @@ def secondary_configs(P, spec0, model, q, args):
     m70, _, _, _ = build(spec70)
     q70 = P.generate((m70.units, spec70.group, d), torch.float16, seed=QSEED, tensor=2)
     us, _ = graph_step_us(P, m70, q70, min(args.steps, 100))
-    byts = m70.decode_bytes(io_bytes=2)
+    byts = m70.survey_bytes(io_bytes=2)
     out["llama70b_1seq_per_gpu"] = {"config": "configs[4]: LLaMA-3.1-70B KV shape (80 layers, 64 q / 8 kv heads), "
                                               "128K ctx, n=128, one sequence per GPU (batch 8 over 8 GPUs)",
                                     "us_per_step": us, "tok_s_per_gpu": 1 / (us / 1e6),
@@ -438,7 +465,7 @@ def secondary_configs(P, spec0, model, q, args):
     mhh, _, sthh, _ = build(spec_hh)
     qhh = P.generate((mhh.units, spec_hh.group, d), torch.float16, seed=QSEED, tensor=2)
     us, _ = graph_step_us(P, mhh, qhh, min(args.steps, 100))
-    byts = mhh.decode_bytes(io_bytes=2)
+    byts = mhh.survey_bytes(io_bytes=2)
     out["heavy_hitters"] = {"config": "configs[2] shape with heavy-hitter injection (every 64th key boosted): "
                                       "mixed 2/4-bit tiles", "us_per_step": us, "tok_s": spec_hh.batch / (us / 1e6),
                             "roofline_frac": byts / (us / 1e6) / 1e9 / peak,
@@ -450,7 +477,7 @@ def secondary_configs(P, spec0, model, q, args):
     m2, _, st2, _ = build(spec)
     q2 = P.generate((m2.units, spec.group, d), torch.float16, seed=QSEED, tensor=2)
     us, _ = graph_step_us(P, m2, q2, min(args.steps, 100))
-    byts = m2.decode_bytes(io_bytes=2)
+    byts = m2.survey_bytes(io_bytes=2)
     out["budget_512"] = {"config": "LLaMA-3.1-8B KV shape, 128K ctx, n=512 tokens/layer (configs[3] budget point), "
                                    f"batch {spec.batch}, kept tokens/head {float(np.mean([s['n_kept'].mean() for s in st2])):.1f}",
                          "us_per_step": us, "tok_s": spec.batch / (us / 1e6),
@@ -467,7 +494,7 @@ def secondary_configs(P, spec0, model, q, args):
             m4, _, st4, _ = build(spec)
             q4 = P.generate((m4.units, spec.group, d), torch.float16, seed=QSEED, tensor=2)
             us, _ = graph_step_us(P, m4, q4, min(args.steps, 50))
-            byts = m4.decode_bytes(io_bytes=2)
+            byts = m4.survey_bytes(io_bytes=2)
             c4[f"{model}_n{n}"] = {"us_per_step": us, "tok_s": spec.batch / (us / 1e6),
                                    "roofline_frac": byts / (us / 1e6) / 1e9 / peak, "bytes_per_step": byts,
                                    "plan_uniform2": int(m4.plan.uniform2),
@@ -482,6 +509,7 @@ def secondary_configs(P, spec0, model, q, args):
 
 def main():
     args = parse()
+    check_env()
     world, rank, local = dist_setup()
     if args.impl == "reference":
         run_reference_arm(args, world, rank)
@@ -608,7 +636,11 @@ def main():
 
     # ---- roofline of the decode kernel
     peak, peak_kind = load_peaks()
-    alg_bytes = model.decode_bytes(io_bytes=2)
+    # SURVEY.md §8(d) bytes (the allocation's own codes, params, map, q, out) are
+    # the roofline's numerator; what the tile layout adds on top (header, 16-bit
+    # perm entries, class padding) is reported beside it, not counted
+    alg_bytes = model.survey_bytes(io_bytes=2)
+    layout_bytes = model.decode_bytes(io_bytes=2)
     achieved = alg_bytes / (ms_local / 1e3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "decode_ncu_summary.json")
@@ -637,7 +669,10 @@ def main():
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": alg_bytes},
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "layout_bytes_per_launch": layout_bytes,
+                     "layout_overhead_bytes": layout_bytes - alg_bytes,
+                     "frac_incl_layout_overhead": layout_bytes / (ms_local / 1e3) / 1e9 / peak},
         "e2e": {"value": spec.batch * world / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": qh.numel() * qh.element_size(),
                 "d2h_bytes_per_step": oh.numel() * oh.element_size(),
@@ -667,7 +702,7 @@ def main():
             scale = spec.batch * spec.layers
             cpu_step = info["sample_step_s"] * scale
             line["cpu_baseline"] = {"value": spec.batch / cpu_step, "unit": "tok/s", "cores": info["cores"],
-                                    "kind": info["kind"],
+                                    "kind": info["kind"], **host_cpu(),
                                     "sample": f"sequence 0 layer 0 (8 KV heads, 32 q-heads, T={spec.ctx}): "
                                               f"{info['sample_step_s'] * 1e3:.3f} ms per slice-step x {scale} slices",
                                     "alloc_s_sample": info.get("alloc_s"), "pack_s_sample": info.get("pack_s")}

@@ -381,8 +381,10 @@ RDKV_API int rdkv_cache_read_header(const char* path, rdkv_cache_header* header)
  * (RDKV_F32 bit-exact, RDKV_F16 round-to-nearest), through pinned double
  * buffers overlapping the file reads with the H2D copies. Returns
  * RDKV_ENUMERIC when an entry is non-finite (KVCache::validate,
- * cache.cpp:114-130) or overflows fp16. Returns after `stream` has finished
- * the copies. */
+ * cache.cpp:114-130) or overflows fp16. The reference accepts every finite
+ * f32; |x| > 65504 is rejected only because an fp16 target cannot hold it
+ * (load as RDKV_F32 to accept exactly the reference's inputs). Returns after
+ * `stream` has finished the copies. */
 RDKV_API int rdkv_cuda_cache_load(const char* path, const rdkv_cache_header* header, void* k,
                                   void* v, void* probe_q, int32_t dtype, void* stream);
 

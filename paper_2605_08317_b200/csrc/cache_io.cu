@@ -54,6 +54,33 @@ struct Json {
         p += n;
         return true;
     }
+    bool hex4(const char* q, uint32_t& v) {
+        if (e - q < 4) return false;
+        v = 0;
+        for (int i = 0; i < 4; ++i) {
+            const unsigned char c = (unsigned char)q[i];
+            if (!isxdigit(c)) return false;
+            v = v * 16 + (uint32_t)(isdigit(c) ? c - '0' : (tolower(c) - 'a' + 10));
+        }
+        return true;
+    }
+    static void utf8(uint32_t cp, std::string& out) {
+        if (cp < 0x80) {
+            out.push_back((char)cp);
+        } else if (cp < 0x800) {
+            out.push_back((char)(0xC0 | (cp >> 6)));
+            out.push_back((char)(0x80 | (cp & 0x3F)));
+        } else if (cp < 0x10000) {
+            out.push_back((char)(0xE0 | (cp >> 12)));
+            out.push_back((char)(0x80 | ((cp >> 6) & 0x3F)));
+            out.push_back((char)(0x80 | (cp & 0x3F)));
+        } else {
+            out.push_back((char)(0xF0 | (cp >> 18)));
+            out.push_back((char)(0x80 | ((cp >> 12) & 0x3F)));
+            out.push_back((char)(0x80 | ((cp >> 6) & 0x3F)));
+            out.push_back((char)(0x80 | (cp & 0x3F)));
+        }
+    }
     bool string(std::string* out) {
         if (p >= e || *p != '"') return ok = false;
         ++p;
@@ -64,11 +91,20 @@ struct Json {
                 if (++p >= e) return ok = false;
                 char x = *p;
                 if (x == 'u') {
-                    if (e - p < 5) return ok = false;
-                    for (int i = 1; i <= 4; ++i)
-                        if (!isxdigit((unsigned char)p[i])) return ok = false;
-                    if (out) out->push_back('?');  // header fields of interest are ASCII
+                    // \uXXXX (and surrogate pairs) to UTF-8, like nlohmann::json;
+                    // a lone or mismatched surrogate is a parse error there too
+                    uint32_t cp = 0;
+                    if (!hex4(p + 1, cp)) return ok = false;
                     p += 5;
+                    if (cp >= 0xDC00 && cp <= 0xDFFF) return ok = false;
+                    if (cp >= 0xD800 && cp <= 0xDBFF) {
+                        uint32_t lo = 0;
+                        if (e - p < 6 || p[0] != '\\' || p[1] != 'u' || !hex4(p + 2, lo) || lo < 0xDC00 || lo > 0xDFFF)
+                            return ok = false;
+                        p += 6;
+                        cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+                    }
+                    if (out) utf8(cp, *out);
                     continue;
                 }
                 const char* esc = strchr("\"\\/bfnrt", x);
@@ -115,7 +151,7 @@ struct Json {
         return true;
     }
     bool value(JsonField* f, int depth) {
-        if (depth > 64) return ok = false;
+        if (depth > 4096) return ok = false;  // nesting guard for the recursive reader only
         ws();
         if (p >= e) return ok = false;
         char c = *p;

@@ -28,6 +28,9 @@ extern "C" RDKV_API int rdkv_cuda_decode(const rdkv_decode_args* a, void* stream
         return RDKV_EINVAL;
     if (a->io_dtype != RDKV_F32 && a->io_dtype != RDKV_F16) return RDKV_EINVAL;
     if (a->zc_len && (!a->zc_k || !a->zc_v || a->zc_cap < 1)) return RDKV_EINVAL;
+    // the Zone C bound is the caller's promise that every zc_len[u] <= zc_bound
+    if ((a->flags & RDKV_DECODE_ZC_BOUND) && (a->zc_bound < 0 || (a->zc_len && a->zc_bound > a->zc_cap)))
+        return RDKV_EINVAL;
     const int split = a->split < 1 ? 1 : a->split;
     if (split > 1 && (!a->workspace ||
                       a->workspace_bytes < rdkv_cuda_decode_workspace(a->units, a->group, a->head_dim, split)))
@@ -153,6 +156,12 @@ static int enqueue_pipelined(rdkv_decode_ctx* c, const rdkv_decode_args* a, cons
         if (a->tile_decode_bytes) sub.tile_decode_bytes = a->tile_decode_bytes + u0;
         sub.q = static_cast<const uint8_t*>(a->q) + off;
         sub.out = static_cast<uint8_t*>(a->out) + off;
+        // unit_ids index the whole arena (and list units out of order): a chunk
+        // of consecutive units is decoded without them (mixed chunks take the
+        // general body), never through ids that point outside the shifted views
+        sub.unit_ids = nullptr;
+        sub.plan.n_uniform = 0;
+        sub.plan.uniform2_split = 0;
         if (a->zc_len) {
             const size_t zrow = (size_t)a->zc_cap * a->head_dim * 2;
             sub.zc_k = static_cast<const uint8_t*>(a->zc_k) + (size_t)u0 * zrow;

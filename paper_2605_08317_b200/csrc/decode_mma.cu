@@ -2123,14 +2123,27 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
 // the bound, so more resident warps hide more latency; measured 15.7 us at 8
 // pairs vs 16.6 us at 7 on the 4096-tile step), then as many buffers per pair
 // (>= 2, double buffering) as fit.
+// Timing-experiment knobs (loads-only / math-only kernels, forced launch
+// geometry, launch tracing) exist only in a debug build compiled with
+// -DRDKV_DECODE_EXPERIMENTS (make EXPERIMENTS=1); the product library never
+// reads the environment, so no variable can change what a decode computes.
+static const char* experiment_knob(const char* name) {
+#ifdef RDKV_DECODE_EXPERIMENTS
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 static bool verbose_env() {
-    static const bool v = getenv("RDKV_DECODE_VERBOSE") != nullptr;
+    static const bool v = experiment_knob("RDKV_DECODE_VERBOSE") != nullptr;
     return v;
 }
 
 static bool pick_pairs(int units, int nsm, int slot, int scratch, int smem_max, int& W, int& nbuf) {
     const int head = kXPairs * kXMaxBuf * (int)sizeof(uint64_t);  // upper bound of W * kXMaxBuf barriers
-    static const char* env = getenv("RDKV_DECODE_PAIRS");  // experiment knobs: read once per process
+    static const char* env = experiment_knob("RDKV_DECODE_PAIRS");  // read once per process
     const int forced = env ? atoi(env) : 0;
     const int per_sm = (units + nsm - 1) / nsm;
     W = 0;
@@ -2574,9 +2587,9 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
                 zcf ? static_cast<const __half*>(a->zc_k) : nullptr, zcf ? static_cast<const __half*>(a->zc_v) : nullptr,
                 zcf ? a->zc_len : nullptr, a->units, a->group, zcf ? a->zc_cap : 0, nbuf, W, slot, scratch, 0, 0, -1, -1,
                 0, 0, a->unit_ids};
-    static const char* smsp_env = getenv("RDKV_DECODE_SMSP");
+    static const char* smsp_env = experiment_knob("RDKV_DECODE_SMSP");
     if (smsp_env) p.smsp_pairs = atoi(smsp_env);
-    static const char* nenv = getenv("RDKV_DECODE_NULL");
+    static const char* nenv = experiment_knob("RDKV_DECODE_NULL");
     const int mode = nenv ? atoi(nenv) : 0;
     const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
     const bool g8 = a->group > 4;
@@ -2591,8 +2604,11 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
               : zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true>
                             : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, true>)
               : bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true>
+#ifdef RDKV_DECODE_EXPERIMENTS
               : mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
-              : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2> : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
+              : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2>
+#endif
+                          : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
     static std::atomic<int> smem_set[14][kMaxDevices];  // one slot per instantiation above
     set_smem_once(kern, (int)smem,
                   smem_set[mix ? 10 + (g8 ? 2 : 0) + (bulk ? 1 : 0) : g8 ? 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0)
@@ -2608,7 +2624,7 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
     // retires its own CTA, so under programmatic dependent launch the next
     // kernel's CTAs take a pair's smem / warp slots as soon as it finishes
     // instead of when the SM's slowest pair does.
-    static const char* cta_env = getenv("RDKV_DECODE_CTA");
+    static const char* cta_env = experiment_knob("RDKV_DECODE_CTA");
     if (cta_env && atoi(cta_env) == 1 && W > 1 && mode == 0 && !zcf && !g8 && !mix && max_blocks == 0) {
         const size_t smem1 = kXMaxBuf * sizeof(uint64_t) + (size_t)2 * slot + scratch + slack;
         auto k1 = bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, true> : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, true>;

@@ -383,6 +383,25 @@ class PackedModel:
         qo = self.units * self.group * self.head_dim * io_bytes * 2
         return tiles + zc + qo
 
+    def survey_bytes(self, io_bytes=2) -> int:
+        """SURVEY.md §8(d)'s algorithmic bytes of one decode step, from the
+        allocation alone: K codes N_k (pad4(c2)/4 + pad2(c4)/2 + c8) + k16
+        N_k c16 2 + V codes (r2 d/4 + r4 d/2 + r8 d) + Zone B r16 d 2 + params
+        8 (r2 + r4 + r8) + 8 (c2 + c4 + c8) + channel map (d - c0) + Zone C
+        + q and out. decode_bytes() minus this = the layout's own overhead
+        (tile header, 16-bit perm entries, class padding)."""
+        d = self.head_dim
+        tot = 0
+        for i in self.infos():
+            n = int(i.n_kept)
+            r2, r4, r8, r16 = (int(x) for x in i.rows)
+            c2, c4, c8, c16 = (int(x) for x in i.chans)
+            kq = n * ((c2 + 3) // 4 + (c4 + 1) // 2 + c8) + n * c16 * 2
+            vq = r2 * d // 4 + r4 * d // 2 + r8 * d + r16 * d * 2
+            tot += kq + vq + 8 * (r2 + r4 + r8) + 8 * (c2 + c4 + c8) + (c2 + c4 + c8 + c16)
+        zc = 0 if self.zc_len is None else int(self.zc_len.sum().item()) * d * 2 * 2
+        return tot + zc + self.units * self.group * d * io_bytes * 2
+
     def export(self, unit: int) -> dict:
         """Canonical reference view of one tile (see rdkv_tile_export)."""
         t = self.tile_bytes(unit)
@@ -588,7 +607,7 @@ class HostDecoder:
         shape = (model.units, model.group, model.head_dim)
         self.q_dev = torch.empty(shape, dtype=dtype, device=model.arena.device)
         self.out_dev = torch.empty_like(self.q_dev)
-        self.args = decode_args(model, self.q_dev, self.out_dev, 1, kernel)
+        self.kernel = kernel
         ctx = C.c_void_p()
         raise_for(capi.lib().rdkv_cuda_decode_ctx_create(chunks, C.byref(ctx)), "decode_ctx_create")
         self.ctx = ctx
@@ -603,6 +622,13 @@ class HostDecoder:
                                                              out_host.data_ptr(),
                                                              _stream() if stream is None else stream),
                   "decode_host_pipelined")
+
+    @property
+    def args(self) -> capi.DecodeArgs:
+        """Decode arguments rebuilt from the model at every step: the Zone C bound
+        (RDKV_DECODE_ZC_BOUND / zc_bound) follows the appends made since the last
+        step, and a changed bound changes the native graph-cache key."""
+        return decode_args(self.model, self.q_dev, self.out_dev, 1, self.kernel)
 
     def close(self) -> None:
         if getattr(self, "ctx", None):
@@ -621,9 +647,16 @@ def append_new_token(model: PackedModel, k_new, v_new) -> None:
     if model.zc_len is None:
         raise capi.InvalidArgument(capi.RDKV_EINVAL, "model built without Zone C capacity")
     _check_cuda(k_new, v_new)
+    # the reference appends without limit (trizone.cpp:307-314); the device Zone C
+    # has a fixed capacity, so a full cache is an error instead of a dropped row
+    full = (model.zc_count >= model.zc_cap if model.zc_count is not None
+            else int(model.zc_len.max().item()) >= model.zc_cap)
+    if full:
+        raise capi.InvalidArgument(capi.RDKV_EINVAL,
+                                   f"append_new_token: Zone C capacity {model.zc_cap} exhausted")
     raise_for(capi.lib().rdkv_cuda_append(model.zc_k.data_ptr(), model.zc_v.data_ptr(),
                                           model.zc_len.data_ptr(), model.zc_cap, k_new.data_ptr(),
                                           v_new.data_ptr(), _dtype_code(k_new), model.units,
                                           model.head_dim, _stream()), "append")
     if model.zc_count is not None:
-        model.zc_count = min(model.zc_count + 1, model.zc_cap)
+        model.zc_count += 1

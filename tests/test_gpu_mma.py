@@ -377,6 +377,84 @@ def test_split_dispatch_mixed_arena(cuda, orc, io, g):
     assert float(err.max()) < (2 * U2X_TOL if io == torch.float32 else 2e-3)
 
 
+@pytest.mark.parametrize("chunks", [1, 3, 8])
+def test_pipelined_host_decode_mixed_arena(cuda, orc, chunks):
+    """The pipelined end-to-end call on a mixed arena that carries split lists
+    (unit_ids): per-chunk launches drop the whole-arena ids (they would index
+    past the chunk's shifted offsets / q / out), outputs equal the oracle and
+    the no-split device step."""
+    rng = np.random.default_rng(77 + chunks)
+    cases = []
+    for i in range(30):
+        k, v, vb, kb, q = _random_case(rng, 300, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(300, int(rng.integers(100, 150)), replace=False))] = 2
+        kb[:] = 2
+        if i % 5 == 2:
+            vb[np.nonzero(vb)[0][:3]] = 8
+            kb[rng.choice(D, 3, replace=False)] = 4
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, 4, io=torch.float16)
+    assert model.plan.uniform2 == 0 and 0 < model.plan.n_uniform < len(cases)
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).half()
+    ids, model.unit_ids = model.unit_ids, None
+    want = P.packed_decode_step(model, q).cpu()
+    model.unit_ids = ids
+    dec = P.HostDecoder(model, torch.float16, chunks=chunks)
+    qh = q.cpu().pin_memory()
+    oh = torch.full_like(qh, float("nan")).pin_memory()
+    dec.step(qh, oh)
+    torch.cuda.current_stream().synchronize()
+    dec.close()
+    assert torch.equal(oh, want)
+    for u, (k, v, vbs, kbs, qq) in enumerate(cases):
+        tz = orc.tz_build(k, v, vbs, kbs)
+        for j in range(4):
+            assert rel(oh[u, j].float().numpy(), tz.decode(qq[j])) < 1e-3
+
+
+def test_append_capacity_and_zone_c_bound(cuda, orc):
+    """append_new_token past the Zone C capacity raises (no silently dropped
+    rows); the HostDecoder's Zone C bound follows appends made after it was
+    created (fused path for <= 4 rows, chunked beyond), matching the oracle."""
+    rng = np.random.default_rng(9)
+    cases = []
+    for _ in range(12):
+        k, v, vb, kb, q = _random_case(rng, 300, 4)
+        vb[:] = 0
+        vb[np.sort(rng.choice(300, 120, replace=False))] = 2
+        kb[:] = 2
+        cases.append((k, v, vb, kb, q))
+    cap = 7
+    _, model = _run_batch(cuda, orc, cases, 4, io=torch.float16, appends=0)
+    model.zc_k = torch.zeros((len(cases), cap, D), dtype=torch.float16, device=cuda)
+    model.zc_v = torch.zeros_like(model.zc_k)
+    model.zc_len = torch.zeros(len(cases), dtype=torch.int32, device=cuda)
+    model.zc_cap, model.zc_count = cap, 0
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).half()
+    dec = P.HostDecoder(model, torch.float16, chunks=2)
+    qh = q.cpu().pin_memory()
+    oh = torch.empty_like(qh).pin_memory()
+    zk = f16r(rng.standard_normal((cap, len(cases), D)))
+    zv = f16r(rng.standard_normal((cap, len(cases), D)))
+    for a in range(cap):
+        P.append_new_token(model, torch.from_numpy(zk[a]).to(cuda), torch.from_numpy(zv[a]).to(cuda))
+        dec.step(qh, oh)
+        torch.cuda.current_stream().synchronize()
+        assert torch.equal(oh, P.packed_decode_step(model, q).cpu())
+        for u, (k, v, vbs, kbs, qq) in enumerate(cases):
+            tz = orc.tz_build(k, v, vbs, kbs)
+            for r in range(a + 1):
+                tz.append(zk[r, u], zv[r, u])
+            assert rel(oh[u, 0].float().numpy(), tz.decode(qq[0])) < 1e-3, (a, u)
+    dec.close()
+    with pytest.raises(capi.InvalidArgument):
+        P.append_new_token(model, torch.from_numpy(zk[0]).to(cuda), torch.from_numpy(zv[0]).to(cuda))
+    model.zc_count = None  # unknown bound: the capacity check reads zc_len on the device
+    with pytest.raises(capi.InvalidArgument):
+        P.append_new_token(model, torch.from_numpy(zk[0]).to(cuda), torch.from_numpy(zv[0]).to(cuda))
+
+
 @pytest.mark.parametrize("world,appends,io", [(2, 0, torch.float16), (3, 0, torch.float32), (2, 20, torch.float32),
                                               (4, 3, torch.float16)])
 def test_sequence_split_partials_merge(cuda, orc, world, appends, io):

@@ -1,4 +1,4 @@
-"""scratch: generic-kernel split sweep on configs[3] points (model, n)."""
+"""tools: generic-kernel split sweep on configs[3] points (model, n)."""
 import sys
 import torch
 sys.path.insert(0, ".")

@@ -1,4 +1,4 @@
-"""scratch: summarise an ncu report of the decode kernel (metrics, stalls, per-line instructions)."""
+"""tools: summarise an ncu report of the decode kernel (metrics, stalls, per-line instructions)."""
 import csv, collections, io, re, subprocess, sys
 rep = sys.argv[1]
 units = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
