@@ -50,6 +50,13 @@ WeightVector channel_weights(MatrixView q, MatrixView k);
 DiscreteAllocation mckp_bisect(std::span<const float> weights, const DistortionTable& eps,
                                double target_avg_bits, const BitSet& bits = {},
                                const SolverConfig& cfg = {});
+// pipeline.hpp:73-75 / pipeline.cpp:74-94 — Stage 2 (device bisection over the tokens)
+VAllocation allocate_v(const WeightVector& token_w, const DistortionTable& eps_v, double v_budget_bits,
+                       int head_dim, const BitSet& bits, const SolverConfig& cfg);
+// pipeline.hpp:79-81 / pipeline.cpp:96-112 — Stage 3 (device bisection over the channels)
+DiscreteAllocation allocate_k(const WeightVector& channel_w, const DistortionTable& eps_k,
+                              double k_budget_bits, int kept_count, const BitSet& bits,
+                              const SolverConfig& cfg);
 // pipeline.hpp:91-93 / pipeline.cpp:114-183
 HeadAllocation allocate_head(const KVCache& cache, int layer, int kv_head, const BudgetSpec& spec,
                              const DistortionTable& eps_v, const DistortionTable& eps_k,
@@ -60,6 +67,9 @@ ModelAllocation allocate_model(const KVCache& cache, const BudgetSpec& spec,
                                const PipelineConfig& cfg);
 
 // ---- TriZone packing --------------------------------------------------------
+// trizone.hpp:16-17 / trizone.cpp:59-88 (device kernels, 16-byte vectorised stores)
+std::vector<std::uint8_t> pack_bits(std::span<const std::uint8_t> codes, int bits);
+std::vector<std::uint8_t> unpack_bits(std::span<const std::uint8_t> bytes, int bits, int logical_len);
 // quantizer.hpp:41 / quantizer.cpp:104-131
 QuantizedUnit quantize_unit(std::span<const float> values, int bits);
 // trizone.hpp:80 / trizone.cpp:91-208

@@ -291,6 +291,19 @@ RDKV_API int rdkv_cuda_quantize_units(const float* values, int32_t units, int32_
                                       uint8_t* codes, float* scale, int64_t* zero_point,
                                       int32_t* status, void* stream);
 
+/* pack_bits (trizone.cpp:59-75; reference trizone.hpp:16): n codes
+ * (< 2^bits each) -> ceil(n * bits / 8) bytes in the reference's quarter- /
+ * half-split layout, 16-byte vectorised stores. *status (device) = RDKV_EINVAL
+ * when a code overflows the bit-width ("pack_bits: code overflows bit-width"),
+ * else RDKV_OK. bits must be 2, 4 or 8. */
+RDKV_API int rdkv_cuda_pack_bits(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* out,
+                                 int32_t* status, void* stream);
+/* unpack_bits (trizone.cpp:76-88; reference trizone.hpp:17): the first
+ * logical_len codes of `bytes` (nbytes long). RDKV_EINVAL when bits is not
+ * 2/4/8 or the buffer is too short for logical_len codes. */
+RDKV_API int rdkv_cuda_unpack_bits(const uint8_t* bytes, int64_t nbytes, int32_t bits, int64_t logical_len,
+                                   uint8_t* out, void* stream);
+
 /* fused_k_logits (trizone.cpp:210-249) per token slot of every tile:
  * q [units][group][head_dim] f32 -> logits [units][group][max_slots] f32
  * (slot order; NaN for pad slots). max_slots / max_kslots from the plan. */

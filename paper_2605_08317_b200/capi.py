@@ -165,6 +165,8 @@ _SIGS = {
     "rdkv_cuda_mckp_bisect": (C.c_int, [_VP, C.c_int32, C.c_int32, _VP, _VP, C.c_int32, C.c_double,
                                         C.c_double, C.c_int32, C.c_int32, _VP, _VP, _VP]),
     "rdkv_cuda_quantize_units": (C.c_int, [_VP, C.c_int32, C.c_int32, C.c_int32, _VP, _VP, _VP, _VP, _VP]),
+    "rdkv_cuda_pack_bits": (C.c_int, [_VP, C.c_int64, C.c_int32, _VP, _VP, _VP]),
+    "rdkv_cuda_unpack_bits": (C.c_int, [_VP, C.c_int64, C.c_int32, C.c_int64, _VP, _VP]),
     "rdkv_cuda_tile_logits": (C.c_int, [_VP, _VP, C.c_int32, C.c_int32, C.c_int32, _VP, C.c_int32,
                                         C.c_int32, _VP, _VP]),
     "rdkv_tile_import_bytes": (C.c_size_t, [C.c_int32, C.c_int32, _VP, _VP]),

@@ -460,3 +460,89 @@ extern "C" RDKV_API int rdkv_cuda_quantize_units(const float* values, int32_t un
         values, units, len, bits, codes, scale, zero_point, status);
     return launch_status();
 }
+
+// ---- pack_bits / unpack_bits (trizone.cpp:59-88) ---------------------------
+// Byte layout of the reference: 2-bit quarter-split (code j at bits 2 (j & 3) of
+// byte j >> 2), 4-bit half-split (bits 4 (j & 1) of byte j >> 1), 8-bit one code
+// per byte. One thread per 16 output bytes, written as one uint4 (the tail
+// thread stores bytewise); a code above 2^bits - 1 raises the status flag.
+namespace rdkv_b200 {
+__global__ void __launch_bounds__(256) pack_bits_kernel(const uint8_t* __restrict__ codes, int64_t n, int bits,
+                                                        uint8_t* __restrict__ out, int64_t nbytes,
+                                                        int32_t* __restrict__ status) {
+    const int per = 8 / bits;
+    const uint32_t limit = (1u << bits) - 1u;
+    for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; b0 < nbytes;
+         b0 += (int64_t)gridDim.x * blockDim.x * 16) {
+        uint8_t o[16];
+        bool bad = false;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            uint32_t acc = 0;
+            for (int e = 0; e < per; ++e) {
+                const int64_t j = (b0 + i) * per + e;
+                const uint32_t c = j < n ? codes[j] : 0u;
+                bad |= c > limit;
+                acc |= (c & limit) << (e * bits);
+            }
+            o[i] = (uint8_t)acc;
+        }
+        if (bad) atomicExch(status, RDKV_EINVAL);
+        if (b0 + 16 <= nbytes && ((reinterpret_cast<uintptr_t>(out + b0) & 15) == 0)) {
+            *reinterpret_cast<uint4*>(out + b0) = *reinterpret_cast<const uint4*>(o);
+        } else {
+            for (int i = 0; i < 16 && b0 + i < nbytes; ++i) out[b0 + i] = o[i];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) unpack_bits_kernel(const uint8_t* __restrict__ bytes, int bits, int64_t len,
+                                                          uint8_t* __restrict__ out) {
+    const int per = 8 / bits;
+    const uint32_t mask = (1u << bits) - 1u;
+    for (int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; j0 < len;
+         j0 += (int64_t)gridDim.x * blockDim.x * 16) {
+        uint8_t o[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int64_t j = j0 + i;
+            o[i] = j < len ? (uint8_t)((bytes[j / per] >> ((j % per) * bits)) & mask) : 0;
+        }
+        if (j0 + 16 <= len && ((reinterpret_cast<uintptr_t>(out + j0) & 15) == 0)) {
+            *reinterpret_cast<uint4*>(out + j0) = *reinterpret_cast<const uint4*>(o);
+        } else {
+            for (int i = 0; i < 16 && j0 + i < len; ++i) out[j0 + i] = o[i];
+        }
+    }
+}
+}  // namespace rdkv_b200
+
+static int grid_for(int64_t items16) {
+    const int64_t b = (items16 + 255) / 256;
+    return (int)(b < 1 ? 1 : b > 148 * 16 ? 148 * 16 : b);
+}
+
+extern "C" RDKV_API int rdkv_cuda_pack_bits(const uint8_t* codes, int64_t n, int32_t bits, uint8_t* out,
+                                            int32_t* status, void* stream) {
+    if (bits != 2 && bits != 4 && bits != 8) return RDKV_EINVAL;
+    if (n < 0 || (n > 0 && (!codes || !out)) || !status) return RDKV_EINVAL;
+    const int per = 8 / bits;
+    const int64_t nbytes = (n + per - 1) / per;
+    auto st = static_cast<cudaStream_t>(stream);
+    RDKV_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), st));
+    if (nbytes == 0) return RDKV_OK;
+    rdkv_b200::pack_bits_kernel<<<grid_for((nbytes + 15) / 16), 256, 0, st>>>(codes, n, bits, out, nbytes, status);
+    return rdkv_b200::launch_status();
+}
+
+extern "C" RDKV_API int rdkv_cuda_unpack_bits(const uint8_t* bytes, int64_t nbytes, int32_t bits,
+                                              int64_t logical_len, uint8_t* out, void* stream) {
+    if (bits != 2 && bits != 4 && bits != 8) return RDKV_EINVAL;
+    const int per = 8 / bits;
+    if (logical_len < 0 || (logical_len + per - 1) / per > nbytes) return RDKV_EINVAL;  // "byte buffer too short"
+    if (logical_len == 0) return RDKV_OK;
+    if (!bytes || !out) return RDKV_EINVAL;
+    auto st = static_cast<cudaStream_t>(stream);
+    rdkv_b200::unpack_bits_kernel<<<grid_for((logical_len + 15) / 16), 256, 0, st>>>(bytes, bits, logical_len, out);
+    return rdkv_b200::launch_status();
+}

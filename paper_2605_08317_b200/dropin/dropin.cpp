@@ -681,6 +681,39 @@ DiscreteAllocation mckp_bisect(std::span<const float> weights, const DistortionT
     return out;
 }
 
+VAllocation allocate_v(const WeightVector& token_w, const DistortionTable& eps_v, double v_budget_bits, int head_dim,
+                       const BitSet& bits, const SolverConfig& cfg) {  // pipeline.cpp:74-94
+    require(token_w.kind == WeightKind::token, "allocate_v: token weights required");
+    const int t_len = static_cast<int>(token_w.values.size());
+    require(t_len >= 1, "allocate_v: empty sequence");
+    VAllocation out;
+    if (!(v_budget_bits > 0.0)) {
+        out.v_bits.assign(t_len, 0);
+        out.kept = derive_kept(out.v_bits);
+        out.raw.bits = out.v_bits;
+        return out;
+    }
+    const double target = std::min(16.0, v_budget_bits / (static_cast<double>(head_dim) * t_len));
+    out.raw = rdkv::cuda::mckp_bisect(token_w.values, eps_v, target, bits, cfg);
+    out.v_bits = out.raw.bits;
+    out.kept = derive_kept(out.v_bits);
+    return out;
+}
+
+DiscreteAllocation allocate_k(const WeightVector& channel_w, const DistortionTable& eps_k, double k_budget_bits,
+                              int kept_count, const BitSet& bits, const SolverConfig& cfg) {  // pipeline.cpp:96-112
+    require(channel_w.kind == WeightKind::channel, "allocate_k: channel weights required");
+    const int d = static_cast<int>(channel_w.values.size());
+    DiscreteAllocation out;
+    if (kept_count == 0) return out;  // all tokens evicted: no K storage at all
+    if (!(k_budget_bits > 0.0)) {
+        out.bits.assign(d, 0);
+        return out;
+    }
+    const double target = std::min(16.0, k_budget_bits / (static_cast<double>(kept_count) * d));
+    return rdkv::cuda::mckp_bisect(channel_w.values, eps_k, target, bits, cfg);
+}
+
 HeadAllocation allocate_head(const KVCache& cache, int layer, int kv_head, const BudgetSpec& spec,
                              const DistortionTable& eps_v, const DistortionTable& eps_k, const PipelineConfig& cfg) {
     validate_spec(spec);
@@ -720,6 +753,36 @@ ModelAllocation allocate_model(const KVCache& cache, const BudgetSpec& spec, con
 }
 
 // ---- packing ----------------------------------------------------------------
+std::vector<std::uint8_t> pack_bits(std::span<const std::uint8_t> codes, int bits) {  // trizone.cpp:59-75
+    require(bits == 2 || bits == 4 || bits == 8, "pack_bits: bits must be 2, 4 or 8");
+    const int per = 8 / bits;
+    const std::size_t nbytes = (codes.size() + per - 1) / per;
+    std::vector<std::uint8_t> out(nbytes, 0);
+    DevBuf c = to_device(codes.data(), codes.size()), o(nbytes > 0 ? nbytes : 1), st(sizeof(int32_t));
+    check(rdkv_cuda_pack_bits(codes.empty() ? nullptr : c.as<uint8_t>(), static_cast<int64_t>(codes.size()), bits,
+                              o.as<uint8_t>(), st.as<int32_t>(), nullptr),
+          "pack_bits");
+    sync();
+    require(to_host<int32_t>(st.get(), 1)[0] == RDKV_OK, "pack_bits: code overflows bit-width");
+    if (nbytes) out = to_host<uint8_t>(o.get(), nbytes);
+    return out;
+}
+
+std::vector<std::uint8_t> unpack_bits(std::span<const std::uint8_t> bytes, int bits, int logical_len) {  // :76-88
+    require(bits == 2 || bits == 4 || bits == 8, "unpack_bits: bits must be 2, 4 or 8");
+    const int per = 8 / bits;
+    // a negative length wraps to a huge size_t in the reference's check: same exception
+    require(logical_len >= 0 && static_cast<std::size_t>((logical_len + per - 1) / per) <= bytes.size(),
+            "unpack_bits: byte buffer too short");
+    if (logical_len == 0) return {};
+    DevBuf b = to_device(bytes.data(), bytes.size()), o(static_cast<std::size_t>(logical_len));
+    check(rdkv_cuda_unpack_bits(b.as<uint8_t>(), static_cast<int64_t>(bytes.size()), bits, logical_len,
+                                o.as<uint8_t>(), nullptr),
+          "unpack_bits");
+    sync();
+    return to_host<uint8_t>(o.get(), static_cast<std::size_t>(logical_len));
+}
+
 QuantizedUnit quantize_unit(std::span<const float> values, int bits) {
     require(is_quant_width(bits), "quantize_unit: bits must be 2, 4 or 8");
     require(!values.empty(), "quantize_unit: empty unit");

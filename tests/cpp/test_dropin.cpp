@@ -669,6 +669,164 @@ void rows() {
     });
 }
 
+// ---- boundary: allocate_v / allocate_k, pack_bits / unpack_bits, RDKVP001 ---------
+// HeadAllocation of a packed head (the CLI's allocation_from_packed, rdkv.cpp:192-204)
+rdkv::HeadAllocation alloc_of(const rdkv::TriZoneCache& t) {
+    rdkv::HeadAllocation a = make_alloc(t.v_bits, t.k_bits);
+    return a;
+}
+
+// cmd_verify's payload check (rdkv.cpp:192-204): every head's stored zones equal a
+// direct re-quantisation of the source cache. Returns the number of mismatching heads.
+size_t verify_payload(const rdkv::KVCache& cache, const rdkv::PackedModel& m) {
+    size_t bad = 0;
+    for (int l = 0; l < cache.shape.layers; ++l)
+        for (int h = 0; h < cache.shape.kv_heads; ++h) {
+            const auto& t = m.at(l, h);
+            const auto expect = rdkv::reconstruct_dense(cache.k_head(l, h), cache.v_head(l, h), alloc_of(t));
+            const auto stored = rdkv::materialize(t);
+            bad += stored.k_hat != expect.k_hat || stored.v_hat != expect.v_hat;
+        }
+    return bad;
+}
+
+std::vector<char> slurp(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    std::vector<char> b;
+    if (!f) return b;
+    char buf[65536];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof buf, f)) > 0) b.insert(b.end(), buf, buf + n);
+    std::fclose(f);
+    return b;
+}
+
+void spit(const std::string& path, const std::vector<char>& b) {
+    FILE* f = std::fopen(path.c_str(), "wb");
+    std::fwrite(b.data(), 1, b.size(), f);
+    std::fclose(f);
+}
+
+void boundary() {
+    run("kat pack_bits 0x39 / 0x3A, overflow throws", [](std::string& d) {
+        // test_trizone.cpp:65-78
+        const auto two = rdkv::cuda::pack_bits(std::vector<uint8_t>{1, 2, 3, 0}, 2);
+        const auto four = rdkv::cuda::pack_bits(std::vector<uint8_t>{0xA, 0x3}, 4);
+        d = two.empty() ? "empty" : std::to_string(two[0]);
+        return two == std::vector<uint8_t>{0x39} && four == std::vector<uint8_t>{0x3A} &&
+               throws<std::invalid_argument>([] { rdkv::cuda::pack_bits(std::vector<uint8_t>{0, 4}, 2); }) &&
+               throws<std::invalid_argument>([] { rdkv::cuda::pack_bits(std::vector<uint8_t>{1}, 3); }) &&
+               throws<std::invalid_argument>([] { rdkv::cuda::unpack_bits(std::vector<uint8_t>{0x00}, 8, 2); }) &&
+               throws<std::invalid_argument>([] { rdkv::cuda::unpack_bits(std::vector<uint8_t>{0x00}, 5, 1); }) &&
+               throws<std::invalid_argument>([] { rdkv::cuda::unpack_bits(std::vector<uint8_t>{0x00}, 2, -3); });
+    });
+    run("pack_bits / unpack_bits == reference (600 rows)", [](std::string& d) {
+        Gen g(404);
+        for (int i = 0; i < 600; ++i) {
+            static const int kBits[3] = {2, 4, 8};
+            const int bits = kBits[i % 3];
+            const int len = i < 30 ? i : g.pick(1, 5000);
+            std::vector<uint8_t> codes(len);
+            for (auto& c : codes) c = (uint8_t)(g.eng() & ((1u << bits) - 1));
+            const auto a = rdkv::cuda::pack_bits(codes, bits);
+            const auto b = rdkv::pack_bits(codes, bits);
+            const int ll = len ? g.pick(0, len) : 0;
+            if (a != b || rdkv::cuda::unpack_bits(b, bits, ll) != rdkv::unpack_bits(b, bits, ll) ||
+                rdkv::cuda::unpack_bits(a, bits, len) != codes) {
+                d = "bits " + std::to_string(bits) + " len " + std::to_string(len);
+                return false;
+            }
+        }
+        return true;
+    });
+    run("allocate_v / allocate_k == reference", [](std::string& d) {
+        Gen g(505);
+        const auto ev = eps_table(true), ek = eps_table(false);
+        rdkv::BitSet bits;
+        rdkv::SolverConfig solver;
+        for (int i = 0; i < 60; ++i) {
+            rdkv::WeightVector wt, wc;
+            wt.kind = rdkv::WeightKind::token;
+            wc.kind = rdkv::WeightKind::channel;
+            const int T = g.pick(1, 3000), dd = g.pick(1, 160);
+            for (int t = 0; t < T; ++t) wt.values.push_back(std::fabs(g.gauss()) * (g.uni() < 0.03 ? 50.0f : 1.0f));
+            for (int c = 0; c < dd; ++c) wc.values.push_back(std::fabs(g.gauss()) * (c % 17 == 0 ? 8.0f : 1.0f));
+            const double vb = i % 10 == 0 ? 0.0 : g.uni() * 16.0 * dd * T * (i % 3 ? 0.05 : 1.2);
+            const auto a = rdkv::cuda::allocate_v(wt, ev, vb, dd, bits, solver);
+            const auto b = rdkv::allocate_v(wt, ev, vb, dd, bits, solver);
+            if (a.v_bits != b.v_bits || a.kept.kept != b.kept.kept || a.kept.v16 != b.kept.v16 ||
+                a.kept.evicted != b.kept.evicted || a.raw.bits != b.raw.bits || a.raw.lambda != b.raw.lambda ||
+                a.raw.objective != b.raw.objective || a.raw.converged != b.raw.converged ||
+                a.raw.achieved_avg_bits != b.raw.achieved_avg_bits) {
+                d = "allocate_v case " + std::to_string(i);
+                return false;
+            }
+            const int kept = i % 11 == 0 ? 0 : (int)b.kept.kept.size();
+            const double kb = i % 7 == 0 ? -1.0 : g.uni() * 16.0 * dd * std::max(kept, 1) * (i % 2 ? 0.1 : 1.1);
+            const auto x = rdkv::cuda::allocate_k(wc, ek, kb, kept, bits, solver);
+            const auto y = rdkv::allocate_k(wc, ek, kb, kept, bits, solver);
+            if (x.bits != y.bits || x.lambda != y.lambda || x.objective != y.objective || x.converged != y.converged ||
+                x.achieved_avg_bits != y.achieved_avg_bits) {
+                d = "allocate_k case " + std::to_string(i);
+                return false;
+            }
+        }
+        rdkv::WeightVector wrong;
+        wrong.kind = rdkv::WeightKind::channel;
+        wrong.values = {1.0f};
+        rdkv::WeightVector empty;
+        empty.kind = rdkv::WeightKind::token;
+        return throws<std::invalid_argument>([&] { rdkv::cuda::allocate_v(wrong, ev, 10.0, 1, bits, solver); }) &&
+               throws<std::invalid_argument>([&] { rdkv::cuda::allocate_v(empty, ev, 10.0, 1, bits, solver); }) &&
+               throws<std::invalid_argument>([&] { rdkv::cuda::allocate_k(empty, ek, 10.0, 3, bits, solver); });
+    });
+    // RDKVP001 (trizone.cpp:532-779) round trip of a GPU-packed model and the
+    // cmd_verify tamper check (test_cli.cpp:165-172)
+    const rdkv::CacheShape shape{2, 8, 2, 128, 2048};
+    const auto cache = rdkv::gen_synthetic_cache(606, shape, 32, 0, 1.0);
+    rdkv::BudgetSpec spec;
+    spec.n_tokens = 256;
+    rdkv::PipelineConfig cfg;
+    const auto ra = rdkv::allocate_model(cache, spec, eps_table(true), eps_table(false), cfg);
+    const std::string path = "/tmp/rdkv_dropin_roundtrip.rdkvp", tpath = "/tmp/rdkv_dropin_tampered.rdkvp";
+    run("RDKVP001 save(download) -> load -> upload -> decode", [&](std::string& d) {
+        auto dev = rdkv::cuda::DevicePackedModel::build(cache, ra, 4);
+        const auto host = dev.download();
+        rdkv::save_packed(host, path);
+        const auto loaded = rdkv::load_packed(path);
+        auto up = rdkv::cuda::DevicePackedModel::upload(loaded, 4);
+        Gen g(7);
+        std::vector<float> q((size_t)shape.layers * shape.q_heads * shape.head_dim);
+        for (auto& x : q) x = g.gauss();
+        const auto a = dev.decode(q), b = up.decode(q);
+        size_t v16 = 0;
+        for (const auto& h : ra.heads) v16 += h.kept.v16.size();
+        const size_t bad = verify_payload(cache, loaded);
+        d = "decode " + std::string(a == b ? "bit-identical" : "differs") + ", verify mismatches " +
+            std::to_string(bad) + ", arena " + std::to_string(up.arena_bytes()) + " vs " + std::to_string(dev.arena_bytes());
+        return a == b && bad == 0 && v16 == 0 && up.arena_bytes() == dev.arena_bytes();
+    });
+    run("RDKVP001 tampered payload fails verify", [&](std::string& d) {
+        auto bytes = slurp(path);
+        if (bytes.size() < 16) return false;
+        bytes[bytes.size() - 5] = static_cast<char>(bytes[bytes.size() - 5] ^ 0x5A);
+        spit(tpath, bytes);
+        const auto tampered = rdkv::load_packed(tpath);
+        // through the device: upload the tampered container, download it again
+        auto up = rdkv::cuda::DevicePackedModel::upload(tampered, 0);
+        const auto back = up.download();
+        const size_t bad_host = verify_payload(cache, tampered), bad_dev = verify_payload(cache, back);
+        auto clean = rdkv::cuda::DevicePackedModel::upload(rdkv::load_packed(path), 0);
+        Gen g(8);
+        std::vector<float> q((size_t)shape.layers * shape.q_heads * shape.head_dim);
+        for (auto& x : q) x = g.gauss();
+        const bool differs = up.decode(q) != clean.decode(q);
+        d = "mismatching heads " + std::to_string(bad_host) + " (device round trip " + std::to_string(bad_dev) +
+            "), decode " + (differs ? "differs" : "same");
+        return bad_host == 1 && bad_dev == 1 && differs;
+    });
+}
+
 }  // namespace
 
 int main() {
@@ -678,6 +836,7 @@ int main() {
     trizone();
     pipeline();
     rows();
+    boundary();
     std::printf("%d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
 }

@@ -1,0 +1,140 @@
+"""Parity at the BASELINE.json shapes the bench runs (VERDICT r1 "untested
+configurations"), on the same K0 inputs the bench generates:
+
+  * configs[2]: one (sequence, layer) slice of the 128K LLaMA-3.1-8B workload
+    against the UNMODIFIED reference (oracle/_ref: allocate_model +
+    build_packed_model + packed_decode_step, trizone.cpp:91-305) — allocation,
+    zone indices and payload bytes bit-exact, decode <= 1e-3 through the fp16
+    production decode;
+  * configs[3]: Qwen2.5-7B (g=7) / Mistral-7B (g=4) KV shapes at budgets whose
+    mixed 2/4/8-bit tiles do not fit shared memory, decoded through the
+    automatic dispatch and checked against the oracle's TriZone decode;
+  * configs[4]: the LLaMA-3.1-70B KV shape (80 layers, GQA group 8) in one
+    launch against the oracle, allocation of a layer against the reference.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2605_08317_b200 import pipeline as P
+from paper_2605_08317_b200.workload import WorkloadSpec, gen_chunk
+
+pytestmark = pytest.mark.gpu
+
+DECODE_TOL = 1e-3
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _slice(spec, b=0, layer=0):
+    """Device K0 chunk of one (sequence, layer) and its host f32 copy (FP16-representable)."""
+    k, v, q = gen_chunk(spec, b, layer)
+    return (k, v, q), (k.float().cpu().numpy(), v.float().cpu().numpy(), q.float().cpu().numpy())
+
+
+def test_configs2_128k_slice_matches_reference(cuda, ref):
+    """Sequence 0, layer 0 of the bench workload (8 KV heads x 32 q-heads, T=131072, n=128)."""
+    spec = WorkloadSpec(batch=1, layers=1, ctx=131072, n_tokens=128)
+    (kd, vd, qd), (k, v, q) = _slice(spec)
+    H, T, d, g, Sw = spec.kv_heads, spec.ctx, spec.head_dim, spec.group, spec.probe_rows
+    cfg = P.default_config(n_tokens=spec.n_tokens, window=Sw)
+    al = P.allocate_model(kd, qd, cfg, kv_heads=H)
+    al.check()
+    model = P.build_packed_model(kd, vd, al, group=g)
+    model.check()
+    rm = oracle.RefModel(ref, k[None], v[None], q.reshape(1, H * g, Sw, d), oracle.default_config(n_tokens=128, window=Sw))
+    vb, kb, st = al.v_bits.cpu().numpy(), al.k_bits.cpu().numpy(), al.stats_host()
+    for h in range(H):
+        want = rm.head(0, h)
+        assert np.array_equal(vb[h], want["v_bits"]), h
+        assert np.array_equal(kb[h][: len(want["k_bits"])], want["k_bits"]), h
+        for f in ("lambda_v", "lambda_k", "objective_v", "objective_k", "achieved_bits"):
+            assert st[h][f] == want[f], (h, f)
+        got, exp = model.export(h), rm.trizone(0, h).canon()
+        for f in ("kept", "payload", "segtab", "perm", "vscale", "vzero", "kscale", "kzero"):
+            assert np.array_equal(got[f], exp[f]), (h, f)
+    assert model.plan.uniform2 >= 1  # the production (u2x) kernel decodes this slice
+    qn = oracle.load().normal_stream(0xD15C0, H * g * d).reshape(H, g, d).astype(np.float16).astype(np.float32)
+    out = P.packed_decode_step(model, torch.from_numpy(qn).to(cuda).half()).float().cpu().numpy()
+    want, _ = rm.decode(qn.reshape(1, H * g, d))
+    worst = max(rel(out.reshape(H * g, d)[j], want[0, j]) for j in range(H * g))
+    assert worst < DECODE_TOL, worst
+
+
+@pytest.mark.parametrize("name,Hq,Hkv,n", [("qwen2.5-7b", 28, 4, 1024), ("qwen2.5-7b", 28, 4, 2048),
+                                           ("mistral-7b", 32, 8, 2048)])
+def test_configs3_large_mixed_tiles_auto_dispatch(cuda, orc, name, Hq, Hkv, n):
+    """configs[3] budget points whose tiles (1,600-3,100 kept slots at 2/4/8 bits,
+    heavy hitters + outlier K channels, the bench's inputs) exceed shared memory:
+    the automatic dispatch vs the oracle's build_trizone + packed_decode_step."""
+    spec = WorkloadSpec(batch=1, layers=2, q_heads=Hq, kv_heads=Hkv, ctx=65536, n_tokens=n, seed=11,
+                        hh_stride=64, hh_boost=1.0, outlier_channels=4, outlier_scale=8.0)
+    g, d = spec.group, spec.head_dim
+    cfg = P.default_config(n_tokens=n, window=spec.probe_rows)
+    rng = np.random.default_rng(n + Hq)
+    worst, classes = 0.0, set()
+    for layer in range(spec.layers):
+        (kd, vd, qd), (k, v, _) = _slice(spec, 0, layer)
+        al = P.allocate_model(kd, qd, cfg, kv_heads=Hkv)
+        al.check()
+        model = P.build_packed_model(kd, vd, al, group=g)
+        model.check()
+        assert model.plan.max_slots > 1024
+        q = rng.standard_normal((Hkv, g, d)).astype(np.float16).astype(np.float32)
+        out = P.packed_decode_step(model, torch.from_numpy(q).to(cuda).half()).float().cpu().numpy()
+        vb, kb = al.v_bits.cpu().numpy(), al.k_bits.cpu().numpy()
+        for h in range(Hkv):
+            classes |= set(np.unique(vb[h]).tolist())
+            tz = orc.tz_build(k[h], v[h], vb[h].astype(np.int32), kb[h].astype(np.int32))
+            for j in range(g):
+                worst = max(worst, rel(out[h, j], tz.decode(q[h, j])))
+    assert {2, 4}.issubset(classes), classes  # mixed tiers, not the uniform fast path
+    assert worst < DECODE_TOL, worst
+
+
+def test_configs4_llama70b_g8_all_layers(cuda, orc, ref):
+    """configs[4] LLaMA-3.1-70B KV shape: 80 layers x 8 KV heads, GQA group 8, n=128,
+    in one decode launch (two 4-head passes per staged tile). T reduced to 8K so the
+    oracle can decode all 640 tiles; the tile shapes match 128K (128 kept tokens, 2 bits)."""
+    spec = WorkloadSpec(batch=1, layers=80, q_heads=64, kv_heads=8, ctx=8192, n_tokens=128, seed=5)
+    H, g, d, Sw = spec.kv_heads, spec.group, spec.head_dim, spec.probe_rows
+    cfg = P.default_config(n_tokens=128, window=Sw)
+    Ks, Vs, vbs, kbs = [], [], [], []
+    host = []
+    checked = (0, 1, 39, 79)  # layers decoded by the oracle (all 80 run in the launch)
+    for layer in range(spec.layers):
+        k, v, qp = gen_chunk(spec, 0, layer)
+        al = P.allocate_model(k, qp, cfg, kv_heads=H)
+        al.check()
+        Ks.append(k), Vs.append(v), vbs.append(al.v_bits), kbs.append(al.k_bits)
+        if layer in checked:
+            hk = (k.float().cpu().numpy(), v.float().cpu().numpy(),
+                  qp.float().cpu().numpy() if layer == 0 else None)
+            host.append((layer, hk, al))
+    K, V = torch.cat(Ks), torch.cat(Vs)
+    alloc = P.Allocation(torch.cat(vbs), torch.cat(kbs), torch.zeros(1, dtype=torch.uint8, device=cuda))
+    model = P.build_packed_model(K, V, alloc, group=g)
+    model.check()
+    assert model.units == 640 and model.plan.uniform2 >= 1
+    rng = np.random.default_rng(70)
+    q = rng.standard_normal((640, g, d)).astype(np.float16).astype(np.float32)
+    out = P.packed_decode_step(model, torch.from_numpy(q).to(cuda).half()).float().cpu().numpy()
+    worst = 0.0
+    for layer, (k, v, pq), al in host:
+        vb, kb = al.v_bits.cpu().numpy(), al.k_bits.cpu().numpy()
+        if pq is not None:  # allocation of this layer vs the reference
+            rm = oracle.RefModel(ref, k[None], v[None], pq.reshape(1, H * g, Sw, d), oracle.default_config(n_tokens=128, window=Sw))
+            for h in range(H):
+                want = rm.head(0, h)
+                assert np.array_equal(vb[h], want["v_bits"]) and np.array_equal(kb[h][: len(want["k_bits"])], want["k_bits"])
+        for h in range(H):
+            u = layer * H + h
+            tz = orc.tz_build(k[h], v[h], vb[h].astype(np.int32), kb[h].astype(np.int32))
+            for j in range(g):
+                worst = max(worst, rel(out[u, j], tz.decode(q[u, j])))
+    assert worst < DECODE_TOL, worst
