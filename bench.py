@@ -47,6 +47,11 @@ def parse():
     p.add_argument("--no-pipeline", action="store_true")
     p.add_argument("--no-secondary", action="store_true", help="skip the Zone C / budget-512 secondary lines")
     p.add_argument("--cpu-budget-s", type=float, default=8.0)
+    p.add_argument("--shard", default="seqs", choices=["seqs", "heads"],
+                   help="multi-GPU partition: seqs = batch sequences per GPU (weak scaling); "
+                        "heads = the batch on every GPU, KV heads split across GPUs (strong scaling)")
+    p.add_argument("--dist-backend", default=None, choices=["nccl", "gloo"],
+                   help="process-group backend (default nccl; gloo lets several ranks share one GPU)")
     return p.parse_args()
 
 
@@ -139,10 +144,10 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
 
 
-def dist_setup():
+def dist_setup(backend=None):
     from paper_2605_08317_b200 import dist as D
 
-    return D.init()
+    return D.init(backend)
 
 
 def barrier_sync(world):
@@ -228,15 +233,17 @@ def run_reference_arm(args, world, rank):
     per_step = max(0.2, args.cpu_budget_s / max(args.steps, 1))
     info = reference_sample(spec, dict(n_tokens=spec.n_tokens, window=spec.probe_rows), per_step * args.steps)
     sample_units = spec.kv_heads  # one (sequence, layer) slice = 8 tiles, 32 q-heads
-    scale = (spec.batch * args.gpus * spec.layers * spec.kv_heads) / sample_units
+    seqs = spec.batch * (args.gpus if args.shard == "seqs" else 1)  # sequences in the whole job
+    scale = (seqs * spec.layers * spec.kv_heads) / sample_units
     step_s = info["sample_step_s"] * scale
-    value = spec.batch * args.gpus / step_s
+    value = seqs / step_s
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "weak" if args.shard == "seqs" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (K0 counter-based generator, FP16-representable)",
         "impl": "reference",
-        "config": workload_config(spec, args),
+        "config": workload_config(spec, args, args.gpus),
         "cpu_baseline": {"value": value, "unit": "tok/s", "cores": info["cores"], "kind": info["kind"], **host_cpu(),
                          "sample": f"1 of {int(scale)} (sequence, layer) slices (8 KV heads x 4 q-heads, T={spec.ctx}) timed "
                                    f"{info['sample_step_s'] * 1e3:.3f} ms/step via parallel_for; step = x{int(scale)}"},
@@ -248,15 +255,19 @@ def run_reference_arm(args, world, rank):
 METRIC = "decode tok/s & us/step at 128K ctx; HBM GB/s vs peak; speedup vs FP16 full-KV"
 
 
-def workload_config(spec, args):
+def workload_config(spec, args, world):
+    seqs = spec.batch * (world if args.shard == "seqs" else 1)
+    part = (f"shard by sequence x{world} (weak scaling, no collective)" if args.shard == "seqs" else
+            f"shard by KV head x{world} (strong scaling: every GPU holds the {spec.batch} sequences and "
+            f"{spec.kv_heads // world}-{-(-spec.kv_heads // world)} of the {spec.kv_heads} KV heads; no collective)")
     return {
         "workload": f"LLaMA-3.1-8B KV shape ({spec.layers} layers, {spec.q_heads} q / {spec.kv_heads} kv heads, "
                     f"d={spec.head_dim}), {spec.ctx} ctx, {spec.n_tokens}-token/layer budget, batch {spec.batch}/GPU, "
                     "one decode step over all layers (configs[2])",
         "layers": spec.layers, "q_heads": spec.q_heads, "kv_heads": spec.kv_heads, "head_dim": spec.head_dim,
-        "ctx": spec.ctx, "batch_per_gpu": spec.batch, "global_batch": spec.batch * args.gpus,
-        "n_tokens": spec.n_tokens, "zone_c": args.zc, "heavy_hitters": bool(args.hh),
-        "parallelism": f"shard by sequence x{args.gpus} (no collective)",
+        "ctx": spec.ctx, "batch_per_gpu": spec.batch if args.shard == "seqs" else f"{spec.batch} (KV-head shard)",
+        "global_batch": seqs, "n_tokens": spec.n_tokens, "zone_c": args.zc, "heavy_hitters": bool(args.hh),
+        "parallelism": part, "shard": args.shard,
         "l2": "inputs larger than L2: step i decodes rotation copy i % NR of the packed arena, q and out "
               "(NR copies >= 3x the 126 MB L2), K steps back to back from one CUDA graph",
         "io": "fp16 q/out",
@@ -510,7 +521,7 @@ def secondary_configs(P, spec0, model, q, args):
 def main():
     args = parse()
     check_env()
-    world, rank, local = dist_setup()
+    world, rank, local = dist_setup(args.dist_backend)
     if args.impl == "reference":
         run_reference_arm(args, world, rank)
         return
@@ -522,7 +533,9 @@ def main():
 
     capi.lib()
     spec = WorkloadSpec(batch=args.batch, layers=args.layers, ctx=args.ctx, n_tokens=args.n_tokens, rank=rank,
-                        hh_stride=64 if args.hh else 0, hh_boost=1.0 if args.hh else 0.0, zc_cap=max(args.zc, 0))
+                        hh_stride=64 if args.hh else 0, hh_boost=1.0 if args.hh else 0.0, zc_cap=max(args.zc, 0),
+                        shard=args.shard, world=world)
+    seqs_job = spec.batch * (world if args.shard == "seqs" else 1)  # sequences decoded per step, all ranks
     t0 = time.perf_counter()
     model, build_timing, stats, first_alloc = build(spec)
     build_s = time.perf_counter() - t0
@@ -579,8 +592,9 @@ def main():
         barrier_sync(world)
     ms_local = ev0.elapsed_time(ev1) / args.steps
     ms = max_over_ranks(ms_local, world)
-    value = spec.batch * world / (ms / 1e3)
-    assert torch.equal(rot[0][2], rot[-1][2]) if n_rot > 1 else True
+    value = seqs_job / (ms / 1e3)
+    last = min(n_rot, args.steps) - 1  # the last rotation copy the timed steps decoded
+    assert torch.equal(rot[0][2], rot[last][2])
     del graph
 
     # ---- the same step timed alone after an L2 flush (one event pair per step):
@@ -663,9 +677,10 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "us_per_step": ms * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "fp32-accum/fp16-io, int codes",
+        "scaling": "weak" if args.shard == "seqs" else "strong", "vs_baseline": None,
+        "dtype": "fp32-accum/fp16-io, int codes",
         "data": "synthetic (K0 counter-based N(0,1)-like KV, FP16-representable), random-init",
-        "config": workload_config(spec, args),
+        "config": workload_config(spec, args, world),
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
@@ -673,14 +688,14 @@ def main():
                      "layout_bytes_per_launch": layout_bytes,
                      "layout_overhead_bytes": layout_bytes - alg_bytes,
                      "frac_incl_layout_overhead": layout_bytes / (ms_local / 1e3) / 1e9 / peak},
-        "e2e": {"value": spec.batch * world / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
+        "e2e": {"value": seqs_job / (e2e_ms / 1e3), "unit": "tok/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": qh.numel() * qh.element_size(),
                 "d2h_bytes_per_step": oh.numel() * oh.element_size(),
                 "path": "rdkv_cuda_decode_host (C-ABI), pinned host q/out: the kernel reads q over PCIe (TMA "
                         "bulk loads) and writes out (TMA bulk stores) inside the step",
                 "copy_engine_pipelined_ms_per_step": pipelined_ms},
         "clocks": sampler.report(),
-        "flushed_step": {"ms_per_step": flushed_ms, "tok_s": spec.batch * world / (flushed_ms / 1e3),
+        "flushed_step": {"ms_per_step": flushed_ms, "tok_s": seqs_job / (flushed_ms / 1e3),
                          "note": "one launch per event pair after a 512 MiB memset (cold L2 + launch latency)"},
         "rotation_copies": n_rot,
         "per_layer_launch": per_layer,
@@ -747,7 +762,7 @@ def per_layer_launch_ms(P, model, spec, q, out, flush, args):
     import torch
 
     subs = []
-    H = spec.kv_heads
+    H = spec.local_heads
     for layer in range(spec.layers):
         # units of this layer across the batch are not contiguous; build a per-layer offsets view
         idx = np.array([(b * spec.layers + layer) * H + h for b in range(spec.batch) for h in range(H)])

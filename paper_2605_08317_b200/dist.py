@@ -64,6 +64,10 @@ def init(backend: str | None = None) -> tuple[int, int, int]:
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
+            # gloo: CPU tests, or several ranks sharing one GPU (NCCL refuses two
+            # ranks on one device) — rank-local GPU work on device local % count
+            if torch.cuda.is_available():
+                torch.cuda.set_device(local % torch.cuda.device_count())
             dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)

@@ -40,11 +40,41 @@ class WorkloadSpec:
     outlier_channels: int = 0
     outlier_scale: float = 1.0
     zc_cap: int = 0
+    # multi-GPU partition (north_star "by batch and KV head"):
+    #   "seqs":  weak scaling, rank r owns sequences r*batch .. r*batch+batch-1, all KV heads
+    #   "heads": strong scaling, every rank holds all `batch` sequences and its own
+    #            contiguous range of KV heads (dist.strong_shard over kv_heads)
+    shard: str = "seqs"
+    world: int = 1
+
+    def __post_init__(self):
+        if self.shard not in ("seqs", "heads"):
+            raise ValueError(f"shard must be 'seqs' or 'heads', not {self.shard!r}")
+        if self.shard == "heads" and self.world > self.kv_heads:
+            raise ValueError(f"cannot split {self.kv_heads} KV heads over {self.world} ranks")
 
     @property
     def first_seq(self):
         """Global id of this rank's first sequence (weak scaling: batch sequences per rank)."""
-        return self.rank * self.batch
+        return self.rank * self.batch if self.shard == "seqs" else 0
+
+    @property
+    def head_range(self) -> range:
+        """Global KV heads this rank owns."""
+        if self.shard == "seqs":
+            return range(self.kv_heads)
+        from .dist import strong_shard
+
+        return strong_shard(self.kv_heads, self.rank, self.world).items
+
+    @property
+    def local_heads(self) -> int:
+        return len(self.head_range)
+
+    def global_unit(self, b: int, layer: int, h_local: int) -> int:
+        """Unit id of (local sequence b, layer, local head) in the whole job
+        ((seq * L + l) * H_kv + h, the reference's l * H_kv + h per sequence)."""
+        return ((self.first_seq + b) * self.layers + layer) * self.kv_heads + self.head_range[h_local]
 
     @property
     def group(self):
@@ -52,17 +82,21 @@ class WorkloadSpec:
 
     @property
     def units(self):
-        return self.batch * self.layers * self.kv_heads
+        return self.batch * self.layers * self.local_heads
 
 
 def gen_chunk(spec: WorkloadSpec, b: int, layer: int, dtype=torch.float16):
-    """K, V [H_kv, T, d] and probe Q [H_kv, g, S_w, d] of one (sequence, layer)."""
+    """K, V [h, T, d] and probe Q [h, g, S_w, d] of one (sequence, layer), for the
+    rank's h KV heads: the counter-based generator makes a head subset the exact
+    slice of the full (sequence, layer) tensors (first_index offsets)."""
     s = chunk_seed(spec.seed, spec.first_seq + b, layer)
-    H, T, d = spec.kv_heads, spec.ctx, spec.head_dim
-    k = P.generate((H, T, d), dtype, seed=s, tensor=0, seq_len=T, outlier_channels=spec.outlier_channels,
-                   outlier_scale=spec.outlier_scale, hh_stride=spec.hh_stride, hh_boost=spec.hh_boost)
-    v = P.generate((H, T, d), dtype, seed=s, tensor=1, seq_len=T)
-    q = P.generate((H, spec.group, spec.probe_rows, d), dtype, seed=s, tensor=2, seq_len=T,
+    T, d, g, Sw = spec.ctx, spec.head_dim, spec.group, spec.probe_rows
+    h0, H = spec.head_range.start, spec.local_heads
+    k = P.generate((H, T, d), dtype, seed=s, tensor=0, first_index=h0 * T * d, seq_len=T,
+                   outlier_channels=spec.outlier_channels, outlier_scale=spec.outlier_scale,
+                   hh_stride=spec.hh_stride, hh_boost=spec.hh_boost)
+    v = P.generate((H, T, d), dtype, seed=s, tensor=1, first_index=h0 * T * d, seq_len=T)
+    q = P.generate((H, g, Sw, d), dtype, seed=s, tensor=2, first_index=h0 * g * Sw * d, seq_len=T,
                    hh_stride=spec.hh_stride)
     return k, v, q
 
@@ -81,6 +115,8 @@ def build(spec: WorkloadSpec, cfg=None, log=None):
             k, v, q = gen_chunk(spec, b, layer)
             torch.cuda.synchronize()
             t1 = time.perf_counter()
+            # head budget over the model's KV heads (head_budget, pipeline.cpp:60-72),
+            # whatever subset of them this rank holds
             alloc = P.allocate_model(k, q, cfg, kv_heads=spec.kv_heads)
             torch.cuda.synchronize()
             t2 = time.perf_counter()
