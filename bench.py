@@ -418,6 +418,7 @@ def secondary_configs(P, spec0, model, q, args):
 
     def loop():
         model.zc_len.zero_()
+        model.zc_count = 0  # host mirror of the reset (append_new_token checks capacity)
         for i in range(nsteps):
             P.append_new_token(model, kv[i], kv[i])
             P.packed_decode_step(model, qs[i], o)
