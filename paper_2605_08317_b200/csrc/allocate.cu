@@ -19,6 +19,8 @@
 // convergence flags are identical given identical weights. The reported
 // objectives are summed by one thread in the reference's order (a sequential
 // fp64 sum, allocator.cpp:301-311), so they are bit-identical too.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace rdkv_b200 {
@@ -258,6 +260,365 @@ __global__ void __launch_bounds__(kAllocThreads) allocate_kernel(
     if (threadIdx.x == 0) stats[unit] = out;
 }
 
+// ---------------------------------------------------------------------------
+// Production path for long contexts: Stage 2 (the V-token bisection, the
+// expensive sweep over T tokens) on a thread-block cluster of kClV CTAs per
+// unit, each sweeping T / kClV tokens; the per-iterate bit totals are exact
+// integers summed across the cluster through distributed shared memory, so
+// every CTA takes the same lambda decision (bit-identical to the one-CTA
+// sweep). Stage 3 and the sequential objectives follow in allocate_finish.
+constexpr int kClV = 8;
+constexpr int kClThreads = 1024;
+
+struct ClScratch {
+    long long part[2];  // this CTA's bit total of the current iterate (double-buffered by parity)
+    float fpart[2];
+    int ipart[2];
+    long long warp_ll[32];
+    float warp_f[32];
+    long long bcast;  // cluster totals, broadcast to the CTA
+    float ftot;
+};
+
+// Exact cluster-wide sum (long long) / max (float) / or (int): block reduce,
+// publish in this CTA's parity slot, cluster barrier, warp 0 gathers the kClV
+// slots over DSMEM. One cluster barrier per call: a slot is rewritten two calls
+// later, after every CTA has passed the barrier of the call in between.
+template <int OP>  // 0 sum ll, 1 max f, 2 or int
+__device__ __forceinline__ void cl_reduce(ClScratch& s, int& parity, long long v, float f, int iv,
+                                          long long& out_ll, float& out_f, int& out_i) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        if (OP == 0) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (OP == 1) f = fmaxf(f, __shfl_xor_sync(0xffffffffu, f, o));
+        if (OP == 2) iv |= __shfl_xor_sync(0xffffffffu, iv, o);
+    }
+    if (lane == 0) {
+        if (OP == 0) s.warp_ll[wid] = v;
+        if (OP == 1) s.warp_f[wid] = f;
+        if (OP == 2) s.warp_ll[wid] = iv;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        long long a = 0;
+        float m = 0.0f;
+        for (int i = lane; i < nw; i += 32) {
+            if (OP == 0 || OP == 2) a += s.warp_ll[i];
+            if (OP == 1) m = fmaxf(m, s.warp_f[i]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        }
+        if (lane == 0) {
+            s.part[parity] = a;
+            s.fpart[parity] = m;
+        }
+    }
+    cl.sync();
+    if (wid == 0) {
+        long long a = 0;
+        float m = 0.0f;
+        if (lane < (int)cl.num_blocks()) {
+            ClScratch* r = cl.map_shared_rank(&s, lane);
+            a = r->part[parity];
+            m = r->fpart[parity];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        }
+        if (lane == 0) {
+            s.bcast = a;
+            s.ftot = m;
+        }
+    }
+    __syncthreads();
+    out_ll = s.bcast;
+    out_f = s.ftot;
+    out_i = (int)out_ll;
+    parity ^= 1;
+}
+
+struct ClTable {
+    int n;
+    int widths[8];
+    double eps[8];
+};
+
+// Bit total of this CTA's tokens at lambda (argmin_entry per token with the
+// lambda * b terms hoisted: the same __dmul_rn values as argmin_bits).
+__device__ __forceinline__ long long cl_local_total(const float* __restrict__ w, int u0, int u1, const ClTable& t,
+                                                    const double (&lb)[8]) {
+    long long tot = 0;
+    for (int u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+        const double wd = (double)__ldg(w + u);
+        int best_bits = t.widths[0];
+        double best = __dadd_rn(__dmul_rn(wd, t.eps[0]), lb[0]);
+#pragma unroll
+        for (int i = 1; i < 8; ++i) {
+            if (i < t.n) {
+                const double cost = __dadd_rn(__dmul_rn(wd, t.eps[i]), lb[i]);
+                if (cost < best) {
+                    best = cost;
+                    best_bits = t.widths[i];
+                }
+            }
+        }
+        tot += best_bits;
+    }
+    return tot;
+}
+
+__global__ void __launch_bounds__(kClThreads, 1) allocate_v_cluster_kernel(const float* __restrict__ w_t, int t_len,
+                                                                           int d, int kv_heads, rdkv_config cfg,
+                                                                           int window, uint8_t* __restrict__ v_bits_all,
+                                                                           rdkv_head_stats* __restrict__ stats) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ ClScratch s;
+    const int rank = (int)cl.block_rank(), ncl = (int)cl.num_blocks();
+    const int unit = blockIdx.x / ncl;
+    const float* w = w_t + (size_t)unit * t_len;
+    uint8_t* vb = v_bits_all + (size_t)unit * t_len;
+    const int u0 = (int)((long long)t_len * rank / ncl), u1 = (int)((long long)t_len * (rank + 1) / ncl);
+    ClTable t;
+    t.n = cfg.n_widths;
+    for (int i = 0; i < 8; ++i) {
+        t.widths[i] = cfg.widths[i];
+        t.eps[i] = cfg.eps_v[i];
+    }
+    int parity = 0;
+    long long ll;
+    float fm;
+    int iv;
+    // check_weights (allocator.cpp:143-149) over the V weights; the K weights are
+    // checked by allocate_finish
+    int bad = 0;
+    float wmax = 0.0f;
+    for (int u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+        const float x = w[u];
+        bad |= !(isfinite(x) && x >= 0.0f);
+        wmax = fmaxf(wmax, x);
+    }
+    cl_reduce<2>(s, parity, 0, 0.0f, bad, ll, fm, iv);
+    bad = iv;
+    const double tokens_per_head = (double)cfg.n_tokens / (double)kv_heads;
+    const double head_bits = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens_per_head), (double)d), 16.0);
+    const double vbud = __dmul_rn(__dadd_rn(1.0, -cfg.r_k), head_bits);
+    rdkv_head_stats out{};
+    if (bad) {
+        out.status = RDKV_EINVAL;
+        if (rank == 0 && threadIdx.x == 0) stats[unit] = out;
+        return;
+    }
+    double lambda = 0.0, avg = 0.0;
+    int converged = 1, all_max = 0;
+    const int max_width = t.widths[t.n - 1];
+    if (!(vbud > 0.0)) {
+        for (int u = u0 + threadIdx.x; u < u1; u += blockDim.x) vb[u] = 0;
+    } else {
+        double target = vbud / __dmul_rn((double)d, (double)t_len);
+        if (target > 16.0) target = 16.0;
+        const double n = (double)t_len;
+        auto avg_at = [&](double lam) {
+            double lb[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) lb[i] = __dmul_rn(lam, (double)t.widths[i]);
+            cl_reduce<0>(s, parity, cl_local_total(w, u0, u1, t, lb), 0.0f, 0, ll, fm, iv);
+            return (double)ll / n;
+        };
+        if (target >= (double)max_width) {  // allocator.cpp:153-161
+            avg = max_width;
+            all_max = 1;
+        } else {
+            cl_reduce<1>(s, parity, 0, wmax, 0, ll, fm, iv);
+            double lo = 0.0, hi = (double)fm;
+            const double floor_avg = t.widths[0];
+            if (hi > 0.0) {  // :171-182
+                double hi_avg = avg_at(hi);
+                int guard = 0;
+                while (hi_avg > target && hi_avg > floor_avg && guard++ < 128) {
+                    hi = __dmul_rn(hi, 2.0);
+                    hi_avg = avg_at(hi);
+                }
+            }
+            lambda = hi;
+            converged = 0;
+            for (int it = 0; it < cfg.max_iterations; ++it) {  // :187-200
+                lambda = __dmul_rn(0.5, __dadd_rn(lo, hi));
+                avg = avg_at(lambda);
+                if (fabs(avg - target) / target < cfg.tolerance) {
+                    converged = 1;
+                    break;
+                }
+                if (avg > target) lo = lambda;
+                else hi = lambda;
+            }
+            if (cfg.strict_budget && avg > target) {  // :202-210
+                lambda = hi;
+                avg = avg_at(lambda);
+                converged = fabs(avg - target) / target < cfg.tolerance;
+            }
+        }
+        double lb[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) lb[i] = __dmul_rn(lambda, (double)t.widths[i]);
+        for (int u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+            int b = max_width;
+            if (!all_max) {
+                const double wd = (double)w[u];
+                b = t.widths[0];
+                double best = __dadd_rn(__dmul_rn(wd, t.eps[0]), lb[0]);
+                for (int i = 1; i < t.n; ++i) {
+                    const double cost = __dadd_rn(__dmul_rn(wd, t.eps[i]), lb[i]);
+                    if (cost < best) {
+                        best = cost;
+                        b = t.widths[i];
+                    }
+                }
+            }
+            vb[u] = (uint8_t)b;
+        }
+    }
+    // force-window override (pipeline.cpp:153-156), after every thread's
+    // materialising stores to the same bytes
+    __syncthreads();
+    if (cfg.force_window_retain)
+        for (int u = max(u0, t_len - window) + threadIdx.x; u < u1; u += blockDim.x) vb[u] = 16;
+    if (rank == 0 && threadIdx.x == 0) {
+        out.lambda_v = lambda;
+        out.avg_v = avg;
+        out.v_converged = converged;
+        out.status = -1;  // Stage 2 done; allocate_finish completes the record
+        stats[unit] = out;
+    }
+}
+
+// Sequential fp64 objective sum_u w_u * eps(b_u) in the reference's order
+// (allocator.cpp:301-311): warps 1.. form the products of the next chunk in
+// shared memory while thread 0 adds the current chunk in order, so the long
+// dependent chain runs at the DADD latency (no load latency on it).
+constexpr int kObjChunk = 2048;
+__device__ double block_sequential_objective(const float* __restrict__ w, const uint8_t* __restrict__ bits, int n,
+                                             const AllocTable& t, double* buf) {
+    double obj = 0.0;
+    const int nch = (n + kObjChunk - 1) / kObjChunk;
+    auto fill = [&](int c, double* dst, int t0, int step) {
+        const int base = c * kObjChunk, cnt = min(kObjChunk, n - base);
+        for (int i = t0; i < cnt; i += step) dst[i] = __dmul_rn((double)w[base + i], eps_of(t, bits[base + i]));
+    };
+    fill(0, buf, threadIdx.x, blockDim.x);
+    __syncthreads();
+    for (int c = 0; c < nch; ++c) {
+        const double* cur = buf + (c & 1) * kObjChunk;
+        if (threadIdx.x == 0) {
+            const int cnt = min(kObjChunk, n - c * kObjChunk);
+            int i = 0;
+            for (; i + 16 <= cnt; i += 16) {
+                double x[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) x[j] = cur[i + j];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) obj = __dadd_rn(obj, x[j]);
+            }
+            for (; i < cnt; ++i) obj = __dadd_rn(obj, cur[i]);
+        } else if (threadIdx.x >= 32 && c + 1 < nch) {
+            fill(c + 1, buf + ((c + 1) & 1) * kObjChunk, threadIdx.x - 32, blockDim.x - 32);
+        }
+        __syncthreads();
+    }
+    return obj;
+}
+
+// Stages 2 (tail) and 3 after allocate_v_cluster: counts, objectives, allocate_k.
+__global__ void __launch_bounds__(kAllocThreads) allocate_finish_kernel(
+    const float* __restrict__ w_t, const float* __restrict__ w_c, int t_len, int d, int kv_heads, rdkv_config cfg,
+    const uint8_t* __restrict__ v_bits_all, uint8_t* __restrict__ k_bits_all, rdkv_head_stats* __restrict__ stats) {
+    __shared__ Scratch s;
+    __shared__ double obj_v;
+    const int unit = blockIdx.x;
+    rdkv_head_stats out = stats[unit];
+    if (out.status != -1) return;  // invalid V weights: already reported
+    const float* wv = w_t + (size_t)unit * t_len;
+    const float* wk = w_c + (size_t)unit * d;
+    const uint8_t* vb = v_bits_all + (size_t)unit * t_len;
+    uint8_t* kb = k_bits_all + (size_t)unit * d;
+    AllocTable tv, tk;
+    tv.n = tk.n = cfg.n_widths;
+    for (int i = 0; i < 8; ++i) {
+        tv.widths[i] = tk.widths[i] = cfg.widths[i];
+        tv.eps[i] = cfg.eps_v[i];
+        tk.eps[i] = cfg.eps_k[i];
+    }
+    int bad = 0;
+    for (int u = threadIdx.x; u < d; u += blockDim.x) bad |= !(isfinite(wk[u]) && wk[u] >= 0.0f);
+    bad = block_reduce_sum<int>(bad, s.i);
+    if (bad) {
+        rdkv_head_stats e{};
+        e.status = RDKV_EINVAL;
+        __syncthreads();
+        if (threadIdx.x == 0) stats[unit] = e;
+        return;
+    }
+    const double tokens_per_head = (double)cfg.n_tokens / (double)kv_heads;
+    const double head_bits = __dmul_rn(__dmul_rn(__dmul_rn(2.0, tokens_per_head), (double)d), 16.0);
+    const double kbud = __dmul_rn(cfg.r_k, head_bits);
+    long long kept = 0, v16 = 0, vsum = 0;
+    for (int u = threadIdx.x; u < t_len; u += blockDim.x) {
+        const int b = vb[u];
+        kept += b > 0;
+        v16 += b == 16;
+        vsum += b;
+    }
+    kept = block_reduce_sum<long long>(kept, s.ll);
+    v16 = block_reduce_sum<long long>(v16, s.ll);
+    vsum = block_reduce_sum<long long>(vsum, s.ll);
+    {
+        __shared__ double objbuf[2 * kObjChunk];
+        const double o = block_sequential_objective(wv, vb, t_len, tv, objbuf);
+        if (threadIdx.x == 0) obj_v = o;
+    }
+    int k_len = d;
+    long long ksum = 0;
+    if (kept == 0) {
+        k_len = 0;
+        for (int u = threadIdx.x; u < d; u += blockDim.x) kb[u] = 0;
+        out.k_converged = 1;
+    } else if (!(kbud > 0.0)) {
+        for (int u = threadIdx.x; u < d; u += blockDim.x) kb[u] = 0;
+        out.k_converged = 1;
+    } else {
+        double target = kbud / __dmul_rn((double)kept, (double)d);
+        if (target > 16.0) target = 16.0;
+        BisectResult r = bisect(wk, d, tk, target, cfg.tolerance, cfg.max_iterations, cfg.strict_budget, s);
+        materialize_bits(wk, d, tk, r.lambda, target >= (double)tk.widths[tk.n - 1], kb);
+        out.lambda_k = r.lambda;
+        out.avg_k = r.avg;
+        out.k_converged = r.converged;
+    }
+    __syncthreads();
+    if (k_len > 0)
+        for (int u = threadIdx.x; u < d; u += blockDim.x) ksum += kb[u];
+    ksum = block_reduce_sum<long long>(ksum, s.ll);
+    if (threadIdx.x == 0) {
+        out.objective_v = obj_v;
+        out.objective_k = k_len > 0 ? sequential_objective(wk, kb, d, tk) : 0.0;
+        out.n_kept = (int)kept;
+        out.n_v16 = (int)v16;
+        out.k_bits_len = k_len;
+        out.achieved_bits = __dadd_rn(__dmul_rn((double)vsum, (double)d), __dmul_rn((double)ksum, (double)kept));
+        out.status = RDKV_OK;
+        stats[unit] = out;
+    }
+}
+
 }  // namespace rdkv_b200
 
 using namespace rdkv_b200;
@@ -292,6 +653,25 @@ extern "C" RDKV_API int rdkv_cuda_allocate(const float* w_t, const float* w_c, c
     if (int st = rdkv_validate_config(cfg)) return st;
     const int window = cfg->window < s->probe_rows ? cfg->window : s->probe_rows;
     if (cfg->force_window_retain && window > s->seq_len) return RDKV_EINVAL;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (s->seq_len >= kClV * kClThreads) {  // long contexts: the cluster sweep (bit-identical)
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(s->units * kClV);
+        lc.blockDim = dim3(kClThreads);
+        lc.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = kClV;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        RDKV_CUDA_TRY(cudaLaunchKernelEx(&lc, allocate_v_cluster_kernel, w_t, s->seq_len, s->head_dim, s->kv_heads,
+                                         *cfg, window, v_bits, stats));
+        allocate_finish_kernel<<<s->units, kAllocThreads, 0, st>>>(w_t, w_c, s->seq_len, s->head_dim, s->kv_heads,
+                                                                   *cfg, v_bits, k_bits, stats);
+        return launch_status();
+    }
     allocate_kernel<<<s->units, kAllocThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         w_t, w_c, s->seq_len, s->head_dim, s->kv_heads, *cfg, window, v_bits, k_bits, stats);
     return launch_status();

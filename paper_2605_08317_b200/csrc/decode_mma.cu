@@ -174,12 +174,16 @@ struct ScratchHead {
     float vinv[3][8];   // 1/sigma per (V class, head)
 };
 constexpr int kDigitBytesOff = 256;
+constexpr int kPartStride = kD + 4;  // floats per head of a chunk partial (16-B aligned rows)
 
-template <int NT, typename IO>
+// PART: `part` receives this (sub-)tile's unnormalised softmax state per head,
+// [g][kPartStride] = (sum_i p_i v_i [d], max logit (natural units), sum_i p_i), for the
+// chunked body (decode_gchunk_kernel) whose chunks are merged afterwards.
+template <int NT, typename IO, bool PART = false>
 __device__ __noinline__ void decode_tile(const uint8_t* __restrict__ t, const IO* __restrict__ qs, int g,
                                          uint8_t* __restrict__ scr, const MmaParams& prm,
                                          const __half* __restrict__ zck, const __half* __restrict__ zcv,
-                                         int nzc, IO* __restrict__ out) {
+                                         int nzc, IO* __restrict__ out, float* __restrict__ part = nullptr) {
     constexpr int G4 = 4 * NT;  // head capacity of the n-tiles
     constexpr int TS = 32 / G4; // lanes per head in the per-head phases
     const int lane = threadIdx.x & 31;
@@ -552,8 +556,19 @@ __device__ __noinline__ void decode_tile(const uint8_t* __restrict__ t, const IO
             o.z = fmaf(p, v23.x, o.z);
             o.w = fmaf(p, v23.y, o.w);
         }
-        const float inv = __frcp_rn(__shfl_sync(0xffffffffu, lsum, hh));
+        const float ls = __shfl_sync(0xffffffffu, lsum, hh);
         const float b = __shfl_sync(0xffffffffu, bv, hh);
+        if constexpr (PART) {
+            const float mh = __shfl_sync(0xffffffffu, mx, hh);
+            float* pr = part + hh * kPartStride;
+            reinterpret_cast<float4*>(pr)[lane] = make_float4(o.x + b, o.y + b, o.z + b, o.w + b);
+            if (lane == 0) {
+                pr[kD] = ls > 0.0f ? mh : -INFINITY;
+                pr[kD + 1] = ls;
+            }
+            continue;
+        }
+        const float inv = __frcp_rn(ls);
         const float r0 = (o.x + b) * inv, r1 = (o.y + b) * inv, r2 = (o.z + b) * inv, r3 = (o.w + b) * inv;
         if constexpr (sizeof(IO) == 2) {
             __half2 h0 = __floats2half2_rn(r0, r1), h1 = __floats2half2_rn(r2, r3);

@@ -204,6 +204,212 @@ __global__ void channel_norm_kernel(const T* __restrict__ k, const T* __restrict
     w_c[idx] = (float)__dmul_rn(__dmul_rn(sqrt(qq), sqrt(kk)), inv_sqrt_d);
 }
 
+// ---------------------------------------------------------------------------
+// Streaming K1 (the production path of rdkv_cuda_weights when d % 16 == 0):
+// the U x R x T probe matrix is never materialised. Two passes of the same
+// fp64 tile GEMM over (128 probe rows x 128 tokens) tiles:
+//   S1 probe_stream<0>: logits -> per (row, token tile) max m and sum of
+//      exp(l - m) over the causal part                      -> stats [U][R][ntt]
+//   S2 probe_rowstat:   per row M = max m, denom = sum_tiles s * exp(m - M)
+//                       (tile order)                        -> rowstat [U][R]
+//   S3 probe_stream<1>: logits again, a = exp(l - M) / denom (cache.cpp:176-180),
+//      column sums over the rows in the reference's heads-outer / rows-inner
+//      order (weights.cpp:36-39), one thread per token      -> rawf [U][T]
+//   W4 token_pool, and channel norms by chunked partial sums (S4/S5).
+// The logits are the same bit-exact fp64 dots as W1 (sequential in c, DFMA of
+// exact f32 products). The denominator's summation order differs from the
+// reference's sequential one (<= 1e-15 relative; the f32 weights match it
+// bit-for-bit except at rounding ties). GEMM tile: thread (tx, ty) holds rows
+// ty + 16 i and tokens tx + 16 j (i, j < 8); per channel the 16 row values of
+// a half-warp are two broadcast addresses and its 16 token values one
+// 128-B wavefront, so shared memory stays under the DFMA rate.
+constexpr int kSRows = 128;
+constexpr int kSToks = 128;
+constexpr int kSK = 16;                     // channels per staged chunk
+constexpr int kSPad = kSRows + 2;           // smem row stride (doubles) of a chunk
+constexpr int kSAStride = kSToks + 1;       // epilogue a-tile stride (doubles)
+constexpr int kSGemmSmem = 2 * 2 * kSK * kSPad * (int)sizeof(double);
+constexpr int kSColSmem = kSRows * kSAStride * (int)sizeof(double);
+constexpr int kSSmem = kSGemmSmem > kSColSmem ? kSGemmSmem : kSColSmem;
+
+template <typename T, int PASS>
+__global__ void __launch_bounds__(256, 1) probe_stream_kernel(
+    const T* __restrict__ k, const T* __restrict__ q, int t_len, int d, int R, int window, int probe_rows,
+    double inv_sqrt_d, int ntt, double2* __restrict__ stats, const double2* __restrict__ rowstat,
+    float* __restrict__ rawf) {
+    extern __shared__ __align__(16) double sm[];
+    const int tile = blockIdx.x, unit = blockIdx.y;
+    const int tok0 = tile * kSToks;
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const T* kb = k + (size_t)unit * t_len * d;
+    const T* qb = q + (size_t)unit * (R / window) * probe_rows * d;
+    // loader mapping: channel lc, rows / tokens lr + 16 m
+    const int lc = tid & 15, lr = tid >> 4;
+    const int nchunk = d / kSK;
+    double colacc = 0.0;  // S3: the column sum of token tok0 + tid (tid < 128), in row order
+    for (int rb = 0; rb < R; rb += kSRows) {
+        double acc[8][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+        float qv_n[8], kv_n[8];
+        auto gload = [&](int c0) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int row = rb + lr + 16 * m, t = tok0 + lr + 16 * m;
+                const int qi = row / window, w = row - qi * window;
+                qv_n[m] = row < R ? load_as_float(qb, ((size_t)qi * probe_rows + probe_rows - window + w) * d + c0 + lc)
+                                  : 0.0f;
+                kv_n[m] = t < t_len ? load_as_float(kb, (size_t)t * d + c0 + lc) : 0.0f;
+            }
+        };
+        gload(0);
+        for (int kc = 0; kc < nchunk; ++kc) {
+            double* Qs = sm + (kc & 1) * 2 * kSK * kSPad;
+            double* Ks = Qs + kSK * kSPad;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                Qs[lc * kSPad + lr + 16 * m] = (double)qv_n[m];
+                Ks[lc * kSPad + lr + 16 * m] = (double)kv_n[m];
+            }
+            __syncthreads();
+            if (kc + 1 < nchunk) gload((kc + 1) * kSK);
+#pragma unroll 4
+            for (int kk = 0; kk < kSK; ++kk) {
+                double a[8], b[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a[i] = Qs[kk * kSPad + ty + 16 * i];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) b[j] = Ks[kk * kSPad + tx + 16 * j];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+            }
+        }
+        __syncthreads();  // all chunk reads done: the smem may be reused below
+        if (PASS == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int row = rb + ty + 16 * i;
+                const int off = t_len - window + (row % window);  // causal offset (pipeline.cpp:129-130)
+                double l[8];
+                double m = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int t = tok0 + tx + 16 * j;
+                    l[j] = __dmul_rn(acc[i][j], inv_sqrt_d);
+                    if (row < R && t < t_len && t <= off) m = fmax(m, l[j]);
+                }
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+                double s = 0.0;
+                if (m != -INFINITY) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int t = tok0 + tx + 16 * j;
+                        if (row < R && t < t_len && t <= off) s = __dadd_rn(s, exp(__dadd_rn(l[j], -m)));
+                    }
+                }
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+                if (tx == 0 && row < R) stats[((size_t)unit * R + row) * ntt + tile] = make_double2(m, s);
+            }
+        } else {
+            double* at = sm;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int row = rb + ty + 16 * i;
+                const int off = t_len - window + (row % window);
+                const double2 ms = row < R ? rowstat[(size_t)unit * R + row] : make_double2(0.0, 1.0);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int t = tok0 + tx + 16 * j;
+                    double a = 0.0;  // entries past the causal offset are exactly zero (cache.cpp:181)
+                    if (row < R && t < t_len && t <= off)
+                        a = exp(__dadd_rn(__dmul_rn(acc[i][j], inv_sqrt_d), -ms.x)) / ms.y;
+                    at[(ty + 16 * i) * kSAStride + tx + 16 * j] = a;
+                }
+            }
+            __syncthreads();
+            if (tid < kSToks) {
+                const int nr = min(kSRows, R - rb);
+                for (int r = 0; r < nr; ++r) colacc = __dadd_rn(colacc, at[r * kSAStride + tid]);
+            }
+            __syncthreads();  // the a-tile aliases the next row block's chunk buffers
+        }
+    }
+    if (PASS == 1 && tid < kSToks && tok0 + tid < t_len) rawf[(size_t)unit * t_len + tok0 + tid] = (float)colacc;
+}
+
+// S2: per (unit, row) global max and softmax denominator from the tile stats,
+// one warp per row (lane-strided tiles, fixed shuffle tree: deterministic).
+__global__ void probe_rowstat_kernel(const double2* __restrict__ stats, int rows, int ntt,
+                                     double2* __restrict__ rowstat) {
+    const int ur = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (ur >= rows) return;
+    const double2* st = stats + (size_t)ur * ntt;
+    double M = -INFINITY;
+    for (int i = lane; i < ntt; i += 32) M = fmax(M, st[i].x);
+    M = warp_max_d(M);
+    double den = 0.0;
+    for (int i = lane; i < ntt; i += 32) {
+        const double2 v = st[i];
+        if (v.y > 0.0) den = __dadd_rn(den, __dmul_rn(v.y, exp(__dadd_rn(v.x, -M))));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) den = __dadd_rn(den, __shfl_xor_sync(0xffffffffu, den, o));
+    if (lane == 0) rowstat[ur] = make_double2(M, den);
+}
+
+// S4: channel norm partials, one CTA per (unit, chunk of kCNChunk tokens):
+// thread j sums k[t][c]^2 for channels c = 2j, 2j + 1 over the chunk's tokens
+// in order (fp64 DFMA of an exact square; one 4-B load per row and thread, so a
+// warp reads 128 contiguous bytes of each row).
+constexpr int kCNChunk = 256;
+template <typename T>
+__global__ void channel_kk_partial_kernel(const T* __restrict__ k, int t_len, int d, int nchunks,
+                                          double* __restrict__ part) {
+    const int chunk = blockIdx.x, unit = blockIdx.y;
+    const int t0 = chunk * kCNChunk, t1 = min(t_len, t0 + kCNChunk);
+    const T* kb = k + (size_t)unit * t_len * d;
+    for (int c = 2 * threadIdx.x; c < d; c += 2 * blockDim.x) {
+        double k0 = 0.0, k1 = 0.0;
+        const bool two = c + 1 < d;
+#pragma unroll 8
+        for (int t = t0; t < t1; ++t) {
+            const double x0 = load_as_float(kb, (size_t)t * d + c);
+            const double x1 = two ? (double)load_as_float(kb, (size_t)t * d + c + 1) : 0.0;
+            k0 = __fma_rn(x0, x0, k0);
+            k1 = __fma_rn(x1, x1, k1);
+        }
+        part[((size_t)unit * nchunks + chunk) * d + c] = k0;
+        if (two) part[((size_t)unit * nchunks + chunk) * d + c + 1] = k1;
+    }
+}
+
+// S5: w_c = f32(sqrt(sum q^2) * sqrt(sum k^2) / sqrt(d)) (weights.cpp:69-91),
+// the K sum combined over the chunk partials in chunk order.
+template <typename T>
+__global__ void channel_norm_combine_kernel(const T* __restrict__ q, const double* __restrict__ part, int units,
+                                            int nchunks, int d, int window, int probe_rows, int group,
+                                            double inv_sqrt_d, float* __restrict__ w_c) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= units * d) return;
+    const int unit = idx / d, c = idx % d;
+    double qq = 0.0;
+    const size_t qbase = (size_t)unit * group * probe_rows * d;
+    for (int qi = 0; qi < group; ++qi)
+        for (int r = 0; r < window; ++r) {
+            const double x = load_as_float(q, qbase + ((size_t)qi * probe_rows + probe_rows - window + r) * d + c);
+            qq = __fma_rn(x, x, qq);
+        }
+    double kk = 0.0;
+    for (int i = 0; i < nchunks; ++i) kk = __dadd_rn(kk, part[((size_t)unit * nchunks + i) * d + c]);
+    w_c[idx] = (float)__dmul_rn(__dmul_rn(sqrt(qq), sqrt(kk)), inv_sqrt_d);
+}
+
 struct WeightsWorkspace {
     double* logits;
     double* tile_max;
@@ -211,6 +417,63 @@ struct WeightsWorkspace {
     float* rawf;
     size_t bytes;
 };
+
+// Workspace of the streaming path: tile stats [U][R][ntt] (m, s), row stats
+// [U][R], raw column sums [U][T] f32, channel partials [U][nchunks][d].
+struct StreamWorkspace {
+    double2* stats;
+    double2* rowstat;
+    float* rawf;
+    double* kpart;
+    size_t bytes;
+};
+
+static bool stream_path(const rdkv_shape* s) { return s->head_dim % kSK == 0; }
+
+static StreamWorkspace carve_stream(const rdkv_shape* s, int window, void* base) {
+    const size_t U = s->units, T = s->seq_len, R = (size_t)s->group * window, d = s->head_dim;
+    const size_t ntt = (T + kSToks - 1) / kSToks, nch = (T + kCNChunk - 1) / kCNChunk;
+    StreamWorkspace w{};
+    char* p = static_cast<char*>(base);
+    size_t off = 0;
+    auto take = [&](size_t n) {
+        char* r = p ? p + off : nullptr;
+        off += (n + 255) / 256 * 256;
+        return r;
+    };
+    w.stats = reinterpret_cast<double2*>(take(U * R * ntt * sizeof(double2)));
+    w.rowstat = reinterpret_cast<double2*>(take(U * R * sizeof(double2)));
+    w.rawf = reinterpret_cast<float*>(take(U * T * sizeof(float)));
+    w.kpart = reinterpret_cast<double*>(take(U * nch * d * sizeof(double)));
+    w.bytes = off;
+    return w;
+}
+
+template <typename T>
+static int run_weights_stream(const T* k, const T* q, const rdkv_shape* s, int window, int pool_kernel, float* w_t,
+                              float* w_c, const StreamWorkspace& ws, cudaStream_t st) {
+    const int U = s->units, t_len = s->seq_len, d = s->head_dim, g = s->group;
+    const int R = g * window;
+    const double inv_sqrt_d = 1.0 / sqrt((double)d);
+    const int ntt = (t_len + kSToks - 1) / kSToks;
+    static std::atomic<int> smem0[kMaxDevices], smem1[kMaxDevices];
+    const int dev = dev_attrs().dev;
+    set_smem_once(probe_stream_kernel<T, 0>, kSSmem, smem0, dev);
+    set_smem_once(probe_stream_kernel<T, 1>, kSSmem, smem1, dev);
+    const dim3 grid(ntt, U);
+    probe_stream_kernel<T, 0><<<grid, 256, kSSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, ntt,
+                                                          ws.stats, nullptr, nullptr);
+    probe_rowstat_kernel<<<(U * R * 32 + 255) / 256, 256, 0, st>>>(ws.stats, U * R, ntt, ws.rowstat);
+    probe_stream_kernel<T, 1><<<grid, 256, kSSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, ntt,
+                                                          nullptr, ws.rowstat, ws.rawf);
+    const size_t nt = (size_t)U * t_len;
+    token_pool_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(ws.rawf, U, t_len, pool_kernel, w_t);
+    const int nch = (t_len + kCNChunk - 1) / kCNChunk;
+    channel_kk_partial_kernel<T><<<dim3(nch, U), 64, 0, st>>>(k, t_len, d, nch, ws.kpart);
+    channel_norm_combine_kernel<T><<<(U * d + 127) / 128, 128, 0, st>>>(q, ws.kpart, U, nch, d, window, s->probe_rows,
+                                                                       g, inv_sqrt_d, w_c);
+    return launch_status();
+}
 
 static WeightsWorkspace carve(const rdkv_shape* s, int window, void* base) {
     const size_t U = s->units, T = s->seq_len, R = (size_t)s->group * window;
@@ -258,7 +521,7 @@ using namespace rdkv_b200;
 extern "C" RDKV_API size_t rdkv_cuda_weights_workspace(const rdkv_shape* s, int32_t window) {
     if (!s || window < 1) return 0;
     const int w = window < s->probe_rows ? window : s->probe_rows;
-    return carve(s, w, nullptr).bytes;
+    return stream_path(s) ? carve_stream(s, w, nullptr).bytes : carve(s, w, nullptr).bytes;
 }
 
 extern "C" RDKV_API int rdkv_cuda_weights(const void* k, const void* probe_q, int32_t dtype,
@@ -271,9 +534,20 @@ extern "C" RDKV_API int rdkv_cuda_weights(const void* k, const void* probe_q, in
     if (s->probe_rows > s->seq_len) return RDKV_EINVAL;  // KVCache::validate (cache.cpp:116-118)
     if (window < 1 || pool_kernel < 1 || pool_kernel % 2 == 0) return RDKV_EINVAL;  // cache.cpp:107-112
     const int w = window < s->probe_rows ? window : s->probe_rows;  // pipeline.cpp:125
+    auto st = static_cast<cudaStream_t>(stream);
+    if (stream_path(s)) {
+        StreamWorkspace ws = carve_stream(s, w, workspace);
+        if (!workspace || workspace_bytes < ws.bytes) return RDKV_EINVAL;
+        if (dtype == RDKV_F32)
+            return run_weights_stream(static_cast<const float*>(k), static_cast<const float*>(probe_q), s, w,
+                                      pool_kernel, w_t, w_c, ws, st);
+        if (dtype == RDKV_F16)
+            return run_weights_stream(static_cast<const __half*>(k), static_cast<const __half*>(probe_q), s, w,
+                                      pool_kernel, w_t, w_c, ws, st);
+        return RDKV_EINVAL;
+    }
     WeightsWorkspace ws = carve(s, w, workspace);
     if (!workspace || workspace_bytes < ws.bytes) return RDKV_EINVAL;
-    auto st = static_cast<cudaStream_t>(stream);
     if (dtype == RDKV_F32)
         return run_weights(static_cast<const float*>(k), static_cast<const float*>(probe_q), s, w,
                            pool_kernel, w_t, w_c, ws, st);

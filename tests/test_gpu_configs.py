@@ -138,3 +138,62 @@ def test_configs4_llama70b_g8_all_layers(cuda, orc, ref):
             for j in range(g):
                 worst = max(worst, rel(out[u, j], tz.decode(q[u, j])))
     assert worst < DECODE_TOL, worst
+
+
+@pytest.mark.parametrize("T,strict,force", [(8192, False, False), (40000, True, False), (131072, False, True)])
+def test_long_context_allocation_given_weights(cuda, orc, T, strict, force):
+    """Long contexts take the cluster-parallel V sweep (allocate.cu allocate_v_cluster,
+    T >= 8192) and allocate_finish: v_bits / k_bits / lambdas / convergence /
+    objectives bit-identical to the C restatement of mckp_bisect (allocator.cpp:135-216)
+    on the same f32 weights, for flat, peaky and heavy-hitter weight shapes."""
+    rng = np.random.default_rng(T)
+    d, Hkv, n = 128, 8, 128
+    flat = rng.random(T).astype(np.float32) * 1e-4
+    peaky = (rng.standard_exponential(T) ** 4).astype(np.float32) * 1e-6
+    heavy = flat.copy()
+    heavy[::64] *= 300.0
+    w_t = np.stack([flat, peaky, heavy])
+    w_c = (rng.random((3, d)) * np.linspace(0.5, 4.0, d)).astype(np.float32)
+    cfg = oracle.default_config(n_tokens=n, window=32, strict_budget=strict, force_window_retain=force)
+    al = P.allocate(torch.from_numpy(w_t).to(cuda), torch.from_numpy(w_c).to(cuda), P.default_config(
+        n_tokens=n, window=32, strict_budget=strict, force_window_retain=force), group=4, probe_rows=32, kv_heads=Hkv)
+    al.check()
+    st, vb, kb = al.stats_host(), al.v_bits.cpu().numpy(), al.k_bits.cpu().numpy()
+    bud = orc.head_budget(n, 0.5, d, Hkv)
+    widths = [cfg.widths[i] for i in range(cfg.n_widths)]
+    eps_v = [cfg.eps_v[i] for i in range(cfg.n_widths)]
+    eps_k = [cfg.eps_k[i] for i in range(cfg.n_widths)]
+    for u in range(3):
+        want = orc.mckp_bisect(w_t[u], widths, eps_v, min(16.0, bud["v_bits"] / (d * T)), strict_budget=strict)
+        wb = want["bits"].copy()
+        if force:
+            wb[T - 32:] = 16
+        assert np.array_equal(vb[u], wb), u
+        assert st[u]["lambda_v"] == want["lambda"] and bool(st[u]["v_converged"]) == want["converged"], u
+        kept = int(np.count_nonzero(wb))
+        assert st[u]["n_kept"] == kept
+        if not force:
+            assert st[u]["objective_v"] == want["objective"], u
+        wk = orc.mckp_bisect(w_c[u], widths, eps_k, min(16.0, bud["k_bits"] / (kept * d)), strict_budget=strict)
+        assert np.array_equal(kb[u], wk["bits"]) and st[u]["lambda_k"] == wk["lambda"], u
+        assert st[u]["objective_k"] == wk["objective"], u
+
+
+def test_streaming_weights_match_reference_long(cuda, ref):
+    """Stage-1 weights at T=16384 through the streaming two-pass K1 (no probe matrix in
+    HBM) vs the reference's attention_probe + token_weights + channel_weights:
+    <= 1e-6 relative, and nearly all f32 values bit-identical."""
+    spec = WorkloadSpec(batch=1, layers=1, ctx=16384, n_tokens=128, seed=3, hh_stride=64, hh_boost=1.0)
+    (kd, vd, qd), (k, v, q) = _slice(spec)
+    H, g, d, Sw = spec.kv_heads, spec.group, spec.head_dim, spec.probe_rows
+    w_t, w_c = P.compute_weights(kd[:2], qd[:2], window=Sw, pool_kernel=5, kv_heads=H)
+    w_t, w_c = w_t.cpu().numpy(), w_c.cpu().numpy()
+    rm = oracle.RefModel(ref, k[None], v[None], q.reshape(1, H * g, Sw, d), oracle.default_config(n_tokens=128, window=Sw))
+    exact = total = 0
+    for h in range(2):
+        want = rm.head(0, h)
+        for got, exp in ((w_t[h], want["v_weights"]), (w_c[h], want["k_weights"])):
+            assert np.max(np.abs(got - exp) / np.maximum(np.abs(exp), 1e-30)) <= 1e-6
+            exact += int(np.sum(got == exp))
+            total += got.size
+    assert exact / total > 0.99, exact / total
