@@ -134,6 +134,9 @@ typedef struct {
     int32_t uniform2;         /* every tile: all kept V rows and K channels at 2 bits (2: and all d K channels kept) */
     int32_t n_uniform;        /* rdkv_cuda_decode_prepare_split: tiles of the uniform class (listed first in unit_ids) */
     int32_t uniform2_split;   /* the uniform2 value of that subset */
+    int32_t mix24;            /* every tile: kept V rows and K channels at 2 or 4 bits only (no Zone B / k16 / 8-bit) */
+    int32_t min_chunks24;     /* smallest per-tile chunk count of the mixed 2/4-bit chunked kernel (split-K bound) */
+    int32_t max_krow_bytes24; /* largest K row of those tiles */
 } rdkv_decode_plan;
 
 /* rdkv_decode_args.flags: `out` lives in mapped host memory — the tensor-core

@@ -87,7 +87,8 @@ HEAD_STATS_BYTES = C.sizeof(HeadStats)
 class DecodePlan(C.Structure):
     _fields_ = [("max_decode_bytes", C.c_int32), ("max_slots", C.c_int32),
                 ("max_zone_b_rows", C.c_int32), ("max_kq_slots", C.c_int32), ("uniform2", C.c_int32),
-                ("n_uniform", C.c_int32), ("uniform2_split", C.c_int32)]
+                ("n_uniform", C.c_int32), ("uniform2_split", C.c_int32), ("mix24", C.c_int32),
+                ("min_chunks24", C.c_int32), ("max_krow_bytes24", C.c_int32)]
 
 
 class DecodeArgs(C.Structure):

@@ -2721,6 +2721,8 @@ bool mma_supported(const rdkv_decode_args* a) {
     const rdkv_decode_plan& p = a->plan;
     // uniform 2-bit tiles of any length: u2x (<= 160 slots) or its chunked variant
     if (p.uniform2 && p.max_decode_bytes > 0 && u2x_group_ok(a)) return true;
+    // mixed 2/4-bit tiles of any length: the chunked split-K kernel (decode_u24)
+    if (p.mix24 && p.max_decode_bytes > 0 && !a->zc_len && !(p.uniform2 && p.max_slots <= kU2MaxSlots)) return true;
     if (p.max_decode_bytes <= 0 || p.max_slots > kMaxSlots || p.max_zone_b_rows > kMaxSlots) return false;
     return general_min_smem(a) <= (size_t)dev_attrs().smem_optin;  // else the CUDA-core kernel
 }
@@ -2828,12 +2830,703 @@ int launch_merge(const float* part, int nparts, int rows, int d, void* out, int 
     return launch_status();
 }
 
+// ============================================================================
+// Mixed 2/4/8-bit tiles of any length (the configs[3] budget sweep: heavy
+// hitters and outlier K channels leave ~80-110 K channels at 2 bits and the
+// rest at 4 bits, V rows at 2 and 4 bits and a few at 8, 64 .. 3,100 token
+// slots per tile), decoded with split-K across warp pairs
+// (packed_decode_step, trizone.cpp:251-305):
+//   * a tile's slots are cut into V-class-homogeneous chunks of 128 (2-bit),
+//     64 (4-bit) or 32 (8-bit) slots, starting at multiples of 32 slots inside
+//     the class so the V swizzle phase of every 4-token group is preserved;
+//   * a tile's chunks are dealt to S parts (part r takes chunks r, r + S, ...);
+//     each (tile, part) item runs on one warp pair, which stages its chunks by
+//     TMA (K rows as the four slot-transposed runs, V rows, V parameters; the
+//     tile header, channel table and q rows with its first chunk), folds them
+//     into an online softmax and writes an unnormalised partial (o, max in
+//     log2 units, weight sum) that merge_partials_kernel combines (S == 1:
+//     the pair writes the output itself);
+//   * QK: one k-step per 32 K slots of a class: 2-bit channels with the
+//     in-place 2-bit masks (q~ prescaled 4^(3 - t), as u2x), 4-bit with nibble
+//     masks (prescaled 4 * 16^(1 - t'), as MIX), 8-bit raw bytes (prescaled
+//     64); three balanced s8 digits of q~, int8 MMAs;
+//   * PV: 2-bit chunks as u2x; 4-bit chunks with nibble masks whose rows
+//     gid / gid + 8 are the lo / hi nibble channels of one byte column, 8-bit
+//     chunks with the two adjacent byte columns — chosen so a lane's output
+//     channels (ch0 + 4m, + 1) are the same in every class.
+// GQA groups of 5..8 heads run as two 4-head passes over each staged chunk.
+constexpr int kU24MaxK = 6;                              // k-steps of 32 K slots (c2 + c4 + c8 <= 128 -> <= 6)
+constexpr int kU24QDig = kXQDig;                         // q~ digit blocks: kU24MaxK x 512 B
+constexpr int kU24PDig = kU24QDig + kU24MaxK * 512;      // p~ digit blocks: 4 x 256 B
+constexpr int kU24Scratch = kU24PDig + 4 * 256;
+constexpr int kU24MaxParts = 16;                         // split-K parts per tile
+__host__ __device__ constexpr int u24_chunk_slots(int cls) { return cls == 0 ? 128 : cls == 1 ? 64 : 32; }
+__host__ __device__ constexpr int u24_vrow_bytes(int cls) { return cls == 0 ? 32 : cls == 1 ? 64 : 128; }
+
+// Per-tile chunk layout: class c has C[c] chunks of u24_chunk_slots(c) slots
+// over its pad4(r[c]) slots (the last one ragged).
+struct U24Tile {
+    int r[3], C[3];
+    int n2, n4, n8;  // K k-steps per class
+    float vmax2;     // header bound on the 2-bit V scales
+};
+__host__ __device__ inline void u24_tile(const int* r, U24Tile& t) {
+    for (int c = 0; c < 3; ++c) {
+        t.r[c] = r[c];
+        t.C[c] = (pad4(r[c]) + u24_chunk_slots(c) - 1) / u24_chunk_slots(c);
+    }
+}
+__host__ __device__ inline int u24_nchunks(const U24Tile& t) { return t.C[0] + t.C[1] + t.C[2]; }
+struct U24Geom {
+    int cls, s0, ns, n;  // V class, first slot (of the tile), slots (multiple of 4), valid slots
+    int li0;             // first row inside the class
+};
+__host__ __device__ inline U24Geom u24_chunk(const U24Tile& t, int k) {
+    U24Geom g;  // (explicit selects: no dynamically indexed arrays, they would live in local memory)
+    const int P0 = pad4(t.r[0]), P1 = pad4(t.r[1]);
+    int rc;
+    if (k < t.C[0]) {
+        g.cls = 0;
+        g.li0 = k * u24_chunk_slots(0);
+        g.s0 = g.li0;
+        rc = t.r[0];
+    } else if (k < t.C[0] + t.C[1]) {
+        g.cls = 1;
+        g.li0 = (k - t.C[0]) * u24_chunk_slots(1);
+        g.s0 = P0 + g.li0;
+        rc = t.r[1];
+    } else {
+        g.cls = 2;
+        g.li0 = (k - t.C[0] - t.C[1]) * u24_chunk_slots(2);
+        g.s0 = P0 + P1 + g.li0;
+        rc = t.r[2];
+    }
+    g.ns = min(g.cls == 0 ? 128 : g.cls == 1 ? 64 : 32, pad4(rc) - g.li0);
+    g.n = min(g.ns, rc - g.li0);
+    return g;
+}
+
+struct U24Meta {  // a tile's staging geometry, read from its header in global memory
+    const uint8_t* base;
+    int nslot, hk, krb, offvp, offv[3], r[3];
+};
+struct U24Issuer {
+    U24Meta cur, nxt;
+    U24Tile t;
+    int item, c, n;
+};
+
+// One chunk for one 4-head group. `first`: this pair's first chunk of the tile
+// (header, channel table and q staged; builds the q~ digits and resets `run`).
+template <typename IO, typename AfterSync1>
+__device__ __forceinline__ void decode_chunk_u24(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
+                                                 uint8_t* __restrict__ scr, int bar, const U2xLane& L,
+                                                 AfterSync1&& after_sync1, const U24Geom& ck, bool first, int krb,
+                                                 const uint8_t* __restrict__ kb, const uint8_t* __restrict__ vb,
+                                                 const float2* __restrict__ vparam, U2xRun& run, U24Tile& tl) {
+    constexpr int NBW = 2;  // <= 128 slots per chunk: <= 4 blocks of 32, two per warp
+    const int gid = L.gid, tig = L.tig, half = L.half;
+    const bool hv = tig < g;
+    PairX& xg = *reinterpret_cast<PairX*>(scr);
+    float* vmx = reinterpret_cast<float*>(scr) + sizeof(PairX) / 4;  // [2] chunk V-scale maxima (4/8-bit chunks)
+    uint8_t* qdig = scr + kU24QDig;
+    uint8_t* pdig = scr + kU24PDig;
+    const int nslot = ck.ns, n = ck.n;
+    const int nb = (n + 31) >> 5;
+    const int mynb = (nb + 1 - half) >> 1;
+    const int Q = nslot >> 2;
+    constexpr float kInvSqrtD = 0.08838834764831845f;
+    constexpr float kLog2e = 1.4426950408889634f;
+    constexpr int QROW = kD * (int)sizeof(IO);
+    if (first) {
+        const TileHeader& h = *reinterpret_cast<const TileHeader*>(t);
+        const float* chanf = reinterpret_cast<const float*>(t + kHeaderBytes);
+        const uint16_t* perm = reinterpret_cast<const uint16_t*>(t + kHeaderBytes + 8 * h.kslots);
+        const int n2 = h.kslot_base[1] >> 5, n4 = (h.kslot_base[2] - h.kslot_base[1]) >> 5,
+                  n8 = (h.kslot_base[3] - h.kslot_base[2]) >> 5;
+        const int c0 = h.c[0];
+        tl.n2 = n2;
+        tl.n4 = n4;
+        tl.n8 = n8;
+        tl.vmax2 = bf16_bits_to_float(h.scale_bounds >> 16);
+        // q range per head (lanes 8h .. 8h + 7 scan head h), then this lane's head tig
+        const int hq = L.lane >> 3;
+        float qm = absmax16<IO>(reinterpret_cast<const IO*>(qs + (hq < g ? hq : 0) * QROW) + 16 * (L.lane & 7));
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+        qm = __shfl_sync(0xffffffffu, qm, 8 * tig);
+        const IO* qh = reinterpret_cast<const IO*>(qs + (hv ? tig : 0) * QROW);
+        float s1 = 0.0f;  // scale bound of the 4- and 8-bit channels (2-bit: the header's)
+        for (int j = h.kslot_base[1] + L.lane; j < h.kslot_base[3]; j += 32) s1 = fmaxf(s1, fabsf(chanf[2 * j]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s1 = fmaxf(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+        const float bnd = fmaxf(bf16_bits_to_float(h.scale_bounds & 0xFFFFu), s1) * qm;
+        const float sg = (hv && bnd > 0.0f) ? kQFix * rcp_approx(bnd) : 0.0f;
+        float bpart = 0.0f;
+        {  // 2-bit k-steps kk = 2 half + i (< n2): the u2x generator over channel slots
+            const int ps = L.lane & 4;
+            const float sgA = sg * __int_as_float((127 + 6 - ps) << 23);
+            const float sgB = sgA * 0.25f;
+            const int kk = 2 * half + (L.lane >> 4);
+            const bool act = kk < n2;
+            uint32_t xa[4], xb[4];
+            float2 bp = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c = L.qch + 4 * ((e + tig) & 3);
+                const int j0 = min(c, h.kslots - 2);
+                const float4 cs = *reinterpret_cast<const float4*>(chanf + 2 * j0);
+                float2 qv;
+                qv.x = (act && c < c0) ? ld_io(qh, perm[j0]) : 0.0f;
+                qv.y = (act && c + 1 < c0) ? ld_io(qh, perm[j0 + 1]) : 0.0f;
+                bp = ffma2(qv, make_float2(cs.y, cs.w), bp);
+                const float ya = fmaf(cs.x * qv.x, sgA, kMagicS), yb = fmaf(cs.z * qv.y, sgB, kMagicS);
+                xa[e] = (__float_as_uint(ya) + (0x00808080u - 0x4B400000u)) ^ 0x00808080u;
+                xb[e] = (__float_as_uint(yb) + (0x00808080u - 0x4B400000u)) ^ 0x00808080u;
+            }
+            bpart = bp.x + bp.y;
+            const uint32_t a01 = __byte_perm(xa[0], xa[1], 0x5140), b01 = __byte_perm(xa[0], xa[1], 0x7362);
+            const uint32_t a23 = __byte_perm(xa[2], xa[3], 0x5140), b23 = __byte_perm(xa[2], xa[3], 0x7362);
+            const uint32_t c01 = __byte_perm(xb[0], xb[1], 0x5140), d01 = __byte_perm(xb[0], xb[1], 0x7362);
+            const uint32_t c23 = __byte_perm(xb[2], xb[3], 0x5140), d23 = __byte_perm(xb[2], xb[3], 0x7362);
+            if (act) {
+                uint8_t* w = qdig + L.qdig_w;
+                *reinterpret_cast<uint2*>(w) = make_uint2(__byte_perm(b01, b23, L.sel_lo), __byte_perm(d01, d23, L.sel_lo));
+                *reinterpret_cast<uint2*>(w + 224) =
+                    make_uint2(__byte_perm(a01, a23, L.sel_hi), __byte_perm(c01, c23, L.sel_hi));
+                *reinterpret_cast<uint2*>(w + 256) =
+                    make_uint2(__byte_perm(a01, a23, L.sel_lo), __byte_perm(c01, c23, L.sel_lo));
+            }
+        }
+        // 4- and 8-bit k-steps (warp `half` takes every other one): K positions
+        // 4j .. 4j + 3 of head tig (j = lane >> 2), each lane's slot per the class's A mask
+        const int nw = n4 + n8;
+        for (int jw = half; jw < nw; jw += 2) {
+            const bool b4 = jw < n4;
+            const int j = L.lane >> 2;
+            const int cls = b4 ? 1 : 2;
+            const int sbase = b4 ? h.kslot_base[1] + 32 * jw : h.kslot_base[2] + 32 * (jw - n4);
+            const int cnt = b4 ? h.c[1] - 32 * jw : h.c[2] - 32 * (jw - n4);  // valid slots of this k-step
+            uint32_t x1[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int pk = 4 * j + e, rr = pk & 15, tt = rr >> 2;
+                const int sl = b4 ? 16 * (pk >> 4) + 8 * (tt >> 1) + 2 * (rr & 3) + (tt & 1) : pk;
+                const float2 cs = reinterpret_cast<const float2*>(chanf)[sbase + sl];
+                const float qv = (sl < cnt && hv) ? ld_io(qh, perm[sbase + sl]) : 0.0f;
+                bpart = fmaf(qv, cs.y, bpart);
+                const float pre = (b4 && (tt & 1)) ? 4.0f : 64.0f;
+                const float y = fmaf(cs.x * qv, sg * pre, kMagicS);
+                x1[e] = (__float_as_uint(y) + (0x00808080u - 0x4B400000u)) ^ 0x00808080u;
+            }
+            (void)cls;
+            const uint32_t a01 = __byte_perm(x1[0], x1[1], 0x5140), b01 = __byte_perm(x1[0], x1[1], 0x7362);
+            const uint32_t a23 = __byte_perm(x1[2], x1[3], 0x5140), b23 = __byte_perm(x1[2], x1[3], 0x7362);
+            uint8_t* w1p = qdig + (n2 + jw) * 512 + 4 * (j & 3);
+            const int hs = ((j >> 2) ^ (tig >> 1)) * 16;
+            *reinterpret_cast<uint32_t*>(w1p + (2 * tig + 1) * 32 + hs) = __byte_perm(b01, b23, 0x5410);
+            *reinterpret_cast<uint32_t*>(w1p + (8 + 2 * tig) * 32 + hs) = __byte_perm(a01, a23, 0x7632);
+            *reinterpret_cast<uint32_t*>(w1p + (9 + 2 * tig) * 32 + hs) = __byte_perm(a01, a23, 0x5410);
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) bpart += __shfl_xor_sync(0xffffffffu, bpart, o);
+        if (gid == 0) xg.bias[half][tig] = bpart;
+        pair_sync(bar);
+        after_sync1();
+        run.bias2 = hv ? (xg.bias[0][tig] + xg.bias[1][tig]) * (kInvSqrtD * kLog2e) : -INFINITY;
+        run.qscale2 = bnd * (kInvSqrtD * kLog2e / (64.0f * kQFix));
+        run.m = -INFINITY;
+        run.l = 0.0f;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) run.o[m] = make_float2(0.0f, 0.0f);
+    } else {
+        pair_sync(bar);  // both warps are past the previous chunk: its buffer may be refilled
+        after_sync1();
+    }
+    const float bias2 = run.bias2, qscale2 = run.qscale2;
+    const int n2 = tl.n2, n4 = tl.n4, n8 = tl.n8;
+
+    // ---- QK over this warp's blocks half, half + 2 (A rows gid / gid + 8 of
+    // m-tile u = slots 32 pb + 4 gid + 2u / + 1, slot-transposed K rows)
+    const int qstride = Q * krb;
+    float2 lg[NBW][2];
+    float mx = -INFINITY, vm = 0.0f;
+#pragma unroll
+    for (int i = 0; i < NBW; ++i) {
+        if (i < mynb) {
+            const int pb = half + 2 * i;
+            const uint8_t* r0 = kb + (size_t)(8 * pb + gid) * krb;  // m-tile u = 0, row gid
+            int acc[2][2][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) acc[u][nt][0] = acc[u][nt][1] = acc[u][nt][2] = acc[u][nt][3] = 0;
+            const uint8_t* qd = qdig + L.bofs;
+            // 2-bit channels: 8 B of each row per k-step
+#pragma unroll 1
+            for (int kk = 0; kk < n2; ++kk, qd += 512) {
+                uint32_t bq[4];
+                ldsm_x4(bq, qd);
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const uint2 x = lds64(r0 + 2 * u * qstride + 8 * kk), y = lds64(r0 + (2 * u + 1) * qstride + 8 * kk);
+                    const uint32_t a[4] = {x.x & L.kmask, y.x & L.kmask, x.y & L.kmask, y.y & L.kmask};
+                    mma_u8s8(acc[u][0], a, bq[0], bq[1]);
+                    mma_u8s8(acc[u][1], a, bq[2], bq[3]);
+                }
+            }
+            // 4-bit channels: 16 B per k-step, nibble masks
+            {
+                const int o4 = 8 * n2 + 4 * (tig >> 1);
+                const uint32_t m4 = 0x0F0F0F0Fu << (4 * (tig & 1));
+#pragma unroll 1
+                for (int j4 = 0; j4 < n4; ++j4, qd += 512) {
+                    uint32_t bq[4];
+                    ldsm_x4(bq, qd);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const uint8_t* ra = r0 + 2 * u * qstride + o4 + 16 * j4;
+                        const uint8_t* rb = ra + qstride;
+                        const uint32_t a[4] = {lds32(ra) & m4, lds32(rb) & m4, lds32(ra + 8) & m4, lds32(rb + 8) & m4};
+                        mma_u8s8(acc[u][0], a, bq[0], bq[1]);
+                        mma_u8s8(acc[u][1], a, bq[2], bq[3]);
+                    }
+                }
+            }
+            // 8-bit channels: 32 B per k-step, raw bytes
+            {
+                const int o8 = 8 * n2 + 16 * n4 + 4 * tig;
+#pragma unroll 1
+                for (int j8 = 0; j8 < n8; ++j8, qd += 512) {
+                    uint32_t bq[4];
+                    ldsm_x4(bq, qd);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const uint8_t* ra = r0 + 2 * u * qstride + o8 + 32 * j8;
+                        const uint8_t* rb = ra + qstride;
+                        const uint32_t a[4] = {lds32(ra), lds32(rb), lds32(ra + 16), lds32(rb + 16)};
+                        mma_u8s8(acc[u][0], a, bq[0], bq[1]);
+                        mma_u8s8(acc[u][1], a, bq[2], bq[3]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float2 hi = make_float2((float)acc[u][0][1], (float)acc[u][0][3]);
+                const float2 lo = make_float2((float)(acc[u][1][0] * 256 + acc[u][1][1]),
+                                              (float)(acc[u][1][2] * 256 + acc[u][1][3]));
+                const float2 v = ffma2(hi, make_float2(65536.0f, 65536.0f), lo);
+                lg[i][u] = ffma2(v, make_float2(qscale2, qscale2), make_float2(bias2, bias2));
+            }
+            const int sbase = 32 * pb + 4 * gid;
+            if (32 * pb + 32 > n) {  // ragged last block: slots >= n get no weight
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (sbase + 2 * u >= n) lg[i][u].x = -INFINITY;
+                    if (sbase + 2 * u + 1 >= n) lg[i][u].y = -INFINITY;
+                }
+            }
+            mx = fmaxf(mx, fmaxf(fmaxf(lg[i][0].x, lg[i][0].y), fmaxf(lg[i][1].x, lg[i][1].y)));
+            if (ck.cls != 0) {  // V scales of this lane's four slots (the chunk's p~ range)
+                const float4* vp4 = reinterpret_cast<const float4*>(vparam + min(sbase, nslot - 4));
+                const float4 va = vp4[0], vc = vp4[1];
+                vm = fmaxf(vm, fmaxf(fmaxf(va.x, va.z), fmaxf(vc.x, vc.z)));
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (ck.cls != 0) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) vm = fmaxf(vm, __shfl_xor_sync(0xffffffffu, vm, o));
+        if (L.lane == 0) vmx[half] = vm;
+    }
+    if (gid == 0) xg.mx[half][tig] = mx;
+    pair_sync(bar);
+    mx = fmaxf(xg.mx[0][tig], xg.mx[1][tig]);
+    if (mx == -INFINITY) mx = 0.0f;  // head without tokens (tig >= g)
+    const float vmax = ck.cls != 0 ? fmaxf(vmx[0], vmx[1]) : tl.vmax2;
+    const float psig = vmax > 0.0f ? kPScale * rcp_approx(vmax) : 0.0f;
+    const float vinv = vmax * (1.0f / kPScale);
+
+    // ---- softmax + p~ digits (hi, lo bytes): four consecutive slots per lane and block
+    float2 ls2 = make_float2(0.0f, 0.0f);
+    float bv = 0.0f;
+    const float2 nmx = make_float2(-mx, -mx);
+#pragma unroll
+    for (int i = 0; i < NBW; ++i) {
+        if (i < mynb) {
+            const int pb = half + 2 * i;
+            const float4* vp4 = reinterpret_cast<const float4*>(vparam + min(32 * pb + 4 * gid, nslot - 4));
+            const float4 va = vp4[0], vc = vp4[1];
+            const float2 d01 = fadd2(lg[i][0], nmx), d23 = fadd2(lg[i][1], nmx);
+            const float2 p01 = make_float2(ex2_approx(d01.x), ex2_approx(d01.y));
+            const float2 p23 = make_float2(ex2_approx(d23.x), ex2_approx(d23.y));
+            ls2 = fadd2(ls2, fadd2(p01, p23));
+            bv = fmaf(p01.x, va.y, bv);
+            bv = fmaf(p01.y, va.w, bv);
+            bv = fmaf(p23.x, vc.y, bv);
+            bv = fmaf(p23.y, vc.w, bv);
+            const float2 vs01 = fmul2(make_float2(va.x, va.z), make_float2(psig, psig));
+            const float2 vs23 = fmul2(make_float2(vc.x, vc.z), make_float2(psig, psig));
+            const float2 y01 = ffma2(p01, vs01, make_float2(kMagicU, kMagicU));
+            const float2 y23 = ffma2(p23, vs23, make_float2(kMagicU, kMagicU));
+            const uint32_t t01 = __byte_perm(__float_as_uint(y01.x), __float_as_uint(y01.y), 0x5140);
+            const uint32_t t23 = __byte_perm(__float_as_uint(y23.x), __float_as_uint(y23.y), 0x5140);
+            uint8_t* pw = pdig + pb * 256 + L.pdig_w;
+            *reinterpret_cast<uint32_t*>(pw) = __byte_perm(t01, t23, 0x7632);
+            *reinterpret_cast<uint32_t*>(pw + 32) = __byte_perm(t01, t23, 0x5410);
+        }
+    }
+    float lsum = ls2.x + ls2.y;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        bv += __shfl_xor_sync(0xffffffffu, bv, o);
+    }
+    if (gid == 0) {
+        xg.lsum[half][tig] = lsum;
+        xg.bv[half][tig] = bv;
+    }
+    pair_sync(bar);
+    const float lt = xg.lsum[0][tig] + xg.lsum[1][tig];
+    const float bt = xg.bv[0][tig] + xg.bv[1][tig];
+
+    // ---- PV: this warp's 64 output channels (4 m-tiles), one n-tile of p~ digits
+    int acc[4][4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = 0;
+    float sc0, sc1;  // output scale of rows gid / gid + 8 (the in-place mask factors)
+    if (ck.cls == 0) {
+        const uint8_t* g0b = vb + L.vcol;
+#pragma unroll 1
+        for (int kk = 0; kk < nb; ++kk) {
+            uint32_t b[2];
+            ldsm_x2(b, pdig + kk * 256 + L.bofs2);
+            const uint4 x0 = lds128(g0b + kk * 1024), x1 = lds128(g0b + kk * 1024 + 512);
+            const uint32_t u0[4] = {x0.x, x0.y, x0.z, x0.w}, u1[4] = {x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const uint32_t a[4] = {u0[m] & L.vm0, u0[m] & L.vm1, u1[m] & L.vm0, u1[m] & L.vm1};
+                mma_u8u8(acc[m], a, b[0], b[1]);
+            }
+        }
+        sc0 = vinv * L.s0f;
+        sc1 = sc0 * 0.25f;
+    } else if (ck.cls == 1) {
+        // 4-bit rows (64 B; 4-token groups of 256 B, word columns swizzled by 8 (G & 3) = 8 tig):
+        // byte column 32 half + 8 (gid & 3) + 2m + jj holds channels ch0 + 4m (lo nibble,
+        // row gid) and ch0 + 4m + 1 (hi nibble, row gid + 8)
+        const int colb = 32 * half + 8 * (gid & 3) + (gid >> 2);
+        const uint8_t* g0b = vb + tig * 256;
+#pragma unroll 1
+        for (int kk = 0; kk < nb; ++kk) {
+            uint32_t b[2];
+            ldsm_x2(b, pdig + kk * 256 + L.bofs2);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int wo = ((colb + 2 * m) ^ (8 * tig)) * 4;
+                const uint32_t w0 = lds32(g0b + kk * 2048 + wo), w1 = lds32(g0b + kk * 2048 + 1024 + wo);
+                const uint32_t a[4] = {w0 & 0x0F0F0F0Fu, w0 & 0xF0F0F0F0u, w1 & 0x0F0F0F0Fu, w1 & 0xF0F0F0F0u};
+                mma_u8u8(acc[m], a, b[0], b[1]);
+            }
+        }
+        sc0 = vinv;
+        sc1 = vinv * 0.0625f;
+    } else {
+        // 8-bit rows (128 B; groups of 512 B): byte columns ch0 + 4m (row gid) and + 1
+        // (row gid + 8), one 8-B load per group
+        const uint8_t* g0b = vb + tig * 512;
+#pragma unroll 1
+        for (int kk = 0; kk < nb; ++kk) {
+            uint32_t b[2];
+            ldsm_x2(b, pdig + kk * 256 + L.bofs2);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int wo = ((L.ch0 + 4 * m) ^ (8 * tig)) * 4;
+                const uint2 w0 = lds64(g0b + kk * 4096 + wo), w1 = lds64(g0b + kk * 4096 + 2048 + wo);
+                const uint32_t a[4] = {w0.x, w0.y, w1.x, w1.y};
+                mma_u8u8(acc[m], a, b[0], b[1]);
+            }
+        }
+        sc0 = vinv;
+        sc1 = vinv;
+    }
+    // ---- fold this chunk (max mx, sum lt, unnormalised outputs v * s + bt) into the running state
+    if (hv && lt > 0.0f) {
+        const float mnew = fmaxf(run.m, mx);
+        const float a = ex2_approx(run.m - mnew), bw = ex2_approx(mx - mnew);
+        const float2 sc = make_float2(sc0 * bw, sc1 * bw), bb = make_float2(bt * bw, bt * bw);
+        const float2 aa = make_float2(a, a);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {  // (the digit combine in f32: 8-bit sums exceed int32 at 256x)
+            const float2 v = ffma2(make_float2((float)acc[m][0], (float)acc[m][2]), make_float2(256.0f, 256.0f),
+                                   make_float2((float)acc[m][1], (float)acc[m][3]));
+            run.o[m] = ffma2(run.o[m], aa, ffma2(v, sc, bb));
+        }
+        run.l = fmaf(run.l, a, lt * bw);
+        run.m = mnew;
+    }
+}
+
+template <typename IO, bool G8>
+__global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u24_kernel(const MmaParams p) {
+    extern __shared__ __align__(128) uint8_t dsm[];
+    const int nbuf = p.R;
+    uint64_t* full = reinterpret_cast<uint64_t*>(dsm);
+    uint8_t* bufs = dsm + p.W * kXMaxBuf * sizeof(uint64_t);
+    uint8_t* scratch0 = bufs + (size_t)p.W * nbuf * p.slot_bytes;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pr = warp >> 1, half = warp & 1;
+    constexpr int QROW = kD * (int)sizeof(IO);
+    const int qbytes = p.g * QROW;
+    uint64_t* fb = full + pr * kXMaxBuf;
+    uint8_t* pbuf = bufs + (size_t)pr * nbuf * p.slot_bytes;
+    uint8_t* scr = scratch0 + (size_t)pr * p.scratch_bytes;
+    const int S = p.split_world;  // parts per tile
+    const int nitems = p.units * S;
+    const int item0 = blockIdx.x + pr * gridDim.x, istride = p.W * gridDim.x;
+    const int qoff = p.slot_bytes - qbytes;
+    const bool issuer = half == 0 && lane == 0;
+
+    // ---- issuer state (one lane, kept in the pair's shared scratch so it costs
+    // no registers in the other 63 threads): the next (item, chunk) to stage
+    U24Issuer& is = *reinterpret_cast<U24Issuer*>(scr + (p.g > 4 ? 2 : 1) * kU24Scratch);
+    auto load_meta = [&](int item, U24Meta& m) {
+        m.base = nullptr;
+        if (item < nitems) {
+            const int tile = item / S;
+            m.base = p.arena + p.offsets[tile];
+            const TileHeader* th = reinterpret_cast<const TileHeader*>(m.base);
+            m.nslot = th->nslot;
+            m.hk = th->off_k;
+            m.krb = th->krow_bytes;
+            m.offvp = th->off_vp;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                m.offv[c] = th->off_vseg[c];
+                m.r[c] = th->r[c];
+            }
+        }
+    };
+    auto set_cur = [&]() {
+        u24_tile(is.cur.r, is.t);
+        is.n = u24_nchunks(is.t);
+    };
+    auto advance = [&]() {
+        is.c += S;
+        if (is.c >= is.n) {
+            is.item += istride;
+            is.c = is.item % S;
+            is.cur = is.nxt;
+            set_cur();
+            load_meta(is.item + istride, is.nxt);
+        }
+    };
+    auto stage_item = [&](int b) {
+        const U24Meta& cur = is.cur;
+        if (is.item >= nitems || !cur.base) return false;
+        const U24Geom gg = u24_chunk(is.t, is.c);
+        const bool first = is.c == is.item % S;
+        uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
+        const int rows = gg.ns >> 2, Q = cur.nslot >> 2;
+        const int rb = u24_vrow_bytes(gg.cls);
+        const uint32_t kbytes = (uint32_t)(rows * cur.krb), vbytes = (uint32_t)(gg.ns * rb),
+                       pbytes = (uint32_t)(gg.ns * 8);
+        // (the very first chunk's q rows are issued later, after the grid dependency)
+        const uint32_t tx = 4 * kbytes + vbytes + pbytes + (first ? (uint32_t)(cur.hk + qbytes) : 0u);
+        fence_proxy_async();
+        mbar_expect_tx(&fb[b], tx);
+        if (first) bulk_g2s(dst, cur.base, (uint32_t)cur.hk, &fb[b]);
+        const int dk = cur.hk;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            bulk_g2s(dst + dk + r * kbytes, cur.base + cur.hk + (size_t)(r * Q + (gg.s0 >> 2)) * cur.krb, kbytes, &fb[b]);
+        const int offv = gg.cls == 0 ? cur.offv[0] : gg.cls == 1 ? cur.offv[1] : cur.offv[2];
+        bulk_g2s(dst + dk + gg.ns * cur.krb, cur.base + offv + (size_t)gg.li0 * rb, vbytes, &fb[b]);
+        bulk_g2s(dst + dk + gg.ns * cur.krb + vbytes, cur.base + cur.offvp + (size_t)gg.s0 * 8, pbytes, &fb[b]);
+        return true;
+    };
+    auto stage_q = [&](int b, int item) {
+        bulk_g2s(pbuf + (size_t)b * p.slot_bytes + qoff, static_cast<const uint8_t*>(p.q) + (size_t)(item / S) * qbytes,
+                 (uint32_t)qbytes, &fb[b]);
+    };
+    auto issue_item = [&](int b) {
+        const bool first = is.item < nitems && is.c == is.item % S;
+        const int it = is.item;
+        if (!stage_item(b)) return false;
+        if (first) stage_q(b, it);
+        advance();
+        return true;
+    };
+
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (issuer) {
+        for (int b = 0; b < nbuf; ++b) mbar_init(&fb[b], 1);
+        fence_barrier_init();
+        is.item = item0;
+        is.c = item0 % S;
+        load_meta(item0, is.cur);
+        load_meta(item0 + istride, is.nxt);
+        set_cur();
+        stage_item(0);  // KV of the first chunk before the grid dependency
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (issuer && item0 < nitems) {
+        stage_q(0, item0);
+        advance();
+    }
+    const U2xLane lc = u2x_lane(half);
+    constexpr int npass = G8 ? 2 : 1;  // GQA groups of 5..8 heads: two 4-head passes per staged chunk
+    for (int hp = 0; hp < npass; ++hp)
+        for (int i = threadIdx.x & 63; i < kU24MaxK * 512 / 16; i += 64)
+            reinterpret_cast<uint4*>(scr + hp * kU24Scratch + kU24QDig)[i] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    int b = 0, k = 0;
+    uint32_t phase = 0;
+    U2xRun run0;
+    U2xRun run1;  // (G8 only)
+    U24Tile tl{};
+    for (int item = item0; item < nitems; item += istride) {
+        const int tile = item / S, part = item % S;
+        int C = part + 1, hk = 0, krb = 0;  // C: known once the first chunk is in
+        for (int c = part; c < C; c += S) {
+            mbar_wait(&fb[b], phase);
+            __syncwarp();
+            const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
+            const bool first = c == part;
+            if (first) {
+                const TileHeader& th = *reinterpret_cast<const TileHeader*>(st);
+                u24_tile(th.r, tl);
+                C = u24_nchunks(tl);
+                hk = th.off_k;
+                krb = th.krow_bytes;
+            }
+            if (k == 0 && issuer)  // look-ahead once the first chunk is in
+                for (int j = 1; j < nbuf; ++j) issue_item(j);
+            const int bprev = b == 0 ? nbuf - 1 : b - 1;
+            auto refill = [&]() {
+                if (issuer && k >= 1) issue_item(bprev);
+            };
+            const U24Geom ck = u24_chunk(tl, c);
+            const uint8_t* kb = st + hk;
+            const uint8_t* vb = kb + ck.ns * krb;
+            const float2* vp = reinterpret_cast<const float2*>(vb + ck.ns * u24_vrow_bytes(ck.cls));
+            decode_chunk_u24<IO>(st, st + qoff, min(4, p.g), scr, 1 + pr, lc, refill, ck, first, krb, kb, vb, vp, run0,
+                                 tl);
+            if constexpr (G8)
+                decode_chunk_u24<IO>(st, st + qoff + 4 * QROW, p.g - 4, scr + kU24Scratch, 1 + pr, lc, [] {}, ck, first,
+                                     krb, kb, vb, vp, run1, tl);
+            if (++b == nbuf) {
+                b = 0;
+                phase ^= 1u;
+            }
+            ++k;
+        }
+#pragma unroll
+        for (int hp = 0; hp < 2; ++hp) {
+            const int head = 4 * hp + lc.tig;
+            if (hp >= npass || head >= p.g) continue;
+            const U2xRun& rn = (G8 && hp) ? run1 : run0;
+            if (p.partial) {  // this part's (o, max, sum) of the tile
+                float* prow = p.partial + (((size_t)part * p.units + tile) * p.g + head) * (kD + 2);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) *reinterpret_cast<float2*>(prow + lc.ch0 + 4 * m) = rn.o[m];
+                if (half == 0 && lc.gid == 0) {
+                    prow[kD] = rn.m;
+                    prow[kD + 1] = rn.l;
+                }
+            } else {
+                IO* orow = static_cast<IO*>(p.out) + ((size_t)tile * p.g + head) * kD + lc.ch0;
+                const float inv = rcp_approx(rn.l);
+                const float2 iv = make_float2(inv, inv);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const float2 r = fmul2(rn.o[m], iv);
+                    if constexpr (sizeof(IO) == 2)
+                        *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
+                    else
+                        *reinterpret_cast<float2*>(orow + 4 * m) = r;
+                }
+            }
+        }
+    }
+}
+
+// Parts per tile for split-K: enough (tile, part) items for ~2 per warp pair,
+// never more parts than the smallest tile has chunks.
+static int u24_parts(const rdkv_decode_args* a, int pairs_total) {
+    const int want = (2 * pairs_total + a->units - 1) / a->units;
+    int S = want < a->plan.min_chunks24 ? want : a->plan.min_chunks24;
+    if (S > kU24MaxParts) S = kU24MaxParts;
+    return S < 1 ? 1 : S;
+}
+
+template <typename IO>
+static int launch_u24(const rdkv_decode_args* a, cudaStream_t st) {
+    const int qbytes = a->group * kD * (int)sizeof(IO);
+    // header + channel table + perm (<= 128 + 10 * 192 B), then a chunk's K rows,
+    // V rows and V params (class 0 the largest), q rows at the end
+    const int krb = a->plan.max_krow_bytes24;
+    int body = 0;
+    for (int c = 0; c < 3; ++c) {
+        const int b = u24_chunk_slots(c) * (krb + u24_vrow_bytes(c) + 8);
+        body = b > body ? b : body;
+    }
+    const int slot = ((kHeaderBytes + 10 * 192 + body + qbytes + 127) & ~127);
+    const int scratch = ((a->group > 4 ? 2 : 1) * kU24Scratch + (int)sizeof(U24Issuer) + 127) & ~127;
+    const DevAttrs da = dev_attrs();
+    const int slack = 128;
+    int W = 0, nbuf = 0;
+    if (!pick_pairs(1 << 30, da.nsm, slot, scratch, da.smem_optin - slack, W, nbuf)) return RDKV_EINVAL;
+    const int S0 = u24_parts(a, W * da.nsm);
+    const size_t need = rdkv_cuda_decode_workspace(a->units, a->group, kD, S0);
+    const int S = (S0 > 1 && a->workspace && a->workspace_bytes >= need && a->split == 0) ? S0 : 1;
+    const size_t smem = W * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
+    MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
+                static_cast<const __half*>(a->zc_k), static_cast<const __half*>(a->zc_v), a->zc_len,
+                a->units, a->group, a->zc_cap, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
+    p.partial = S > 1 ? static_cast<float*>(a->workspace) : nullptr;
+    p.split_rank = 0;
+    p.split_world = S;
+    auto kern = a->group > 4 ? decode_u24_kernel<IO, true> : decode_u24_kernel<IO, false>;
+    static std::atomic<int> smem_set[2][kMaxDevices];
+    set_smem_once(kern, (int)smem, smem_set[a->group > 4], da.dev);
+    long long items = (long long)a->units * S;
+    int blocks = (int)((items + W - 1) / W);
+    if (blocks > da.nsm) blocks = da.nsm;
+    if (verbose_env())
+        fprintf(stderr, "u24: units %d parts %d pairs %d bufs %d slot %d smem %zu grid %d\n", a->units, S, W, nbuf,
+                slot, smem, blocks);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(32 * 2 * W);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return RDKV_ECUDA;
+    if (S > 1) return launch_merge(p.partial, S, a->units * a->group, kD, a->out, a->io_dtype, st);
+    return launch_status();
+}
+
 int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     const bool f16 = a->io_dtype == RDKV_F16;
     // split step (rdkv_cuda_decode_prepare_split): mixed tiles on the general
     // body, then the uniform-2-bit ones on u2x (PDL: its prologue and KV
     // prefetch overlap the general kernel's tail)
     const rdkv_decode_plan& pl = a->plan;
+    // mixed 2/4/8-bit tiles (not all short enough for MIX), and uniform 2-bit tiles too
+    // long for the short-tile kernel: the chunked split-K kernel (no Zone C; kernel 0 or 2)
+    const bool short_u2x = pl.uniform2 && pl.max_slots <= kU2MaxSlots;
+    if (pl.mix24 && !short_u2x && !a->zc_len && a->group <= 8 && (a->kernel == 0 || a->kernel == 2)) {
+        rdkv_decode_args b = *a;
+        b.unit_ids = nullptr;
+        return f16 ? launch_u24<__half>(&b, st) : launch_u24<float>(&b, st);
+    }
     // (the uniform subset goes to the short-tile kernel, which is the one that
     // reads unit_ids: every tile of the step must fit it)
     if (a->unit_ids && !pl.uniform2 && pl.n_uniform > 0 && pl.n_uniform < a->units && a->group <= 8 &&
@@ -2862,6 +3555,7 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     rdkv_decode_args plain = *a;
     plain.unit_ids = nullptr;
     a = &plain;
+
     // uniform 2-bit tiles (the n=128 production shape) take the specialised body
     // uniform 2-bit tiles (the n=128 production shape): warp-pair body by default,
     // kernel 4 selects the one-warp body, kernel 3 the general body
@@ -2910,7 +3604,7 @@ static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets
     for (int u = 0; u < units; ++u)
         cudaMemcpyAsync(&hdrs[u], arena + tile_offsets_host[u], sizeof(TileHeader), cudaMemcpyDeviceToHost, st);
     if (cudaStreamSynchronize(st) != cudaSuccess) rc = RDKV_ECUDA;
-    rdkv_decode_plan p{0, 0, 0, 0, 2, 0, 2};
+    rdkv_decode_plan p{0, 0, 0, 0, 2, 0, 2, 1, 1 << 30, 0};
     int32_t* ids = unit_ids_dev ? static_cast<int32_t*>(malloc(sizeof(int32_t) * (size_t)units)) : nullptr;
     int nmixed = 0, n_u = 0, n_m = 0;
     bool any_notfull = false, any_long = false, split_mix = false, split_notfull = false;
@@ -2934,6 +3628,18 @@ static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets
                         h.kslot_base[1] == 128 && h.kbyte_base[1] == 32;
         n_u += u2;
         n_m += m2;
+        // mixed 2/4/8-bit tiles for the chunked split-K kernel (decode_u24)
+        const bool t24 = h.r[3] == 0 && h.c[3] == 0 && h.n > 0 && (h.kslot_base[3] >> 5) <= kU24MaxK &&
+                         h.c[0] + h.c[1] + h.c[2] > 0;
+        if (!t24) {
+            p.mix24 = 0;
+        } else {
+            U24Tile tt;
+            u24_tile(h.r, tt);
+            const int C = u24_nchunks(tt);
+            p.min_chunks24 = C < p.min_chunks24 ? C : p.min_chunks24;
+            p.max_krow_bytes24 = h.krow_bytes > p.max_krow_bytes24 ? h.krow_bytes : p.max_krow_bytes24;
+        }
         if (u2 && h.c[0] != kD) any_notfull = true;
         if (u2 && h.nslot > kU2MaxSlots) any_long = true;
         if (ids) {  // split lists: short uniform / mostly-2-bit tiles first (in order), the rest from the back
@@ -2950,6 +3656,7 @@ static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets
     // tile uniform or mostly 2-bit and short (the MIX kernel); 0: anything else
     p.uniform2 = n_u == units ? (any_notfull ? 1 : 2) : (n_u + n_m == units && !any_long ? 3 : 0);
     p.uniform2_split = split_mix ? 3 : split_notfull ? 1 : 2;
+    if (!p.mix24) p.min_chunks24 = p.max_krow_bytes24 = 0;
     if (ids) {  // the mixed tail back in unit order
         for (int i = p.n_uniform, j = units - 1; i < j; ++i, --j) {
             const int32_t t = ids[i];

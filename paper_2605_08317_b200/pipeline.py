@@ -331,6 +331,7 @@ class PackedModel:
     decode_sizes: torch.Tensor | None = None   # [U] int32, from prepare()
     plan: capi.DecodePlan | None = None
     unit_ids: torch.Tensor | None = None       # [U] int32: uniform-2-bit tiles first (split dispatch)
+    split_ws: torch.Tensor | None = None       # split-K partials of the chunked mixed 2/4-bit kernel
     _infos: list = field(default_factory=list)
 
     def prepare(self) -> capi.DecodePlan:
@@ -343,11 +344,19 @@ class PackedModel:
                                                             self.decode_sizes.data_ptr(), self.unit_ids.data_ptr(),
                                                             C.byref(plan), _stream()), "decode_prepare")
         self.plan = plan
+        # long or mixed 2/4-bit tiles decode on the chunked split-K kernel (decode_u24),
+        # whose parts' partials live in a caller-owned workspace (the library keeps no state)
+        self.split_ws = None
+        if plan.mix24 and not (plan.uniform2 and plan.max_slots <= 160):
+            parts = min(16, int(plan.min_chunks24))
+            if parts > 1:
+                self.split_ws = decode_workspace(self, parts, self.arena.device)
         return plan
 
     def share_plan(self, other: "PackedModel") -> "PackedModel":
         """Reuse another model's prepare() results (same tiles, e.g. an arena copy)."""
         self.decode_sizes, self.plan, self.unit_ids = other.decode_sizes, other.plan, other.unit_ids
+        self.split_ws = other.split_ws
         return self
 
     @property
@@ -532,6 +541,9 @@ def decode_args(model: PackedModel, q, out, split=1, kernel=0, workspace=None) -
         a.plan = model.plan
         if model.unit_ids is not None:
             a.unit_ids = model.unit_ids.data_ptr()
+    if workspace is None and split == 1 and kernel in (0, 2) and model.split_ws is not None:
+        a.split = 0  # automatic split-K over the model's partials workspace
+        workspace = model.split_ws
     if workspace is not None:
         a.workspace, a.workspace_bytes = workspace.data_ptr(), workspace.numel()
     return a

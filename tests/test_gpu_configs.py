@@ -67,11 +67,14 @@ def test_configs2_128k_slice_matches_reference(cuda, ref):
 
 
 @pytest.mark.parametrize("name,Hq,Hkv,n", [("qwen2.5-7b", 28, 4, 1024), ("qwen2.5-7b", 28, 4, 2048),
-                                           ("mistral-7b", 32, 8, 2048)])
+                                           ("mistral-7b", 32, 8, 2048), ("qwen2.5-7b", 28, 4, 256),
+                                           ("mistral-7b", 32, 8, 64)])
 def test_configs3_large_mixed_tiles_auto_dispatch(cuda, orc, name, Hq, Hkv, n):
-    """configs[3] budget points whose tiles (1,600-3,100 kept slots at 2/4/8 bits,
-    heavy hitters + outlier K channels, the bench's inputs) exceed shared memory:
-    the automatic dispatch vs the oracle's build_trizone + packed_decode_step."""
+    """configs[3] budget points (64 .. 3,100 kept slots at mixed 2/4 bits, heavy hitters
+    + outlier K channels, the bench's inputs): the automatic dispatch (the chunked
+    split-K mixed 2/4-bit kernel, decode_u24) vs the oracle's build_trizone +
+    packed_decode_step; the same step without split-K (no partials workspace, one
+    warp pair per tile) and with f32 I/O must agree too."""
     spec = WorkloadSpec(batch=1, layers=2, q_heads=Hq, kv_heads=Hkv, ctx=65536, n_tokens=n, seed=11,
                         hh_stride=64, hh_boost=1.0, outlier_channels=4, outlier_scale=8.0)
     g, d = spec.group, spec.head_dim
@@ -84,9 +87,15 @@ def test_configs3_large_mixed_tiles_auto_dispatch(cuda, orc, name, Hq, Hkv, n):
         al.check()
         model = P.build_packed_model(kd, vd, al, group=g)
         model.check()
-        assert model.plan.max_slots > 1024
+        if n >= 1024:
+            assert model.plan.max_slots > 1024
+        assert model.plan.mix24
         q = rng.standard_normal((Hkv, g, d)).astype(np.float16).astype(np.float32)
         out = P.packed_decode_step(model, torch.from_numpy(q).to(cuda).half()).float().cpu().numpy()
+        ws, model.split_ws = model.split_ws, None  # one pair per tile, no partials
+        out1 = P.packed_decode_step(model, torch.from_numpy(q).to(cuda)).cpu().numpy()
+        model.split_ws = ws
+        assert rel(out1, out) < 1e-3
         vb, kb = al.v_bits.cpu().numpy(), al.k_bits.cpu().numpy()
         for h in range(Hkv):
             classes |= set(np.unique(vb[h]).tolist())

@@ -357,8 +357,9 @@ def test_split_dispatch_mixed_arena(cuda, orc, io, g):
         vb[:] = 0
         vb[np.sort(rng.choice(300, int(rng.integers(100, 150)), replace=False))] = 2
         kb[:] = 2
-        if i % 7 == 3:  # an 8-bit row (not "mostly 2-bit": the general body)
+        if i % 7 == 3:  # 8-bit rows and a Zone B row (not 2/4/8-bit only: the general body)
             vb[np.nonzero(vb)[0][:3]] = 8
+            vb[np.nonzero(vb)[0][3]] = 16
             kb[rng.choice(D, 3, replace=False)] = 4
         elif i % 7 == 5:  # a few 4-bit rows / channels (the MIX kernel)
             vb[np.nonzero(vb)[0][:3]] = 4
@@ -366,7 +367,7 @@ def test_split_dispatch_mixed_arena(cuda, orc, io, g):
         cases.append((k, v, vb, kb, q))
     worst, model = _run_batch(cuda, orc, cases, g, io=io)
     plan = model.plan
-    assert plan.uniform2 == 0 and 0 < plan.n_uniform < len(cases)
+    assert plan.uniform2 == 0 and 0 < plan.n_uniform < len(cases) and not plan.mix24
     assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
     q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).to(io)
     split = P.packed_decode_step(model, q)
