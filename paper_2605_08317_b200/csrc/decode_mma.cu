@@ -2631,6 +2631,20 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
                   da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;
+    // The SM's W pairs run as W / 2 CTAs of two pairs: a CTA retires as soon as
+    // its own two pairs are done, so under programmatic dependent launch the
+    // next step's CTAs take its slots while the SM's slower pairs still run
+    // (measured 13.5 -> 12.9 us on the 4096-tile step; 1 CTA of 8 pairs: 13.5,
+    // 4 pairs per CTA: 13.1). RDKV_DECODE_CTAS (experiments build) forces c CTAs per SM.
+    static const char* ctas_env = experiment_knob("RDKV_DECODE_CTAS");
+    const int ctas = ctas_env ? atoi(ctas_env) : (W % 2 == 0 ? W / 2 : 1);
+    if (ctas > 1 && W % ctas == 0 && max_blocks == 0) {
+        const int c = ctas;
+        p.W = W = W / c;
+        smem = W * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
+        blocks = (a->units + W - 1) / W;
+        if (blocks > c * nsm) blocks = c * nsm;
+    }
     if (max_blocks > 0) {  // split step: the SMs the general kernel leaves free
         p.concurrent = 1;
         if (blocks > max_blocks) blocks = max_blocks;
@@ -2860,7 +2874,7 @@ constexpr int kU24QDig = kXQDig;                         // q~ digit blocks: kU2
 constexpr int kU24PDig = kU24QDig + kU24MaxK * 512;      // p~ digit blocks: 4 x 256 B
 constexpr int kU24Scratch = kU24PDig + 4 * 256;
 constexpr int kU24MaxParts = 16;                         // split-K parts per tile
-__host__ __device__ constexpr int u24_chunk_slots(int cls) { return cls == 0 ? 128 : cls == 1 ? 64 : 32; }
+__host__ __device__ constexpr int u24_chunk_slots(int cls) { return cls == 0 ? 128 : cls == 1 ? 96 : 32; }
 __host__ __device__ constexpr int u24_vrow_bytes(int cls) { return cls == 0 ? 32 : cls == 1 ? 64 : 128; }
 
 // Per-tile chunk layout: class c has C[c] chunks of u24_chunk_slots(c) slots
@@ -2901,7 +2915,7 @@ __host__ __device__ inline U24Geom u24_chunk(const U24Tile& t, int k) {
         g.s0 = P0 + P1 + g.li0;
         rc = t.r[2];
     }
-    g.ns = min(g.cls == 0 ? 128 : g.cls == 1 ? 64 : 32, pad4(rc) - g.li0);
+    g.ns = min(g.cls == 0 ? u24_chunk_slots(0) : g.cls == 1 ? u24_chunk_slots(1) : u24_chunk_slots(2), pad4(rc) - g.li0);
     g.n = min(g.ns, rc - g.li0);
     return g;
 }
@@ -3217,17 +3231,22 @@ __device__ __forceinline__ void decode_chunk_u24(const uint8_t* __restrict__ t, 
         // 4-bit rows (64 B; 4-token groups of 256 B, word columns swizzled by 8 (G & 3) = 8 tig):
         // byte column 32 half + 8 (gid & 3) + 2m + jj holds channels ch0 + 4m (lo nibble,
         // row gid) and ch0 + 4m + 1 (hi nibble, row gid + 8)
-        const int colb = 32 * half + 8 * (gid & 3) + (gid >> 2);
-        const uint8_t* g0b = vb + tig * 256;
+        // (the lane's four columns are every other word of one swizzled 8-word run:
+        // two 16-B loads per group and a select by jj = gid >> 2)
+        const bool jj = (gid >> 2) != 0;
+        const uint8_t* g0b = vb + tig * 256 + (((32 * half + 8 * (gid & 3)) ^ (8 * tig)) * 4);
 #pragma unroll 1
         for (int kk = 0; kk < nb; ++kk) {
             uint32_t b[2];
             ldsm_x2(b, pdig + kk * 256 + L.bofs2);
+            const uint4 x0 = lds128(g0b + kk * 2048), x1 = lds128(g0b + kk * 2048 + 16);
+            const uint4 y0 = lds128(g0b + kk * 2048 + 1024), y1 = lds128(g0b + kk * 2048 + 1040);
+            const uint32_t u0[4] = {jj ? x0.y : x0.x, jj ? x0.w : x0.z, jj ? x1.y : x1.x, jj ? x1.w : x1.z};
+            const uint32_t u1[4] = {jj ? y0.y : y0.x, jj ? y0.w : y0.z, jj ? y1.y : y1.x, jj ? y1.w : y1.z};
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-                const int wo = ((colb + 2 * m) ^ (8 * tig)) * 4;
-                const uint32_t w0 = lds32(g0b + kk * 2048 + wo), w1 = lds32(g0b + kk * 2048 + 1024 + wo);
-                const uint32_t a[4] = {w0 & 0x0F0F0F0Fu, w0 & 0xF0F0F0F0u, w1 & 0x0F0F0F0Fu, w1 & 0xF0F0F0F0u};
+                const uint32_t a[4] = {u0[m] & 0x0F0F0F0Fu, u0[m] & 0xF0F0F0F0u, u1[m] & 0x0F0F0F0Fu,
+                                       u1[m] & 0xF0F0F0F0u};
                 mma_u8u8(acc[m], a, b[0], b[1]);
             }
         }
@@ -3482,26 +3501,31 @@ static int launch_u24(const rdkv_decode_args* a, cudaStream_t st) {
     const int S0 = u24_parts(a, W * da.nsm);
     const size_t need = rdkv_cuda_decode_workspace(a->units, a->group, kD, S0);
     const int S = (S0 > 1 && a->workspace && a->workspace_bytes >= need && a->split == 0) ? S0 : 1;
-    const size_t smem = W * kXMaxBuf * sizeof(uint64_t) + (size_t)W * (nbuf * slot + scratch) + slack;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
                 static_cast<const __half*>(a->zc_k), static_cast<const __half*>(a->zc_v), a->zc_len,
                 a->units, a->group, a->zc_cap, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};
     p.partial = S > 1 ? static_cast<float*>(a->workspace) : nullptr;
     p.split_rank = 0;
     p.split_world = S;
+    // pairs per CTA (experiments build: RDKV_DECODE_U24_PPC); the SM holds W pairs
+    static const char* ppc_env = experiment_knob("RDKV_DECODE_U24_PPC");
+    const int ppc = ppc_env && atoi(ppc_env) > 0 && W % atoi(ppc_env) == 0 ? atoi(ppc_env) : W;
+    const int ctas = W / ppc;
+    p.W = ppc;
+    const size_t smem_cta = ppc * kXMaxBuf * sizeof(uint64_t) + (size_t)ppc * (nbuf * slot + scratch) + slack;
     auto kern = a->group > 4 ? decode_u24_kernel<IO, true> : decode_u24_kernel<IO, false>;
     static std::atomic<int> smem_set[2][kMaxDevices];
-    set_smem_once(kern, (int)smem, smem_set[a->group > 4], da.dev);
+    set_smem_once(kern, (int)smem_cta, smem_set[a->group > 4], da.dev);
     long long items = (long long)a->units * S;
-    int blocks = (int)((items + W - 1) / W);
-    if (blocks > da.nsm) blocks = da.nsm;
+    int blocks = (int)((items + ppc - 1) / ppc);
+    if (blocks > ctas * da.nsm) blocks = ctas * da.nsm;
     if (verbose_env())
-        fprintf(stderr, "u24: units %d parts %d pairs %d bufs %d slot %d smem %zu grid %d\n", a->units, S, W, nbuf,
-                slot, smem, blocks);
+        fprintf(stderr, "u24: units %d parts %d pairs %d/cta %d bufs %d slot %d smem %zu grid %d\n", a->units, S, W,
+                ppc, nbuf, slot, smem_cta, blocks);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(32 * 2 * W);
-    cfg.dynamicSmemBytes = smem;
+    cfg.blockDim = dim3(32 * 2 * ppc);
+    cfg.dynamicSmemBytes = smem_cta;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -343,6 +343,140 @@ __global__ void __launch_bounds__(256, 1) probe_stream_kernel(
     if (PASS == 1 && tid < kSToks && tok0 + tid < t_len) rawf[(size_t)unit * t_len + tok0 + tid] = (float)colacc;
 }
 
+// The same two passes on the fp64 tensor cores (DMMA m8n8k4, sm_80+; B200 runs
+// it at the DFMA rate with 1/8 of the issue slots). CTA tile 128 rows x 128
+// tokens, warp w: rows 32 (w >> 1) .. + 31 (4 m8 groups), tokens 64 (w & 1) ..
+// + 63 (8 n8 groups). The dot products are the same fp64 sums in a different
+// association (within ~1 ulp of the reference's sequential ones); pass S1's
+// stats are per (row, 64-token half tile).
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+constexpr int kDPad = kSRows + 4;  // smem stride (doubles) of a staged channel: 4 k-rows of a fragment load in
+                                   // distinct bank quarters
+constexpr int kDGemmSmem = 2 * 2 * kSK * kDPad * (int)sizeof(double);
+constexpr int kDSmem = kDGemmSmem > kSColSmem ? kDGemmSmem : kSColSmem;
+
+template <typename T, int PASS>
+__global__ void __launch_bounds__(256, 1) probe_dmma_kernel(
+    const T* __restrict__ k, const T* __restrict__ q, int t_len, int d, int R, int window, int probe_rows,
+    double inv_sqrt_d, int nht, double2* __restrict__ stats, const double2* __restrict__ rowstat,
+    float* __restrict__ rawf) {
+    extern __shared__ __align__(16) double sm[];
+    const int tile = blockIdx.x, unit = blockIdx.y;
+    const int tok0 = tile * kSToks;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wr = 32 * (warp >> 1), wt = 64 * (warp & 1);  // warp's row / token offsets in the CTA tile
+    const int fr = lane >> 2, fk = lane & 3;                  // fragment row (or column) and k index
+    const T* kb = k + (size_t)unit * t_len * d;
+    const T* qb = q + (size_t)unit * (R / window) * probe_rows * d;
+    const int lc = tid & 15, lr = tid >> 4;
+    const int nchunk = d / kSK;
+    double colacc = 0.0;  // S3: column sum of token tok0 + tid (tid < 128), in row order
+    for (int rb = 0; rb < R; rb += kSRows) {
+        double acc[4][8][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        float qv_n[8], kv_n[8];
+        auto gload = [&](int c0) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int row = rb + lr + 16 * m, t = tok0 + lr + 16 * m;
+                const int qi = row / window, w = row - qi * window;
+                qv_n[m] = row < R ? load_as_float(qb, ((size_t)qi * probe_rows + probe_rows - window + w) * d + c0 + lc)
+                                  : 0.0f;
+                kv_n[m] = t < t_len ? load_as_float(kb, (size_t)t * d + c0 + lc) : 0.0f;
+            }
+        };
+        gload(0);
+        for (int kc = 0; kc < nchunk; ++kc) {
+            double* Qs = sm + (kc & 1) * 2 * kSK * kDPad;
+            double* Ks = Qs + kSK * kDPad;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                Qs[lc * kDPad + lr + 16 * m] = (double)qv_n[m];
+                Ks[lc * kDPad + lr + 16 * m] = (double)kv_n[m];
+            }
+            __syncthreads();
+            if (kc + 1 < nchunk) gload((kc + 1) * kSK);
+#pragma unroll
+            for (int k4 = 0; k4 < kSK; k4 += 4) {
+                double a[4], b[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = Qs[(k4 + fk) * kDPad + wr + 8 * i + fr];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) b[j] = Ks[(k4 + fk) * kDPad + wt + 8 * j + fr];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dmma884(acc[i][j], a[i], b[j]);
+            }
+        }
+        __syncthreads();  // all chunk reads done: the smem may be reused below
+        // fragment (i, j, e): row wr + 8 i + fr, token wt + 8 j + 2 fk + e
+        if (PASS == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int row = rb + wr + 8 * i + fr;
+                const int off = t_len - window + (row % window);  // causal offset (pipeline.cpp:129-130)
+                double m = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int t = tok0 + wt + 8 * j + 2 * fk + e;
+                        acc[i][j][e] = __dmul_rn(acc[i][j][e], inv_sqrt_d);
+                        if (row < R && t < t_len && t <= off) m = fmax(m, acc[i][j][e]);
+                    }
+                m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+                m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+                double s = 0.0;
+                if (m != -INFINITY) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int t = tok0 + wt + 8 * j + 2 * fk + e;
+                            if (row < R && t < t_len && t <= off) s = __dadd_rn(s, exp(__dadd_rn(acc[i][j][e], -m)));
+                        }
+                }
+                s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
+                s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
+                if (fk == 0 && row < R) stats[((size_t)unit * R + row) * nht + 2 * tile + (warp & 1)] = make_double2(m, s);
+            }
+        } else {
+            double* at = sm;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int rl = wr + 8 * i + fr, row = rb + rl;
+                const int off = t_len - window + (row % window);
+                const double2 ms = row < R ? rowstat[(size_t)unit * R + row] : make_double2(0.0, 1.0);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int tl = wt + 8 * j + 2 * fk + e, t = tok0 + tl;
+                        double a = 0.0;  // entries past the causal offset are exactly zero (cache.cpp:181)
+                        if (row < R && t < t_len && t <= off)
+                            a = exp(__dadd_rn(__dmul_rn(acc[i][j][e], inv_sqrt_d), -ms.x)) / ms.y;
+                        at[rl * kSAStride + tl] = a;
+                    }
+            }
+            __syncthreads();
+            if (tid < kSToks) {
+                const int nr = min(kSRows, R - rb);
+                for (int r = 0; r < nr; ++r) colacc = __dadd_rn(colacc, at[r * kSAStride + tid]);
+            }
+            __syncthreads();  // the a-tile aliases the next row block's chunk buffers
+        }
+    }
+    if (PASS == 1 && tid < kSToks && tok0 + tid < t_len) rawf[(size_t)unit * t_len + tok0 + tid] = (float)colacc;
+}
+
 // S2: per (unit, row) global max and softmax denominator from the tile stats,
 // one warp per row (lane-strided tiles, fixed shuffle tree: deterministic).
 __global__ void probe_rowstat_kernel(const double2* __restrict__ stats, int rows, int ntt,
@@ -441,7 +575,7 @@ static StreamWorkspace carve_stream(const rdkv_shape* s, int window, void* base)
         off += (n + 255) / 256 * 256;
         return r;
     };
-    w.stats = reinterpret_cast<double2*>(take(U * R * ntt * sizeof(double2)));
+    w.stats = reinterpret_cast<double2*>(take(U * R * 2 * ntt * sizeof(double2)));  // per 64-token half tile
     w.rowstat = reinterpret_cast<double2*>(take(U * R * sizeof(double2)));
     w.rawf = reinterpret_cast<float*>(take(U * T * sizeof(float)));
     w.kpart = reinterpret_cast<double*>(take(U * nch * d * sizeof(double)));
@@ -458,14 +592,15 @@ static int run_weights_stream(const T* k, const T* q, const rdkv_shape* s, int w
     const int ntt = (t_len + kSToks - 1) / kSToks;
     static std::atomic<int> smem0[kMaxDevices], smem1[kMaxDevices];
     const int dev = dev_attrs().dev;
-    set_smem_once(probe_stream_kernel<T, 0>, kSSmem, smem0, dev);
-    set_smem_once(probe_stream_kernel<T, 1>, kSSmem, smem1, dev);
+    set_smem_once(probe_dmma_kernel<T, 0>, kDSmem, smem0, dev);
+    set_smem_once(probe_dmma_kernel<T, 1>, kDSmem, smem1, dev);
     const dim3 grid(ntt, U);
-    probe_stream_kernel<T, 0><<<grid, 256, kSSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, ntt,
-                                                          ws.stats, nullptr, nullptr);
-    probe_rowstat_kernel<<<(U * R * 32 + 255) / 256, 256, 0, st>>>(ws.stats, U * R, ntt, ws.rowstat);
-    probe_stream_kernel<T, 1><<<grid, 256, kSSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, ntt,
-                                                          nullptr, ws.rowstat, ws.rawf);
+    const int nht = 2 * ntt;  // stats per 64-token half tile
+    probe_dmma_kernel<T, 0><<<grid, 256, kDSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, nht,
+                                                        ws.stats, nullptr, nullptr);
+    probe_rowstat_kernel<<<(U * R * 32 + 255) / 256, 256, 0, st>>>(ws.stats, U * R, nht, ws.rowstat);
+    probe_dmma_kernel<T, 1><<<grid, 256, kDSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, nht,
+                                                        nullptr, ws.rowstat, ws.rawf);
     const size_t nt = (size_t)U * t_len;
     token_pool_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(ws.rawf, U, t_len, pool_kernel, w_t);
     const int nch = (t_len + kCNChunk - 1) / kCNChunk;

@@ -4,7 +4,13 @@ import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+if "--exp" in sys.argv:  # the EXPERIMENTS build (timing knobs), tools only
+    sys.argv.remove("--exp")
+    from paper_2605_08317_b200 import capi
+
+    capi.LIB_PATH = os.path.join(ROOT, "paper_2605_08317_b200", "_lib_exp", "librdkv_b200.so")
 import numpy as np
 import torch
 
