@@ -18,12 +18,34 @@ namespace rdkv_b200 {
 
 constexpr int kPackThreads = 256;
 
+// per-class counts of the bit-widths 2/4/8/16 in four bytes (SIMD byte compares)
+__device__ __forceinline__ void class_counts4(uint32_t w, int (&r)[4]) {
+    r[0] += __popc(__vcmpeq4(w, 0x02020202u)) >> 3;
+    r[1] += __popc(__vcmpeq4(w, 0x04040404u)) >> 3;
+    r[2] += __popc(__vcmpeq4(w, 0x08080808u)) >> 3;
+    r[3] += __popc(__vcmpeq4(w, 0x10101010u)) >> 3;
+}
+
 __device__ __forceinline__ void header_counts(const uint8_t* vb, const uint8_t* kb, int t_len,
                                               int d, int* counts /*8 ints in smem*/) {
     int r[4] = {0, 0, 0, 0}, c[4] = {0, 0, 0, 0};
-    for (int t = threadIdx.x; t < t_len; t += blockDim.x) {
-        const int cls = class_of_bits(vb[t]);
-        if (cls >= 0) r[cls]++;
+    // v_bits rows are 16-B aligned when t_len % 16 == 0 (the allocation buffers
+    // are [units][T] u8): 16 widths per load
+    if ((t_len & 15) == 0 && (reinterpret_cast<uintptr_t>(vb) & 15) == 0) {
+        const uint4* v4 = reinterpret_cast<const uint4*>(vb);
+        for (int i = threadIdx.x; i < (t_len >> 4); i += blockDim.x) {
+            const uint4 w = v4[i];
+            if ((w.x | w.y | w.z | w.w) == 0u) continue;  // evicted tokens (the common case)
+            class_counts4(w.x, r);
+            class_counts4(w.y, r);
+            class_counts4(w.z, r);
+            class_counts4(w.w, r);
+        }
+    } else {
+        for (int t = threadIdx.x; t < t_len; t += blockDim.x) {
+            const int cls = class_of_bits(vb[t]);
+            if (cls >= 0) r[cls]++;
+        }
     }
     for (int ch = threadIdx.x; ch < d; ch += blockDim.x) {
         const int cls = class_of_bits(kb[ch]);
@@ -167,10 +189,21 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(
 
     // ---- 1. token slots: contiguous chunk per thread, block scan per class
     {
-        const int per = (t_len + blockDim.x - 1) / blockDim.x;
-        const int t0 = tid * per, t1 = min(t_len, t0 + per);
+        // (chunks of a multiple of 16 tokens: all-evicted 16-B groups are skipped)
+        const int per = ((t_len + blockDim.x - 1) / blockDim.x + 15) & ~15;
+        const int t0 = min(t_len, tid * per), t1 = min(t_len, t0 + per);
+        const bool vec = (t_len & 15) == 0 && (reinterpret_cast<uintptr_t>(vb) & 15) == 0;
+        auto group_empty = [&](int t) {  // tokens t .. t + 15 all evicted (t % 16 == 0)
+            if (!vec || t + 16 > t1) return false;
+            const uint4 w = *reinterpret_cast<const uint4*>(vb + t);
+            return (w.x | w.y | w.z | w.w) == 0u;
+        };
         int cnt[4] = {0, 0, 0, 0};
         for (int t = t0; t < t1; ++t) {
+            if ((t & 15) == 0 && group_empty(t)) {
+                t += 15;
+                continue;
+            }
             const int cls = class_of_bits(vb[t]);
             if (cls >= 0) cnt[cls]++;
         }
@@ -194,6 +227,10 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(
             run[i] = s.cls_base[i] + base + incl[i] - cnt[i];
         }
         for (int t = t0; t < t1; ++t) {
+            if ((t & 15) == 0 && group_empty(t)) {
+                t += 15;
+                continue;
+            }
             const int cls = class_of_bits(vb[t]);
             if (cls >= 0) ids[run[cls]++] = t;
         }
@@ -381,7 +418,7 @@ extern "C" RDKV_API int rdkv_cuda_pack_plan(const uint8_t* v_bits, const uint8_t
     auto st = static_cast<cudaStream_t>(stream);
     int64_t* sizes = nullptr;
     RDKV_CUDA_TRY(cudaMallocAsync(&sizes, sizeof(int64_t) * s->units, st));
-    pack_plan_kernel<<<s->units, 128, 0, st>>>(v_bits, k_bits, s->seq_len, s->head_dim, sizes);
+    pack_plan_kernel<<<s->units, 512, 0, st>>>(v_bits, k_bits, s->seq_len, s->head_dim, sizes);
     scan_kernel<<<1, 1024, 0, st>>>(sizes, s->units, tile_offsets);
     const int rc = launch_status();
     RDKV_CUDA_TRY(cudaFreeAsync(sizes, st));

@@ -26,6 +26,8 @@
 //   W5 channel_norms  one thread per (unit, channel): sequential fp64 norms
 // This file is compiled with -fmad=false; the only fused multiply-adds are
 // the explicit __fma_rn calls in W1/W5, which are exact-equivalent there.
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace rdkv_b200 {
@@ -314,7 +316,10 @@ __global__ void __launch_bounds__(256, 1) probe_stream_kernel(
                 }
 #pragma unroll
                 for (int o = 1; o < 16; o <<= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-                if (tx == 0 && row < R) stats[((size_t)unit * R + row) * ntt + tile] = make_double2(m, s);
+                if (tx == 0 && row < R) {  // (one stat per 128-token tile; the second half-tile slot stays empty)
+                    stats[((size_t)unit * R + row) * ntt + 2 * tile] = make_double2(m, s);
+                    stats[((size_t)unit * R + row) * ntt + 2 * tile + 1] = make_double2(-INFINITY, 0.0);
+                }
             }
         } else {
             double* at = sm;
@@ -343,138 +348,181 @@ __global__ void __launch_bounds__(256, 1) probe_stream_kernel(
     if (PASS == 1 && tid < kSToks && tok0 + tid < t_len) rawf[(size_t)unit * t_len + tok0 + tid] = (float)colacc;
 }
 
-// The same two passes on the fp64 tensor cores (DMMA m8n8k4, sm_80+; B200 runs
-// it at the DFMA rate with 1/8 of the issue slots). CTA tile 128 rows x 128
-// tokens, warp w: rows 32 (w >> 1) .. + 31 (4 m8 groups), tokens 64 (w & 1) ..
-// + 63 (8 n8 groups). The dot products are the same fp64 sums in a different
-// association (within ~1 ulp of the reference's sequential ones); pass S1's
-// stats are per (row, 64-token half tile).
-__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d[0]), "+d"(d[1])
-                 : "d"(a), "d"(b));
-}
-constexpr int kDPad = kSRows + 4;  // smem stride (doubles) of a staged channel: 4 k-rows of a fragment load in
-                                   // distinct bank quarters
-constexpr int kDGemmSmem = 2 * 2 * kSK * kDPad * (int)sizeof(double);
-constexpr int kDSmem = kDGemmSmem > kSColSmem ? kDGemmSmem : kSColSmem;
+// Staging helpers and sizes of the persistent probe kernel (probe_exact_kernel).
+constexpr int kD128 = 128;
+constexpr int kTMaxR = 256;              // probe rows resident (g * window <= 256)
 
-template <typename T, int PASS>
-__global__ void __launch_bounds__(256, 1) probe_dmma_kernel(
-    const T* __restrict__ k, const T* __restrict__ q, int t_len, int d, int R, int window, int probe_rows,
-    double inv_sqrt_d, int nht, double2* __restrict__ stats, const double2* __restrict__ rowstat,
-    float* __restrict__ rawf) {
-    extern __shared__ __align__(16) double sm[];
-    const int tile = blockIdx.x, unit = blockIdx.y;
-    const int tok0 = tile * kSToks;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wr = 32 * (warp >> 1), wt = 64 * (warp & 1);  // warp's row / token offsets in the CTA tile
-    const int fr = lane >> 2, fk = lane & 3;                  // fragment row (or column) and k index
-    const T* kb = k + (size_t)unit * t_len * d;
-    const T* qb = q + (size_t)unit * (R / window) * probe_rows * d;
-    const int lc = tid & 15, lr = tid >> 4;
-    const int nchunk = d / kSK;
-    double colacc = 0.0;  // S3: column sum of token tok0 + tid (tid < 128), in row order
-    for (int rb = 0; rb < R; rb += kSRows) {
-        double acc[4][8][2];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-        float qv_n[8], kv_n[8];
-        auto gload = [&](int c0) {
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const int row = rb + lr + 16 * m, t = tok0 + lr + 16 * m;
-                const int qi = row / window, w = row - qi * window;
-                qv_n[m] = row < R ? load_as_float(qb, ((size_t)qi * probe_rows + probe_rows - window + w) * d + c0 + lc)
-                                  : 0.0f;
-                kv_n[m] = t < t_len ? load_as_float(kb, (size_t)t * d + c0 + lc) : 0.0f;
-            }
-        };
-        gload(0);
-        for (int kc = 0; kc < nchunk; ++kc) {
-            double* Qs = sm + (kc & 1) * 2 * kSK * kDPad;
-            double* Ks = Qs + kSK * kDPad;
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                Qs[lc * kDPad + lr + 16 * m] = (double)qv_n[m];
-                Ks[lc * kDPad + lr + 16 * m] = (double)kv_n[m];
-            }
-            __syncthreads();
-            if (kc + 1 < nchunk) gload((kc + 1) * kSK);
-#pragma unroll
-            for (int k4 = 0; k4 < kSK; k4 += 4) {
-                double a[4], b[8];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = Qs[(k4 + fk) * kDPad + wr + 8 * i + fr];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) b[j] = Ks[(k4 + fk) * kDPad + wt + 8 * j + fr];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) dmma884(acc[i][j], a[i], b[j]);
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// The production path (fp16, d = 128) with the reference's arithmetic order:
+// the persistent, cp.async-pipelined staging of probe_tma_kernel with the DFMA
+// register tile of probe_stream_kernel (thread (tx, ty): rows ty + 16 i, tokens
+// tx + 16 j, channels in order c = 0 .. 127, each an exact f32 x f32 product
+// fused into the fp64 sum — bit-identical logits), fp16 operands read 8
+// channels at a time (16-B loads, rows padded to 272 B: the 16 token rows of a
+// load fall in distinct bank quarters) and widened in registers. S3's a-tile
+// goes through shared memory in 32-row slices, summed per token in row order.
+constexpr int kERow = 136;                     // padded row stride (fp16) = 272 B
+constexpr int kEKBuf = kSToks * kERow;
+constexpr int kESlice = 32;                    // S3 a-tile rows per slice
+constexpr int kESmem = (2 * kEKBuf + kTMaxR * kERow) * 2 + kESlice * kSAStride * 8;
+
+template <int PASS>
+__global__ void __launch_bounds__(256, 1) probe_exact_kernel(
+    const __half* __restrict__ k, const __half* __restrict__ q, int units, int t_len, int R, int window,
+    int probe_rows, double inv_sqrt_d, int ntt, int nht, double2* __restrict__ stats,
+    const double2* __restrict__ rowstat, float* __restrict__ rawf) {
+    constexpr int d = kD128;
+    extern __shared__ __align__(16) __half esm[];
+    __half* kbuf = esm;                                // [2][128 tokens][kERow]
+    __half* qbuf = esm + 2 * kEKBuf;                   // [R][kERow]
+    double* at = reinterpret_cast<double*>(qbuf + kTMaxR * kERow);  // [kESlice][kSAStride]
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const long long items = (long long)units * ntt;
+    const long long i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
+    auto load_k = [&](long long it, int buf) {
+        if (it < i1) {
+            const int unit = (int)(it / ntt), tile = (int)(it % ntt);
+            const __half* kb = k + ((size_t)unit * t_len + (size_t)tile * kSToks) * d;
+            __half* dst = kbuf + buf * kEKBuf;
+            for (int e = tid; e < kSToks * (d / 8); e += 256) {
+                const int r = e >> 4, c8 = e & 15;
+                const bool ok = tile * kSToks + r < t_len;
+                cp_async16(dst + r * kERow + 8 * c8, ok ? kb + (size_t)r * d + 8 * c8 : kb, ok);
             }
         }
-        __syncthreads();  // all chunk reads done: the smem may be reused below
-        // fragment (i, j, e): row wr + 8 i + fr, token wt + 8 j + 2 fk + e
-        if (PASS == 0) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int row = rb + wr + 8 * i + fr;
-                const int off = t_len - window + (row % window);  // causal offset (pipeline.cpp:129-130)
-                double m = -INFINITY;
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int t = tok0 + wt + 8 * j + 2 * fk + e;
-                        acc[i][j][e] = __dmul_rn(acc[i][j][e], inv_sqrt_d);
-                        if (row < R && t < t_len && t <= off) m = fmax(m, acc[i][j][e]);
-                    }
-                m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
-                m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
-                double s = 0.0;
-                if (m != -INFINITY) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int t = tok0 + wt + 8 * j + 2 * fk + e;
-                            if (row < R && t < t_len && t <= off) s = __dadd_rn(s, exp(__dadd_rn(acc[i][j][e], -m)));
-                        }
-                }
-                s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 1));
-                s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, 2));
-                if (fk == 0 && row < R) stats[((size_t)unit * R + row) * nht + 2 * tile + (warp & 1)] = make_double2(m, s);
-            }
-        } else {
-            double* at = sm;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int rl = wr + 8 * i + fr, row = rb + rl;
-                const int off = t_len - window + (row % window);
-                const double2 ms = row < R ? rowstat[(size_t)unit * R + row] : make_double2(0.0, 1.0);
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int tl = wt + 8 * j + 2 * fk + e, t = tok0 + tl;
-                        double a = 0.0;  // entries past the causal offset are exactly zero (cache.cpp:181)
-                        if (row < R && t < t_len && t <= off)
-                            a = exp(__dadd_rn(__dmul_rn(acc[i][j][e], inv_sqrt_d), -ms.x)) / ms.y;
-                        at[rl * kSAStride + tl] = a;
-                    }
-            }
-            __syncthreads();
-            if (tid < kSToks) {
-                const int nr = min(kSRows, R - rb);
-                for (int r = 0; r < nr; ++r) colacc = __dadd_rn(colacc, at[r * kSAStride + tid]);
-            }
-            __syncthreads();  // the a-tile aliases the next row block's chunk buffers
+        cp_async_commit();
+    };
+    auto load_q = [&](int unit) {
+        const __half* qb = q + (size_t)unit * (R / window) * probe_rows * d;
+        for (int e = tid; e < R * (d / 8); e += 256) {
+            const int r = e >> 4, c8 = e & 15;
+            const int qi = r / window, w = r - qi * window;
+            cp_async16(qbuf + r * kERow + 8 * c8, qb + ((size_t)qi * probe_rows + probe_rows - window + w) * d + 8 * c8,
+                       true);
         }
+    };
+    int qunit = -1;
+    if (i0 < i1) {
+        qunit = (int)(i0 / ntt);
+        load_q(qunit);
     }
-    if (PASS == 1 && tid < kSToks && tok0 + tid < t_len) rawf[(size_t)unit * t_len + tok0 + tid] = (float)colacc;
+    load_k(i0, 0);
+    load_k(i0 + 1, 1);
+    for (long long it = i0; it < i1; ++it) {
+        const int buf = (int)((it - i0) & 1);
+        const int unit = (int)(it / ntt), tile = (int)(it % ntt);
+        const int tok0 = tile * kSToks;
+        if (unit != qunit) {
+            cp_async_wait<0>();
+            __syncthreads();
+            load_q(unit);
+            cp_async_commit();
+            qunit = unit;
+        }
+        cp_async_wait<1>();
+        __syncthreads();
+        const __half* Ks = kbuf + buf * kEKBuf;
+        double colacc = 0.0;
+        for (int rb = 0; rb < R; rb += kSRows) {
+            double acc[8][8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+            const __half* Qs = qbuf + (size_t)rb * kERow;
+#pragma unroll 1
+            for (int c8 = 0; c8 < d; c8 += 8) {
+                uint4 av[8], bv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const uint4*>(Qs + (ty + 16 * i) * kERow + c8);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) bv[j] = *reinterpret_cast<const uint4*>(Ks + (tx + 16 * j) * kERow + c8);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    double a[8], b[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) a[i] = (double)__half2float(reinterpret_cast<const __half*>(&av[i])[e]);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) b[j] = (double)__half2float(reinterpret_cast<const __half*>(&bv[j])[e]);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+                }
+            }
+            if (PASS == 0) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int row = rb + ty + 16 * i;
+                    const int off = t_len - window + (row % window);  // causal offset (pipeline.cpp:129-130)
+                    double l[8];
+                    double m = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int t = tok0 + tx + 16 * j;
+                        l[j] = __dmul_rn(acc[i][j], inv_sqrt_d);
+                        if (row < R && t < t_len && t <= off) m = fmax(m, l[j]);
+                    }
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    double sm_ = 0.0;
+                    if (m != -INFINITY) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int t = tok0 + tx + 16 * j;
+                            if (row < R && t < t_len && t <= off) sm_ = __dadd_rn(sm_, exp(__dadd_rn(l[j], -m)));
+                        }
+                    }
+#pragma unroll
+                    for (int o = 1; o < 16; o <<= 1) sm_ = __dadd_rn(sm_, __shfl_xor_sync(0xffffffffu, sm_, o));
+                    if (tx == 0 && row < R) {
+                        stats[((size_t)unit * R + row) * nht + 2 * tile] = make_double2(m, sm_);
+                        stats[((size_t)unit * R + row) * nht + 2 * tile + 1] = make_double2(-INFINITY, 0.0);
+                    }
+                }
+            } else {
+                // a = exp(l - M) / denom (cache.cpp:176-180) through 32-row slices of shared memory,
+                // each token's column summed in row order (weights.cpp:36-39)
+#pragma unroll
+                for (int sl = 0; sl < kSRows / kESlice; ++sl) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int rl = ty + 16 * i;  // this thread's rows of slice sl: rl in [32 sl, 32 sl + 32)
+                        if ((rl >> 5) != sl) continue;
+                        const int row = rb + rl;
+                        const int off = t_len - window + (row % window);
+                        const double2 ms = row < R ? rowstat[(size_t)unit * R + row] : make_double2(0.0, 1.0);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int t = tok0 + tx + 16 * j;
+                            double a = 0.0;  // past the causal offset: exactly zero (cache.cpp:181)
+                            if (row < R && t < t_len && t <= off)
+                                a = exp(__dadd_rn(__dmul_rn(acc[i][j], inv_sqrt_d), -ms.x)) / ms.y;
+                            at[(rl & (kESlice - 1)) * kSAStride + tx + 16 * j] = a;
+                        }
+                    }
+                    __syncthreads();
+                    if (tid < kSToks) {
+                        const int nr = min(kESlice, R - rb - kESlice * sl);
+                        for (int r = 0; r < nr; ++r) colacc = __dadd_rn(colacc, at[r * kSAStride + tid]);
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+        if (PASS == 1 && tid < kSToks && tok0 + tid < t_len) rawf[(size_t)unit * t_len + tok0 + tid] = (float)colacc;
+        __syncthreads();
+        load_k(it + 2, buf);
+    }
+    cp_async_wait<0>();
 }
 
 // S2: per (unit, row) global max and softmax denominator from the tile stats,
@@ -592,15 +640,32 @@ static int run_weights_stream(const T* k, const T* q, const rdkv_shape* s, int w
     const int ntt = (t_len + kSToks - 1) / kSToks;
     static std::atomic<int> smem0[kMaxDevices], smem1[kMaxDevices];
     const int dev = dev_attrs().dev;
-    set_smem_once(probe_dmma_kernel<T, 0>, kDSmem, smem0, dev);
-    set_smem_once(probe_dmma_kernel<T, 1>, kDSmem, smem1, dev);
     const dim3 grid(ntt, U);
     const int nht = 2 * ntt;  // stats per 64-token half tile
-    probe_dmma_kernel<T, 0><<<grid, 256, kDSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, nht,
-                                                        ws.stats, nullptr, nullptr);
-    probe_rowstat_kernel<<<(U * R * 32 + 255) / 256, 256, 0, st>>>(ws.stats, U * R, nht, ws.rowstat);
-    probe_dmma_kernel<T, 1><<<grid, 256, kDSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, nht,
-                                                        nullptr, ws.rowstat, ws.rawf);
+    if (std::is_same<T, __half>::value && d == kD128 && R <= kTMaxR) {
+        static std::atomic<int> tsm0[kMaxDevices], tsm1[kMaxDevices];
+        set_smem_once(probe_exact_kernel<0>, kESmem, tsm0, dev);
+        set_smem_once(probe_exact_kernel<1>, kESmem, tsm1, dev);
+        const long long items = (long long)U * ntt;
+        const int g = (int)(items < dev_attrs().nsm ? items : dev_attrs().nsm);
+        const __half* kh = reinterpret_cast<const __half*>(k);
+        const __half* qh = reinterpret_cast<const __half*>(q);
+        probe_exact_kernel<0><<<g, 256, kESmem, st>>>(kh, qh, U, t_len, R, window, s->probe_rows, inv_sqrt_d, ntt,
+                                                      nht, ws.stats, nullptr, nullptr);
+        probe_rowstat_kernel<<<(U * R * 32 + 255) / 256, 256, 0, st>>>(ws.stats, U * R, nht, ws.rowstat);
+        probe_exact_kernel<1><<<g, 256, kESmem, st>>>(kh, qh, U, t_len, R, window, s->probe_rows, inv_sqrt_d, ntt,
+                                                      nht, nullptr, ws.rowstat, ws.rawf);
+    } else {
+        // f32 inputs (the reference-shaped drop-in path) and other shapes: the DFMA tile
+        // GEMM, whose dots keep the reference's sequential fp64 order (bit-identical logits)
+        set_smem_once(probe_stream_kernel<T, 0>, kSSmem, smem0, dev);
+        set_smem_once(probe_stream_kernel<T, 1>, kSSmem, smem1, dev);
+        probe_stream_kernel<T, 0><<<grid, 256, kSSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, nht,
+                                                              ws.stats, nullptr, nullptr);
+        probe_rowstat_kernel<<<(U * R * 32 + 255) / 256, 256, 0, st>>>(ws.stats, U * R, nht, ws.rowstat);
+        probe_stream_kernel<T, 1><<<grid, 256, kSSmem, st>>>(k, q, t_len, d, R, window, s->probe_rows, inv_sqrt_d, nht,
+                                                              nullptr, ws.rowstat, ws.rawf);
+    }
     const size_t nt = (size_t)U * t_len;
     token_pool_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(ws.rawf, U, t_len, pool_kernel, w_t);
     const int nch = (t_len + kCNChunk - 1) / kCNChunk;
