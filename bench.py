@@ -415,13 +415,26 @@ def secondary_configs(P, spec0, model, q, args):
     kv = [P.generate((U, d), torch.float16, seed=900 + i, tensor=1) for i in range(nsteps)]
     qs = [P.generate(tuple(q.shape), torch.float16, seed=700 + i, tensor=2) for i in range(nsteps)]
     o = torch.empty_like(q)
+    # token step i decodes rotation copy i % n of the packed arena (>= 3x L2 in total), all
+    # copies sharing the one Zone C that the loop appends to: the packed tiles stream from HBM
+    l2 = torch.cuda.get_device_properties(torch.cuda.current_device()).L2_cache_size
+    n_rot = max(2, -(-3 * l2 // model.arena_bytes))
+    views = [model]
+    for r in range(1, n_rot):
+        mr = P.PackedModel(model.arena.clone(), model.offsets, model.offsets_host, U, model.group, d,
+                           model.zc_k, model.zc_v, model.zc_len, model.zc_cap, 0)
+        mr.share_plan(model)
+        views.append(mr)
 
     def loop():
         model.zc_len.zero_()
-        model.zc_count = 0  # host mirror of the reset (append_new_token checks capacity)
+        for mv in views:
+            mv.zc_count = 0  # host mirror of the reset (append_new_token checks capacity)
         for i in range(nsteps):
             P.append_new_token(model, kv[i], kv[i])
-            P.packed_decode_step(model, qs[i], o)
+            mv = views[i % n_rot]
+            mv.zc_count = model.zc_count
+            P.packed_decode_step(mv, qs[i], o)
 
     side = torch.cuda.Stream()
     side.wait_stream(torch.cuda.current_stream())
@@ -443,9 +456,15 @@ def secondary_configs(P, spec0, model, q, args):
         e1.record(side)
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / (reps * nsteps) * 1e3
+    byts_loop = model.survey_bytes(io_bytes=2) + U * (nsteps + 1) / 2 * d * 2 * 2  # mean Zone C rows per step
+    step_ms = getattr(args, "_step_ms", None)  # the headline (no Zone C) step of this run
     out["decode_loop_16"] = {"config": "16 generated tokens: append (Zone C) + decode per step, one CUDA graph; "
-                                       "Zone C grows 1..16 rows per tile (L2-warm: the step re-reads one arena)",
-                             "us_per_token_step": us, "tok_s": spec0.batch / (us / 1e6)}
+                                       f"Zone C grows 1..16 rows per tile; step i reads rotation copy i % {n_rot} "
+                                       "of the arena (L2 cold for the packed tiles)",
+                             "us_per_token_step": us, "tok_s": spec0.batch / (us / 1e6),
+                             "vs_no_zone_c_step": us / (step_ms * 1e3) if step_ms else None,
+                             "roofline_frac": byts_loop / (us / 1e6) / 1e9 / peak}
+    del views
     model.zc_cap, model.zc_k, model.zc_v, model.zc_len = 0, None, None, None
     # (3) batch sweep (configs[2] is "batch 1-16"): the first b sequences of the
     # packed arena (a prefix of the units), same timing method
@@ -740,6 +759,7 @@ def main():
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"error": f"{type(e).__name__}: {str(e)[:300]}"}
     if rank == 0 and world == 1 and not args.no_secondary:
+        args._step_ms = ms
         try:
             line["secondary"] = secondary_configs(P, spec, model, q, args)
         except Exception as e:  # noqa: BLE001

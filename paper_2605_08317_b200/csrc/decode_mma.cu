@@ -1481,20 +1481,21 @@ struct U2xRun {
     float2 o[4];                 // running unnormalised outputs (channels ch0 + 4m, + 1)
 };
 
-// ZCF (short tiles with a few Zone C rows, <= kZcFused): the tile's Zone C K / V
+// ZCN > 0 (short tiles with a few Zone C rows, <= ZCN = 4 or 16): the tile's Zone C K / V
 // rows are staged in its own buffer (zk / zv) and folded in after PV: QK on an
 // fp16 m16n8k16 MMA (rows = the z tokens), PV on CUDA cores in the lanes'
 // output mapping, one shared softmax.
-constexpr int kZcFused = 4;
+constexpr int kZcFused = 4;      // fused rows of the default short-tile Zone C variant
+constexpr int kZcFusedMax = 16;  // ... and of the long-generation variant (more smem per buffer)
 constexpr int kZcKStride = 272;                        // padded K-row stride: conflict-free ldmatrix
-constexpr int kZcStage = kZcFused * (kZcKStride + 256);  // fused Zone C staging bytes (K rows + V rows)
+__host__ __device__ constexpr int zc_stage(int rows) { return rows * (kZcKStride + 256); }  // K + V rows staged
 // MIX ("mostly 2-bit" tiles, heavy-hitter caches): besides the 2-bit V rows
 // and K channels, up to 32 K channels at 4 bits (one extra QK k-step, class-1
 // digit block 4) and up to 8 V rows at 4 bits (their logits come from QK like
 // any slot; their PV terms are added on CUDA cores after the 2-bit PV, whose
 // p~ digits for those slots are zero).
 constexpr int kMixMaxRows = 16;  // 4-bit V rows per MIX tile (the pt1 weight table)
-template <typename IO, int NBMAX, bool FULLK, bool BULK, bool CHUNKED = false, bool ZCF = false, bool MIX = false,
+template <typename IO, int NBMAX, bool FULLK, bool BULK, bool CHUNKED = false, int ZCN = 0, bool MIX = false,
           typename AfterSync1>
 __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, const uint8_t* __restrict__ qs, int g,
                                                 uint8_t* __restrict__ scr, IO* __restrict__ out, int bar,
@@ -1878,7 +1879,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                 }
             }
         }
-        if (ZCF && z > 0) {
+        if (ZCN > 0 && z > 0) {
             // QK: A rows = Zone C tokens (rows >= z read neighbouring bytes, masked
             // below), B columns 2h / 2h + 1 = hi / lo fp16 parts of q_h
             float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -1908,20 +1909,22 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                 hmma16816(c, a, bw[0], bw[1]);
             }
             constexpr float kZScale = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(d)
-            float l = (c[0] + c[1]) * kZScale;  // token gid, head tig
-            if (!hv || gid >= z) l = -INFINITY;
-            float mz = l;
+            float l0 = (c[0] + c[1]) * kZScale;  // token gid, head tig
+            float l1 = (c[2] + c[3]) * kZScale;  // token gid + 8 (ZCN > 8)
+            if (!hv || gid >= z) l0 = -INFINITY;
+            if (ZCN <= 8 || !hv || gid + 8 >= z) l1 = -INFINITY;
+            float mz = fmaxf(l0, l1);
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) mz = fmaxf(mz, __shfl_xor_sync(0xffffffffu, mz, o));
             if (mz == -INFINITY) mz = 0.0f;
-            const float pz = ex2_approx(l - mz);
-            lz = pz;
+            const float pz0 = ex2_approx(l0 - mz), pz1 = ZCN > 8 ? ex2_approx(l1 - mz) : 0.0f;
+            lz = pz0 + pz1;
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) lz += __shfl_xor_sync(0xffffffffu, lz, o);
             // PV: this lane's output channels ch0 + 4m, + 1 of head tig
 #pragma unroll
-            for (int tk = 0; tk < kZcFused; ++tk) {
-                const float pt = __shfl_sync(0xffffffffu, pz, 4 * tk + tig);
+            for (int tk = 0; tk < ZCN; ++tk) {
+                const float pt = __shfl_sync(0xffffffffu, tk < 8 ? pz0 : pz1, 4 * (tk & 7) + tig);
                 if (tk < z) {
                     const float2 ptt = make_float2(pt, pt);
 #pragma unroll
@@ -1945,7 +1948,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                 const float2 v =
                     make_float2((float)(acc[m][0] * 256 + acc[m][1]), (float)(acc[m][2] * 256 + acc[m][3]));
                 float2 r = ffma2(v, sc, bb);
-                if (ZCF) r = ffma2(oz[m], zz, r);
+                if (ZCN > 0) r = ffma2(oz[m], zz, r);
                 if (MIX) r = ffma2(o4[m], ww, r);
                 if constexpr (sizeof(IO) == 2)
                     *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
@@ -1979,7 +1982,7 @@ constexpr int kXMaxBuf = 4;  // tile buffers per pair
 // (no math), 2 math only (tiles past the first buffers are not reloaded).
 // PERCTA: one pair per CTA (a compile-time barrier id, so a CTA reserves 2
 // hardware barriers instead of 16 and 8 CTAs fit on an SM).
-template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false, bool ZCF = false,
+template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false, int ZCN = 0,
           bool G8 = false, bool MIX = false>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
     extern __shared__ __align__(128) uint8_t dsm[];
@@ -2018,7 +2021,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         return m;
     };
     // A tile arrives in two parts on its buffer's mbarrier: the KV copy (tx only,
-    // may run before the grid dependency), then q (+ ZCF: the tile's Zone C
+    // may run before the grid dependency), then q (+ ZCN > 0: the tile's Zone C
     // rows) with the arrive — so the phase cannot complete early.
     auto issue_kv = [&](const Meta& m, int b) {
         fence_proxy_async();
@@ -2030,19 +2033,19 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
         mbar_expect_tx(&fb[b], (uint32_t)(qbytes + 2 * 256 * zrows));
         bulk_g2s(dst + qoff, static_cast<const uint8_t*>(p.q) + (size_t)tile * qbytes, (uint32_t)qbytes, &fb[b]);
-        if (ZCF && zrows > 0) {
+        if (ZCN > 0 && zrows > 0) {
             const size_t row0 = (size_t)tile * p.zc_cap;
             for (int r = 0; r < zrows; ++r)  // K rows at a padded stride
-                bulk_g2s(dst + qoff - kZcStage + r * kZcKStride,
+                bulk_g2s(dst + qoff - zc_stage(ZCN) + r * kZcKStride,
                          reinterpret_cast<const uint8_t*>(p.zc_k + (row0 + r) * kD), 256u, &fb[b]);
-            bulk_g2s(dst + qoff - kZcFused * 256, reinterpret_cast<const uint8_t*>(p.zc_v + row0 * kD),
+            bulk_g2s(dst + qoff - ZCN * 256, reinterpret_cast<const uint8_t*>(p.zc_v + row0 * kD),
                      (uint32_t)(zrows * 256), &fb[b]);
         }
     };
     // Zone C rows of a tile (written by the previous kernel: after griddepcontrol.wait only)
     auto zrows_of = [&](int k) {
         const int tile = tile0 + k * tstride;
-        return (ZCF && tile < p.units) ? min(p.zc_len[unit_of(p, tile)], kZcFused) : 0;
+        return (ZCN > 0 && tile < p.units) ? min(p.zc_len[unit_of(p, tile)], ZCN) : 0;
     };
     // Programmatic dependent launch: this grid may start while the previous
     // kernel on the stream drains. The packed KV tiles are immutable during
@@ -2071,7 +2074,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         if (tile0 < p.units) issue_q(0, 0, zrows_of(0));
         next_z = zrows_of(nbuf);
     }
-    if (ZCF && half == 1 && lane == 0)
+    if (ZCN > 0 && half == 1 && lane == 0)
         for (int j = 1; j < kXMaxBuf; ++j) ahead_z[j - 1] = j < nbuf ? zrows_of(j) : 0;
     const U2xLane lc = u2x_lane(half);
     // the q~ digit rows of d3 (never written: |N| < 2^22) must read as zero
@@ -2120,9 +2123,9 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
                 auto rf = [&]() {
                     if (hp == 0) refill();
                 };
-                decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCF, MIX>(
+                decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCN, MIX>(
                     st, st + qoff + 4 * hp * QROW, G8 ? min(4, p.g - 4 * hp) : p.g, scr, o + 4 * hp * kD,
-                    PERCTA ? 1 : 1 + pr, lc, rf, nullptr, nullptr, zl, st + qoff - kZcStage, st + qoff - kZcFused * 256);
+                    PERCTA ? 1 : 1 + pr, lc, rf, nullptr, nullptr, zl, st + qoff - zc_stage(ZCN), st + qoff - ZCN * 256);
             }
         }
         if (++b == nbuf) {
@@ -2572,7 +2575,7 @@ static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st, float* partial
 
 // Zone C small enough to stage with each short tile (host-known bound)
 static bool zc_fusable(const rdkv_decode_args* a) {
-    return a->zc_len && (a->flags & RDKV_DECODE_ZC_BOUND) && a->zc_bound <= kZcFused;
+    return a->zc_len && (a->flags & RDKV_DECODE_ZC_BOUND) && a->zc_bound <= kZcFusedMax;
 }
 // groups of 5..8 heads run as two 4-head passes in the short-tile kernel only
 // (the chunked kernel's running softmax state is per 4-head lane group)
@@ -2587,7 +2590,8 @@ template <typename IO, int NBMAX, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_blocks = 0) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
     const bool zcf = zc_fusable(a);
-    const int slot = (a->plan.max_decode_bytes + (zcf ? kZcStage : 0) + qbytes + 127) & ~127;
+    const bool zc16 = zcf && a->zc_bound > kZcFused;  // the long-generation variant (16 fused rows)
+    const int slot = (a->plan.max_decode_bytes + (zcf ? zc_stage(zc16 ? kZcFusedMax : kZcFused) : 0) + qbytes + 127) & ~127;
     const bool mix = a->plan.uniform2 == 3;  // some tiles carry a few 4-bit rows / channels
     const int scratch = (kXPDig + (mix ? 512 + kMixMaxRows * 16 : 0) + NBMAX * 256 + 127) & ~127;
     const DevAttrs da = dev_attrs();
@@ -2608,26 +2612,32 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
     const int mode = nenv ? atoi(nenv) : 0;
     const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
     const bool g8 = a->group > 4;
-    auto kern = mix ? (g8 ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, false, true, true>
-                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, false, true, true>)
-                          : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, false, false, true>
-                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, false, false, true>))
-              : g8 ? (zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true, true>
-                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, true, true>)
-                          : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, false, true>
-                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, false, true>))
-              : zcf ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, true>
-                            : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, true>)
+    auto kern = mix ? (g8 ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, 0, true, true>
+                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, 0, true, true>)
+                          : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, 0, false, true>
+                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, 0, false, true>))
+              : g8 ? (zcf ? (zc16 ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, kZcFusedMax, true>
+                                          : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, kZcFusedMax, true>)
+                                  : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, kZcFused, true>
+                                          : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, kZcFused, true>))
+                          : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, 0, true>
+                                  : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, 0, true>))
+              : zcf ? (zc16 ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, kZcFusedMax>
+                                    : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, kZcFusedMax>)
+                            : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, kZcFused>
+                                    : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, kZcFused>))
               : bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true>
 #ifdef RDKV_DECODE_EXPERIMENTS
               : mode == 1 ? decode_u2x_kernel<IO, NBMAX, FULLK, 1>
               : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2>
 #endif
                           : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
-    static std::atomic<int> smem_set[14][kMaxDevices];  // one slot per instantiation above
+    static std::atomic<int> smem_set[18][kMaxDevices];  // one slot per instantiation above
     set_smem_once(kern, (int)smem,
-                  smem_set[mix ? 10 + (g8 ? 2 : 0) + (bulk ? 1 : 0) : g8 ? 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0)
-                              : zcf ? 4 + (bulk ? 1 : 0) : bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0],
+                  smem_set[mix ? 10 + (g8 ? 2 : 0) + (bulk ? 1 : 0)
+                           : g8 ? (zc16 ? 14 + (bulk ? 1 : 0) : 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0))
+                           : zcf ? (zc16 ? 16 + (bulk ? 1 : 0) : 4 + (bulk ? 1 : 0))
+                           : bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0],
                   da.dev);
     int blocks = (a->units + W - 1) / W;
     if (blocks > nsm) blocks = nsm;

@@ -297,12 +297,13 @@ def test_mma_uniform_two_bit_long_tiles(cuda, orc, g, fullk, io):
 
 @pytest.mark.parametrize("n_max,appends,io", [(150, 1, torch.float16), (150, 17, torch.float32), (600, 40, torch.float16),
                                               (130, 5, torch.float32), (128, 3, torch.float32), (160, 4, torch.float16),
-                                              (600, 2, torch.float32)])
+                                              (600, 2, torch.float32), (132, 9, torch.float16), (160, 16, torch.float32),
+                                              (128, 12, torch.float16)])
 def test_mma_uniform_two_bit_zone_c(cuda, orc, n_max, appends, io):
     """Zone C (appended fp16 K/V rows) on the uniform-2-bit fast path: up to 4
-    rows staged with each short tile (fused), more as 16-token fp16
-    tensor-core chunks folded into the online softmax, after short or chunked
-    long packed tiles."""
+    (or, in the long-generation variant, 16) rows staged with each short tile
+    (fused), more as 16-token fp16 tensor-core chunks folded into the online
+    softmax, after short or chunked long packed tiles."""
     rng = np.random.default_rng(80 + appends)
     cases = []
     for n in (3, 64, 100, n_max):
