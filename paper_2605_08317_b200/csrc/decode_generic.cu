@@ -329,6 +329,40 @@ __global__ void append_kernel(__half* __restrict__ zc_k, __half* __restrict__ zc
     if (threadIdx.x == 0) zc_len[unit] = pos + 1;
 }
 
+// d % 8 == 0: one warp per unit, 8 channels (16 B of fp16) per lane and row —
+// a 4096-unit step's append is one short launch instead of 4096 CTAs.
+template <typename T>
+__global__ void __launch_bounds__(256) append_vec_kernel(__half* __restrict__ zc_k, __half* __restrict__ zc_v,
+                                                         int32_t* __restrict__ zc_len, int zc_cap, int units,
+                                                         const T* __restrict__ k_new, const T* __restrict__ v_new,
+                                                         int d) {
+    const int unit = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (unit >= units) return;
+    const int pos = zc_len[unit];
+    if (pos >= zc_cap) return;  // caller checks capacity
+    const size_t src = (size_t)unit * d, dst = ((size_t)unit * zc_cap + pos) * d;
+    for (int c = 8 * lane; c < d; c += 256) {
+        uint4 kk, vv;
+        if constexpr (sizeof(T) == 2) {
+            kk = *reinterpret_cast<const uint4*>(k_new + src + c);
+            vv = *reinterpret_cast<const uint4*>(v_new + src + c);
+        } else {
+            __half2 kh[4], vh[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                kh[j] = __floats2half2_rn(load_as_float(k_new, src + c + 2 * j), load_as_float(k_new, src + c + 2 * j + 1));
+                vh[j] = __floats2half2_rn(load_as_float(v_new, src + c + 2 * j), load_as_float(v_new, src + c + 2 * j + 1));
+            }
+            kk = *reinterpret_cast<const uint4*>(kh);
+            vv = *reinterpret_cast<const uint4*>(vh);
+        }
+        *reinterpret_cast<uint4*>(zc_k + dst + c) = kk;
+        *reinterpret_cast<uint4*>(zc_v + dst + c) = vv;
+    }
+    __syncwarp();
+    if (lane == 0) zc_len[unit] = pos + 1;
+}
+
 size_t generic_smem_bytes(int g, int d, int kslots) {
     return sizeof(float) * ((size_t)((g * d + 3) & ~3) + (size_t)((g + 3) & ~3) * kslots + (size_t)g * kGenChunk);
 }
@@ -371,6 +405,23 @@ extern "C" RDKV_API int rdkv_cuda_append(void* zc_k, void* zc_v, int32_t* zc_len
     if (!zc_k || !zc_v || !zc_len || !k_new || !v_new || units < 1 || head_dim < 1 || zc_cap < 1)
         return RDKV_EINVAL;
     auto st = static_cast<cudaStream_t>(stream);
+    const bool vec = head_dim % 8 == 0 && (reinterpret_cast<uintptr_t>(k_new) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(v_new) & 15) == 0 && (reinterpret_cast<uintptr_t>(zc_k) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(zc_v) & 15) == 0;
+    if (vec) {
+        const unsigned blocks = (unsigned)(((size_t)units * 32 + 255) / 256);
+        if (dtype == RDKV_F32)
+            append_vec_kernel<float><<<blocks, 256, 0, st>>>(static_cast<__half*>(zc_k), static_cast<__half*>(zc_v), zc_len,
+                                                             zc_cap, units, static_cast<const float*>(k_new),
+                                                             static_cast<const float*>(v_new), head_dim);
+        else if (dtype == RDKV_F16)
+            append_vec_kernel<__half><<<blocks, 256, 0, st>>>(static_cast<__half*>(zc_k), static_cast<__half*>(zc_v),
+                                                              zc_len, zc_cap, units, static_cast<const __half*>(k_new),
+                                                              static_cast<const __half*>(v_new), head_dim);
+        else
+            return RDKV_EINVAL;
+        return launch_status();
+    }
     if (dtype == RDKV_F32)
         append_kernel<float><<<units, 128, 0, st>>>(static_cast<__half*>(zc_k), static_cast<__half*>(zc_v),
                                                     zc_len, zc_cap, static_cast<const float*>(k_new),

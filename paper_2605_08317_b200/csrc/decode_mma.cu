@@ -3555,8 +3555,11 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
     const rdkv_decode_plan& pl = a->plan;
     // mixed 2/4/8-bit tiles (not all short enough for MIX), and uniform 2-bit tiles too
     // long for the short-tile kernel: the chunked split-K kernel (no Zone C; kernel 0 or 2)
+    // (long uniform-2-bit tiles stay on the chunked u2x body when there are enough of them to
+    // fill every warp pair — split-K only pays for few tiles: budget_512, 4096 tiles: 54 vs 71 us)
     const bool short_u2x = pl.uniform2 && pl.max_slots <= kU2MaxSlots;
-    if (pl.mix24 && !short_u2x && !a->zc_len && a->group <= 8 && (a->kernel == 0 || a->kernel == 2)) {
+    const bool many_u2 = pl.uniform2 && u2x_group_ok(a) && a->units >= kXPairs * dev_attrs().nsm;
+    if (pl.mix24 && !short_u2x && !many_u2 && !a->zc_len && a->group <= 8 && (a->kernel == 0 || a->kernel == 2)) {
         rdkv_decode_args b = *a;
         b.unit_ids = nullptr;
         return f16 ? launch_u24<__half>(&b, st) : launch_u24<float>(&b, st);
