@@ -505,3 +505,29 @@ def test_mix_mostly_two_bit_tiles(cuda, orc, g, io):
     worst, model = _run_batch(cuda, orc, cases, g, io=io, tol=U2X_TOL)
     assert model.plan.uniform2 == 3, model.plan.uniform2
     assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
+
+
+@pytest.mark.parametrize("g,T,io,nkept", [(4, 700, torch.float32, 300), (7, 2000, torch.float16, 1500),
+                                          (4, 3000, torch.float16, 2600), (8, 400, torch.float32, 90)])
+def test_mixed_248_split_k_kernel(cuda, orc, g, T, io, nkept):
+    """Every class the chunked split-K kernel (decode_u24) handles — V rows and K channels
+    at 2, 4 and 8 bits (no Zone B / k16), short and long tiles, GQA 4 / 7 / 8 — against
+    the oracle, with and without the split-K partials workspace."""
+    rng = np.random.default_rng(300 + g + T)
+    cases = []
+    for i in range(6):
+        k, v, vb, kb, q = _random_case(rng, T, g)
+        vb[:] = 0
+        kept = np.sort(rng.choice(T, nkept - 37 * i, replace=False))
+        vb[kept] = rng.choice([2, 4, 8], kept.size, p=[0.6, 0.3, 0.1])
+        kb[:] = rng.choice([0, 2, 4, 8], D, p=[0.05, 0.55, 0.3, 0.1])
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, g, io=io, rng=rng, tol=U2X_TOL)
+    assert model.plan.mix24 and not model.plan.uniform2
+    assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
+    qd = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).to(io)
+    split = P.packed_decode_step(model, qd).float()
+    ws, model.split_ws = model.split_ws, None
+    whole = P.packed_decode_step(model, qd).float()
+    model.split_ws = ws
+    assert float(((split - whole).norm() / whole.norm()).item()) < 1e-3
