@@ -518,7 +518,7 @@ def test_mixed_248_split_k_kernel(cuda, orc, g, T, io, nkept):
     for i in range(6):
         k, v, vb, kb, q = _random_case(rng, T, g)
         vb[:] = 0
-        kept = np.sort(rng.choice(T, nkept - 37 * i, replace=False))
+        kept = np.sort(rng.choice(T, max(8, nkept - (nkept // 8) * i), replace=False))
         vb[kept] = rng.choice([2, 4, 8], kept.size, p=[0.6, 0.3, 0.1])
         kb[:] = rng.choice([0, 2, 4, 8], D, p=[0.05, 0.55, 0.3, 0.1])
         cases.append((k, v, vb, kb, q))
