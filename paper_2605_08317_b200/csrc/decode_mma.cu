@@ -3028,7 +3028,6 @@ __device__ __forceinline__ void decode_chunk_u24(const uint8_t* __restrict__ t, 
         for (int jw = half; jw < nw; jw += 2) {
             const bool b4 = jw < n4;
             const int j = L.lane >> 2;
-            const int cls = b4 ? 1 : 2;
             const int sbase = b4 ? h.kslot_base[1] + 32 * jw : h.kslot_base[2] + 32 * (jw - n4);
             const int cnt = b4 ? h.c[1] - 32 * jw : h.c[2] - 32 * (jw - n4);  // valid slots of this k-step
             uint32_t x1[4];
@@ -3043,7 +3042,6 @@ __device__ __forceinline__ void decode_chunk_u24(const uint8_t* __restrict__ t, 
                 const float y = fmaf(cs.x * qv, sg * pre, kMagicS);
                 x1[e] = (__float_as_uint(y) + (0x00808080u - 0x4B400000u)) ^ 0x00808080u;
             }
-            (void)cls;
             const uint32_t a01 = __byte_perm(x1[0], x1[1], 0x5140), b01 = __byte_perm(x1[0], x1[1], 0x7362);
             const uint32_t a23 = __byte_perm(x1[2], x1[3], 0x5140), b23 = __byte_perm(x1[2], x1[3], 0x7362);
             uint8_t* w1p = qdig + (n2 + jw) * 512 + 4 * (j & 3);
