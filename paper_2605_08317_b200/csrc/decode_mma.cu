@@ -3607,7 +3607,16 @@ int launch_mma(const rdkv_decode_args* a, cudaStream_t st) {
 
 }  // namespace rdkv_b200
 
-// Scans every tile header once (one small D2H copy per tile) and writes the
+// the 128-B header of every tile, gathered for one D2H copy
+__global__ void gather_headers_kernel(const uint8_t* __restrict__ arena, const int64_t* __restrict__ offs, int units,
+                                      uint4* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= units * (kHeaderBytes / 16)) return;
+    const int u = i / (kHeaderBytes / 16), j = i % (kHeaderBytes / 16);
+    out[i] = reinterpret_cast<const uint4*>(arena + offs[u])[j];
+}
+
+// Scans every tile header once (one device gather + one D2H copy) and writes the
 // per-tile decode sizes the persistent kernel stages with cp.async.bulk, plus
 // the maxima that select the kernel variant and size its smem ring.
 static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets_host, int32_t units,
@@ -3636,9 +3645,38 @@ static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets
     TileHeader* hdrs = static_cast<TileHeader*>(malloc(sizeof(TileHeader) * (size_t)units));
     int32_t* ds = static_cast<int32_t*>(malloc(sizeof(int32_t) * (size_t)units));
     int rc = RDKV_OK;
+    // offsets come from rdkv_cuda_pack_plan (128-B aligned, any unit order); the gather reads
+    // device memory at them, so reject malformed ones before launching it
     for (int u = 0; u < units; ++u)
-        cudaMemcpyAsync(&hdrs[u], arena + tile_offsets_host[u], sizeof(TileHeader), cudaMemcpyDeviceToHost, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess) rc = RDKV_ECUDA;
+        if (tile_offsets_host[u] < 0 || (tile_offsets_host[u] & (kTileAlign - 1))) {
+            free(hdrs);
+            free(ds);
+            return RDKV_EINVAL;
+        }
+    if (units <= 64) {  // a few tiles: one small copy each
+        for (int u = 0; u < units; ++u)
+            cudaMemcpyAsync(&hdrs[u], arena + tile_offsets_host[u], sizeof(TileHeader), cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) rc = RDKV_ECUDA;
+    } else {  // every tile header in one device gather and one D2H copy (not one copy per tile)
+        int64_t* d_offs = nullptr;
+        uint4* d_hdrs = nullptr;
+        if (cudaMallocAsync(&d_offs, sizeof(int64_t) * (size_t)units, st) != cudaSuccess ||
+            cudaMallocAsync(&d_hdrs, sizeof(TileHeader) * (size_t)units, st) != cudaSuccess ||
+            cudaMemcpyAsync(d_offs, tile_offsets_host, sizeof(int64_t) * (size_t)units, cudaMemcpyHostToDevice, st) !=
+                cudaSuccess) {
+            rc = RDKV_ECUDA;
+        } else {
+            const int pieces = units * (kHeaderBytes / 16);
+            gather_headers_kernel<<<(pieces + 255) / 256, 256, 0, st>>>(arena, d_offs, units, d_hdrs);
+            if (cudaGetLastError() != cudaSuccess ||
+                cudaMemcpyAsync(hdrs, d_hdrs, sizeof(TileHeader) * (size_t)units, cudaMemcpyDeviceToHost, st) !=
+                    cudaSuccess)
+                rc = RDKV_ECUDA;
+        }
+        if (d_offs) cudaFreeAsync(d_offs, st);
+        if (d_hdrs) cudaFreeAsync(d_hdrs, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) rc = RDKV_ECUDA;
+    }
     rdkv_decode_plan p{0, 0, 0, 0, 2, 0, 2, 1, 1 << 30, 0};
     int32_t* ids = unit_ids_dev ? static_cast<int32_t*>(malloc(sizeof(int32_t) * (size_t)units)) : nullptr;
     int nmixed = 0, n_u = 0, n_m = 0;

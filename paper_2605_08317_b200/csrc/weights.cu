@@ -420,14 +420,16 @@ __global__ void __launch_bounds__(256, 1) probe_exact_kernel(
         const int buf = (int)((it - i0) & 1);
         const int unit = (int)(it / ntt), tile = (int)(it % ntt);
         const int tok0 = tile * kSToks;
-        if (unit != qunit) {
+        if (unit != qunit) {  // the unit's probe rows replace the previous unit's
             cp_async_wait<0>();
-            __syncthreads();
+            __syncthreads();  // every thread is past its reads of the old rows
             load_q(unit);
             cp_async_commit();
+            cp_async_wait<0>();  // the new rows (and the K tiles in flight) have landed
             qunit = unit;
+        } else {
+            cp_async_wait<1>();  // K(it) has landed; K(it + 1) may still be in flight
         }
-        cp_async_wait<1>();
         __syncthreads();
         const __half* Ks = kbuf + buf * kEKBuf;
         double colacc = 0.0;

@@ -210,3 +210,20 @@ def test_streaming_weights_match_reference_long(cuda, ref):
             exact += int(np.sum(got == exp))
             total += got.size
     assert exact / total > 0.99, exact / total
+
+
+def test_weights_unit_boundaries_bit_identical(cuda):
+    """The persistent probe kernel walks (unit, token tile) ranges that cross units
+    inside a CTA (the unit's probe rows are swapped in shared memory there): the
+    weights of every unit must equal those of the unit computed alone, bit for bit,
+    and two runs must agree."""
+    spec = WorkloadSpec(batch=1, layers=1, ctx=12288, n_tokens=128, seed=9, hh_stride=64, hh_boost=1.0)
+    (kd, vd, qd), _ = _slice(spec)
+    H, Sw = spec.kv_heads, spec.probe_rows
+    w_t, w_c = P.compute_weights(kd, qd, window=Sw, pool_kernel=5, kv_heads=H)
+    w_t2, w_c2 = P.compute_weights(kd, qd, window=Sw, pool_kernel=5, kv_heads=H)
+    assert torch.equal(w_t, w_t2) and torch.equal(w_c, w_c2)
+    for h in range(H):
+        a_t, a_c = P.compute_weights(kd[h:h + 1].contiguous(), qd[h:h + 1].contiguous(), window=Sw, pool_kernel=5,
+                                     kv_heads=H)
+        assert torch.equal(a_t[0], w_t[h]) and torch.equal(a_c[0], w_c[h]), h
