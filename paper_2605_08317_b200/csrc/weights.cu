@@ -26,6 +26,7 @@
 //   W5 channel_norms  one thread per (unit, channel): sequential fp64 norms
 // This file is compiled with -fmad=false; the only fused multiply-adds are
 // the explicit __fma_rn calls in W1/W5, which are exact-equivalent there.
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -365,25 +366,28 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // the persistent, cp.async-pipelined staging of probe_tma_kernel with the DFMA
 // register tile of probe_stream_kernel (thread (tx, ty): rows ty + 16 i, tokens
 // tx + 16 j, channels in order c = 0 .. 127, each an exact f32 x f32 product
-// fused into the fp64 sum — bit-identical logits), fp16 operands read 8
-// channels at a time (16-B loads, rows padded to 272 B: the 16 token rows of a
-// load fall in distinct bank quarters) and widened in registers. S3's a-tile
-// goes through shared memory in 32-row slices, summed per token in row order.
+// fused into the fp64 sum — bit-identical logits). Every 32-channel chunk of
+// the 128 probe rows and the 128-token K tile is widened to fp64 in shared
+// memory once per CTA (rows padded to 272 B: a thread's two-channel 16-B loads
+// are broadcast / conflict-free), so the fp64 pipe runs DFMAs, not one
+// conversion per operand use (each value feeds 16 threads). This is S1:
+// besides the half-tile (max, sum exp) stats it stores the logits [U][R][T] so
+// S3 (probe_colsum_kernel) reads them back instead of running the GEMM again.
 constexpr int kERow = 136;                     // padded row stride (fp16) = 272 B
 constexpr int kEKBuf = kSToks * kERow;
-constexpr int kESlice = 32;                    // S3 a-tile rows per slice
-constexpr int kESmem = (2 * kEKBuf + kTMaxR * kERow) * 2 + kESlice * kSAStride * 8;
+constexpr int kEChunk = 32;                    // channels widened to fp64 per step
+constexpr int kDRow = kEChunk + 2;             // fp64 row stride of a widened chunk (272 B: conflict-free)
+constexpr int kESmem = (2 * kEKBuf + kTMaxR * kERow) * 2 + 2 * kSRows * kDRow * 8;
 
-template <int PASS>
 __global__ void __launch_bounds__(256, 1) probe_exact_kernel(
     const __half* __restrict__ k, const __half* __restrict__ q, int units, int t_len, int R, int window,
-    int probe_rows, double inv_sqrt_d, int ntt, int nht, double2* __restrict__ stats,
-    const double2* __restrict__ rowstat, float* __restrict__ rawf) {
+    int probe_rows, double inv_sqrt_d, int ntt, int nht, double2* __restrict__ stats, double* __restrict__ logits) {
     constexpr int d = kD128;
     extern __shared__ __align__(16) __half esm[];
     __half* kbuf = esm;                                // [2][128 tokens][kERow]
     __half* qbuf = esm + 2 * kEKBuf;                   // [R][kERow]
-    double* at = reinterpret_cast<double*>(qbuf + kTMaxR * kERow);  // [kESlice][kSAStride]
+    double* qd = reinterpret_cast<double*>(qbuf + kTMaxR * kERow);  // [kSRows][kDRow] fp64 chunk of 128 probe rows
+    double* kd = qd + kSRows * kDRow;                                // [kSToks][kDRow] fp64 chunk of the K tile
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const long long items = (long long)units * ntt;
     const long long i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
@@ -432,99 +436,111 @@ __global__ void __launch_bounds__(256, 1) probe_exact_kernel(
         }
         __syncthreads();
         const __half* Ks = kbuf + buf * kEKBuf;
-        double colacc = 0.0;
         for (int rb = 0; rb < R; rb += kSRows) {
             double acc[8][8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-            const __half* Qs = qbuf + (size_t)rb * kERow;
 #pragma unroll 1
-            for (int c8 = 0; c8 < d; c8 += 8) {
-                uint4 av[8], bv[8];
+            for (int c0 = 0; c0 < d; c0 += kEChunk) {
+                // widen this chunk's probe rows and K tokens to fp64 once per CTA
+                // (not once per use: 16 threads read every value)
+                __syncthreads();  // the previous chunk's readers are done
 #pragma unroll
-                for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const uint4*>(Qs + (ty + 16 * i) * kERow + c8);
+                for (int e = tid; e < 2 * kSRows * (kEChunk / 8); e += 256) {
+                    const bool isk = e >= kSRows * (kEChunk / 8);
+                    const int u = isk ? e - kSRows * (kEChunk / 8) : e;
+                    const int r = u % kSRows, c8 = u / kSRows;  // a quarter-warp: 8 rows, one column group
+                    const __half* src = isk ? Ks + r * kERow + c0 + 8 * c8 : qbuf + (size_t)(rb + r) * kERow + c0 + 8 * c8;
+                    const uint4 v = (isk || rb + r < R) ? *reinterpret_cast<const uint4*>(src) : make_uint4(0, 0, 0, 0);
+                    const __half* hv = reinterpret_cast<const __half*>(&v);
+                    double2* dst = reinterpret_cast<double2*>((isk ? kd : qd) + r * kDRow + 8 * c8);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) bv[j] = *reinterpret_cast<const uint4*>(Ks + (tx + 16 * j) * kERow + c8);
+                    for (int m = 0; m < 4; ++m)
+                        dst[m] = make_double2((double)__half2float(hv[2 * m]), (double)__half2float(hv[2 * m + 1]));
+                }
+                __syncthreads();
+#pragma unroll 2
+                for (int c = 0; c < kEChunk; c += 2) {
+                    double2 a[8], b[8];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    double a[8], b[8];
+                    for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const double2*>(qd + (ty + 16 * i) * kDRow + c);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) a[i] = (double)__half2float(reinterpret_cast<const __half*>(&av[i])[e]);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) b[j] = (double)__half2float(reinterpret_cast<const __half*>(&bv[j])[e]);
+                    for (int j = 0; j < 8; ++j) b[j] = *reinterpret_cast<const double2*>(kd + (tx + 16 * j) * kDRow + c);
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+                        for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i].x, b[j].x, acc[i][j]);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i].y, b[j].y, acc[i][j]);
                 }
             }
-            if (PASS == 0) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int row = rb + ty + 16 * i;
-                    const int off = t_len - window + (row % window);  // causal offset (pipeline.cpp:129-130)
-                    double l[8];
-                    double m = -INFINITY;
+            for (int i = 0; i < 8; ++i) {
+                const int row = rb + ty + 16 * i;
+                const int off = t_len - window + (row % window);  // causal offset (pipeline.cpp:129-130)
+                double l[8];
+                double m = -INFINITY;
+                double* lrow = logits + ((size_t)unit * R + row) * t_len;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int t = tok0 + tx + 16 * j;
+                    l[j] = __dmul_rn(acc[i][j], inv_sqrt_d);
+                    if (row < R && t < t_len && t <= off) m = fmax(m, l[j]);
+                    if (row < R && t < t_len) lrow[t] = l[j];
+                }
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+                double sm_ = 0.0;
+                if (m != -INFINITY) {
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int t = tok0 + tx + 16 * j;
-                        l[j] = __dmul_rn(acc[i][j], inv_sqrt_d);
-                        if (row < R && t < t_len && t <= off) m = fmax(m, l[j]);
-                    }
-#pragma unroll
-                    for (int o = 1; o < 16; o <<= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-                    double sm_ = 0.0;
-                    if (m != -INFINITY) {
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const int t = tok0 + tx + 16 * j;
-                            if (row < R && t < t_len && t <= off) sm_ = __dadd_rn(sm_, exp(__dadd_rn(l[j], -m)));
-                        }
-                    }
-#pragma unroll
-                    for (int o = 1; o < 16; o <<= 1) sm_ = __dadd_rn(sm_, __shfl_xor_sync(0xffffffffu, sm_, o));
-                    if (tx == 0 && row < R) {
-                        stats[((size_t)unit * R + row) * nht + 2 * tile] = make_double2(m, sm_);
-                        stats[((size_t)unit * R + row) * nht + 2 * tile + 1] = make_double2(-INFINITY, 0.0);
+                        if (row < R && t < t_len && t <= off) sm_ = __dadd_rn(sm_, exp(__dadd_rn(l[j], -m)));
                     }
                 }
-            } else {
-                // a = exp(l - M) / denom (cache.cpp:176-180) through 32-row slices of shared memory,
-                // each token's column summed in row order (weights.cpp:36-39)
 #pragma unroll
-                for (int sl = 0; sl < kSRows / kESlice; ++sl) {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int rl = ty + 16 * i;  // this thread's rows of slice sl: rl in [32 sl, 32 sl + 32)
-                        if ((rl >> 5) != sl) continue;
-                        const int row = rb + rl;
-                        const int off = t_len - window + (row % window);
-                        const double2 ms = row < R ? rowstat[(size_t)unit * R + row] : make_double2(0.0, 1.0);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const int t = tok0 + tx + 16 * j;
-                            double a = 0.0;  // past the causal offset: exactly zero (cache.cpp:181)
-                            if (row < R && t < t_len && t <= off)
-                                a = exp(__dadd_rn(__dmul_rn(acc[i][j], inv_sqrt_d), -ms.x)) / ms.y;
-                            at[(rl & (kESlice - 1)) * kSAStride + tx + 16 * j] = a;
-                        }
-                    }
-                    __syncthreads();
-                    if (tid < kSToks) {
-                        const int nr = min(kESlice, R - rb - kESlice * sl);
-                        for (int r = 0; r < nr; ++r) colacc = __dadd_rn(colacc, at[r * kSAStride + tid]);
-                    }
-                    __syncthreads();
+                for (int o = 1; o < 16; o <<= 1) sm_ = __dadd_rn(sm_, __shfl_xor_sync(0xffffffffu, sm_, o));
+                if (tx == 0 && row < R) {
+                    stats[((size_t)unit * R + row) * nht + 2 * tile] = make_double2(m, sm_);
+                    stats[((size_t)unit * R + row) * nht + 2 * tile + 1] = make_double2(-INFINITY, 0.0);
                 }
             }
         }
-        if (PASS == 1 && tid < kSToks && tok0 + tid < t_len) rawf[(size_t)unit * t_len + tok0 + tid] = (float)colacc;
         __syncthreads();
         load_k(it + 2, buf);
     }
     cp_async_wait<0>();
+}
+
+// S3 from the logits S1 stored (fp16, d = 128): a = exp(l - M) / denom
+// (cache.cpp:176-180), each token's column summed over the rows in order
+// (weights.cpp:36-39) — the same expressions on the same values as the
+// recomputing pass, so the same bits, without the second GEMM. Thread per
+// token; the row loop is unrolled so the coalesced loads run ahead of the
+// sequential sum.
+__global__ void __launch_bounds__(256) probe_colsum_kernel(const double* __restrict__ logits,
+                                                           const double2* __restrict__ rowstat, int R, int t_len,
+                                                           int window, float* __restrict__ rawf) {
+    const int unit = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= t_len) return;
+    const double* lu = logits + (size_t)unit * R * t_len + t;
+    const double2* rs = rowstat + (size_t)unit * R;
+    double colacc = 0.0;
+    // causal offset of row r = qi * window + w: t_len - window + w (pipeline.cpp:129-130)
+    for (int r0 = 0; r0 < R; r0 += window) {
+#pragma unroll 8
+        for (int w = 0; w < window; ++w) {
+            const double l = lu[(size_t)(r0 + w) * t_len];
+            const double2 ms = rs[r0 + w];
+            const double a = t <= t_len - window + w ? exp(__dadd_rn(l, -ms.x)) / ms.y : 0.0;  // past it: exactly zero
+            colacc = __dadd_rn(colacc, a);
+        }
+    }
+    rawf[(size_t)unit * t_len + t] = (float)colacc;
 }
 
 // S2: per (unit, row) global max and softmax denominator from the tile stats,
@@ -609,10 +625,17 @@ struct StreamWorkspace {
     double2* rowstat;
     float* rawf;
     double* kpart;
+    double* logits;  // fp16 d = 128 path: S1's logits of a batch of `ubatch` units, [ubatch][R][T]
+    int ubatch;
     size_t bytes;
 };
 
 static bool stream_path(const rdkv_shape* s) { return s->head_dim % kSK == 0; }
+// shapes the persistent exact kernel takes (for fp16 inputs)
+static bool exact_shape(const rdkv_shape* s, int window) {
+    return s->head_dim == kD128 && (size_t)s->group * window <= (size_t)kTMaxR;
+}
+constexpr size_t kLogitBudget = size_t(2) << 30;  // bytes of stored S1 logits per unit batch
 
 static StreamWorkspace carve_stream(const rdkv_shape* s, int window, void* base) {
     const size_t U = s->units, T = s->seq_len, R = (size_t)s->group * window, d = s->head_dim;
@@ -629,6 +652,13 @@ static StreamWorkspace carve_stream(const rdkv_shape* s, int window, void* base)
     w.rowstat = reinterpret_cast<double2*>(take(U * R * sizeof(double2)));
     w.rawf = reinterpret_cast<float*>(take(U * T * sizeof(float)));
     w.kpart = reinterpret_cast<double*>(take(U * nch * d * sizeof(double)));
+    w.logits = nullptr;
+    w.ubatch = 0;
+    if (exact_shape(s, window)) {
+        const size_t per_unit = R * T * sizeof(double);
+        w.ubatch = (int)std::max<size_t>(1, std::min<size_t>(U, kLogitBudget / per_unit));
+        w.logits = reinterpret_cast<double*>(take((size_t)w.ubatch * per_unit));
+    }
     w.bytes = off;
     return w;
 }
@@ -644,19 +674,24 @@ static int run_weights_stream(const T* k, const T* q, const rdkv_shape* s, int w
     const int dev = dev_attrs().dev;
     const dim3 grid(ntt, U);
     const int nht = 2 * ntt;  // stats per 64-token half tile
-    if (std::is_same<T, __half>::value && d == kD128 && R <= kTMaxR) {
-        static std::atomic<int> tsm0[kMaxDevices], tsm1[kMaxDevices];
-        set_smem_once(probe_exact_kernel<0>, kESmem, tsm0, dev);
-        set_smem_once(probe_exact_kernel<1>, kESmem, tsm1, dev);
-        const long long items = (long long)U * ntt;
-        const int g = (int)(items < dev_attrs().nsm ? items : dev_attrs().nsm);
-        const __half* kh = reinterpret_cast<const __half*>(k);
-        const __half* qh = reinterpret_cast<const __half*>(q);
-        probe_exact_kernel<0><<<g, 256, kESmem, st>>>(kh, qh, U, t_len, R, window, s->probe_rows, inv_sqrt_d, ntt,
-                                                      nht, ws.stats, nullptr, nullptr);
-        probe_rowstat_kernel<<<(U * R * 32 + 255) / 256, 256, 0, st>>>(ws.stats, U * R, nht, ws.rowstat);
-        probe_exact_kernel<1><<<g, 256, kESmem, st>>>(kh, qh, U, t_len, R, window, s->probe_rows, inv_sqrt_d, ntt,
-                                                      nht, nullptr, ws.rowstat, ws.rawf);
+    if (std::is_same<T, __half>::value && ws.logits) {
+        // S1 stores its logits (a batch of units at a time), S3 reads them back
+        static std::atomic<int> tsm0[kMaxDevices];
+        set_smem_once(probe_exact_kernel, kESmem, tsm0, dev);
+        for (int u0 = 0; u0 < U; u0 += ws.ubatch) {
+            const int ub = std::min(ws.ubatch, U - u0);
+            const long long items = (long long)ub * ntt;
+            const int nblk = (int)(items < dev_attrs().nsm ? items : dev_attrs().nsm);
+            const __half* kh = reinterpret_cast<const __half*>(k) + (size_t)u0 * t_len * d;
+            const __half* qh = reinterpret_cast<const __half*>(q) + (size_t)u0 * g * s->probe_rows * d;
+            double2* stats = ws.stats + (size_t)u0 * R * nht;
+            double2* rowstat = ws.rowstat + (size_t)u0 * R;
+            probe_exact_kernel<<<nblk, 256, kESmem, st>>>(kh, qh, ub, t_len, R, window, s->probe_rows, inv_sqrt_d,
+                                                          ntt, nht, stats, ws.logits);
+            probe_rowstat_kernel<<<(ub * R * 32 + 255) / 256, 256, 0, st>>>(stats, ub * R, nht, rowstat);
+            probe_colsum_kernel<<<dim3((t_len + 255) / 256, ub), 256, 0, st>>>(ws.logits, rowstat, R, t_len, window,
+                                                                              ws.rawf + (size_t)u0 * t_len);
+        }
     } else {
         // f32 inputs (the reference-shaped drop-in path) and other shapes: the DFMA tile
         // GEMM, whose dots keep the reference's sequential fp64 order (bit-identical logits)

@@ -227,3 +227,19 @@ def test_weights_unit_boundaries_bit_identical(cuda):
         a_t, a_c = P.compute_weights(kd[h:h + 1].contiguous(), qd[h:h + 1].contiguous(), window=Sw, pool_kernel=5,
                                      kv_heads=H)
         assert torch.equal(a_t[0], w_t[h]) and torch.equal(a_c[0], w_c[h]), h
+
+
+def test_weights_logit_batches_bit_identical(cuda):
+    """S1 stores the logits of at most 2 GiB of units at a time (R x T fp64 per
+    unit) and S3 reads them back: 9 units of T = 262144 (268 MB each) run as two
+    batches, and every unit must equal the unit computed alone."""
+    g_, rows, T, U = 4, 32, 262144, 9
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    k = (torch.randn((U, T, 128), generator=gen, device="cuda") * 0.5).half()
+    q = (torch.randn((U, g_, rows, 128), generator=gen, device="cuda") * 0.5).half()
+    w_t, w_c = P.compute_weights(k, q, window=rows, pool_kernel=5, kv_heads=U)
+    assert torch.isfinite(w_t).all() and float(w_t.sum()) > 0
+    for u in (0, 7, 8):  # first batch, its last unit, the second batch
+        a_t, a_c = P.compute_weights(k[u:u + 1].contiguous(), q[u:u + 1].contiguous(), window=rows, pool_kernel=5,
+                                     kv_heads=U)
+        assert torch.equal(a_t[0], w_t[u]) and torch.equal(a_c[0], w_c[u]), u
