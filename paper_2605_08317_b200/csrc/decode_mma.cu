@@ -1982,6 +1982,27 @@ constexpr int kXMaxBuf = 4;  // tile buffers per pair
 // (no math), 2 math only (tiles past the first buffers are not reloaded).
 // PERCTA: one pair per CTA (a compile-time barrier id, so a CTA reserves 2
 // hardware barriers instead of 16 and 8 CTAs fit on an SM).
+#ifdef RDKV_DECODE_EXPERIMENTS
+// Timeline trace (experiments build only, tools/u2x_trace.py): per pair of the
+// last launch, the globaltimer at entry, after the grid dependency, and per tile
+// the buffer wait and the tile's end; slot 19 = SM id.
+constexpr int kTraceSlots = 20;
+__device__ unsigned long long* g_u2x_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define U2X_TRACE(slot)                                                                                   \
+    do {                                                                                                   \
+        if (g_u2x_trace && half == 0 && lane == 0 && (slot) < kTraceSlots)                                 \
+            g_u2x_trace[((size_t)blockIdx.x * p.W + pr) * kTraceSlots + (slot)] = gtimer();                \
+    } while (0)
+#else
+#define U2X_TRACE(slot) \
+    do {                \
+    } while (0)
+#endif
 template <typename IO, int NBMAX, bool FULLK, int MODE = 0, bool BULK = false, bool PERCTA = false, int ZCN = 0,
           bool G8 = false, bool MIX = false>
 __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const MmaParams p) {
@@ -2053,6 +2074,14 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     // previous kernel in a model) is read and out written only after
     // griddepcontrol.wait. Dependents of this grid may launch right away: their
     // CTAs take SMs as ours retire.
+    U2X_TRACE(0);
+#ifdef RDKV_DECODE_EXPERIMENTS
+    if (g_u2x_trace && half == 0 && lane == 0) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        g_u2x_trace[((size_t)blockIdx.x * p.W + pr) * kTraceSlots + 19] = smid;
+    }
+#endif
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     Meta ahead[kXMaxBuf - 1];  // half 1, lane 0: tiles 1 .. nbuf - 1 (look-ahead at tile 0)
     Meta next{nullptr, 0u};    // half 0, lane 0: the next refill target
@@ -2069,6 +2098,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
     // ready now; this grid waits for it at exit instead, so kernels after this
     // one still see both halves of the step done
     if (!p.concurrent) asm volatile("griddepcontrol.wait;" ::: "memory");
+    U2X_TRACE(1);
     int next_z = 0, ahead_z[kXMaxBuf - 1] = {0, 0, 0};
     if (half == 0 && lane == 0) {
         if (tile0 < p.units) issue_q(0, 0, zrows_of(0));
@@ -2089,6 +2119,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
         const int zl = zl_next;
         zl_next = zrows_of(k + 1);
         if (MODE != 2 || k < nbuf) mbar_wait(&fb[b], phase);
+        U2X_TRACE(2 + 2 * k);
         __syncwarp();
         const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
         if (k == 0 && half == 1 && lane == 0) {  // look-ahead once the first tile is in
@@ -2128,6 +2159,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
                     PERCTA ? 1 : 1 + pr, lc, rf, nullptr, nullptr, zl, st + qoff - zc_stage(ZCN), st + qoff - ZCN * 256);
             }
         }
+        U2X_TRACE(3 + 2 * k);
         if (++b == nbuf) {
             b = 0;
             phase ^= 1u;
@@ -3623,6 +3655,11 @@ static int decode_prepare_impl(const uint8_t* arena, const int64_t* tile_offsets
                                int32_t* decode_bytes_dev, int32_t* unit_ids_dev, rdkv_decode_plan* plan,
                                void* stream);
 
+#ifdef RDKV_DECODE_EXPERIMENTS
+extern "C" RDKV_API int rdkv_exp_set_u2x_trace(unsigned long long* buf) {
+    return cudaMemcpyToSymbol(g_u2x_trace, &buf, sizeof(buf)) == cudaSuccess ? RDKV_OK : RDKV_ECUDA;
+}
+#endif
 extern "C" RDKV_API int rdkv_cuda_decode_prepare(const uint8_t* arena, const int64_t* tile_offsets_host,
                                                  int32_t units, int32_t* decode_bytes_dev,
                                                  rdkv_decode_plan* plan, void* stream) {
