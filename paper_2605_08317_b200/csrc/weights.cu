@@ -363,9 +363,9 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // The production path (fp16, d = 128) with the reference's arithmetic order:
-// the persistent, cp.async-pipelined staging of probe_tma_kernel with the DFMA
-// register tile of probe_stream_kernel (thread (tx, ty): rows ty + 16 i, tokens
-// tx + 16 j, channels in order c = 0 .. 127, each an exact f32 x f32 product
+// the persistent, cp.async-pipelined staging of probe_tma_kernel with a DFMA
+// register tile (thread (tx, ty): rows ty + 32 i, tokens tx + 16 j (i < 4,
+// j < 8), channels in order c = 0 .. 127, each an exact f32 x f32 product
 // fused into the fp64 sum — bit-identical logits). Every 32-channel chunk of
 // the 128 probe rows and the 128-token K tile is widened to fp64 in shared
 // memory once per CTA (rows padded to 272 B: a thread's two-channel 16-B loads
@@ -378,11 +378,16 @@ constexpr int kEKBuf = kSToks * kERow;
 constexpr int kEChunk = 32;                    // channels widened to fp64 per step
 constexpr int kDRow = kEChunk + 2;             // fp64 row stride of a widened chunk (272 B: conflict-free)
 constexpr int kESmem = (2 * kEKBuf + kTMaxR * kERow) * 2 + 2 * kSRows * kDRow * 8;
+constexpr int kETile = 4;  // 4 x 8 tiles, 16 warps: S1 1.95 ms vs 2.04 with 8 x 8 tiles and 8 warps (same bits)
 
-__global__ void __launch_bounds__(256, 1) probe_exact_kernel(
+// TI probe rows per thread: 8 (256 threads, 8 x 8 DFMA register tile) or 4 (512
+// threads, 4 x 8: half the registers, twice the warps to hide the latencies)
+template <int TI>
+__global__ void __launch_bounds__(16 * (kSRows / TI), 1) probe_exact_kernel(
     const __half* __restrict__ k, const __half* __restrict__ q, int units, int t_len, int R, int window,
     int probe_rows, double inv_sqrt_d, int ntt, int nht, double2* __restrict__ stats, double* __restrict__ logits) {
     constexpr int d = kD128;
+    constexpr int NT = 16 * (kSRows / TI), RS = kSRows / TI;  // threads; row stride of a thread's rows
     extern __shared__ __align__(16) __half esm[];
     __half* kbuf = esm;                                // [2][128 tokens][kERow]
     __half* qbuf = esm + 2 * kEKBuf;                   // [R][kERow]
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(256, 1) probe_exact_kernel(
             const int unit = (int)(it / ntt), tile = (int)(it % ntt);
             const __half* kb = k + ((size_t)unit * t_len + (size_t)tile * kSToks) * d;
             __half* dst = kbuf + buf * kEKBuf;
-            for (int e = tid; e < kSToks * (d / 8); e += 256) {
+            for (int e = tid; e < kSToks * (d / 8); e += NT) {
                 const int r = e >> 4, c8 = e & 15;
                 const bool ok = tile * kSToks + r < t_len;
                 cp_async16(dst + r * kERow + 8 * c8, ok ? kb + (size_t)r * d + 8 * c8 : kb, ok);
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(256, 1) probe_exact_kernel(
     };
     auto load_q = [&](int unit) {
         const __half* qb = q + (size_t)unit * (R / window) * probe_rows * d;
-        for (int e = tid; e < R * (d / 8); e += 256) {
+        for (int e = tid; e < R * (d / 8); e += NT) {
             const int r = e >> 4, c8 = e & 15;
             const int qi = r / window, w = r - qi * window;
             cp_async16(qbuf + r * kERow + 8 * c8, qb + ((size_t)qi * probe_rows + probe_rows - window + w) * d + 8 * c8,
@@ -437,9 +442,9 @@ __global__ void __launch_bounds__(256, 1) probe_exact_kernel(
         __syncthreads();
         const __half* Ks = kbuf + buf * kEKBuf;
         for (int rb = 0; rb < R; rb += kSRows) {
-            double acc[8][8];
+            double acc[TI][8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < TI; ++i)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
 #pragma unroll 1
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(256, 1) probe_exact_kernel(
                 // (not once per use: 16 threads read every value)
                 __syncthreads();  // the previous chunk's readers are done
 #pragma unroll
-                for (int e = tid; e < 2 * kSRows * (kEChunk / 8); e += 256) {
+                for (int e = tid; e < 2 * kSRows * (kEChunk / 8); e += NT) {
                     const bool isk = e >= kSRows * (kEChunk / 8);
                     const int u = isk ? e - kSRows * (kEChunk / 8) : e;
                     const int r = u % kSRows, c8 = u / kSRows;  // a quarter-warp: 8 rows, one column group
@@ -463,24 +468,24 @@ __global__ void __launch_bounds__(256, 1) probe_exact_kernel(
                 __syncthreads();
 #pragma unroll 2
                 for (int c = 0; c < kEChunk; c += 2) {
-                    double2 a[8], b[8];
+                    double2 a[TI], b[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const double2*>(qd + (ty + 16 * i) * kDRow + c);
+                    for (int i = 0; i < TI; ++i) a[i] = *reinterpret_cast<const double2*>(qd + (ty + RS * i) * kDRow + c);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) b[j] = *reinterpret_cast<const double2*>(kd + (tx + 16 * j) * kDRow + c);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < TI; ++i)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i].x, b[j].x, acc[i][j]);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < TI; ++i)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i].y, b[j].y, acc[i][j]);
                 }
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int row = rb + ty + 16 * i;
+            for (int i = 0; i < TI; ++i) {
+                const int row = rb + ty + RS * i;
                 const int off = t_len - window + (row % window);  // causal offset (pipeline.cpp:129-130)
                 double l[8];
                 double m = -INFINITY;
@@ -677,7 +682,7 @@ static int run_weights_stream(const T* k, const T* q, const rdkv_shape* s, int w
     if (std::is_same<T, __half>::value && ws.logits) {
         // S1 stores its logits (a batch of units at a time), S3 reads them back
         static std::atomic<int> tsm0[kMaxDevices];
-        set_smem_once(probe_exact_kernel, kESmem, tsm0, dev);
+        set_smem_once(probe_exact_kernel<kETile>, kESmem, tsm0, dev);
         for (int u0 = 0; u0 < U; u0 += ws.ubatch) {
             const int ub = std::min(ws.ubatch, U - u0);
             const long long items = (long long)ub * ntt;
@@ -686,7 +691,8 @@ static int run_weights_stream(const T* k, const T* q, const rdkv_shape* s, int w
             const __half* qh = reinterpret_cast<const __half*>(q) + (size_t)u0 * g * s->probe_rows * d;
             double2* stats = ws.stats + (size_t)u0 * R * nht;
             double2* rowstat = ws.rowstat + (size_t)u0 * R;
-            probe_exact_kernel<<<nblk, 256, kESmem, st>>>(kh, qh, ub, t_len, R, window, s->probe_rows, inv_sqrt_d,
+            probe_exact_kernel<kETile><<<nblk, 16 * (kSRows / kETile), kESmem, st>>>(kh, qh, ub, t_len, R, window,
+                                                                               s->probe_rows, inv_sqrt_d,
                                                           ntt, nht, stats, ws.logits);
             probe_rowstat_kernel<<<(ub * R * 32 + 255) / 256, 256, 0, st>>>(stats, ub * R, nht, rowstat);
             probe_colsum_kernel<<<dim3((t_len + 255) / 256, ub), 256, 0, st>>>(ws.logits, rowstat, R, t_len, window,

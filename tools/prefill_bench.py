@@ -9,6 +9,13 @@ import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import json
 
+if "--exp" in sys.argv:  # the EXPERIMENTS build (timing variants), tools only
+    from paper_2605_08317_b200 import capi
+
+    capi.LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2605_08317_b200",
+                                 "_lib_exp", "librdkv_b200.so")
+    sys.argv.remove("--exp")
+
 import torch
 
 from paper_2605_08317_b200 import pipeline as P
@@ -36,6 +43,10 @@ al.check()
 out = {k2: min(v2) for k2, v2 in res.items()}
 out["config"] = f"one (sequence, layer): {spec.kv_heads} KV heads x T={spec.ctx}, g={spec.group}, n=128"
 out["kept_mean"] = float(al.stats_host()["n_kept"].mean())
+import hashlib
+
+out["w_t_sha1"] = hashlib.sha1(w_t.cpu().numpy().tobytes()).hexdigest()[:16]
+out["v_bits_sha1"] = hashlib.sha1(al.v_bits.cpu().numpy().tobytes()).hexdigest()[:16]
 print(json.dumps(out), flush=True)
 if os.environ.get("C1", "1") == "1":
     spec1 = WorkloadSpec(batch=1, layers=32, ctx=32768, n_tokens=128)
