@@ -1,7 +1,8 @@
 """tools: timeline of one headline decode launch (EXPERIMENTS build): per warp
 pair the globaltimer at entry, after griddepcontrol.wait, and per tile the
 buffer wait and the tile end, for the last of K back-to-back graph launches.
-usage: python tools/u2x_trace.py [K]"""
+usage: python tools/u2x_trace.py [K] [--host]   (--host: one end-to-end step through
+rdkv_cuda_decode_host with pinned host q / out instead of the device graph)"""
 import ctypes as C
 import json
 import os
@@ -20,6 +21,9 @@ from paper_2605_08317_b200.workload import WorkloadSpec, build
 
 import bench
 
+HOST = "--host" in sys.argv
+if HOST:
+    sys.argv.remove("--host")
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 50
 spec = WorkloadSpec(batch=16, layers=32, ctx=131072, n_tokens=128)
 model, _, _, _ = build(spec)
@@ -29,7 +33,21 @@ buf = torch.zeros(1024 * 16 * S, dtype=torch.int64, device="cuda")
 lib = capi.lib()
 lib.rdkv_exp_set_u2x_trace.argtypes = [C.c_void_p]
 assert lib.rdkv_exp_set_u2x_trace(buf.data_ptr()) == 0
-us, _ = bench.graph_step_us(P, model, q, K)
+if HOST:
+    qh = q.cpu().pin_memory()
+    oh = torch.empty_like(qh).pin_memory()
+    out = torch.empty_like(q)
+    args_c = P.decode_args(model, q, out)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(K):
+        e0.record(st)
+        assert lib.rdkv_cuda_decode_host(C.byref(args_c), qh.data_ptr(), oh.data_ptr(), st.cuda_stream) == 0
+        e1.record(st)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3
+else:
+    us, _ = bench.graph_step_us(P, model, q, K)
 torch.cuda.synchronize()
 t = buf.cpu().numpy().reshape(-1, S)
 t = t[t[:, 0] > 0]
