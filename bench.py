@@ -353,7 +353,7 @@ def pipeline_config2(P, steps):
             "note": "allocate/pack timed per (layer) chunk incl. host syncs; decode back-to-back (L2-warm)"}
 
 
-def graph_step_us(P, model, q, steps, kernel=0):
+def graph_step_us(P, model, q, steps, kernel=0, split=1):
     """Back-to-back decode steps from one CUDA graph over rotation copies of the
     arena (>= 3x L2), one event pair: the same method as the headline number."""
     import torch
@@ -370,7 +370,7 @@ def graph_step_us(P, model, q, steps, kernel=0):
         rot.append((m, q if r == 0 else q.clone(), torch.empty_like(q)))
     for i in range(3):
         m, qq, oo = rot[i % n_rot]
-        P.packed_decode_step(m, qq, oo, kernel=kernel)
+        P.packed_decode_step(m, qq, oo, kernel=kernel, split=split, workspace=m.split_ws if split > 1 else None)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     side = torch.cuda.Stream()
@@ -378,7 +378,8 @@ def graph_step_us(P, model, q, steps, kernel=0):
     with torch.cuda.graph(g, stream=side):
         for i in range(steps):
             m, qq, oo = rot[i % n_rot]
-            P.packed_decode_step(m, qq, oo, kernel=kernel)
+            P.packed_decode_step(m, qq, oo, kernel=kernel, split=split,
+                                 workspace=m.split_ws if split > 1 else None)
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -190,6 +190,8 @@ RDKV_API int rdkv_cuda_decode_prepare_split(const uint8_t* arena, const int64_t*
                                             int32_t units, int32_t* tile_decode_bytes, int32_t* unit_ids,
                                             rdkv_decode_plan* plan, void* stream);
 
+/* Bytes of the split-K workspace for `split` parts (0 for split <= 1): the
+ * partials [split][units][group][head_dim + 2] f32. */
 RDKV_API size_t rdkv_cuda_decode_workspace(int32_t units, int32_t group, int32_t head_dim,
                                            int32_t split);
 RDKV_API int rdkv_cuda_decode(const rdkv_decode_args* a, void* stream);

@@ -2854,14 +2854,93 @@ int launch_partial(const rdkv_decode_args* a, int rank, int world, float* partia
 }
 
 // out = sum_r 2^(m_r - M) o_r / sum_r 2^(m_r - M) l_r over nparts partials
-// [nparts][units * g][d + 2] (m in log2 units, as the kernels keep it)
+// [nparts][units * g][d + 2] (m in log2 units, as the kernels keep it).
+// One warp per row: lane r holds part r's (max, sum) and weight, the weights
+// and the denominator are combined in part order (fixed, deterministic), and
+// every channel's S loads are independent (in flight together). Launched with
+// programmatic dependent launch: its CTAs are resident while the producing
+// kernel drains and start at griddepcontrol.wait.
+constexpr int kMergeRows = 8;        // rows (warps) per CTA
+constexpr int kMergeFastParts = 16;  // parts whose loads are all in flight at once
 template <typename IO>
-__global__ void merge_partials_kernel(const float* __restrict__ part, int nparts, int rows, int d, IO* __restrict__ out) {
+__global__ void __launch_bounds__(32 * kMergeRows) merge_partials_kernel(const float* __restrict__ part, int nparts,
+                                                                         int rows, int d, IO* __restrict__ out) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * kMergeRows + (threadIdx.x >> 5);
+    if (row >= rows) return;
+    const size_t stride = (size_t)rows * (d + 2);
+    const float* base = part + (size_t)row * (d + 2);
+    // d = 128, <= 16 parts: every part's channels (2 lane, + 1, 64 + 2 lane, + 1;
+    // 8-B aligned rows) are loaded before anything waits on them
+    const bool fast = d == 128 && nparts <= kMergeFastParts;
+    float2 xs[kMergeFastParts], ys[kMergeFastParts];
+    if (fast) {
+#pragma unroll
+        for (int r = 0; r < kMergeFastParts; ++r)
+            if (r < nparts) {
+                xs[r] = *reinterpret_cast<const float2*>(base + r * stride + 2 * lane);
+                ys[r] = *reinterpret_cast<const float2*>(base + r * stride + 64 + 2 * lane);
+            }
+    }
+    float m = -INFINITY, l = 0.0f;
+    if (lane < nparts) {
+        m = base[lane * stride + d];
+        l = base[lane * stride + d + 1];
+        if (!(l > 0.0f)) m = -INFINITY;
+    }
+    float M = m;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float w = (lane < nparts && l > 0.0f) ? exp2f(m - M) : 0.0f;
+    float L = 0.0f;
+    for (int r = 0; r < nparts; ++r) L += __shfl_sync(0xffffffffu, w * l, r);
+    const float inv = L > 0.0f ? 1.0f / L : 0.0f;
+    if (fast) {
+        float2 a = make_float2(0.0f, 0.0f), b = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int r = 0; r < kMergeFastParts; ++r)
+            if (r < nparts) {
+                const float wr = __shfl_sync(0xffffffffu, w, r);
+                if (wr != 0.0f) {
+                    a.x += wr * xs[r].x;
+                    a.y += wr * xs[r].y;
+                    b.x += wr * ys[r].x;
+                    b.y += wr * ys[r].y;
+                }
+            }
+        IO* o = out + (size_t)row * d;
+        o[2 * lane] = (IO)(a.x * inv);
+        o[2 * lane + 1] = (IO)(a.y * inv);
+        o[64 + 2 * lane] = (IO)(b.x * inv);
+        o[65 + 2 * lane] = (IO)(b.y * inv);
+        return;
+    }
+    for (int c = lane; c < d; c += 32) {
+        float acc = 0.0f;
+#pragma unroll 4
+        for (int r = 0; r < nparts; ++r) {
+            const float wr = __shfl_sync(0xffffffffu, w, r);
+            const float v = base[r * stride + c];
+            if (wr != 0.0f) acc += wr * v;
+        }
+        out[(size_t)row * d + c] = (IO)(acc * inv);
+    }
+}
+
+// more than 32 parts (a wide sequence split): one CTA per row, parts in order
+template <typename IO>
+__global__ void merge_partials_wide_kernel(const float* __restrict__ part, int nparts, int rows, int d,
+                                           IO* __restrict__ out) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int row = blockIdx.x;
     if (row >= rows) return;
     const size_t stride = (size_t)rows * (d + 2);
     float M = -INFINITY;
-    for (int r = 0; r < nparts; ++r) M = fmaxf(M, part[r * stride + (size_t)row * (d + 2) + d]);
+    for (int r = 0; r < nparts; ++r) {
+        const float* pr = part + r * stride + (size_t)row * (d + 2);
+        if (pr[d + 1] > 0.0f) M = fmaxf(M, pr[d]);
+    }
     float L = 0.0f;
     for (int r = 0; r < nparts; ++r) {
         const float* pr = part + r * stride + (size_t)row * (d + 2);
@@ -2878,12 +2957,31 @@ __global__ void merge_partials_kernel(const float* __restrict__ part, int nparts
     }
 }
 
+template <typename IO>
+static int launch_merge_t(const float* part, int nparts, int rows, int d, IO* out, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.stream = st;
+    cudaError_t e;
+    if (nparts <= 32) {
+        cfg.gridDim = dim3((rows + kMergeRows - 1) / kMergeRows);
+        cfg.blockDim = dim3(32 * kMergeRows);
+        e = cudaLaunchKernelEx(&cfg, merge_partials_kernel<IO>, part, nparts, rows, d, out);
+    } else {
+        cfg.gridDim = dim3(rows);
+        cfg.blockDim = dim3(128);
+        e = cudaLaunchKernelEx(&cfg, merge_partials_wide_kernel<IO>, part, nparts, rows, d, out);
+    }
+    return e == cudaSuccess ? RDKV_OK : RDKV_ECUDA;
+}
+
 int launch_merge(const float* part, int nparts, int rows, int d, void* out, int io, cudaStream_t st) {
-    if (io == RDKV_F16)
-        merge_partials_kernel<__half><<<rows, 128, 0, st>>>(part, nparts, rows, d, static_cast<__half*>(out));
-    else
-        merge_partials_kernel<float><<<rows, 128, 0, st>>>(part, nparts, rows, d, static_cast<float*>(out));
-    return launch_status();
+    if (io == RDKV_F16) return launch_merge_t(part, nparts, rows, d, static_cast<__half*>(out), st);
+    return launch_merge_t(part, nparts, rows, d, static_cast<float*>(out), st);
 }
 
 // ============================================================================
@@ -2970,6 +3068,10 @@ struct U24Issuer {
     U24Meta cur, nxt;
     U24Tile t;
     int item, c, n;
+    int nxt_item;            // the item after `item` (its header is loaded one item ahead)
+    int done;                // the end-of-work marker has been staged
+    int bitem[kXMaxBuf];     // per buffer: the staged chunk's (item, chunk), item -1 = no more work
+    int bc[kXMaxBuf];
 };
 
 // One chunk for one 4-head group. `first`: this pair's first chunk of the tile
@@ -3353,7 +3455,7 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u24_kernel(const M
     U24Issuer& is = *reinterpret_cast<U24Issuer*>(scr + (p.g > 4 ? 2 : 1) * kU24Scratch);
     auto load_meta = [&](int item, U24Meta& m) {
         m.base = nullptr;
-        if (item < nitems) {
+        if (item >= 0 && item < nitems) {
             const int tile = item / S;
             m.base = p.arena + p.offsets[tile];
             const TileHeader* th = reinterpret_cast<const TileHeader*>(m.base);
@@ -3372,21 +3474,31 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u24_kernel(const M
         u24_tile(is.cur.r, is.t);
         is.n = u24_nchunks(is.t);
     };
+    // the pair's next item (static striding: items of a round are spread over
+    // all pairs; measured faster than claiming items from a global counter)
+    auto next_item = [&](int it) {
+        if (it < 0 || it >= nitems) return -1;
+        const int v = it + istride;
+        return v < nitems ? v : -1;
+    };
     auto advance = [&]() {
         is.c += S;
         if (is.c >= is.n) {
-            is.item += istride;
+            is.item = is.nxt_item;
+            if (is.item < 0) return;
             is.c = is.item % S;
             is.cur = is.nxt;
             set_cur();
-            load_meta(is.item + istride, is.nxt);
+            is.nxt_item = next_item(is.item);
+            load_meta(is.nxt_item, is.nxt);
         }
     };
     auto stage_item = [&](int b) {
         const U24Meta& cur = is.cur;
-        if (is.item >= nitems || !cur.base) return false;
         const U24Geom gg = u24_chunk(is.t, is.c);
         const bool first = is.c == is.item % S;
+        is.bitem[b] = is.item;
+        is.bc[b] = is.c;
         uint8_t* dst = pbuf + (size_t)b * p.slot_bytes;
         const int rows = gg.ns >> 2, Q = cur.nslot >> 2;
         const int rb = u24_vrow_bytes(gg.cls);
@@ -3404,36 +3516,48 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u24_kernel(const M
         const int offv = gg.cls == 0 ? cur.offv[0] : gg.cls == 1 ? cur.offv[1] : cur.offv[2];
         bulk_g2s(dst + dk + gg.ns * cur.krb, cur.base + offv + (size_t)gg.li0 * rb, vbytes, &fb[b]);
         bulk_g2s(dst + dk + gg.ns * cur.krb + vbytes, cur.base + cur.offvp + (size_t)gg.s0 * 8, pbytes, &fb[b]);
-        return true;
     };
     auto stage_q = [&](int b, int item) {
         bulk_g2s(pbuf + (size_t)b * p.slot_bytes + qoff, static_cast<const uint8_t*>(p.q) + (size_t)(item / S) * qbytes,
                  (uint32_t)qbytes, &fb[b]);
     };
+    // stage the next chunk into buffer b, or (once) the end-of-work marker
     auto issue_item = [&](int b) {
-        const bool first = is.item < nitems && is.c == is.item % S;
+        if (is.done) return;
+        if (is.item < 0 || is.item >= nitems || !is.cur.base) {
+            is.bitem[b] = -1;
+            mbar_arrive(&fb[b]);
+            is.done = 1;
+            return;
+        }
+        const bool first = is.c == is.item % S;
         const int it = is.item;
-        if (!stage_item(b)) return false;
+        stage_item(b);
         if (first) stage_q(b, it);
         advance();
-        return true;
     };
 
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (issuer) {
         for (int b = 0; b < nbuf; ++b) mbar_init(&fb[b], 1);
         fence_barrier_init();
-        is.item = item0;
+        is.done = 0;
+        is.item = item0 < nitems ? item0 : -1;
         is.c = item0 % S;
         load_meta(item0, is.cur);
-        load_meta(item0 + istride, is.nxt);
         set_cur();
-        stage_item(0);  // KV of the first chunk before the grid dependency
+        if (is.item >= 0) stage_item(0);  // KV of the first chunk before the grid dependency
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (issuer && item0 < nitems) {
-        stage_q(0, item0);
-        advance();
+    if (issuer) {
+        if (is.item >= 0) {
+            stage_q(0, item0);
+            is.nxt_item = next_item(item0);
+            load_meta(is.nxt_item, is.nxt);
+            advance();
+        } else {
+            issue_item(0);  // no work: the end marker
+        }
     }
     const U2xLane lc = u2x_lane(half);
     constexpr int npass = G8 ? 2 : 1;  // GQA groups of 5..8 heads: two 4-head passes per staged chunk
@@ -3446,42 +3570,44 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u24_kernel(const M
     U2xRun run0;
     U2xRun run1;  // (G8 only)
     U24Tile tl{};
-    for (int item = item0; item < nitems; item += istride) {
-        const int tile = item / S, part = item % S;
-        int C = part + 1, hk = 0, krb = 0;  // C: known once the first chunk is in
-        for (int c = part; c < C; c += S) {
-            mbar_wait(&fb[b], phase);
-            __syncwarp();
-            const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
-            const bool first = c == part;
-            if (first) {
-                const TileHeader& th = *reinterpret_cast<const TileHeader*>(st);
-                u24_tile(th.r, tl);
-                C = u24_nchunks(tl);
-                hk = th.off_k;
-                krb = th.krow_bytes;
-            }
-            if (k == 0 && issuer)  // look-ahead once the first chunk is in
-                for (int j = 1; j < nbuf; ++j) issue_item(j);
-            const int bprev = b == 0 ? nbuf - 1 : b - 1;
-            auto refill = [&]() {
-                if (issuer && k >= 1) issue_item(bprev);
-            };
-            const U24Geom ck = u24_chunk(tl, c);
-            const uint8_t* kb = st + hk;
-            const uint8_t* vb = kb + ck.ns * krb;
-            const float2* vp = reinterpret_cast<const float2*>(vb + ck.ns * u24_vrow_bytes(ck.cls));
-            decode_chunk_u24<IO>(st, st + qoff, min(4, p.g), scr, 1 + pr, lc, refill, ck, first, krb, kb, vb, vp, run0,
-                                 tl);
-            if constexpr (G8)
-                decode_chunk_u24<IO>(st, st + qoff + 4 * QROW, p.g - 4, scr + kU24Scratch, 1 + pr, lc, [] {}, ck, first,
-                                     krb, kb, vb, vp, run1, tl);
-            if (++b == nbuf) {
-                b = 0;
-                phase ^= 1u;
-            }
-            ++k;
+    int tile = 0, part = 0, C = 1, hk = 0, krb = 0;
+    for (;;) {
+        mbar_wait(&fb[b], phase);
+        __syncwarp();
+        const int item = is.bitem[b], c = is.bc[b];
+        if (item < 0) break;
+        const uint8_t* st = pbuf + (size_t)b * p.slot_bytes;
+        const bool first = c < S;  // an item's first chunk is its part index
+        if (first) {
+            tile = item / S;
+            part = item % S;
+            const TileHeader& th = *reinterpret_cast<const TileHeader*>(st);
+            u24_tile(th.r, tl);
+            C = u24_nchunks(tl);
+            hk = th.off_k;
+            krb = th.krow_bytes;
         }
+        if (k == 0 && issuer)  // look-ahead once the first chunk is in
+            for (int j = 1; j < nbuf; ++j) issue_item(j);
+        const int bprev = b == 0 ? nbuf - 1 : b - 1;
+        auto refill = [&]() {
+            if (issuer && k >= 1) issue_item(bprev);
+        };
+        const U24Geom ck = u24_chunk(tl, c);
+        const uint8_t* kb = st + hk;
+        const uint8_t* vb = kb + ck.ns * krb;
+        const float2* vp = reinterpret_cast<const float2*>(vb + ck.ns * u24_vrow_bytes(ck.cls));
+        decode_chunk_u24<IO>(st, st + qoff, min(4, p.g), scr, 1 + pr, lc, refill, ck, first, krb, kb, vb, vp, run0,
+                             tl);
+        if constexpr (G8)
+            decode_chunk_u24<IO>(st, st + qoff + 4 * QROW, p.g - 4, scr + kU24Scratch, 1 + pr, lc, [] {}, ck, first,
+                                 krb, kb, vb, vp, run1, tl);
+        if (++b == nbuf) {
+            b = 0;
+            phase ^= 1u;
+        }
+        ++k;
+        if (c + S < C) continue;  // more chunks of this item follow
 #pragma unroll
         for (int hp = 0; hp < 2; ++hp) {
             const int head = 4 * hp + lc.tig;
@@ -3512,13 +3638,29 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u24_kernel(const M
     }
 }
 
-// Parts per tile for split-K: enough (tile, part) items for ~2 per warp pair,
-// never more parts than the smallest tile has chunks.
+// Parts per tile for split-K. Items (tile, part) are dealt to the warp pairs
+// round by round, so the step costs about rounds(S) x ceil(C / S) chunk times
+// (C = chunks per tile) plus a per-part cost (its q~ setup, partial row and
+// merge share), ~0.75 chunk per part as measured over the configs[3] points
+// (tools/c3_bench.py --sweep: e.g. Qwen2.5-7B, 448 tiles of 14 chunks on 888
+// pairs, S = 3 at 78.5 us against 89.7 at S = 4 and 97.5 at S = 1). Never more
+// parts than the smallest tile has chunks (no empty parts).
+constexpr double kU24PartCost = 0.75;
 static int u24_parts(const rdkv_decode_args* a, int pairs_total) {
-    const int want = (2 * pairs_total + a->units - 1) / a->units;
-    int S = want < a->plan.min_chunks24 ? want : a->plan.min_chunks24;
-    if (S > kU24MaxParts) S = kU24MaxParts;
-    return S < 1 ? 1 : S;
+    const int C = a->plan.min_chunks24 > 1 ? a->plan.min_chunks24 : 1;
+    const int smax = C < kU24MaxParts ? C : kU24MaxParts;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int S = 1; S <= smax; ++S) {
+        const long long items = (long long)a->units * S;
+        const long long rounds = (items + pairs_total - 1) / pairs_total;
+        const double cost = (double)rounds * ((C + S - 1) / S) + kU24PartCost * S;
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = S;
+        }
+    }
+    return best;
 }
 
 template <typename IO>
@@ -3538,9 +3680,12 @@ static int launch_u24(const rdkv_decode_args* a, cudaStream_t st) {
     const int slack = 128;
     int W = 0, nbuf = 0;
     if (!pick_pairs(1 << 30, da.nsm, slot, scratch, da.smem_optin - slack, W, nbuf)) return RDKV_EINVAL;
-    const int S0 = u24_parts(a, W * da.nsm);
+    // a->split: 0 automatic, 1 one part per tile, > 1 that many parts (capped)
+    int S0 = a->split == 0 ? u24_parts(a, W * da.nsm) : a->split;
+    if (S0 > a->plan.min_chunks24) S0 = a->plan.min_chunks24;
+    if (S0 > kU24MaxParts) S0 = kU24MaxParts;
     const size_t need = rdkv_cuda_decode_workspace(a->units, a->group, kD, S0);
-    const int S = (S0 > 1 && a->workspace && a->workspace_bytes >= need && a->split == 0) ? S0 : 1;
+    const int S = (S0 > 1 && a->workspace && a->workspace_bytes >= need) ? S0 : 1;
     MmaParams p{a->arena, a->tile_offsets, a->tile_decode_bytes, a->q, a->out,
                 static_cast<const __half*>(a->zc_k), static_cast<const __half*>(a->zc_v), a->zc_len,
                 a->units, a->group, a->zc_cap, nbuf, W, slot, scratch, 0, 0, -1, -1, 0, 0};

@@ -110,6 +110,32 @@ def test_configs3_large_mixed_tiles_auto_dispatch(cuda, orc, name, Hq, Hkv, n):
     assert worst < DECODE_TOL, worst
 
 
+@pytest.mark.parametrize("name,L,Hq,Hkv,n", [("mistral-7b", 32, 32, 8, 256), ("qwen2.5-7b", 28, 28, 4, 1024)])
+def test_configs3_full_step_dynamic_claims(cuda, name, L, Hq, Hkv, n):
+    """A whole configs[3] step (batch 4, every layer: 448 / 1024 tiles) has more
+    (tile, part) items than warp pairs, so the chunked split-K kernel hands out
+    items after the first round from its claim counter. The step must equal the
+    one-pair-per-tile decode (no partials) and the CUDA-core kernel, and repeat
+    bit-identically (which pair takes an item must not change a bit)."""
+    from paper_2605_08317_b200.workload import build
+
+    spec = WorkloadSpec(batch=4, layers=L, q_heads=Hq, kv_heads=Hkv, ctx=65536, n_tokens=n, seed=11,
+                        hh_stride=64, hh_boost=1.0, outlier_channels=4, outlier_scale=8.0)
+    m, _, _, _ = build(spec)
+    assert m.plan.mix24 and m.split_ws is not None
+    q = P.generate((m.units, spec.group, spec.head_dim), torch.float16, seed=5, tensor=2)
+    a = P.packed_decode_step(m, q)
+    outs = [P.packed_decode_step(m, q) for _ in range(3)]
+    for o in outs:
+        assert torch.equal(o, a)
+    gen = P.packed_decode_step(m, q, kernel=1).float()
+    ws, m.split_ws = m.split_ws, None
+    whole = P.packed_decode_step(m, q).float()
+    m.split_ws = ws
+    assert rel(a.float().cpu(), gen.cpu()) < DECODE_TOL
+    assert rel(whole.cpu(), a.float().cpu()) < DECODE_TOL
+
+
 def test_configs4_llama70b_g8_all_layers(cuda, orc, ref):
     """configs[4] LLaMA-3.1-70B KV shape: 80 layers x 8 KV heads, GQA group 8, n=128,
     in one decode launch (two 4-head passes per staged tile). T reduced to 8K so the

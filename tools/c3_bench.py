@@ -20,7 +20,8 @@ from paper_2605_08317_b200.workload import WorkloadSpec, build
 
 peak, _ = bench.load_peaks()
 pts = [("qwen2.5-7b", (28, 28, 4), n) for n in (64, 256, 1024, 2048)] + [("mistral-7b", (32, 32, 8), n) for n in (64, 2048)]
-sel = sys.argv[1:] or None
+sweep = "--sweep" in sys.argv
+sel = [a for a in sys.argv[1:] if a != "--sweep"] or None
 for model, (L, Hq, Hkv), n in pts:
     if sel and f"{model}_n{n}" not in sel:
         continue
@@ -29,6 +30,11 @@ for model, (L, Hq, Hkv), n in pts:
     m, _, st, _ = build(spec)
     q = P.generate((m.units, spec.group, spec.head_dim), torch.float16, seed=bench.QSEED, tensor=2)
     us, _ = bench.graph_step_us(P, m, q, 50)
+    if sweep:  # the chunked split-K kernel at forced parts per tile
+        for S in (1, 2, 3, 4, 5, 6, 7, 8, 10, 14):
+            if S <= int(m.plan.min_chunks24) and (S == 1 or m.split_ws is not None):
+                su, _ = bench.graph_step_us(P, m, q, 50, kernel=2, split=S)
+                print(json.dumps({"point": f"{model}_n{n}", "parts": S, "us_per_step": round(su, 2)}), flush=True)
     byts = m.survey_bytes(io_bytes=2)
     ref = P.packed_decode_step(m, q, kernel=1).float()
     out = P.packed_decode_step(m, q).float()
