@@ -1797,6 +1797,16 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
     const float lt = xg.lsum[0][tig] + xg.lsum[1][tig];
     const float bt = xg.bv[0][tig] + xg.bv[1][tig];
 
+    // Zone C prepass row of this head (ZCN < 0): loaded here so the PV loop hides its latency
+    float2 zpo[4];
+    float zpm = -INFINITY, zpl = 0.0f;
+    if constexpr (ZCN < 0 && !CHUNKED) {
+        const float* zp = reinterpret_cast<const float*>(zk) + (hv ? tig : 0) * (kD + 2);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) zpo[m] = *reinterpret_cast<const float2*>(zp + L.ch0 + 4 * m);
+        zpm = zp[kD];
+        zpl = zp[kD + 1];
+    }
     // ---- PV: this warp's 4 m-tiles (byte columns 16 half + 4 (gid & 3) + m), one n-tile
     int acc[4][4];
 #pragma unroll
@@ -1879,6 +1889,19 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                 }
             }
         }
+        if (ZCN < 0 && hv) {
+            // Zone C from the prepass (zc_partial_kernel): this head's unnormalised
+            // (o, max, sum) row, loaded before the PV loop (zpo, zpm, zpl)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) oz[m] = zpo[m];
+            const float mz = zpm;
+            lz = zpl;
+            if (lz > 0.0f) {
+                const float mm = fmaxf(mx, mz);
+                wa = ex2_approx(mx - mm);
+                wb = ex2_approx(mz - mm);
+            }
+        }
         if (ZCN > 0 && z > 0) {
             // QK: A rows = Zone C tokens (rows >= z read neighbouring bytes, masked
             // below), B columns 2h / 2h + 1 = hi / lo fp16 parts of q_h
@@ -1948,7 +1971,7 @@ __device__ __forceinline__ void decode_tile_u2x(const uint8_t* __restrict__ t, c
                 const float2 v =
                     make_float2((float)(acc[m][0] * 256 + acc[m][1]), (float)(acc[m][2] * 256 + acc[m][3]));
                 float2 r = ffma2(v, sc, bb);
-                if (ZCN > 0) r = ffma2(oz[m], zz, r);
+                if (ZCN != 0) r = ffma2(oz[m], zz, r);
                 if (MIX) r = ffma2(o4[m], ww, r);
                 if constexpr (sizeof(IO) == 2)
                     *reinterpret_cast<__half2*>(orow + 4 * m) = __float22half2_rn(r);
@@ -2156,7 +2179,10 @@ __global__ void __launch_bounds__(32 * 2 * kXPairs, 1) decode_u2x_kernel(const M
                 };
                 decode_tile_u2x<IO, NBMAX, FULLK, BULK, false, ZCN, MIX>(
                     st, st + qoff + 4 * hp * QROW, G8 ? min(4, p.g - 4 * hp) : p.g, scr, o + 4 * hp * kD,
-                    PERCTA ? 1 : 1 + pr, lc, rf, nullptr, nullptr, zl, st + qoff - zc_stage(ZCN), st + qoff - ZCN * 256);
+                    PERCTA ? 1 : 1 + pr, lc, rf, nullptr, nullptr, zl,
+                    ZCN < 0 ? reinterpret_cast<const uint8_t*>(p.partial + ((size_t)unit_of(p, tile) * p.g + 4 * hp) * (kD + 2))
+                            : st + qoff - zc_stage(ZCN),
+                    st + qoff - ZCN * 256);
             }
         }
         U2X_TRACE(3 + 2 * k);
@@ -2606,6 +2632,155 @@ static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st, float* partial
 }
 
 // Zone C small enough to stage with each short tile (host-known bound)
+// ---- Zone C prepass (append_new_token rows, trizone.cpp:261-303): one warp per
+// unit computes, for each of its g query heads, the softmax state of the unit's
+// appended fp16 rows alone — unnormalised o over the lane's channels 4 lane ..
+// 4 lane + 3, the running max (log2 units, the decode kernels' convention) and
+// the weight sum — into [units][g][d + 2] f32; the short-tile kernel (ZCN < 0)
+// folds that row into its epilogue. The tile kernel keeps its 8 warp pairs per
+// SM (no Zone C staging in its buffers); the rows are read once, here.
+// Logits of 4 heads are reduced together: two exchange stages halve the values
+// a lane carries, three more finish the sum in 8-lane groups (head h in lanes
+// 8h .. 8h + 7), four broadcasts return them — 10 shuffles per token and group.
+constexpr int kZcpUnits = 8;  // units (warps) per CTA
+template <typename IO>
+__device__ __forceinline__ void zcp_load_q(const IO* qrow, int lane, float (&q)[4]) {
+    if constexpr (sizeof(IO) == 2) {
+        const uint2 w = *reinterpret_cast<const uint2*>(qrow + 4 * lane);
+        const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&w.x));
+        const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&w.y));
+        q[0] = a.x, q[1] = a.y, q[2] = b.x, q[3] = b.y;
+    } else {
+        const float4 v = *reinterpret_cast<const float4*>(qrow + 4 * lane);
+        q[0] = v.x, q[1] = v.y, q[2] = v.z, q[3] = v.w;
+    }
+}
+template <typename IO, int NG>  // NG: groups of 4 heads (1: g <= 4, 2: g <= 8)
+__global__ void __launch_bounds__(32 * kZcpUnits) zc_partial_kernel(const IO* __restrict__ q,
+                                                                    const __half* __restrict__ zk,
+                                                                    const __half* __restrict__ zv,
+                                                                    const int32_t* __restrict__ zlen, int units, int g,
+                                                                    int cap, float* __restrict__ part) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // q and the appended rows come from earlier kernels
+    const int lane = threadIdx.x & 31;
+    const int u = blockIdx.x * kZcpUnits + (threadIdx.x >> 5);
+    if (u >= units) return;
+    constexpr float kScale = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(d)
+    int z = zlen[u];
+    z = z < cap ? z : cap;
+    float qv[4 * NG][4], o[4 * NG][4], m[4 * NG], l[4 * NG];
+#pragma unroll
+    for (int h = 0; h < 4 * NG; ++h) {
+        if (h < g)
+            zcp_load_q(q + ((size_t)u * g + h) * kD, lane, qv[h]);
+        else
+            qv[h][0] = qv[h][1] = qv[h][2] = qv[h][3] = 0.0f;
+        m[h] = -INFINITY;
+        l[h] = 0.0f;
+        o[h][0] = o[h][1] = o[h][2] = o[h][3] = 0.0f;
+    }
+    const __half* kr = zk + (size_t)u * cap * kD + 4 * lane;
+    const __half* vr = zv + (size_t)u * cap * kD + 4 * lane;
+    constexpr int kBatch = 8;  // rows whose loads are in flight together
+    for (int t0 = 0; t0 < z; t0 += kBatch) {
+    uint2 kb[kBatch], vb[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j)
+        if (t0 + j < z) {
+            kb[j] = *reinterpret_cast<const uint2*>(kr + (size_t)(t0 + j) * kD);
+            vb[j] = *reinterpret_cast<const uint2*>(vr + (size_t)(t0 + j) * kD);
+        }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+        if (t0 + j >= z) break;
+        const uint2 kw = kb[j], vw = vb[j];
+        const float2 k01 = __half22float2(*reinterpret_cast<const __half2*>(&kw.x));
+        const float2 k23 = __half22float2(*reinterpret_cast<const __half2*>(&kw.y));
+        const float2 v01 = __half22float2(*reinterpret_cast<const __half2*>(&vw.x));
+        const float2 v23 = __half22float2(*reinterpret_cast<const __half2*>(&vw.y));
+#pragma unroll
+        for (int gr = 0; gr < NG; ++gr) {
+            float sp[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float* qq = qv[4 * gr + j];
+                sp[j] = fmaf(qq[3], k23.y, fmaf(qq[2], k23.x, fmaf(qq[1], k01.y, qq[0] * k01.x)));
+            }
+            const bool hi16 = (lane & 16) != 0, hi8 = (lane & 8) != 0;
+            float a0 = hi16 ? sp[2] : sp[0], a1 = hi16 ? sp[3] : sp[1];
+            const float b0 = hi16 ? sp[0] : sp[2], b1 = hi16 ? sp[1] : sp[3];
+            a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
+            a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
+            float c = (hi8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+            c += __shfl_xor_sync(0xffffffffu, c, 4);
+            c += __shfl_xor_sync(0xffffffffu, c, 2);
+            c += __shfl_xor_sync(0xffffffffu, c, 1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int h = 4 * gr + j;
+                const float lg = __shfl_sync(0xffffffffu, c, 8 * j) * kScale;
+                const float mn = fmaxf(m[h], lg);
+                const float al = ex2_approx(m[h] - mn), pw = ex2_approx(lg - mn);
+                l[h] = fmaf(l[h], al, pw);
+                o[h][0] = fmaf(o[h][0], al, pw * v01.x);
+                o[h][1] = fmaf(o[h][1], al, pw * v01.y);
+                o[h][2] = fmaf(o[h][2], al, pw * v23.x);
+                o[h][3] = fmaf(o[h][3], al, pw * v23.y);
+                m[h] = mn;
+            }
+        }
+    }
+    }
+#pragma unroll
+    for (int h = 0; h < 4 * NG; ++h) {
+        if (h >= g) continue;
+        float* row = part + ((size_t)u * g + h) * (kD + 2);
+        *reinterpret_cast<float2*>(row + 4 * lane) = make_float2(o[h][0], o[h][1]);
+        *reinterpret_cast<float2*>(row + 4 * lane + 2) = make_float2(o[h][2], o[h][3]);
+        if (lane == 0) {
+            row[kD] = m[h];
+            row[kD + 1] = l[h];
+        }
+    }
+}
+
+template <typename IO>
+static int launch_zc_partial(const rdkv_decode_args* a, cudaStream_t st) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.stream = st;
+    cfg.gridDim = dim3((a->units + kZcpUnits - 1) / kZcpUnits);
+    cfg.blockDim = dim3(32 * kZcpUnits);
+    auto kern = a->group > 4 ? zc_partial_kernel<IO, 2> : zc_partial_kernel<IO, 1>;
+    const cudaError_t e =
+        cudaLaunchKernelEx(&cfg, kern, static_cast<const IO*>(a->q), static_cast<const __half*>(a->zc_k),
+                           static_cast<const __half*>(a->zc_v), a->zc_len, a->units, a->group, a->zc_cap,
+                           static_cast<float*>(a->workspace));
+    return e == cudaSuccess ? RDKV_OK : RDKV_ECUDA;
+}
+
+// Zone C through the prepass: short uniform-2-bit tiles, the whole arena in one
+// launch (no unit subset), device output, and the caller's workspace holds one
+// [units][g][d + 2] f32 row set (rdkv_cuda_decode_workspace(units, g, d, 2) / 2).
+// The experiments build can force the fused variants (RDKV_DECODE_ZC_FUSED=1).
+static bool zc_prepass_ok(const rdkv_decode_args* a) {
+#ifdef RDKV_DECODE_EXPERIMENTS
+    static const char* fused_env = getenv("RDKV_DECODE_ZC_FUSED");
+    if (fused_env && atoi(fused_env) == 1) return false;
+#endif
+    // (a known bound of <= kZcFused rows keeps the fused variant: staging <= 4 rows with
+    // each tile costs less than the prepass launch)
+    if ((a->flags & RDKV_DECODE_ZC_BOUND) && a->zc_bound <= kZcFused) return false;
+    return a->zc_len && !a->unit_ids && a->workspace && a->group <= 8 &&
+           a->workspace_bytes >= sizeof(float) * (size_t)a->units * a->group * (kD + 2) && a->plan.uniform2 != 3 &&
+           a->plan.max_slots <= kU2MaxSlots && !(a->flags & RDKV_DECODE_OUT_HOST);
+}
+
 static bool zc_fusable(const rdkv_decode_args* a) {
     return a->zc_len && (a->flags & RDKV_DECODE_ZC_BOUND) && a->zc_bound <= kZcFusedMax;
 }
@@ -2615,13 +2790,14 @@ static bool u2x_group_ok(const rdkv_decode_args* a) {
     if (a->plan.uniform2 == 3)  // MIX tiles: short-tile kernel only, no Zone C
         return a->group <= 8 && a->plan.max_slots <= kU2MaxSlots && !a->zc_len;
     if (a->group <= 4) return true;
-    return a->group <= 8 && a->plan.max_slots <= kU2MaxSlots && (!a->zc_len || zc_fusable(a));
+    return a->group <= 8 && a->plan.max_slots <= kU2MaxSlots && (!a->zc_len || zc_fusable(a) || zc_prepass_ok(a));
 }
 
 template <typename IO, int NBMAX, bool FULLK>
 static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_blocks = 0) {
     const int qbytes = a->group * kD * (int)sizeof(IO);
-    const bool zcf = zc_fusable(a);
+    const bool zcp = zc_prepass_ok(a);  // Zone C folded from the prepass rows (no staging)
+    const bool zcf = !zcp && zc_fusable(a);
     const bool zc16 = zcf && a->zc_bound > kZcFused;  // the long-generation variant (16 fused rows)
     const int slot = (a->plan.max_decode_bytes + (zcf ? zc_stage(zc16 ? kZcFusedMax : kZcFused) : 0) + qbytes + 127) & ~127;
     const bool mix = a->plan.uniform2 == 3;  // some tiles carry a few 4-bit rows / channels
@@ -2644,7 +2820,13 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
     const int mode = nenv ? atoi(nenv) : 0;
     const bool bulk = (a->flags & RDKV_DECODE_OUT_HOST) != 0;
     const bool g8 = a->group > 4;
-    auto kern = mix ? (g8 ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, 0, true, true>
+    if (zcp) {
+        if (int rc = launch_zc_partial<IO>(a, st)) return rc;
+        p.partial = static_cast<float*>(a->workspace);
+    }
+    auto kern = zcp ? (g8 ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, -1, true>
+                          : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, -1>)
+              : mix ? (g8 ? (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, 0, true, true>
                                   : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, 0, true, true>)
                           : (bulk ? decode_u2x_kernel<IO, NBMAX, FULLK, 0, true, false, 0, false, true>
                                   : decode_u2x_kernel<IO, NBMAX, FULLK, 0, false, false, 0, false, true>))
@@ -2664,9 +2846,10 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
               : mode == 2 ? decode_u2x_kernel<IO, NBMAX, FULLK, 2>
 #endif
                           : decode_u2x_kernel<IO, NBMAX, FULLK, 0>;
-    static std::atomic<int> smem_set[18][kMaxDevices];  // one slot per instantiation above
+    static std::atomic<int> smem_set[20][kMaxDevices];  // one slot per instantiation above
     set_smem_once(kern, (int)smem,
-                  smem_set[mix ? 10 + (g8 ? 2 : 0) + (bulk ? 1 : 0)
+                  smem_set[zcp ? 18 + (g8 ? 1 : 0)
+                           : mix ? 10 + (g8 ? 2 : 0) + (bulk ? 1 : 0)
                            : g8 ? (zc16 ? 14 + (bulk ? 1 : 0) : 6 + (zcf ? 2 : 0) + (bulk ? 1 : 0))
                            : zcf ? (zc16 ? 16 + (bulk ? 1 : 0) : 4 + (bulk ? 1 : 0))
                            : bulk ? 3 : mode == 1 ? 1 : mode == 2 ? 2 : 0],
@@ -2732,7 +2915,8 @@ static int launch_u2x_t(const rdkv_decode_args* a, cudaStream_t st, int max_bloc
 template <typename IO, bool FULLK>
 static int launch_u2x_k(const rdkv_decode_args* a, cudaStream_t st, int max_blocks) {
     // long tiles or Zone C rows beyond the fused bound: the chunked kernel
-    if (a->plan.max_slots > kU2MaxSlots || (a->zc_len && !zc_fusable(a))) return launch_u2c<IO, FULLK>(a, st);
+    if (a->plan.max_slots > kU2MaxSlots || (a->zc_len && !zc_fusable(a) && !zc_prepass_ok(a)))
+        return launch_u2c<IO, FULLK>(a, st);
     const int nb = (a->plan.max_slots + 31) / 32;  // 32-token blocks of the largest tile
     if (nb <= 2) return launch_u2x_t<IO, 2, FULLK>(a, st, max_blocks);
     if (nb <= 4) return launch_u2x_t<IO, 4, FULLK>(a, st, max_blocks);

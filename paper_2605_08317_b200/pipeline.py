@@ -332,6 +332,7 @@ class PackedModel:
     plan: capi.DecodePlan | None = None
     unit_ids: torch.Tensor | None = None       # [U] int32: uniform-2-bit tiles first (split dispatch)
     split_ws: torch.Tensor | None = None       # split-K partials of the chunked mixed 2/4-bit kernel
+    zc_ws: torch.Tensor | None = None          # Zone C prepass rows [U][g][d + 2] f32 (zc_workspace())
     _infos: list = field(default_factory=list)
 
     def prepare(self) -> capi.DecodePlan:
@@ -357,7 +358,17 @@ class PackedModel:
         """Reuse another model's prepare() results (same tiles, e.g. an arena copy)."""
         self.decode_sizes, self.plan, self.unit_ids = other.decode_sizes, other.plan, other.unit_ids
         self.split_ws = other.split_ws
+        self.zc_ws = other.zc_ws
         return self
+
+    def zc_workspace(self) -> torch.Tensor:
+        """Scratch of the Zone C prepass (one [g][d + 2] f32 row set per unit): with it the
+        short-tile decode folds the appended rows in without staging them (csrc/decode_mma.cu
+        zc_partial_kernel); without it the fused / chunked Zone C variants run."""
+        need = self.units * self.group * (self.head_dim + 2) * 4
+        if self.zc_ws is None or self.zc_ws.numel() < need:
+            self.zc_ws = torch.empty(need, dtype=torch.uint8, device=self.arena.device)
+        return self.zc_ws
 
     @property
     def arena_bytes(self) -> int:
@@ -544,6 +555,8 @@ def decode_args(model: PackedModel, q, out, split=1, kernel=0, workspace=None) -
     if workspace is None and split == 1 and kernel in (0, 2) and model.split_ws is not None:
         a.split = 0  # automatic split-K over the model's partials workspace
         workspace = model.split_ws
+    elif workspace is None and split == 1 and kernel in (0, 2) and model.zc_len is not None:
+        workspace = model.zc_workspace()  # Zone C prepass rows (short uniform-2-bit tiles)
     if workspace is not None:
         a.workspace, a.workspace_bytes = workspace.data_ptr(), workspace.numel()
     return a

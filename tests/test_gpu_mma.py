@@ -335,9 +335,14 @@ def test_host_decode_zero_copy_zone_c(cuda, orc, appends, known):
     if not known:
         model.zc_count = None
     q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).half()
-    want = P.packed_decode_step(model, q).cpu()
+    # the zero-copy path stages Zone C itself (fused / chunked): compare with the device
+    # step on the same variant (no prepass workspace), and with the prepass step to 1e-3
+    tiny = torch.empty(1, dtype=torch.uint8, device=cuda)
+    want = P.packed_decode_step(model, q, workspace=tiny).cpu()
+    pre = P.packed_decode_step(model, q).float().cpu()
+    assert float(((pre - want.float()).norm() / want.float().norm()).item()) < 1e-3
     qd, od = torch.empty_like(q), torch.empty_like(q)
-    a = P.decode_args(model, qd, od)
+    a = P.decode_args(model, qd, od, workspace=tiny)
     qh = q.cpu().pin_memory()
     oh = torch.full_like(qh, float("nan")).pin_memory()
     assert capi.lib().rdkv_cuda_decode_host(C.byref(a), qh.data_ptr(), oh.data_ptr(),
@@ -531,3 +536,35 @@ def test_mixed_248_split_k_kernel(cuda, orc, g, T, io, nkept):
     whole = P.packed_decode_step(model, qd).float()
     model.split_ws = ws
     assert float(((split - whole).norm() / whole.norm()).item()) < 1e-3
+
+
+@pytest.mark.parametrize("g,appends,io", [(4, 1, torch.float16), (4, 7, torch.float32), (8, 3, torch.float16),
+                                          (7, 20, torch.float32), (4, 33, torch.float16)])
+def test_zone_c_prepass_matches_fused_and_oracle(cuda, orc, g, appends, io):
+    """Zone C through the prepass (zc_partial_kernel: one warp per unit folds the appended
+    rows into a [g][d + 2] softmax row, the short-tile kernel merges it in its epilogue) —
+    the default whenever the model carries its Zone C workspace — against the oracle, the
+    fused / chunked variants (no workspace) and the bound-less path."""
+    rng = np.random.default_rng(700 + 10 * g + appends)
+    cases = []
+    for n in (1, 40, 128, 150, 160, 96):
+        k, v, vb, kb, q = _random_case(rng, 500, g)
+        vb[:] = 0
+        vb[np.sort(rng.choice(500, n, replace=False))] = 2
+        kb[:] = 2
+        cases.append((k, v, vb, kb, q))
+    worst, model = _run_batch(cuda, orc, cases, g, io=io, appends=appends, rng=rng, tol=U2X_TOL)
+    assert model.plan.uniform2 == 2 and model.zc_ws is not None
+    assert worst < (U2X_TOL if io == torch.float32 else 1e-3), worst
+    q = torch.from_numpy(np.stack([c[4] for c in cases])).to(cuda).to(io)
+    tiny = torch.empty(1, dtype=torch.uint8, device=cuda)  # too small: no prepass
+    count, model.zc_count = model.zc_count, None
+    pre = P.packed_decode_step(model, q).float()  # no host bound: the prepass
+    chunked = P.packed_decode_step(model, q, workspace=tiny).float()  # chunked Zone C
+    model.zc_count = count
+    dflt = P.packed_decode_step(model, q).float()  # bound known: fused (<= 4 rows) or prepass
+    fused = P.packed_decode_step(model, q, workspace=tiny).float()
+    for other in (fused, chunked, dflt):
+        assert float(((pre - other).norm() / other.norm()).item()) < 1e-3
+    if appends > 4:
+        assert torch.equal(pre, dflt)  # the same prepass path, bound or not
