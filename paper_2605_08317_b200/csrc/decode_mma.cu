@@ -2639,9 +2639,12 @@ static int launch_u2c(const rdkv_decode_args* a, cudaStream_t st, float* partial
 // the weight sum — into [units][g][d + 2] f32; the short-tile kernel (ZCN < 0)
 // folds that row into its epilogue. The tile kernel keeps its 8 warp pairs per
 // SM (no Zone C staging in its buffers); the rows are read once, here.
-// Logits of 4 heads are reduced together: two exchange stages halve the values
-// a lane carries, three more finish the sum in 8-lane groups (head h in lanes
-// 8h .. 8h + 7), four broadcasts return them — 10 shuffles per token and group.
+// Rows go in batches of 8 (loads in flight together). Logits of 4 heads are
+// reduced together: two exchange stages halve the values a lane carries, three
+// more finish the sum in 8-lane groups (head h in lanes 8h .. 8h + 7) — 6
+// shuffles per row and group, 8 independent chains per batch; the batch max then
+// rescales the running state once per head, and the weights reach every lane's
+// PV channels by broadcast from lane 8h.
 constexpr int kZcpUnits = 8;  // units (warps) per CTA
 template <typename IO>
 __device__ __forceinline__ void zcp_load_q(const IO* qrow, int lane, float (&q)[4]) {
@@ -2669,68 +2672,97 @@ __global__ void __launch_bounds__(32 * kZcpUnits) zc_partial_kernel(const IO* __
     constexpr float kScale = 0.08838834764831845f * 1.4426950408889634f;  // log2(e) / sqrt(d)
     int z = zlen[u];
     z = z < cap ? z : cap;
-    float qv[4 * NG][4], o[4 * NG][4], m[4 * NG], l[4 * NG];
+    float qv[4 * NG][4], o[4 * NG][4];
+    float mrun[NG], lrun[NG];  // running max / sum of head 4 gr + (lane >> 3), per 8-lane group
 #pragma unroll
     for (int h = 0; h < 4 * NG; ++h) {
         if (h < g)
             zcp_load_q(q + ((size_t)u * g + h) * kD, lane, qv[h]);
         else
             qv[h][0] = qv[h][1] = qv[h][2] = qv[h][3] = 0.0f;
-        m[h] = -INFINITY;
-        l[h] = 0.0f;
         o[h][0] = o[h][1] = o[h][2] = o[h][3] = 0.0f;
+    }
+#pragma unroll
+    for (int gr = 0; gr < NG; ++gr) {
+        mrun[gr] = -INFINITY;
+        lrun[gr] = 0.0f;
     }
     const __half* kr = zk + (size_t)u * cap * kD + 4 * lane;
     const __half* vr = zv + (size_t)u * cap * kD + 4 * lane;
+    const bool hi16 = (lane & 16) != 0, hi8 = (lane & 8) != 0;
     constexpr int kBatch = 8;  // rows whose loads are in flight together
     for (int t0 = 0; t0 < z; t0 += kBatch) {
-    uint2 kb[kBatch], vb[kBatch];
+        uint2 kb[kBatch], vb[kBatch];
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j)
-        if (t0 + j < z) {
-            kb[j] = *reinterpret_cast<const uint2*>(kr + (size_t)(t0 + j) * kD);
-            vb[j] = *reinterpret_cast<const uint2*>(vr + (size_t)(t0 + j) * kD);
+        for (int j = 0; j < kBatch; ++j) {
+            kb[j] = vb[j] = make_uint2(0u, 0u);
+            if (t0 + j < z) {
+                kb[j] = *reinterpret_cast<const uint2*>(kr + (size_t)(t0 + j) * kD);
+                vb[j] = *reinterpret_cast<const uint2*>(vr + (size_t)(t0 + j) * kD);
+            }
         }
+        // phase 1: the batch's logits (independent chains), head 4 gr + (lane >> 3)
+        float lgt[NG][kBatch];
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-        if (t0 + j >= z) break;
-        const uint2 kw = kb[j], vw = vb[j];
-        const float2 k01 = __half22float2(*reinterpret_cast<const __half2*>(&kw.x));
-        const float2 k23 = __half22float2(*reinterpret_cast<const __half2*>(&kw.y));
-        const float2 v01 = __half22float2(*reinterpret_cast<const __half2*>(&vw.x));
-        const float2 v23 = __half22float2(*reinterpret_cast<const __half2*>(&vw.y));
+        for (int j = 0; j < kBatch; ++j) {
+            const float2 k01 = __half22float2(*reinterpret_cast<const __half2*>(&kb[j].x));
+            const float2 k23 = __half22float2(*reinterpret_cast<const __half2*>(&kb[j].y));
+#pragma unroll
+            for (int gr = 0; gr < NG; ++gr) {
+                float sp[4];
+#pragma unroll
+                for (int hh = 0; hh < 4; ++hh) {
+                    const float* qq = qv[4 * gr + hh];
+                    sp[hh] = fmaf(qq[3], k23.y, fmaf(qq[2], k23.x, fmaf(qq[1], k01.y, qq[0] * k01.x)));
+                }
+                float a0 = hi16 ? sp[2] : sp[0], a1 = hi16 ? sp[3] : sp[1];
+                const float b0 = hi16 ? sp[0] : sp[2], b1 = hi16 ? sp[1] : sp[3];
+                a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
+                a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
+                float c = (hi8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+                c += __shfl_xor_sync(0xffffffffu, c, 4);
+                c += __shfl_xor_sync(0xffffffffu, c, 2);
+                c += __shfl_xor_sync(0xffffffffu, c, 1);
+                lgt[gr][j] = t0 + j < z ? c * kScale : -INFINITY;
+            }
+        }
+        // phase 2: per head, the batch max rescales the running state once; weights
+        // of the batch's rows; PV for every head of the group over this lane's channels
 #pragma unroll
         for (int gr = 0; gr < NG; ++gr) {
-            float sp[4];
+            float bm = lgt[gr][0];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float* qq = qv[4 * gr + j];
-                sp[j] = fmaf(qq[3], k23.y, fmaf(qq[2], k23.x, fmaf(qq[1], k01.y, qq[0] * k01.x)));
+            for (int j = 1; j < kBatch; ++j) bm = fmaxf(bm, lgt[gr][j]);
+            const float mn = fmaxf(mrun[gr], bm);
+            const float al = ex2_approx(mrun[gr] - mn);
+            float pj[kBatch], ps = 0.0f;
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                pj[j] = ex2_approx(lgt[gr][j] - mn);
+                ps += pj[j];
             }
-            const bool hi16 = (lane & 16) != 0, hi8 = (lane & 8) != 0;
-            float a0 = hi16 ? sp[2] : sp[0], a1 = hi16 ? sp[3] : sp[1];
-            const float b0 = hi16 ? sp[0] : sp[2], b1 = hi16 ? sp[1] : sp[3];
-            a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
-            a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
-            float c = (hi8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
-            c += __shfl_xor_sync(0xffffffffu, c, 4);
-            c += __shfl_xor_sync(0xffffffffu, c, 2);
-            c += __shfl_xor_sync(0xffffffffu, c, 1);
+            lrun[gr] = fmaf(lrun[gr], al, ps);
+            mrun[gr] = mn;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int h = 4 * gr + j;
-                const float lg = __shfl_sync(0xffffffffu, c, 8 * j) * kScale;
-                const float mn = fmaxf(m[h], lg);
-                const float al = ex2_approx(m[h] - mn), pw = ex2_approx(lg - mn);
-                l[h] = fmaf(l[h], al, pw);
-                o[h][0] = fmaf(o[h][0], al, pw * v01.x);
-                o[h][1] = fmaf(o[h][1], al, pw * v01.y);
-                o[h][2] = fmaf(o[h][2], al, pw * v23.x);
-                o[h][3] = fmaf(o[h][3], al, pw * v23.y);
-                m[h] = mn;
+            for (int hh = 0; hh < 4; ++hh) {
+                float* oh = o[4 * gr + hh];
+                const float ah = __shfl_sync(0xffffffffu, al, 8 * hh);
+                oh[0] *= ah;
+                oh[1] *= ah;
+                oh[2] *= ah;
+                oh[3] *= ah;
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    const float pw = __shfl_sync(0xffffffffu, pj[j], 8 * hh);
+                    const float2 v01 = __half22float2(*reinterpret_cast<const __half2*>(&vb[j].x));
+                    const float2 v23 = __half22float2(*reinterpret_cast<const __half2*>(&vb[j].y));
+                    oh[0] = fmaf(pw, v01.x, oh[0]);
+                    oh[1] = fmaf(pw, v01.y, oh[1]);
+                    oh[2] = fmaf(pw, v23.x, oh[2]);
+                    oh[3] = fmaf(pw, v23.y, oh[3]);
+                }
             }
         }
-    }
     }
 #pragma unroll
     for (int h = 0; h < 4 * NG; ++h) {
@@ -2738,9 +2770,9 @@ __global__ void __launch_bounds__(32 * kZcpUnits) zc_partial_kernel(const IO* __
         float* row = part + ((size_t)u * g + h) * (kD + 2);
         *reinterpret_cast<float2*>(row + 4 * lane) = make_float2(o[h][0], o[h][1]);
         *reinterpret_cast<float2*>(row + 4 * lane + 2) = make_float2(o[h][2], o[h][3]);
-        if (lane == 0) {
-            row[kD] = m[h];
-            row[kD + 1] = l[h];
+        if (lane == 8 * (h & 3)) {
+            row[kD] = mrun[h >> 2];
+            row[kD + 1] = lrun[h >> 2];
         }
     }
 }
