@@ -111,12 +111,12 @@ def test_configs3_large_mixed_tiles_auto_dispatch(cuda, orc, name, Hq, Hkv, n):
 
 
 @pytest.mark.parametrize("name,L,Hq,Hkv,n", [("mistral-7b", 32, 32, 8, 256), ("qwen2.5-7b", 28, 28, 4, 1024)])
-def test_configs3_full_step_dynamic_claims(cuda, name, L, Hq, Hkv, n):
+def test_configs3_full_step_split_k(cuda, name, L, Hq, Hkv, n):
     """A whole configs[3] step (batch 4, every layer: 448 / 1024 tiles) has more
-    (tile, part) items than warp pairs, so the chunked split-K kernel hands out
-    items after the first round from its claim counter. The step must equal the
+    (tile, part) items than warp pairs, so the chunked split-K kernel deals items
+    over several rounds and merges the parts. The step must equal the
     one-pair-per-tile decode (no partials) and the CUDA-core kernel, and repeat
-    bit-identically (which pair takes an item must not change a bit)."""
+    bit-identically."""
     from paper_2605_08317_b200.workload import build
 
     spec = WorkloadSpec(batch=4, layers=L, q_heads=Hq, kv_heads=Hkv, ctx=65536, n_tokens=n, seed=11,
